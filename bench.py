@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Benchmark: additive-kernel NFFT matvecs/s on BASELINE config 4.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[3], the one the metric is quoted on):
+N = 1,000,000 points, d = 30 (seeded 5-component Gaussian mixture), 10
+consecutive windows of 3 features, Gaussian kernel, ell = 1 (prescaled
+1/sqrt(3)), sigma_f = 1, one RHS, reference default NFFT setup (m = 32,
+n = 64, cutoff 6, Kaiser-Bessel).  A step is one full K v over all windows.
+
+* ``value``: K v per second with v and the plan resident in HBM (device API).
+* ``e2e``: the same through the public numpy API (fast_matvec with a host
+  vector): H2D of v and D2H of K v inside every timed step.
+* ``deriv``: (K v, dK/d ell v, dK/d sigma_f v) triples per second from one
+  shared spread (fast_matvecs).
+* ``roofline``: the dominant kernel (q=3 spread or interp) timed alone with
+  CUDA events on the launching stream; FP64-FMA-bound, so achieved TFLOP/s of
+  algorithmic FLOPs (2 * 12^3 per point per window) against the FP64 DFMA
+  peak measured in this run (MEASURED_PEAKS.json has no FP64 entry).
+* ``cpu_baseline``: the CPU oracle port (oracle/, serial C loops + numpy FFT,
+  the reference's algorithm and cost structure) timed on one window at full N.
+
+Multi-GPU (torchrun): windows are sharded over ranks and the partial K v is
+summed with one NCCL all-reduce; timing is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "additive-kernel matvecs/sec at N=1M, 10 windows (+dK mvs); rel. err vs dense/oracle"
+WORKLOAD = ("C4: N=1,000,000, d=30 seeded 5-component Gaussian mixture (means U[-1,1], std 0.3), "
+            "min-max scaled, 10 consecutive windows of 3, gauss ell=1 (prescaled 1/sqrt(3)), sigma_f=1, "
+            "1 RHS v~N(0,1), preset default (m=32, n=64, cutoff 6, Kaiser-Bessel)")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=1_000_000, help="points (default: the config's 1M)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="skip extras (for profilers)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm (CPU oracle port)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import restate as R
+    from paper_2404_17344_b200 import configs
+
+    wl = configs.config4(args.n)
+    cores = len(os.sched_getaffinity(0))
+    P = len(wl.window_set)
+    T = max(1, min(P, cores))
+    cols = [wl.window_set.columns(w) for w in wl.window_set]
+    fs = R.FastSum("gauss", wl.spec.ell, wl.spec.sigma_f, cols[:T], wl.data.features)
+    v = wl.V[0]
+    from concurrent.futures import ThreadPoolExecutor
+
+    def step():
+        with ThreadPoolExecutor(max_workers=T) as ex:
+            list(ex.map(lambda k: fs.window_product(k, v), range(T)))
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    value = (T / P) / dt
+    sample = f"{T} of {P} windows at full N={wl.data.n_rows} per step, run concurrently on {T} threads"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "matvecs/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "parallelism": f"cpu threads={T}"},
+        "cpu_baseline": {"value": value, "unit": "matvecs/s", "cores": T, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "matvecs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference is pure Python+numba and cannot travel to the GPU box; this is the oracle/ port "
+                "(same algorithm: serial C gridding loops + numpy pocketfft), windows in parallel threads",
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def cuda_time(torch, fn, reps):
+    """Average ms of fn() over reps, CUDA events on the current stream."""
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(reps):
+        fn()
+    e1.record(st)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def kernel_roofline(torch, plan, wl, peaks, reps=10):
+    """Time the q=3 spread and interp kernels alone (ak_spread / ak_interp: the
+    same kernels ak_op_apply launches) and express them against the FP64 peak."""
+    import ctypes
+
+    from paper_2404_17344_b200 import _native
+    from paper_2404_17344_b200.nufft import _stream_ptr
+
+    lib = _native.lib()
+    geom = plan.geometries
+    N = wl.data.n_rows
+    P3 = sum(1 for w in wl.window_set if len(w) == 3)
+    T = plan.nufft_plans[3].taps
+    V = torch.as_tensor(wl.V[:1], device="cuda").contiguous()
+    grids = torch.zeros(geom.canon_total, dtype=torch.float64, device="cuda")
+    out = torch.zeros(N, dtype=torch.float64, device="cuda")
+    scale = torch.ones(geom.n_windows, dtype=torch.float64, device="cuda")
+    st = _stream_ptr(torch)
+
+    def spread():
+        _native.check(lib.ak_spread(geom.handle, V.data_ptr(), 1, N, grids.data_ptr(), st))
+
+    def interp():
+        _native.check(lib.ak_interp(geom.handle, grids.data_ptr(), 1, scale.data_ptr(), out.data_ptr(), N, 1, 0, st))
+
+    for _ in range(2):
+        spread()
+        interp()
+    t_spread = cuda_time(torch, spread, reps)
+    t_interp = cuda_time(torch, interp, reps)
+    flops = 2.0 * T ** 3 * N * P3  # algorithmic: one FMA per tap per point per window
+    fp64 = peaks["fp64_tflops"]
+    name, t = ("spread_q3", t_spread) if t_spread >= t_interp else ("interp_q3", t_interp)
+    achieved = flops / (t * 1e-3) / 1e12
+    alg_bytes = N * P3 * (24 + 8)  # coordinates + value (spread) / output (interp), compulsory
+    return {
+        "bound": "fp64", "kernel": name, "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
+        "frac": achieved / fp64, "traffic": None,
+        "peak_source": "ak_probe_fp64 DFMA microbenchmark in this run (MEASURED_PEAKS.json has no FP64 figure)",
+        "flops_per_launch": flops, "ms_per_launch": t,
+        "spread_ms": t_spread, "interp_ms": t_interp,
+        "hbm_algorithmic_gbs": alg_bytes / (t * 1e-3) / 1e9, "hbm_peak_gbs": peaks.get("hbm_gbs"),
+    }
+
+
+def fp64_peak(torch):
+    import ctypes
+
+    from paper_2404_17344_b200 import _native
+    from paper_2404_17344_b200.nufft import _stream_ptr
+
+    lib = _native.lib()
+    best = 0.0
+    dmma = 0.0
+    for _ in range(3):
+        v = ctypes.c_double()
+        _native.check(lib.ak_probe_fp64(20000, _stream_ptr(torch), ctypes.byref(v)))
+        best = max(best, v.value)
+        _native.check(lib.ak_probe_dmma(5000, _stream_ptr(torch), ctypes.byref(v)))
+        dmma = max(dmma, v.value)
+    return best, dmma
+
+
+def cpu_baseline(wl, gpu_window_out):
+    """Oracle port, one window at full N, one core: K_0 v; returns (baseline, rel err)."""
+    from oracle import restate as R
+
+    cols = [wl.window_set.columns(w) for w in wl.window_set]
+    fs = R.FastSum("gauss", wl.spec.ell, wl.spec.sigma_f, cols[:1], wl.data.features)
+    v = wl.V[0]
+    t0 = time.perf_counter()
+    ref = fs.matvec(v)
+    dt = time.perf_counter() - t0
+    P = len(cols)
+    err = float(np.linalg.norm(gpu_window_out - ref) / np.linalg.norm(ref))
+    base = {"value": 1.0 / (P * dt), "unit": "matvecs/s", "cores": 1, "kind": "port",
+            "sample": f"window 1 of {P} at full N={wl.data.n_rows} (1 RHS), scaled x{P}; "
+                      f"{dt:.1f} s for the window; plan build excluded"}
+    return base, err
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2404_17344_b200 import _native, configs
+    from paper_2404_17344_b200.fastsum import build_plan, fast_matvec, fast_matvecs
+    from paper_2404_17344_b200.windows import WindowSet
+
+    wl = configs.config4(args.n)
+    N = wl.data.n_rows
+    wins = wl.window_set.windows
+    mine = tuple(w for i, w in enumerate(wins) if i % world == rank) if world > 1 else wins
+    ws = WindowSet(mine, d_max=3)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    t0 = time.perf_counter()
+    plan = build_plan(wl.spec, ws, "default", wl.data)
+    torch.cuda.synchronize()
+    plan_s = time.perf_counter() - t0
+
+    v_host = np.ascontiguousarray(wl.V[0])
+    v_dev = torch.as_tensor(v_host, device="cuda")
+
+    def step_dev():
+        out = fast_matvec(plan, v_dev)
+        if world > 1:
+            dist.all_reduce(out)
+        return out
+
+    def step_e2e():
+        if world > 1:
+            out = fast_matvec(plan, torch.as_tensor(v_host).pin_memory().cuda(non_blocking=True))
+            dist.all_reduce(out)
+            return out.cpu().numpy()
+        return fast_matvec(plan, v_host)
+
+    def step_deriv():
+        res = fast_matvecs(plan, v_dev, dell=True, dsigma=True)
+        if world > 1:
+            for k in ("K", "dK_dell", "dK_dsigma"):
+                dist.all_reduce(res[k])
+        return res
+
+    def timed(fn, steps, warmup):
+        for _ in range(warmup):
+            fn()
+        barrier()
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = _native.launch_count()
+        e0.record(st)
+        for _ in range(steps):
+            fn()
+        e1.record(st)
+        torch.cuda.synchronize()
+        barrier()
+        launches = _native.launch_count() - l0
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms / steps, launches
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    ms_step, launches = timed(step_dev, args.steps, args.warmup)
+    clocks = sampler.stop()
+
+    result = {
+        "metric": METRIC, "value": 1000.0 / ms_step, "unit": "matvecs/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "N": N, "windows": len(wins), "rhs": 1,
+                   "parallelism": f"window-shard x{world} + NCCL all-reduce" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2: per-step geometry stream 32 B x 1M x 10 windows = 320 MB"},
+        "clocks": clocks, "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
+        "plan_build_s": plan_s,
+    }
+
+    if not args.quick:
+        ms_e2e, _ = timed(step_e2e, max(3, args.steps // 2), 2)
+        result["e2e"] = {"value": 1000.0 / ms_e2e, "unit": "matvecs/s", "h2d_bytes_per_step": 8 * N,
+                         "d2h_bytes_per_step": 8 * N, "ms_per_step": ms_e2e,
+                         "api": "fastsum.fast_matvec(plan, numpy v) -> numpy"}
+        ms_d, _ = timed(step_deriv, max(3, args.steps // 2), 2)
+        result["deriv"] = {"value": 1000.0 / ms_d, "unit": "(K v, dK/dl v, dK/ds v) triples/s",
+                           "ms_per_step": ms_d, "matvecs_per_s": 3000.0 / ms_d}
+        if rank == 0:
+            peaks_file = ROOT / "MEASURED_PEAKS.json"
+            peaks = json.loads(peaks_file.read_text()) if peaks_file.exists() else {"hbm_gbs": 6650.0}
+            fp64, dmma = fp64_peak(torch)
+            peaks["fp64_tflops"] = fp64
+            result["fp64_probe"] = {"dfma_tflops": fp64, "dmma_tflops": dmma}
+            if world == 1:
+                result["roofline"] = kernel_roofline(torch, plan, wl, peaks)
+            if world == 1 and not args.no_cpu_baseline:
+                one = build_plan(wl.spec, WindowSet((wins[0],), d_max=3), "default", wl.data)
+                gpu_w0 = fast_matvec(one, v_host)
+                base, err = cpu_baseline(wl, gpu_w0)
+                result["cpu_baseline"] = base
+                result["rel_err_vs_oracle"] = {"value": err, "scope": "window 1 at full N (oracle port)",
+                                               "tolerance": 1e-8}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,178 @@
+/*
+ * addkern_b200.h -- C ABI of the B200 (sm_100a) NFFT fast-summation path.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `addkern` (arXiv 2404.17344).  The reference runs it in-process as numba
+ * kernels called from numpy code; the entry points below replace, one for
+ * one, the pieces of that path (citations are /root/reference/pkg/src/addkern):
+ *
+ *   ak_geom_create     prepare_points            nufft.py:169-191
+ *                      (called per window by build_plan, fastsum.py:128-130)
+ *   ak_spread          _spread_1/_spread_2/_spread_3 nufft.py:197-254
+ *   ak_interp          _interp_1/_interp_2/_interp_3 nufft.py:257-320
+ *   ak_op_apply        the per-window loop of fast_matvec fastsum.py:150-160
+ *                      (type-1 NUFFT nufft.py:346-365 -> coefficient multiply
+ *                      fastsum.py:159 -> type-2 NUFFT nufft.py:368-394, summed
+ *                      over windows and scaled, fastsum.py:136-138)
+ *   ak_type1_band      fftn + band + deconvolution of nufft_type1 (nufft.py:362-365)
+ *   ak_type2_grid      deconvolution + zero-pad + ifftn of nufft_type2 (nufft.py:379-383)
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers owned by the caller unless noted.
+ *    Scalars and small descriptor arrays are host memory and are copied.
+ *  - `stream` is a cudaStream_t passed as void*; NULL means the legacy stream.
+ *    Every call is stream-ordered and asynchronous unless documented.
+ *  - Return value: AK_OK (0) or a negative AK_ERR_* code.  Nothing throws
+ *    across the ABI; ak_last_error() returns a thread-local message.
+ *  - Handles are immutable after creation (ak_op owns mutable workspace: use
+ *    one ak_op per concurrent stream).
+ *  - Arithmetic is IEEE float64 throughout (real arithmetic: for real inputs
+ *    the reference's complex pipeline has an exactly zero imaginary part up to
+ *    rounding, fastsum.py:141-147).
+ */
+#ifndef ADDKERN_B200_H
+#define ADDKERN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AK_OK              0
+#define AK_ERR_INVALID    -1   /* bad argument (maps to ValueError)                  */
+#define AK_ERR_CUDA       -2   /* CUDA runtime error                                  */
+#define AK_ERR_DOMAIN     -3   /* point outside [-1/2,1/2) (PointOutOfDomainError)    */
+#define AK_ERR_ALLOC      -4   /* device allocation failed                            */
+#define AK_ERR_CUFFT      -5   /* cuFFT error                                         */
+#define AK_ERR_UNSUPPORTED -6  /* configuration has no kernel (e.g. taps > 16)        */
+
+#define AK_MAX_TAPS   16
+#define AK_MAX_PAIRS   8
+#define AK_NCOEF       7       /* coefficients per even/odd window polynomial (degree 13) */
+
+/*
+ * Separable window function (Kaiser-Bessel or Gaussian, nufft.py:125-131)
+ * tabulated as one polynomial per tap in s = 2*frac - 1, frac = t - floor(t),
+ * t = (x + 1/2) * n.  Tap a (0 <= a < taps) sits at offset z_a = frac + cutoff-1-a
+ * (nufft.py:185-187).  Because the window is even, taps a and taps-1-a share
+ * one even/odd split:  w_a = E_a(s^2) + s*O_a(s^2),  w_{taps-1-a} = E_a - s*O_a.
+ * Coefficients are stored highest power first.
+ */
+typedef struct ak_window_fn {
+    int32_t taps;                              /* 2*cutoff, even, 4..16 */
+    int32_t ncoef;                             /* must equal AK_NCOEF    */
+    double  ce[AK_MAX_PAIRS][AK_NCOEF];        /* even parts             */
+    double  co[AK_MAX_PAIRS][AK_NCOEF];        /* odd parts              */
+} ak_window_fn;
+
+/* Opaque handles */
+typedef struct ak_geom ak_geom;  /* bin-sorted points of P windows (replaces SpreadGeometry, nufft.py:160-166) */
+typedef struct ak_op   ak_op;    /* workspace + cuFFT plans for one (geometry, R, C) apply shape */
+
+const char* ak_last_error(void);
+const char* ak_version(void);
+
+/* Number of kernel launches issued by this library since load (evidence counter). */
+int64_t ak_launch_count(void);
+
+/*
+ * ak_geom_create -- bin-sort the points of every window (replaces prepare_points).
+ *   n         oversampled grid size per axis (NufftPlan.n, nufft.py:108)
+ *   P         number of windows
+ *   q         host int[P]: window lengths (1..3)
+ *   cols      host int[P*3]: 0-based feature columns of each window (row-major, unused slots ignored)
+ *   X         device double[N*ld]: row-major feature matrix (Dataset.features)
+ *   wf        host window polynomial table (copied)
+ * Checks every coordinate lies in [-1/2, 1/2) (nufft.py:180-181) -> AK_ERR_DOMAIN.
+ * Synchronises `stream` (plan time).
+ */
+int ak_geom_create(int32_t n, int32_t P, const int32_t* q, const int32_t* cols,
+                   const double* X, int64_t N, int64_t ld,
+                   const ak_window_fn* wf, void* stream, ak_geom** out);
+int     ak_geom_destroy(ak_geom* g);
+int64_t ak_geom_num_points(const ak_geom* g);
+int32_t ak_geom_num_windows(const ak_geom* g);
+int64_t ak_geom_num_items(const ak_geom* g);   /* work items (supercell chunks) over all windows */
+
+/* Grid elements (doubles) of one RHS of window w: n^q[w]. */
+int64_t ak_geom_grid_elems(const ak_geom* g, int32_t w);
+/* Canonical grid layout used by every entry point: windows ordered by
+ * decreasing q (stable), the R grids of window w consecutive:
+ *   grid(w, r) = grids + R * ak_geom_canon_offset(g, w) + r * n^q[w]
+ * ak_geom_canon_total(g) = sum_w n^q[w]  (total doubles for R = 1). */
+int64_t ak_geom_canon_offset(const ak_geom* g, int32_t w);
+int64_t ak_geom_canon_total(const ak_geom* g);
+
+/*
+ * ak_spread -- real-valued spreading of R right-hand sides onto per-window grids
+ * (replaces _spread_q, nufft.py:197-254; accumulates (+=), like the reference).
+ *   V        device double[R][ldv], RHS r value of original row i at V[r*ldv + i]
+ *   grids    device double[R * canon_total], canonical layout (above)
+ */
+int ak_spread(const ak_geom* g, const double* V, int32_t R, int64_t ldv,
+              double* grids, void* stream);
+
+/*
+ * ak_interp -- interpolation from per-window real grids (canonical layout)
+ * back to the points (replaces _interp_q, nufft.py:257-320), scaled:
+ *   sum_windows=1: out[r*ldo + i] += scale[w] * interp(window w, grid r)(row i)
+ *   sum_windows=0: out[w*wstride + r*ldo + i] = scale[w] * ...
+ *   scale    device double[P]
+ */
+int ak_interp(const ak_geom* g, const double* grids, int32_t R,
+              const double* scale, double* out, int64_t ldo, int32_t sum_windows,
+              int64_t wstride, void* stream);
+
+/*
+ * Fast-summation operator: one spread per (window, RHS) serves C coefficient
+ * sets (K, dK/dl, ...).  H is the real band multiplier per (set, window):
+ *   H = Re(c_hat_k) / prod_a psi_hat(k_a/n)^2 on the band I_m (FFT order,
+ *   last axis k >= 0 only: compact shape m^(q-1) * (m/2)),
+ * i.e. coefficient multiply (fastsum.py:159) fused with both deconvolutions
+ * (nufft.py:336-343, the (-1)^k signs cancel).
+ *   spread_geom / interp_geom may differ (fast_cross_matvec, fastsum.py:180-191)
+ *   but must have identical windows (n, q).
+ */
+int ak_op_create(const ak_geom* spread_geom, const ak_geom* interp_geom,
+                 int32_t m, int32_t R, int32_t C, void* stream, ak_op** out);
+int ak_op_destroy(ak_op* op);
+
+/*
+ *   V          device double[R][ldv]
+ *   H          DEVICE array [C*P] of device pointers to compact band multipliers
+ *              (set c, window w at index c*P + w)
+ *   scale      device double[C*P] per (set, window) operator scale (fastsum.py:136-138)
+ *   outs       host array [C] of device output pointers;
+ *              sum_windows[c]=1: out[c] is double[R][ldo] summed over windows
+ *              sum_windows[c]=0: out[c] is double[P][R][ldo] (per-window products)
+ *   accumulate 0: outputs are overwritten (zeroed first); 1: added to
+ */
+int ak_op_apply(ak_op* op, const double* V, int64_t ldv,
+                const double* const* H, const double* scale,
+                double* const* outs, int64_t ldo, const int32_t* sum_windows,
+                int32_t accumulate, void* stream);
+
+/*
+ * Complex NUFFT building blocks (nufft_type1 / nufft_type2 API parity).
+ * ak_type1_band: real grids gre, gim (n^q each, the spread of Re/Im weights)
+ *   -> S (m^q complex interleaved, FFT order) = deconv * band(fftn(gre + i gim))
+ * ak_type2_grid: coefficients c (m^q complex interleaved) -> real grids
+ *   gre, gim = Re/Im of ifftn(pad(deconv * c)) * n^q
+ *   deconv  device double[3][m]: per-axis (-1)^k / psi_hat(k/n) (nufft.py:149-157)
+ */
+int ak_type1_band(int32_t q, int32_t n, int32_t m, const double* gre, const double* gim,
+                  const double* deconv, double* S, void* stream);
+int ak_type2_grid(int32_t q, int32_t n, int32_t m, const double* c,
+                  const double* deconv, double* gre, double* gim, void* stream);
+
+/* FP64 FMA throughput probe (roofline denominator; MEASURED_PEAKS.json has no FP64 entry).
+ * Runs `iters` dependent-chain-free DFMA loops on all SMs; returns achieved TFLOP/s. */
+int ak_probe_fp64(int64_t iters, void* stream, double* tflops);
+/* Same for FP64 tensor-core mma.sync.m8n8k4 (design probe, not on the hot path). */
+int ak_probe_dmma(int64_t iters, void* stream, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADDKERN_B200_H */

@@ -1,0 +1,130 @@
+"""ctypes binding of libaddkern_b200.so (the C ABI in include/addkern_b200.h).
+
+There is no CPU fallback: if the library is missing or cannot be loaded the
+import of the compute modules fails loudly with ``NativeLibraryError``.
+Device memory, streams and pointers come from torch CUDA tensors.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from .errors import NativeLibraryError, PointOutOfDomainError
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libaddkern_b200.so"
+
+AK_OK = 0
+AK_ERR_INVALID = -1
+AK_ERR_CUDA = -2
+AK_ERR_DOMAIN = -3
+AK_ERR_ALLOC = -4
+AK_ERR_CUFFT = -5
+AK_ERR_UNSUPPORTED = -6
+
+AK_MAX_TAPS = 16
+AK_MAX_PAIRS = 8
+AK_NCOEF = 7
+
+#: symbols the header declares; tests check the library exports every one
+EXPORTED = (
+    "ak_last_error", "ak_version", "ak_launch_count",
+    "ak_geom_create", "ak_geom_destroy", "ak_geom_num_points", "ak_geom_num_windows",
+    "ak_geom_num_items", "ak_geom_grid_elems", "ak_geom_canon_offset", "ak_geom_canon_total",
+    "ak_spread", "ak_interp", "ak_op_create", "ak_op_destroy", "ak_op_apply",
+    "ak_type1_band", "ak_type2_grid", "ak_probe_fp64", "ak_probe_dmma",
+)
+
+
+class WindowFn(ctypes.Structure):
+    _fields_ = [
+        ("taps", ctypes.c_int32),
+        ("ncoef", ctypes.c_int32),
+        ("ce", (ctypes.c_double * AK_NCOEF) * AK_MAX_PAIRS),
+        ("co", (ctypes.c_double * AK_NCOEF) * AK_MAX_PAIRS),
+    ]
+
+
+_c_int = ctypes.c_int
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_vp = ctypes.c_void_p
+_dp = ctypes.c_void_p  # device pointers travel as integers
+
+
+def _declare(lib: ctypes.CDLL) -> None:
+    sig = {
+        "ak_last_error": (ctypes.c_char_p, []),
+        "ak_version": (ctypes.c_char_p, []),
+        "ak_launch_count": (_i64, []),
+        "ak_geom_create": (_c_int, [_i32, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32), _dp, _i64, _i64,
+                                    ctypes.POINTER(WindowFn), _vp, ctypes.POINTER(_vp)]),
+        "ak_geom_destroy": (_c_int, [_vp]),
+        "ak_geom_num_points": (_i64, [_vp]),
+        "ak_geom_num_windows": (_i32, [_vp]),
+        "ak_geom_num_items": (_i64, [_vp]),
+        "ak_geom_grid_elems": (_i64, [_vp, _i32]),
+        "ak_geom_canon_offset": (_i64, [_vp, _i32]),
+        "ak_geom_canon_total": (_i64, [_vp]),
+        "ak_spread": (_c_int, [_vp, _dp, _i32, _i64, _dp, _vp]),
+        "ak_interp": (_c_int, [_vp, _dp, _i32, _dp, _dp, _i64, _i32, _i64, _vp]),
+        "ak_op_create": (_c_int, [_vp, _vp, _i32, _i32, _i32, _vp, ctypes.POINTER(_vp)]),
+        "ak_op_destroy": (_c_int, [_vp]),
+        "ak_op_apply": (_c_int, [_vp, _dp, _i64, _dp, _dp, ctypes.POINTER(_vp), _i64, ctypes.POINTER(_i32),
+                                 _i32, _vp]),
+        "ak_type1_band": (_c_int, [_i32, _i32, _i32, _dp, _dp, _dp, _dp, _vp]),
+        "ak_type2_grid": (_c_int, [_i32, _i32, _i32, _dp, _dp, _dp, _dp, _vp]),
+        "ak_probe_fp64": (_c_int, [_i64, _vp, ctypes.POINTER(ctypes.c_double)]),
+        "ak_probe_dmma": (_c_int, [_i64, _vp, ctypes.POINTER(ctypes.c_double)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+
+
+_LIB = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load (once) and return the native library; raises if it is unavailable."""
+    global _LIB
+    if _LIB is None:
+        if not LIB_PATH.exists():
+            if os.environ.get("AK_AUTOBUILD", "1") == "1":
+                from .build import build
+                build()
+            if not LIB_PATH.exists():
+                raise NativeLibraryError(f"{LIB_PATH} is missing; run `python -m paper_2404_17344_b200.build`")
+        try:
+            handle = ctypes.CDLL(str(LIB_PATH))
+        except OSError as exc:  # pragma: no cover - environment dependent
+            raise NativeLibraryError(f"cannot load {LIB_PATH}: {exc}") from exc
+        _declare(handle)
+        _LIB = handle
+    return _LIB
+
+
+def last_error() -> str:
+    msg = lib().ak_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, what: str = "") -> None:
+    """Map a C-ABI return code onto the package's exception types."""
+    if rc == AK_OK:
+        return
+    msg = f"{what}: {last_error()}" if what else last_error()
+    if rc == AK_ERR_DOMAIN:
+        raise PointOutOfDomainError(msg)
+    if rc in (AK_ERR_INVALID, AK_ERR_UNSUPPORTED):
+        raise ValueError(msg)
+    if rc == AK_ERR_ALLOC:
+        raise MemoryError(msg)
+    raise NativeLibraryError(msg)
+
+
+def launch_count() -> int:
+    return int(lib().ak_launch_count())

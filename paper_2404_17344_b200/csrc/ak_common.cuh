@@ -1,0 +1,81 @@
+// Shared device-side definitions for the B200 fast-summation kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "../../include/addkern_b200.h"
+
+namespace ak {
+
+// One bin-sorted point of one window (32 B, two 16-B vector loads).
+//   s[a]  = 2*frac_a - 1, frac_a = t_a - floor(t_a), t_a = (x_a + 1/2) * n
+//   cell  = packed floor(t) mod n, 10 bits per axis (axis 0 lowest)
+//   idx   = original row
+struct alignas(16) Point {
+    double s[3];
+    int32_t cell;
+    int32_t idx;
+};
+
+// A chunk of at most `chunk` points of one supercell of one window.
+struct alignas(16) WorkItem {
+    int32_t window;
+    int32_t sc;      // packed supercell coordinates, 10 bits per axis
+    int32_t start;   // global index into the sorted point array
+    int32_t count;
+};
+
+// Supercell edge (cells per axis) per window length.  A CTA accumulates one
+// supercell chunk into a (S+T-1)^q shared tile before flushing to HBM/L2.
+template <int Q> struct SuperCell;
+template <> struct SuperCell<3> { static constexpr int S = 4;  };
+template <> struct SuperCell<2> { static constexpr int S = 16; };
+template <> struct SuperCell<1> { static constexpr int S = 32; };
+
+__host__ __device__ inline int supercell_edge(int q) { return q == 3 ? 4 : (q == 2 ? 16 : 32); }
+
+__device__ __forceinline__ int cell_axis(int32_t packed, int a) { return (packed >> (10 * a)) & 1023; }
+
+// Window weights of one axis: w[a] for the T taps of a point with polynomial
+// variable s (see ak_window_fn in the public header).
+template <int T>
+__device__ __forceinline__ void window_weights(const ak_window_fn& wf, double s, double* w) {
+    const double s2 = s * s;
+#pragma unroll
+    for (int a = 0; a < T / 2; ++a) {
+        double e = wf.ce[a][0];
+        double o = wf.co[a][0];
+#pragma unroll
+        for (int k = 1; k < AK_NCOEF; ++k) {
+            e = fma(e, s2, wf.ce[a][k]);
+            o = fma(o, s2, wf.co[a][k]);
+        }
+        w[a] = fma(s, o, e);
+        w[T - 1 - a] = fma(-s, o, e);
+    }
+}
+
+// Runtime-taps variant used by the generic kernels.
+__device__ __forceinline__ double window_weight_rt(const ak_window_fn& wf, double s, int a) {
+    const int T = wf.taps;
+    const bool mirror = a >= T / 2;
+    const int p = mirror ? T - 1 - a : a;
+    const double s2 = s * s;
+    double e = wf.ce[p][0], o = wf.co[p][0];
+#pragma unroll
+    for (int k = 1; k < AK_NCOEF; ++k) {
+        e = fma(e, s2, wf.ce[p][k]);
+        o = fma(o, s2, wf.co[p][k]);
+    }
+    return mirror ? fma(-s, o, e) : fma(s, o, e);
+}
+
+__device__ __forceinline__ int wrap(int i, int n) {
+    i %= n;
+    return i < 0 ? i + n : i;
+}
+
+__device__ __forceinline__ void red_add(double* p, double v) {
+    atomicAdd(p, v);  // compiles to RED.E.ADD.F64 when the result is unused
+}
+
+}  // namespace ak

@@ -1,0 +1,871 @@
+// libaddkern_b200: plan-time geometry, operator apply, FFT stage and the C ABI.
+//
+// Canonical grid layout (all entry points): windows ordered by decreasing
+// window length q (stable), window w's R grids consecutive:
+//   grid(w, r) = grids + R * canon_off[w] + r * n^q[w]
+// so that all windows of one length form one contiguous cuFFT batch.
+#include <cub/cub.cuh>
+#include <cufft.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "ak_common.cuh"
+#include "ak_kernels.cuh"
+
+using namespace ak;
+
+// ---------------------------------------------------------------------------
+// errors
+
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+static int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define AK_CUDA(call)                                                                       \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(e_ == cudaErrorMemoryAllocation ? AK_ERR_ALLOC : AK_ERR_CUDA,       \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                \
+    } while (0)
+
+#define AK_CUFFT(call)                                                                      \
+    do {                                                                                    \
+        cufftResult r_ = (call);                                                            \
+        if (r_ != CUFFT_SUCCESS)                                                            \
+            return fail(AK_ERR_CUFFT, std::string(#call) + ": cufft error " + std::to_string((int)r_)); \
+    } while (0)
+
+#define AK_TRY(call)              \
+    do {                          \
+        int rc_ = (call);         \
+        if (rc_ != AK_OK) return rc_; \
+    } while (0)
+
+static int launched() {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(AK_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+    return AK_OK;
+}
+
+static inline int64_t ipow_rt(int64_t b, int q) {
+    int64_t r = 1;
+    for (int i = 0; i < q; ++i) r *= b;
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// geometry
+
+struct ak_geom {
+    int n = 0, P = 0;
+    int64_t N = 0;
+    std::vector<int> q;                 // per window
+    std::vector<int64_t> canon_off;     // per window (R = 1 units)
+    int64_t canon_total = 0;            // sum n^q
+    int64_t* canon_off_d = nullptr;
+    ak_window_fn wf{};
+    Point* pts = nullptr;               // [P][N]
+    WorkItem* items = nullptr;
+    int64_t nitems = 0;
+    int64_t item_begin[4] = {0, 0, 0, 0}, item_end[4] = {0, 0, 0, 0};
+    std::vector<int> windows_of_q[4];   // window ids per q, canonical order
+};
+
+static int chunk_for_q(int q) { return q == 3 ? 1024 : (q == 2 ? 4096 : 8192); }
+
+__global__ void k_keys(const double* __restrict__ X, int64_t ld, int q, int c0, int c1, int c2, int n, int S,
+                       int nsc, int64_t N, uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
+                       int* __restrict__ counts, int* __restrict__ bad)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int col[3] = {c0, c1, c2};
+    int sc = 0, sub = 0;
+    for (int a = 0; a < q; ++a) {
+        double x = X[i * ld + col[a]];
+        if (!(x >= -0.5 && x < 0.5)) {
+            atomicOr(bad, 1);
+            x = 0.0;
+        }
+        const double t = (x + 0.5) * n;
+        int c = (int)floor(t);
+        if (c >= n) c -= n;
+        sc = sc * nsc + c / S;
+        sub = sub * S + c % S;
+    }
+    int sq = 1;
+    for (int a = 0; a < q; ++a) sq *= S;
+    keys[i] = (uint32_t)sc * (uint32_t)sq + (uint32_t)sub;
+    vals[i] = (int32_t)i;
+    atomicAdd(&counts[sc], 1);
+}
+
+__global__ void k_points(const double* __restrict__ X, int64_t ld, int q, int c0, int c1, int c2, int n,
+                         const int32_t* __restrict__ order, int64_t N, Point* __restrict__ out)
+{
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    const int i = order[j];
+    const int col[3] = {c0, c1, c2};
+    Point p;
+    p.s[0] = p.s[1] = p.s[2] = 0.0;
+    int packed = 0;
+    for (int a = 0; a < q; ++a) {
+        double x = X[(int64_t)i * ld + col[a]];
+        if (!(x >= -0.5 && x < 0.5)) x = 0.0;
+        const double t = (x + 0.5) * n;
+        const double fl = floor(t);
+        const double frac = t - fl;            // exact
+        int c = (int)fl;
+        if (c >= n) c -= n;
+        p.s[a] = fma(2.0, frac, -1.0);
+        packed |= c << (10 * a);
+    }
+    p.cell = packed;
+    p.idx = i;
+    out[j] = p;
+}
+
+__global__ void k_items(const int* __restrict__ counts, const int* __restrict__ starts, int nsc_total, int q,
+                        int nsc, int chunk, int64_t pt_base, int w, int* __restrict__ counter,
+                        WorkItem* __restrict__ items)
+{
+    const int sc = blockIdx.x * blockDim.x + threadIdx.x;
+    if (sc >= nsc_total) return;
+    const int cnt = counts[sc];
+    if (cnt == 0) return;
+    const int k = (cnt + chunk - 1) / chunk;
+    const int size = (cnt + k - 1) / k;
+    const int base = atomicAdd(counter, k);
+    int s[3] = {0, 0, 0};
+    int rest = sc;
+    for (int a = q - 1; a >= 0; --a) {
+        s[a] = rest % nsc;
+        rest /= nsc;
+    }
+    const int packed = s[0] | (s[1] << 10) | (s[2] << 20);
+    for (int j = 0; j < k; ++j) {
+        WorkItem it;
+        it.window = w;
+        it.sc = packed;
+        it.start = (int)(pt_base + starts[sc] + (int64_t)j * size);
+        it.count = min(size, cnt - j * size);
+        items[base + j] = it;
+    }
+}
+
+extern "C" const char* ak_last_error(void) { return g_err.c_str(); }
+extern "C" const char* ak_version(void) { return "addkern_b200 0.1.0 (sm_100a)"; }
+extern "C" int64_t ak_launch_count(void) { return g_launches.load(); }
+
+extern "C" int ak_geom_destroy(ak_geom* g) {
+    if (!g) return AK_OK;
+    cudaFree(g->pts);
+    cudaFree(g->items);
+    cudaFree(g->canon_off_d);
+    delete g;
+    return AK_OK;
+}
+
+static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t ld, cudaStream_t st) {
+    const int n = g->n, P = g->P;
+    const int64_t N = g->N;
+    // canonical order: q descending, stable
+    int64_t off = 0;
+    g->canon_off.assign(P, 0);
+    for (int q = 3; q >= 1; --q)
+        for (int w = 0; w < P; ++w)
+            if (g->q[w] == q) {
+                g->canon_off[w] = off;
+                off += ipow_rt(n, q);
+                g->windows_of_q[q].push_back(w);
+            }
+    g->canon_total = off;
+    AK_CUDA(cudaMalloc(&g->canon_off_d, sizeof(int64_t) * P));
+    AK_CUDA(cudaMemcpyAsync(g->canon_off_d, g->canon_off.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice, st));
+
+    AK_CUDA(cudaMalloc(&g->pts, sizeof(Point) * (size_t)std::max<int64_t>(1, N * P)));
+    // item capacity
+    int64_t cap = 0;
+    int max_nsc_total = 1;
+    for (int w = 0; w < P; ++w) {
+        const int S = supercell_edge(g->q[w]);
+        const int nsc = (n + S - 1) / S;
+        const int tot = (int)ipow_rt(nsc, g->q[w]);
+        max_nsc_total = std::max(max_nsc_total, tot);
+        cap += (N + chunk_for_q(g->q[w]) - 1) / chunk_for_q(g->q[w]) + tot;
+    }
+    AK_CUDA(cudaMalloc(&g->items, sizeof(WorkItem) * (size_t)std::max<int64_t>(1, cap)));
+
+    uint32_t *keys = nullptr, *keys2 = nullptr;
+    int32_t *vals = nullptr, *vals2 = nullptr;
+    int *counts = nullptr, *starts = nullptr, *dflags = nullptr;
+    void* temp = nullptr;
+    size_t temp_bytes = 0, need = 0;
+    const int64_t NN = std::max<int64_t>(N, 1);
+    AK_CUDA(cudaMalloc(&keys, sizeof(uint32_t) * NN));
+    AK_CUDA(cudaMalloc(&keys2, sizeof(uint32_t) * NN));
+    AK_CUDA(cudaMalloc(&vals, sizeof(int32_t) * NN));
+    AK_CUDA(cudaMalloc(&vals2, sizeof(int32_t) * NN));
+    AK_CUDA(cudaMalloc(&counts, sizeof(int) * max_nsc_total));
+    AK_CUDA(cudaMalloc(&starts, sizeof(int) * max_nsc_total));
+    AK_CUDA(cudaMalloc(&dflags, sizeof(int) * 2));  // [0] bad, [1] item counter
+    AK_CUDA(cudaMemsetAsync(dflags, 0, sizeof(int) * 2, st));
+    cub::DeviceRadixSort::SortPairs(nullptr, need, keys, keys2, vals, vals2, (int)N, 0, 32, st);
+    temp_bytes = need;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, counts, starts, max_nsc_total, st);
+    temp_bytes = std::max(temp_bytes, need);
+    AK_CUDA(cudaMalloc(&temp, std::max<size_t>(temp_bytes, 16)));
+
+    int rc = AK_OK;
+    int host_counter = 0;
+    for (int q = 3; q >= 1 && rc == AK_OK; --q) {
+        g->item_begin[q] = host_counter;
+        for (int w : g->windows_of_q[q]) {
+            const int S = supercell_edge(q);
+            const int nsc = (n + S - 1) / S;
+            const int tot = (int)ipow_rt(nsc, q);
+            int bits = 1;
+            while ((int64_t)1 << bits < (int64_t)tot * ipow_rt(S, q)) ++bits;
+            const int c0 = cols[3 * w], c1 = cols[3 * w + 1], c2 = cols[3 * w + 2];
+            if (N == 0) continue;
+            cudaMemsetAsync(counts, 0, sizeof(int) * tot, st);
+            const int tb = 256;
+            const int nblk = (int)((N + tb - 1) / tb);
+            k_keys<<<nblk, tb, 0, st>>>(X, ld, q, c0, c1, c2, n, S, nsc, N, keys, vals, counts, dflags);
+            if ((rc = launched()) != AK_OK) break;
+            size_t tb2 = temp_bytes;
+            if (cub::DeviceRadixSort::SortPairs(temp, tb2, keys, keys2, vals, vals2, (int)N, 0, bits, st) != cudaSuccess) {
+                rc = fail(AK_ERR_CUDA, "radix sort failed");
+                break;
+            }
+            g_launches.fetch_add(1);
+            k_points<<<nblk, tb, 0, st>>>(X, ld, q, c0, c1, c2, n, vals2, N, g->pts + (int64_t)w * N);
+            if ((rc = launched()) != AK_OK) break;
+            tb2 = temp_bytes;
+            if (cub::DeviceScan::ExclusiveSum(temp, tb2, counts, starts, tot, st) != cudaSuccess) {
+                rc = fail(AK_ERR_CUDA, "scan failed");
+                break;
+            }
+            g_launches.fetch_add(1);
+            k_items<<<(tot + 255) / 256, 256, 0, st>>>(counts, starts, tot, q, nsc, chunk_for_q(q), (int64_t)w * N, w,
+                                                       dflags + 1, g->items);
+            if ((rc = launched()) != AK_OK) break;
+        }
+        if (rc != AK_OK) break;
+        int hf[2];
+        if (cudaMemcpyAsync(hf, dflags, sizeof(hf), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) {
+            rc = fail(AK_ERR_CUDA, "geometry sync failed");
+            break;
+        }
+        if (hf[0]) {
+            rc = fail(AK_ERR_DOMAIN, "points must lie in [-1/2, 1/2)");
+            break;
+        }
+        host_counter = hf[1];
+        g->item_end[q] = host_counter;
+    }
+    g->nitems = host_counter;
+    cudaStreamSynchronize(st);
+    cudaFree(keys);
+    cudaFree(keys2);
+    cudaFree(vals);
+    cudaFree(vals2);
+    cudaFree(counts);
+    cudaFree(starts);
+    cudaFree(dflags);
+    cudaFree(temp);
+    return rc;
+}
+
+extern "C" int ak_geom_create(int32_t n, int32_t P, const int32_t* q, const int32_t* cols, const double* X,
+                              int64_t N, int64_t ld, const ak_window_fn* wf, void* stream, ak_geom** out)
+{
+    if (!out || !q || !cols || !wf) return fail(AK_ERR_INVALID, "null argument");
+    *out = nullptr;
+    if (n < 2 || n > 1024) return fail(AK_ERR_INVALID, "grid size n must be in [2, 1024]");
+    if (P < 1) return fail(AK_ERR_INVALID, "need at least one window");
+    if (N < 0 || (N > 0 && !X)) return fail(AK_ERR_INVALID, "bad point array");
+    if (N * (int64_t)P >= ((int64_t)1 << 31)) return fail(AK_ERR_INVALID, "N * P must be < 2^31");
+    if (wf->taps < 4 || wf->taps > AK_MAX_TAPS || wf->taps % 2 || wf->ncoef != AK_NCOEF)
+        return fail(AK_ERR_UNSUPPORTED, "window taps must be even in [4, 16] with AK_NCOEF coefficients");
+    for (int w = 0; w < P; ++w) {
+        if (q[w] < 1 || q[w] > 3) return fail(AK_ERR_INVALID, "window length must be 1..3");
+        for (int a = 0; a < q[w]; ++a)
+            if (cols[3 * w + a] < 0 || cols[3 * w + a] >= ld) return fail(AK_ERR_INVALID, "column out of range");
+    }
+    ak_geom* g = new ak_geom();
+    g->n = n;
+    g->P = P;
+    g->N = N;
+    g->q.assign(q, q + P);
+    g->wf = *wf;
+    int rc = geom_build(g, cols, X, ld, (cudaStream_t)stream);
+    if (rc != AK_OK) {
+        std::string keep = g_err;
+        ak_geom_destroy(g);
+        g_err = keep;
+        return rc;
+    }
+    *out = g;
+    return AK_OK;
+}
+
+extern "C" int64_t ak_geom_num_points(const ak_geom* g) { return g ? g->N : -1; }
+extern "C" int32_t ak_geom_num_windows(const ak_geom* g) { return g ? g->P : -1; }
+extern "C" int64_t ak_geom_num_items(const ak_geom* g) { return g ? g->nitems : -1; }
+extern "C" int64_t ak_geom_grid_elems(const ak_geom* g, int32_t w) {
+    if (!g || w < 0 || w >= g->P) return -1;
+    return ipow_rt(g->n, g->q[w]);
+}
+extern "C" int64_t ak_geom_canon_offset(const ak_geom* g, int32_t w) {
+    if (!g || w < 0 || w >= g->P) return -1;
+    return g->canon_off[w];
+}
+extern "C" int64_t ak_geom_canon_total(const ak_geom* g) { return g ? g->canon_total : -1; }
+
+// ---------------------------------------------------------------------------
+// generic kernels (any taps)
+
+namespace ak {
+__global__ void k_spread_generic(const Point* __restrict__ pts, int64_t p0, int64_t np, int q,
+                                 const double* __restrict__ V, int64_t ldv, double* __restrict__ g_w, int n,
+                                 const ak_window_fn wf)
+{
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= np) return;
+    const int r = blockIdx.y;
+    const Point p = pts[p0 + j];
+    const double v = V[(int64_t)r * ldv + p.idx];
+    double* g = g_w + (int64_t)r * (q == 3 ? (int64_t)n * n * n : (q == 2 ? (int64_t)n * n : n));
+    const int T = wf.taps;
+    double w[3][AK_MAX_TAPS];
+    for (int a = 0; a < q; ++a)
+        for (int t = 0; t < T; ++t) w[a][t] = window_weight_rt(wf, p.s[a], t);
+    const int f0 = cell_axis(p.cell, 0) - (T / 2 - 1);
+    const int f1 = cell_axis(p.cell, 1) - (T / 2 - 1);
+    const int f2 = cell_axis(p.cell, 2) - (T / 2 - 1);
+    if (q == 1) {
+        for (int a = 0; a < T; ++a) red_add(g + wrap(f0 + a, n), v * w[0][a]);
+    } else if (q == 2) {
+        for (int a = 0; a < T; ++a) {
+            const double va = v * w[0][a];
+            const int64_t row = (int64_t)wrap(f0 + a, n) * n;
+            for (int b = 0; b < T; ++b) red_add(g + row + wrap(f1 + b, n), va * w[1][b]);
+        }
+    } else {
+        for (int a = 0; a < T; ++a) {
+            const double va = v * w[0][a];
+            const int64_t pl = (int64_t)wrap(f0 + a, n) * n;
+            for (int b = 0; b < T; ++b) {
+                const double vb = va * w[1][b];
+                const int64_t row = (pl + wrap(f1 + b, n)) * n;
+                for (int c = 0; c < T; ++c) red_add(g + row + wrap(f2 + c, n), vb * w[2][c]);
+            }
+        }
+    }
+}
+
+__global__ void k_interp_generic(const Point* __restrict__ pts, int64_t p0, int64_t np, int q,
+                                 const double* __restrict__ g_w, int n, const ak_window_fn wf,
+                                 const double* __restrict__ scale, int w, double* __restrict__ out_w, int64_t ldo,
+                                 int sum_windows)
+{
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= np) return;
+    const int r = blockIdx.y;
+    const Point p = pts[p0 + j];
+    const double* g = g_w + (int64_t)r * (q == 3 ? (int64_t)n * n * n : (q == 2 ? (int64_t)n * n : n));
+    const int T = wf.taps;
+    double wt[3][AK_MAX_TAPS];
+    for (int a = 0; a < q; ++a)
+        for (int t = 0; t < T; ++t) wt[a][t] = window_weight_rt(wf, p.s[a], t);
+    const int f0 = cell_axis(p.cell, 0) - (T / 2 - 1);
+    const int f1 = cell_axis(p.cell, 1) - (T / 2 - 1);
+    const int f2 = cell_axis(p.cell, 2) - (T / 2 - 1);
+    double acc = 0.0;
+    if (q == 1) {
+        for (int a = 0; a < T; ++a) acc = fma(wt[0][a], g[wrap(f0 + a, n)], acc);
+    } else if (q == 2) {
+        for (int a = 0; a < T; ++a) {
+            const int64_t row = (int64_t)wrap(f0 + a, n) * n;
+            double s = 0.0;
+            for (int b = 0; b < T; ++b) s = fma(wt[1][b], g[row + wrap(f1 + b, n)], s);
+            acc = fma(wt[0][a], s, acc);
+        }
+    } else {
+        for (int a = 0; a < T; ++a) {
+            const int64_t pl = (int64_t)wrap(f0 + a, n) * n;
+            double sa = 0.0;
+            for (int b = 0; b < T; ++b) {
+                const int64_t row = (pl + wrap(f1 + b, n)) * n;
+                double sb = 0.0;
+                for (int c = 0; c < T; ++c) sb = fma(wt[2][c], g[row + wrap(f2 + c, n)], sb);
+                sa = fma(wt[1][b], sb, sa);
+            }
+            acc = fma(wt[0][a], sa, acc);
+        }
+    }
+    double* o = out_w + (int64_t)r * ldo + p.idx;
+    const double v = scale[w] * acc;
+    if (sum_windows) red_add(o, v);
+    else *o = v;
+}
+}  // namespace ak
+
+// ---------------------------------------------------------------------------
+// spread / interp dispatch
+
+// AK_FORCE_GENERIC=1 routes every spread/interp through the one-thread-per-point
+// kernels (test hook: cross-checks the tiled kernels).  Read per call.
+static bool force_generic() {
+    const char* e = getenv("AK_FORCE_GENERIC");
+    return e && e[0] == '1';
+}
+
+template <int Q, int T>
+static void launch_spread_tile(const ak_geom* g, int64_t i0, int64_t ni, const double* V, int R, int64_t ldv,
+                               double* grids, cudaStream_t st)
+{
+    dim3 grid((unsigned)ni, (unsigned)R);
+    k_spread_tile<Q, T><<<grid, 32, 0, st>>>(g->pts, g->items + i0, V, ldv, grids, g->canon_off_d, R, g->n, g->wf);
+}
+
+static int spread_group(const ak_geom* g, int q, const double* V, int R, int64_t ldv, double* grids, cudaStream_t st) {
+    const int64_t i0 = g->item_begin[q], ni = g->item_end[q] - g->item_begin[q];
+    if (g->windows_of_q[q].empty() || g->N == 0) return AK_OK;
+    const int T = g->wf.taps;
+    bool done = false;
+    if (!force_generic() && ni > 0) {
+        done = true;
+        if (q == 3 && T == 12) launch_spread_tile<3, 12>(g, i0, ni, V, R, ldv, grids, st);
+        else if (q == 3 && T == 8) launch_spread_tile<3, 8>(g, i0, ni, V, R, ldv, grids, st);
+        else if (q == 3 && T == 4) launch_spread_tile<3, 4>(g, i0, ni, V, R, ldv, grids, st);
+        else if (q == 2 && T == 12) launch_spread_tile<2, 12>(g, i0, ni, V, R, ldv, grids, st);
+        else if (q == 2 && T == 8) launch_spread_tile<2, 8>(g, i0, ni, V, R, ldv, grids, st);
+        else if (q == 2 && T == 16) launch_spread_tile<2, 16>(g, i0, ni, V, R, ldv, grids, st);
+        else if (q == 2 && T == 4) launch_spread_tile<2, 4>(g, i0, ni, V, R, ldv, grids, st);
+        else if (q == 1 && T == 12) launch_spread_tile<1, 12>(g, i0, ni, V, R, ldv, grids, st);
+        else if (q == 1 && T == 8) launch_spread_tile<1, 8>(g, i0, ni, V, R, ldv, grids, st);
+        else if (q == 1 && T == 16) launch_spread_tile<1, 16>(g, i0, ni, V, R, ldv, grids, st);
+        else if (q == 1 && T == 4) launch_spread_tile<1, 4>(g, i0, ni, V, R, ldv, grids, st);
+        else done = false;
+        if (done) return launched();
+    }
+    for (int w : g->windows_of_q[q]) {
+        dim3 grid((unsigned)((g->N + 127) / 128), (unsigned)R);
+        k_spread_generic<<<grid, 128, 0, st>>>(g->pts, (int64_t)w * g->N, g->N, q, V, ldv,
+                                               grids + (int64_t)R * g->canon_off[w], g->n, g->wf);
+        AK_TRY(launched());
+    }
+    return AK_OK;
+}
+
+template <int T>
+static void launch_interp3(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R, const double* scale,
+                           double* out, int64_t ldo, int atomic_out, int64_t wstride, cudaStream_t st)
+{
+    dim3 grid((unsigned)ni, (unsigned)R);
+    k_interp3_tile<T><<<grid, 32, 0, st>>>(g->pts, g->items + i0, grids, g->canon_off_d, R, g->n, g->wf, scale, out,
+                                           ldo, atomic_out, wstride);
+}
+
+template <int Q, int T>
+static void launch_interp_lane(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R,
+                               const double* scale, double* out, int64_t ldo, int atomic_out, int64_t wstride,
+                               cudaStream_t st)
+{
+    dim3 grid((unsigned)ni, (unsigned)R);
+    k_interp_lane<Q, T><<<grid, 32, 0, st>>>(g->pts, g->items + i0, grids, g->canon_off_d, R, g->n, g->wf, scale,
+                                             out, ldo, atomic_out, wstride);
+}
+
+// out(w) = out + (sum_windows ? 0 : w * wstride); atomic_out: RED instead of store
+static int interp_group(const ak_geom* g, int q, const double* grids, int R, const double* scale, double* out,
+                        int64_t ldo, int sum_windows, int atomic_out, int64_t wstride, cudaStream_t st)
+{
+    const int64_t i0 = g->item_begin[q], ni = g->item_end[q] - g->item_begin[q];
+    if (g->windows_of_q[q].empty() || g->N == 0) return AK_OK;
+    const int T = g->wf.taps;
+    const int64_t ws = sum_windows ? 0 : wstride;
+    bool done = false;
+    if (!force_generic() && ni > 0) {
+        done = true;
+        if (q == 3 && T == 12) launch_interp3<12>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, ws, st);
+        else if (q == 3 && T == 8) launch_interp3<8>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, ws, st);
+        else if (q == 3 && T == 4) launch_interp3<4>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, ws, st);
+#define AK_LANE(QQ, TT) \
+        else if (q == QQ && T == TT) launch_interp_lane<QQ, TT>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, ws, st);
+        AK_LANE(2, 4) AK_LANE(2, 6) AK_LANE(2, 8) AK_LANE(2, 10) AK_LANE(2, 12) AK_LANE(2, 14) AK_LANE(2, 16)
+        AK_LANE(1, 4) AK_LANE(1, 6) AK_LANE(1, 8) AK_LANE(1, 10) AK_LANE(1, 12) AK_LANE(1, 14) AK_LANE(1, 16)
+#undef AK_LANE
+        else done = false;
+        if (done) return launched();
+    }
+    for (int w : g->windows_of_q[q]) {
+        dim3 grid((unsigned)((g->N + 127) / 128), (unsigned)R);
+        k_interp_generic<<<grid, 128, 0, st>>>(g->pts, (int64_t)w * g->N, g->N, q, grids + (int64_t)R * g->canon_off[w],
+                                               g->n, g->wf, scale, w, out + (int64_t)w * ws, ldo, atomic_out);
+        AK_TRY(launched());
+    }
+    return AK_OK;
+}
+
+extern "C" int ak_spread(const ak_geom* g, const double* V, int32_t R, int64_t ldv, double* grids, void* stream) {
+    if (!g || R < 1 || (g->N > 0 && (!V || !grids))) return fail(AK_ERR_INVALID, "bad spread arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int q = 3; q >= 1; --q) AK_TRY(spread_group(g, q, V, R, ldv, grids, st));
+    return AK_OK;
+}
+
+extern "C" int ak_interp(const ak_geom* g, const double* grids, int32_t R, const double* scale, double* out,
+                         int64_t ldo, int32_t sum_windows, int64_t wstride, void* stream)
+{
+    if (!g || R < 1 || !scale || (g->N > 0 && (!grids || !out))) return fail(AK_ERR_INVALID, "bad interp arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int q = 3; q >= 1; --q)
+        AK_TRY(interp_group(g, q, grids, R, scale, out, ldo, sum_windows, sum_windows ? 1 : 0, wstride, st));
+    return AK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// FFT stage
+
+// Y2 = H (compact band multiplier of the window) * Y on the band, 0 elsewhere.
+__global__ void k_band_multiply(const double2* __restrict__ Y, double2* __restrict__ Y2, int q, int n, int m,
+                                int R, int64_t hs, int64_t total, const int* __restrict__ gwin,
+                                const double* const* __restrict__ H, int hbase)
+{
+    const int nh = n / 2 + 1, mh = m / 2;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = e / hs;
+        const int64_t k = e - b * hs;
+        const int k2 = (int)(k % nh);
+        const int64_t rest = k / nh;
+        int k0 = 0, k1 = 0;
+        if (q == 3) {
+            k1 = (int)(rest % n);
+            k0 = (int)(rest / n);
+        } else if (q == 2) {
+            k1 = (int)rest;
+        }
+        bool in = k2 < mh;
+        int b0 = 0, b1 = 0;
+        if (q >= 2) {
+            in = in && (k1 < mh || k1 >= n - mh);
+            b1 = k1 < mh ? k1 : k1 - (n - m);
+        }
+        if (q == 3) {
+            in = in && (k0 < mh || k0 >= n - mh);
+            b0 = k0 < mh ? k0 : k0 - (n - m);
+        }
+        double2 out = make_double2(0.0, 0.0);
+        if (in) {
+            const int w = gwin[b / R];
+            int64_t ci;
+            if (q == 3) ci = ((int64_t)b0 * m + b1) * mh + k2;
+            else if (q == 2) ci = (int64_t)b1 * mh + k2;
+            else ci = k2;
+            const double h = H[hbase + w][ci];
+            const double2 y = Y[e];
+            out = make_double2(h * y.x, h * y.y);
+        }
+        Y2[e] = out;
+    }
+}
+
+struct ak_op {
+    const ak_geom* gs = nullptr;
+    const ak_geom* gi = nullptr;
+    int m = 0, R = 0, C = 0;
+    double* grids = nullptr;      // canonical, R rhs
+    double* gbuf = nullptr;       // canonical, R rhs
+    double2* spec = nullptr;
+    double2* spec2 = nullptr;
+    int64_t spec_off[4] = {0, 0, 0, 0};   // complex elements, per q group
+    int64_t hs[4] = {0, 0, 0, 0};         // half-spectrum elements per grid
+    int64_t grid_off[4] = {0, 0, 0, 0};   // doubles, per q group (R units applied)
+    int nwin[4] = {0, 0, 0, 0};
+    cufftHandle fwd[4] = {0, 0, 0, 0}, inv[4] = {0, 0, 0, 0};
+    bool has[4] = {false, false, false, false};
+    int* gwin_d[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+extern "C" int ak_op_destroy(ak_op* op) {
+    if (!op) return AK_OK;
+    for (int q = 1; q <= 3; ++q) {
+        if (op->has[q]) {
+            cufftDestroy(op->fwd[q]);
+            cufftDestroy(op->inv[q]);
+        }
+        cudaFree(op->gwin_d[q]);
+    }
+    cudaFree(op->grids);
+    cudaFree(op->gbuf);
+    cudaFree(op->spec);
+    cudaFree(op->spec2);
+    delete op;
+    return AK_OK;
+}
+
+static int op_build(ak_op* op, cudaStream_t st) {
+    const ak_geom* g = op->gs;
+    const int n = g->n;
+    const int64_t total = g->canon_total * op->R;
+    AK_CUDA(cudaMalloc(&op->grids, sizeof(double) * total));
+    AK_CUDA(cudaMalloc(&op->gbuf, sizeof(double) * total));
+    int64_t soff = 0;
+    for (int q = 3; q >= 1; --q) {
+        const auto& ws = g->windows_of_q[q];
+        op->nwin[q] = (int)ws.size();
+        op->hs[q] = ipow_rt(n, q - 1) * (n / 2 + 1);
+        op->spec_off[q] = soff;
+        if (ws.empty()) continue;
+        op->grid_off[q] = (int64_t)op->R * g->canon_off[ws[0]];
+        soff += op->hs[q] * op->R * (int64_t)ws.size();
+        AK_CUDA(cudaMalloc(&op->gwin_d[q], sizeof(int) * ws.size()));
+        AK_CUDA(cudaMemcpyAsync(op->gwin_d[q], ws.data(), sizeof(int) * ws.size(), cudaMemcpyHostToDevice, st));
+        int dims[3] = {n, n, n};
+        const int batch = op->R * (int)ws.size();
+        AK_CUFFT(cufftPlanMany(&op->fwd[q], q, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_D2Z, batch));
+        if (cufftPlanMany(&op->inv[q], q, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2D, batch) != CUFFT_SUCCESS) {
+            cufftDestroy(op->fwd[q]);
+            return fail(AK_ERR_CUFFT, "cufftPlanMany Z2D failed");
+        }
+        op->has[q] = true;
+    }
+    AK_CUDA(cudaMalloc(&op->spec, sizeof(double2) * std::max<int64_t>(soff, 1)));
+    AK_CUDA(cudaMalloc(&op->spec2, sizeof(double2) * std::max<int64_t>(soff, 1)));
+    AK_CUDA(cudaStreamSynchronize(st));
+    return AK_OK;
+}
+
+extern "C" int ak_op_create(const ak_geom* spread_geom, const ak_geom* interp_geom, int32_t m, int32_t R, int32_t C,
+                            void* stream, ak_op** out)
+{
+    if (!out || !spread_geom) return fail(AK_ERR_INVALID, "null argument");
+    *out = nullptr;
+    if (!interp_geom) interp_geom = spread_geom;
+    if (R < 1 || C < 1) return fail(AK_ERR_INVALID, "R and C must be >= 1");
+    if (m < 2 || m % 2 || m > spread_geom->n) return fail(AK_ERR_INVALID, "m must be even, 2 <= m <= n");
+    if (interp_geom->n != spread_geom->n || interp_geom->q != spread_geom->q)
+        return fail(AK_ERR_INVALID, "spread and interp geometries must share windows and n");
+    ak_op* op = new ak_op();
+    op->gs = spread_geom;
+    op->gi = interp_geom;
+    op->m = m;
+    op->R = R;
+    op->C = C;
+    int rc = op_build(op, (cudaStream_t)stream);
+    if (rc != AK_OK) {
+        std::string keep = g_err;
+        ak_op_destroy(op);
+        g_err = keep;
+        return rc;
+    }
+    *out = op;
+    return AK_OK;
+}
+
+extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double* const* H, const double* scale,
+                           double* const* outs, int64_t ldo, const int32_t* sum_windows, int32_t accumulate,
+                           void* stream)
+{
+    if (!op || !H || !scale || !outs || !sum_windows) return fail(AK_ERR_INVALID, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const ak_geom* gs = op->gs;
+    const ak_geom* gi = op->gi;
+    const int R = op->R, P = gs->P;
+    if (ldo < gi->N || ldv < gs->N) return fail(AK_ERR_INVALID, "leading dimension too small");
+    for (int c = 0; c < op->C; ++c) {
+        if (!outs[c]) return fail(AK_ERR_INVALID, "null output");
+        if (!accumulate) {
+            const int64_t rows = sum_windows[c] ? R : (int64_t)R * P;
+            AK_CUDA(cudaMemsetAsync(outs[c], 0, sizeof(double) * rows * ldo, st));
+        }
+    }
+    if (gs->N == 0 || gi->N == 0) return AK_OK;
+    AK_CUDA(cudaMemsetAsync(op->grids, 0, sizeof(double) * gs->canon_total * R, st));
+    for (int q = 3; q >= 1; --q) AK_TRY(spread_group(gs, q, V, R, ldv, op->grids, st));
+    for (int q = 3; q >= 1; --q)
+        if (op->has[q]) {
+            AK_CUFFT(cufftSetStream(op->fwd[q], st));
+            AK_CUFFT(cufftExecD2Z(op->fwd[q], op->grids + op->grid_off[q], (cufftDoubleComplex*)(op->spec + op->spec_off[q])));
+            g_launches.fetch_add(1);
+        }
+    for (int c = 0; c < op->C; ++c) {
+        for (int q = 3; q >= 1; --q) {
+            if (!op->has[q]) continue;
+            const int64_t total = op->hs[q] * R * op->nwin[q];
+            const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+            k_band_multiply<<<blocks, 256, 0, st>>>(op->spec + op->spec_off[q], op->spec2 + op->spec_off[q], q, gs->n,
+                                                    op->m, R, op->hs[q], total, op->gwin_d[q], H, c * P);
+            AK_TRY(launched());
+            AK_CUFFT(cufftSetStream(op->inv[q], st));
+            AK_CUFFT(cufftExecZ2D(op->inv[q], (cufftDoubleComplex*)(op->spec2 + op->spec_off[q]), op->gbuf + op->grid_off[q]));
+            g_launches.fetch_add(1);
+        }
+        const int atomic_out = (sum_windows[c] || accumulate) ? 1 : 0;
+        for (int q = 3; q >= 1; --q)
+            AK_TRY(interp_group(gi, q, op->gbuf, R, scale + (int64_t)c * P, outs[c], ldo, sum_windows[c], atomic_out,
+                                (int64_t)R * ldo, st));
+    }
+    return AK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// complex NUFFT building blocks
+
+struct PlanKey {
+    int q, n, type;
+    bool operator<(const PlanKey& o) const { return std::tie(q, n, type) < std::tie(o.q, o.n, o.type); }
+};
+static std::mutex g_plan_mu;
+static std::map<PlanKey, cufftHandle> g_plans;
+
+static int cached_plan(int q, int n, cufftType type, cufftHandle* out) {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    PlanKey k{q, n, (int)type};
+    auto it = g_plans.find(k);
+    if (it != g_plans.end()) {
+        *out = it->second;
+        return AK_OK;
+    }
+    int dims[3] = {n, n, n};
+    cufftHandle h;
+    AK_CUFFT(cufftPlanMany(&h, q, dims, nullptr, 1, 0, nullptr, 1, 0, type, 1));
+    g_plans[k] = h;
+    *out = h;
+    return AK_OK;
+}
+
+__global__ void k_type1_extract(const double2* __restrict__ Yr, const double2* __restrict__ Yi, int q, int n, int m,
+                                const double* __restrict__ deconv, double2* __restrict__ S)
+{
+    const int64_t tot = q == 3 ? (int64_t)m * m * m : (q == 2 ? (int64_t)m * m : m);
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= tot) return;
+    int ja[3] = {0, 0, 0};
+    int64_t rest = j;
+    for (int a = q - 1; a >= 0; --a) {
+        ja[a] = (int)(rest % m);
+        rest /= m;
+    }
+    int kn[3];
+    double dc = 1.0;
+    for (int a = 0; a < q; ++a) {
+        const int k = ja[a] < m / 2 ? ja[a] : ja[a] - m;
+        kn[a] = k >= 0 ? k : k + n;
+        dc *= deconv[a * m + ja[a]];
+    }
+    const int nh = n / 2 + 1;
+    bool conj = kn[q - 1] > n / 2;
+    int idx[3];
+    for (int a = 0; a < q; ++a) idx[a] = conj ? (n - kn[a]) % n : kn[a];
+    int64_t lin = 0;
+    for (int a = 0; a < q; ++a) lin = lin * (a == q - 1 ? nh : n) + idx[a];
+    double2 yr = Yr[lin], yi = Yi[lin];
+    if (conj) {
+        yr.y = -yr.y;
+        yi.y = -yi.y;
+    }
+    S[j] = make_double2(dc * (yr.x - yi.y), dc * (yr.y + yi.x));
+}
+
+extern "C" int ak_type1_band(int32_t q, int32_t n, int32_t m, const double* gre, const double* gim,
+                             const double* deconv, double* S, void* stream)
+{
+    if (q < 1 || q > 3 || m < 2 || m > n || !gre || !gim || !deconv || !S) return fail(AK_ERR_INVALID, "bad type1 args");
+    cudaStream_t st = (cudaStream_t)stream;
+    cufftHandle h;
+    AK_TRY(cached_plan(q, n, CUFFT_D2Z, &h));
+    const int64_t hs = ipow_rt(n, q - 1) * (n / 2 + 1);
+    double2* Y = nullptr;
+    AK_CUDA(cudaMallocAsync(&Y, sizeof(double2) * hs * 2, st));
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        AK_CUFFT(cufftSetStream(h, st));
+        AK_CUFFT(cufftExecD2Z(h, const_cast<double*>(gre), (cufftDoubleComplex*)Y));
+        AK_CUFFT(cufftExecD2Z(h, const_cast<double*>(gim), (cufftDoubleComplex*)(Y + hs)));
+    }
+    g_launches.fetch_add(2);
+    const int64_t tot = ipow_rt(m, q);
+    k_type1_extract<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(Y, Y + hs, q, n, m, deconv, (double2*)S);
+    int rc = launched();
+    cudaFreeAsync(Y, st);
+    return rc;
+}
+
+__global__ void k_type2_pad(const double2* __restrict__ c, int q, int n, int m, const double* __restrict__ deconv,
+                            double2* __restrict__ G)
+{
+    const int64_t tot = q == 3 ? (int64_t)m * m * m : (q == 2 ? (int64_t)m * m : m);
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= tot) return;
+    int ja[3] = {0, 0, 0};
+    int64_t rest = j;
+    for (int a = q - 1; a >= 0; --a) {
+        ja[a] = (int)(rest % m);
+        rest /= m;
+    }
+    double dc = 1.0;
+    int64_t lin = 0;
+    for (int a = 0; a < q; ++a) {
+        const int k = ja[a] < m / 2 ? ja[a] : ja[a] - m;
+        lin = lin * n + (k >= 0 ? k : k + n);
+        dc *= deconv[a * m + ja[a]];
+    }
+    const double2 v = c[j];
+    G[lin] = make_double2(dc * v.x, dc * v.y);
+}
+
+__global__ void k_split(const double2* __restrict__ G, int64_t tot, double* __restrict__ re, double* __restrict__ im) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= tot) return;
+    const double2 v = G[i];
+    re[i] = v.x;
+    im[i] = v.y;
+}
+
+extern "C" int ak_type2_grid(int32_t q, int32_t n, int32_t m, const double* c, const double* deconv, double* gre,
+                             double* gim, void* stream)
+{
+    if (q < 1 || q > 3 || m < 2 || m > n || !c || !deconv || !gre || !gim) return fail(AK_ERR_INVALID, "bad type2 args");
+    cudaStream_t st = (cudaStream_t)stream;
+    cufftHandle h;
+    AK_TRY(cached_plan(q, n, CUFFT_Z2Z, &h));
+    const int64_t tot = ipow_rt(n, q);
+    double2* G = nullptr;
+    AK_CUDA(cudaMallocAsync(&G, sizeof(double2) * tot, st));
+    AK_CUDA(cudaMemsetAsync(G, 0, sizeof(double2) * tot, st));
+    const int64_t tm = ipow_rt(m, q);
+    k_type2_pad<<<(unsigned)((tm + 255) / 256), 256, 0, st>>>((const double2*)c, q, n, m, deconv, G);
+    AK_TRY(launched());
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        AK_CUFFT(cufftSetStream(h, st));
+        AK_CUFFT(cufftExecZ2Z(h, (cufftDoubleComplex*)G, (cufftDoubleComplex*)G, CUFFT_INVERSE));
+    }
+    g_launches.fetch_add(1);
+    k_split<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(G, tot, gre, gim);
+    int rc = launched();
+    cudaFreeAsync(G, st);
+    return rc;
+}

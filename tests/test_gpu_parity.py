@@ -1,0 +1,171 @@
+"""GPU parity: the CUDA path (through libaddkern_b200's C ABI) against the
+reference's golden vectors and the CPU oracle.
+
+Tolerance (north_star): relative l2 <= 1e-8 in float64 against the
+reference's own NFFT matvec on the same inputs.  Expected ~1e-13: both sides
+carry the same NUFFT (error ~1e-12 vs the exact trig sum) and differ only by
+rounding and the ~1e-14 window polynomial.
+"""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel, windows_of
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-8
+
+
+def _ds(X, d_max):
+    from paper_2404_17344_b200.dataset import PRESCALED, Dataset
+
+    return Dataset(X, np.zeros(X.shape[0]), tuple(f"x{i + 1}" for i in range(X.shape[1])),
+                   scaling_state=PRESCALED, d_max=int(d_max))
+
+
+def _ws(g):
+    from paper_2404_17344_b200.windows import WindowSet
+
+    return WindowSet(tuple(tuple(int(c) for c in row[:q]) for row, q in zip(g["windows"], g["lengths"])),
+                     d_max=int(g["d_max"]))
+
+
+def _plan(g, family=None, preset="default", **kw):
+    from paper_2404_17344_b200.fastsum import build_plan
+    from paper_2404_17344_b200.kernels import KernelSpec
+
+    spec = KernelSpec(family or str(g["families"][0]), float(g["ells"][0]), float(g["sigma_f"]))
+    return build_plan(spec, _ws(g), preset, _ds(g["X"], g["d_max"]), **kw)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_configs_match_reference(cuda, name):
+    from paper_2404_17344_b200.fastsum import fast_dsigma_matvec, fast_matvec, fast_matvecs
+
+    g = golden(name)
+    plan = _plan(g)
+    for r, v in enumerate(g["V"]):
+        assert rel(fast_matvec(plan, v), g["K_default"][r]) <= TOL
+    res = fast_matvecs(plan, g["V"], dell="dK_dell_default" in g, dsigma="dK_dsigma_default" in g)
+    assert rel(res["K"], g["K_default"]) <= TOL
+    if "dK_dell_default" in g:
+        assert rel(res["dK_dell"], g["dK_dell_default"]) <= TOL
+        dplan = _plan(g, family="der_" + str(g["families"][0]))
+        for r, v in enumerate(g["V"]):
+            assert rel(fast_matvec(dplan, v), g["dK_dell_default"][r]) <= TOL
+    if "dK_dsigma_default" in g:
+        assert rel(res["dK_dsigma"], g["dK_dsigma_default"]) <= TOL
+        assert rel(fast_dsigma_matvec(plan, g["V"][0]), g["dK_dsigma_default"][0]) <= TOL
+    if "K_dense" in g:
+        # both fast paths carry the same Fourier error against the exact dense sum
+        ref_err = rel(g["K_default"], g["K_dense"])
+        gpu_err = rel(res["K"], g["K_dense"])
+        assert abs(gpu_err - ref_err) <= 1e-8
+
+
+def test_mixed_c5_matches_sum_of_reference_plans(cuda):
+    from paper_2404_17344_b200.fastsum import build_mixed_plan, mixed_matvecs
+    from paper_2404_17344_b200.kernels import KernelSpec
+
+    g = golden("c5")
+    specs = [KernelSpec(str(f), float(l), 1.0) for f, l in zip(g["families"], g["ells"])]
+    plan = build_mixed_plan(specs, _ws(g), "default", _ds(g["X"], g["d_max"]))
+    res = mixed_matvecs(plan, g["V"])
+    assert rel(res["K"], g["K_default"]) <= TOL
+    assert rel(res["dK_dsigma"], g["dK_dsigma_default"]) <= TOL
+    for w in range(len(specs)):
+        assert rel(res["dK_dell"][w], g["dK_dell_default"][w]) <= TOL
+
+
+def test_presets_match_reference(cuda):
+    g = golden("c1_presets")
+    from paper_2404_17344_b200.fastsum import fast_matvec
+
+    for preset in ("rough", "fine"):
+        assert rel(fast_matvec(_plan(g, preset=preset), g["V"][0]), g[f"K_{preset}"][0]) <= TOL
+
+
+def test_family_ell_preset_grid(cuda):
+    """Reference test_fastsum.py:62-84 grid: 4 families x ell {0.1,1,10} x 3 presets."""
+    from paper_2404_17344_b200.fastsum import build_plan, fast_matvec
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    g = golden("family_grid")
+    ds = _ds(g["X"], 3)
+    ws = WindowSet(((1, 2, 3), (4, 5, 6)), d_max=3)
+    for fam in ("gauss", "der_gauss", "matern12", "der_matern12"):
+        for ell in (0.1, 1.0, 10.0):
+            for preset in ("rough", "default", "fine"):
+                plan = build_plan(KernelSpec(fam, ell, math.sqrt(0.5)), ws, preset, ds)
+                assert rel(fast_matvec(plan, g["v"]), g[f"{fam}_{ell}_{preset}"]) <= TOL, (fam, ell, preset)
+
+
+@pytest.mark.parametrize("q", [1, 2, 3])
+@pytest.mark.parametrize("m", [8, 16])
+def test_nufft_type1_type2_match_reference(cuda, q, m):
+    from paper_2404_17344_b200.nufft import NufftPlan, nufft_type1, nufft_type2, prepare_points
+
+    g = golden("nufft")
+    plan = NufftPlan(dims=q, m=m)
+    geom = prepare_points(plan, g[f"q{q}_m{m}_pts"])
+    assert rel(nufft_type1(plan, geom, g[f"q{q}_m{m}_w"]), g[f"q{q}_m{m}_type1"]) <= TOL
+    assert rel(nufft_type2(plan, geom, g[f"q{q}_m{m}_c"]), g[f"q{q}_m{m}_type2"]) <= TOL
+
+
+def test_nufft_windows_and_cutoffs(cuda):
+    from paper_2404_17344_b200.nufft import GAUSSIAN_WINDOW, NufftPlan, nufft_type2
+
+    g = golden("nufft")
+    out = nufft_type2(NufftPlan(dims=2, m=16, window=GAUSSIAN_WINDOW), g["gw_pts"], g["gw_c"])
+    assert rel(out, g["gw_type2"]) <= TOL
+    for cutoff in (2, 4, 5, 8):
+        assert rel(nufft_type2(NufftPlan(dims=2, m=16, cutoff=cutoff), g["gw_pts"], g["gw_c"]),
+                   g[f"cut{cutoff}_type2"]) <= TOL
+        assert rel(nufft_type2(NufftPlan(dims=3, m=8, cutoff=cutoff), g["q3cut_pts"], g["q3cut_c"]),
+                   g[f"q3cut{cutoff}_type2"]) <= TOL
+
+
+def test_cross_matvec_matches_reference(cuda):
+    from paper_2404_17344_b200.fastsum import build_plan, fast_cross_matvec, prepare_eval_points
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    g = golden("cross")
+    ws = WindowSet(((1, 2), (3, 4)), d_max=2)
+    tr = _ds(g["Xtr"], 2)
+    te = _ds(g["Xte"], 2)
+    plan = build_plan(KernelSpec("gauss", 1.0 / np.sqrt(2.0)), ws, "default", tr)
+    geoms = prepare_eval_points(plan, te)
+    out = fast_cross_matvec(plan, geoms, g["v"], 80)
+    assert rel(out, g["fast"]) <= TOL
+    assert rel(out, g["dense"]) < 1e-3
+
+
+def test_generic_kernels_agree_with_tiled(cuda, monkeypatch):
+    """The one-thread-per-point kernels (AK_FORCE_GENERIC=1) and the tiled ones."""
+    from paper_2404_17344_b200.fastsum import fast_matvec
+
+    for name in ("c2", "c4"):
+        g = golden(name)
+        plan = _plan(g)
+        tiled = fast_matvec(plan, g["V"][0])
+        monkeypatch.setenv("AK_FORCE_GENERIC", "1")
+        generic = fast_matvec(plan, g["V"][0])
+        monkeypatch.delenv("AK_FORCE_GENERIC")
+        assert rel(tiled, generic) <= 1e-13
+
+
+def test_native_library_is_what_runs(cuda):
+    from paper_2404_17344_b200 import _native
+    from paper_2404_17344_b200.fastsum import fast_matvec
+
+    g = golden("c1")
+    plan = _plan(g)
+    before = _native.launch_count()
+    fast_matvec(plan, g["V"][0])
+    assert _native.launch_count() > before

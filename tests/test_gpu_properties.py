@@ -1,0 +1,195 @@
+"""GPU properties at full BASELINE sizes and edge cases (size-independent
+checks: linearity, symmetry, exact rescales, zero input), plus parity against
+the CPU oracle where the oracle finishes in seconds."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+
+def _ds(X, d_max):
+    from paper_2404_17344_b200.dataset import PRESCALED, Dataset
+
+    return Dataset(X, np.zeros(X.shape[0]), tuple(f"x{i + 1}" for i in range(X.shape[1])),
+                   scaling_state=PRESCALED, d_max=d_max)
+
+
+@pytest.fixture(scope="module")
+def c4_plan(cuda):
+    from paper_2404_17344_b200 import configs
+    from paper_2404_17344_b200.fastsum import build_plan
+
+    wl = configs.config4()
+    return wl, build_plan(wl.spec, wl.window_set, "default", wl.data)
+
+
+def test_c4_full_linearity_symmetry_zero(c4_plan):
+    from paper_2404_17344_b200.fastsum import fast_dsigma_matvec, fast_matvec
+
+    wl, plan = c4_plan
+    N = wl.data.n_rows
+    rng = np.random.default_rng(5)
+    v, w = rng.normal(size=N), rng.normal(size=N)
+    Kv, Kw = fast_matvec(plan, v), fast_matvec(plan, w)
+    combo = fast_matvec(plan, 1.5 * v - 2.0 * w)
+    assert np.max(np.abs(combo - (1.5 * Kv - 2.0 * Kw))) <= 1e-10 * np.max(np.abs(Kv))
+    assert abs(Kv @ w - v @ Kw) <= 1e-8 * np.linalg.norm(v) * np.linalg.norm(w)
+    np.testing.assert_array_equal(fast_matvec(plan, np.zeros(N)), np.zeros(N))
+    np.testing.assert_allclose(fast_dsigma_matvec(plan, v), 2.0 * Kv, rtol=0, atol=1e-13 * np.max(np.abs(Kv)))
+
+
+def test_c4_full_window_parity_vs_oracle(c4_plan):
+    """One 3-D window of config 4 at the full N = 1,000,000 against the oracle."""
+    from oracle import restate as R
+    from paper_2404_17344_b200.fastsum import build_plan, fast_matvec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    wl, _ = c4_plan
+    v = wl.V[0]
+    one = WindowSet(((1, 2, 3),), d_max=3)
+    plan = build_plan(wl.spec, one, "default", wl.data)
+    ref = R.FastSum("gauss", wl.spec.ell, 1.0, [(0, 1, 2)], wl.data.features).matvec(v)
+    assert rel(fast_matvec(plan, v), ref) <= 1e-8
+
+
+def test_batched_rhs_equal_single(c4_plan):
+    from paper_2404_17344_b200.fastsum import fast_matvec, fast_matvecs
+
+    wl, plan = c4_plan
+    rng = np.random.default_rng(9)
+    V = rng.normal(size=(3, wl.data.n_rows))
+    res = fast_matvecs(plan, V, dell=True, dsigma=True)
+    for r in range(3):
+        assert rel(res["K"][r], fast_matvec(plan, V[r])) <= 1e-13
+    assert res["dK_dell"].shape == V.shape
+    assert rel(res["dK_dsigma"], 2.0 * res["K"]) <= 1e-15
+
+
+def test_device_tensors_stay_on_device(c4_plan, cuda):
+    from paper_2404_17344_b200.fastsum import fast_matvec
+
+    wl, plan = c4_plan
+    v = cuda.as_tensor(wl.V[0], device="cuda")
+    out = fast_matvec(plan, v)
+    assert out.is_cuda and out.dtype == cuda.float64
+    assert rel(out.cpu().numpy(), fast_matvec(plan, wl.V[0])) <= 1e-14
+
+
+def _oracle_check(X, windows, v, family="gauss", ell=0.3, d_max=3, preset="default", sf=1.0, tol=1e-8):
+    from oracle import restate as R
+    from paper_2404_17344_b200.fastsum import PRESETS, build_plan, fast_matvec
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    ws = WindowSet(tuple(tuple(c + 1 for c in w) for w in windows), d_max=d_max)
+    plan = build_plan(KernelSpec(family, ell, sf), ws, preset, _ds(X, d_max))
+    out = fast_matvec(plan, v)
+    ref = R.FastSum(family, ell, sf, windows, X, m=PRESETS[preset]).matvec(v)
+    assert rel(out, ref) <= tol
+    return out, ref
+
+
+def test_single_point(cuda):
+    X = np.array([[0.01, -0.02, 0.03]])
+    out, ref = _oracle_check(X, [(0, 1, 2)], np.array([2.5]))
+    assert out.shape == (1,)
+
+
+def test_points_on_the_box_boundary_and_wraparound(cuda):
+    """Nodes at -1/2, just below +1/2 and on cell boundaries: footprints wrap."""
+    rng = np.random.default_rng(1)
+    X = rng.uniform(-0.5, 0.5, size=(600, 6))
+    X[:50] = -0.5
+    X[50:100] = np.nextafter(0.5, 0.0)
+    X[100:150] = np.floor(X[100:150] * 64) / 64  # exact cell boundaries (t integer)
+    _oracle_check(X, [(0, 1, 2), (3, 4), (5,)], rng.normal(size=600), ell=0.2)
+
+
+def test_all_points_in_one_cell(cuda):
+    """One heavy cell: exercises work-item chunking (several chunks per supercell)."""
+    rng = np.random.default_rng(2)
+    X = 0.001 + 1e-5 * rng.random(size=(5000, 3))
+    _oracle_check(X, [(0, 1, 2), (0, 1), (2,)], rng.normal(size=5000))
+
+
+def test_clustered_data_many_chunks(cuda):
+    rng = np.random.default_rng(3)
+    X = np.concatenate([0.02 * rng.normal(size=(20000, 3)), rng.uniform(-0.14, 0.14, size=(3000, 3))])
+    X = np.clip(X, -0.49, 0.49)
+    _oracle_check(X, [(0, 1, 2)], rng.normal(size=X.shape[0]), ell=0.5)
+
+
+@pytest.mark.parametrize("preset", ["rough", "fine", 48])
+def test_other_grid_sizes(cuda, preset):
+    rng = np.random.default_rng(4)
+    X = rng.uniform(-0.25, 0.25, size=(700, 6)) / math.sqrt(3)
+    _oracle_check(X, [(0, 1, 2), (3, 4, 5), (1, 4), (2,)], rng.normal(size=700), preset=preset, ell=0.4)
+
+
+@pytest.mark.parametrize("fam", ["gauss", "der_gauss", "matern12", "der_matern12"])
+def test_families_q123(cuda, fam):
+    rng = np.random.default_rng(6)
+    X = rng.uniform(-0.25, 0.25, size=(900, 6)) / math.sqrt(3)
+    _oracle_check(X, [(0, 1, 2), (3, 4), (5,), (0, 5)], rng.normal(size=900), family=fam, ell=0.35, sf=0.7)
+
+
+def test_domain_error_from_device_check(cuda):
+    from paper_2404_17344_b200.errors import PointOutOfDomainError
+    from paper_2404_17344_b200.fastsum import build_plan
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    X = np.zeros((10, 3))
+    X[3, 1] = 0.5
+    with pytest.raises(PointOutOfDomainError):
+        build_plan(KernelSpec("gauss", 0.5), WindowSet(((1, 2, 3),), d_max=3), "default", _ds(X, 3))
+
+
+def test_wrong_vector_length(cuda):
+    from paper_2404_17344_b200.fastsum import build_plan, fast_matvec
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    plan = build_plan(KernelSpec("gauss", 0.5), WindowSet(((1, 2),), d_max=2), "rough", _ds(np.zeros((5, 2)), 2))
+    with pytest.raises(ValueError):
+        fast_matvec(plan, np.ones(4))
+    with pytest.raises(ValueError):
+        fast_matvec(plan, np.ones((2, 5)))
+
+
+@pytest.mark.parametrize("q", [1, 2, 3])
+def test_adjointness(cuda, q):
+    """<type2(c), w> = <c, conj(type1(w))> (reference test_nufft.py:162-175)."""
+    from paper_2404_17344_b200.nufft import NufftPlan, nufft_type1, nufft_type2, prepare_points
+
+    for m in (8, 16, 32):
+        plan = NufftPlan(dims=q, m=m)
+        for seed in range(5):
+            rng = np.random.default_rng(seed)
+            pts = rng.uniform(-0.5, 0.4999, size=(7, q))
+            w = rng.normal(size=7) + 1j * rng.normal(size=7)
+            c = rng.normal(size=(m,) * q) + 1j * rng.normal(size=(m,) * q)
+            geom = prepare_points(plan, pts)
+            lhs = np.sum(nufft_type2(plan, geom, c) * np.conj(w))
+            rhs = np.sum(c * np.conj(nufft_type1(plan, geom, w)))
+            assert abs(lhs - rhs) / max(abs(lhs), abs(rhs), 1e-30) <= 1e-8
+
+
+def test_known_answers(cuda):
+    from paper_2404_17344_b200.nufft import NufftPlan, nufft_type1, nufft_type2
+
+    plan = NufftPlan(dims=2, m=8)
+    c = np.zeros((8, 8), dtype=complex)
+    c[0, 0] = 1.0
+    pts = np.random.default_rng(0).uniform(-0.5, 0.5, size=(20, 2))
+    np.testing.assert_allclose(nufft_type2(plan, pts, c), np.ones(20), atol=1e-9)
+    np.testing.assert_allclose(nufft_type1(plan, np.array([[0.0, 0.0]]), np.array([1.0])), np.ones((8, 8)),
+                               atol=1e-9)
+    out = nufft_type1(NufftPlan(dims=1, m=8), np.random.default_rng(0).uniform(-0.5, 0.5, size=(5, 1)),
+                      np.zeros(5))
+    np.testing.assert_array_equal(out, np.zeros(8, dtype=complex))

@@ -1,0 +1,105 @@
+"""Pin the CPU oracle (oracle/) against the reference's own golden vectors
+(tests/golden/, produced by the reference by make_golden.py) and against the
+reference test suite's known answers.  CPU only."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel, windows_of
+from oracle import restate as R
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_oracle_matches_reference_configs(name):
+    g = golden(name)
+    fam = str(g["families"][0])
+    ell = float(g["ells"][0])
+    sf = float(g["sigma_f"])
+    wins = windows_of(g)
+    fs = R.FastSum(fam, ell, sf, wins, g["X"])
+    for r, v in enumerate(g["V"]):
+        assert rel(fs.matvec(v), g["K_default"][r]) <= 1e-14
+    if "dK_dell_default" in g:
+        dfs = R.FastSum("der_" + fam, ell, sf, wins, g["X"])
+        for r, v in enumerate(g["V"]):
+            assert rel(dfs.matvec(v), g["dK_dell_default"][r]) <= 1e-14
+    if "K_dense" in g:
+        for r, v in enumerate(g["V"]):
+            assert rel(R.dense_matvec(fam, ell, sf, wins, g["X"], v), g["K_dense"][r]) <= 1e-13
+
+
+def test_oracle_matches_reference_mixed_c5():
+    g = golden("c5")
+    wins = windows_of(g)
+    for r, v in enumerate(g["V"]):
+        acc = np.zeros_like(v)
+        for k, w in enumerate(wins):
+            fs = R.FastSum(str(g["families"][k]), float(g["ells"][k]), 1.0, [w], g["X"])
+            acc += fs.matvec(v)
+            d = R.FastSum("der_" + str(g["families"][k]), float(g["ells"][k]), 1.0, [w], g["X"]).matvec(v)
+            assert rel(d, g["dK_dell_default"][k, r]) <= 1e-14
+        assert rel(acc, g["K_default"][r]) <= 1e-14
+
+
+def test_oracle_presets():
+    g = golden("c1_presets")
+    wins = windows_of(g)
+    for preset in ("rough", "fine"):
+        fs = R.FastSum("gauss", float(g["ells"][0]), 1.0, wins, g["X"], m=R.PRESETS[preset])
+        assert rel(fs.matvec(g["V"][0]), g[f"K_{preset}"][0]) <= 1e-14
+
+
+def test_oracle_family_grid():
+    g = golden("family_grid")
+    for fam in ("gauss", "der_gauss", "matern12", "der_matern12"):
+        for ell in (0.1, 1.0, 10.0):
+            for preset in ("rough", "default", "fine"):
+                fs = R.FastSum(fam, ell, math.sqrt(0.5), [(0, 1, 2), (3, 4, 5)], g["X"], m=R.PRESETS[preset])
+                assert rel(fs.matvec(g["v"]), g[f"{fam}_{ell}_{preset}"]) <= 1e-13
+
+
+@pytest.mark.parametrize("q", [1, 2, 3])
+@pytest.mark.parametrize("m", [8, 16])
+def test_oracle_nufft_golden(q, m):
+    g = golden("nufft")
+    plan = R.Nufft(q, m)
+    geom = R.Geometry(plan, g[f"q{q}_m{m}_pts"])
+    assert rel(R.type1(plan, geom, g[f"q{q}_m{m}_w"]), g[f"q{q}_m{m}_type1"]) <= 1e-14
+    assert rel(R.type2(plan, geom, g[f"q{q}_m{m}_c"]), g[f"q{q}_m{m}_type2"]) <= 1e-14
+
+
+def test_oracle_nufft_windows_and_cutoffs():
+    g = golden("nufft")
+    plan = R.Nufft(2, 16, window="gaussian_window")
+    assert rel(R.type2(plan, R.Geometry(plan, g["gw_pts"]), g["gw_c"]), g["gw_type2"]) <= 1e-14
+    for cutoff in (2, 4, 5, 8):
+        plan = R.Nufft(2, 16, cutoff=cutoff)
+        assert rel(R.type2(plan, R.Geometry(plan, g["gw_pts"]), g["gw_c"]), g[f"cut{cutoff}_type2"]) <= 1e-14
+        plan3 = R.Nufft(3, 8, cutoff=cutoff)
+        out = R.type2(plan3, R.Geometry(plan3, g["q3cut_pts"]), g["q3cut_c"])
+        assert rel(out, g[f"q3cut{cutoff}_type2"]) <= 1e-14
+
+
+@pytest.mark.parametrize("q", [1, 2, 3])
+def test_oracle_type1_type2_vs_direct(q):
+    """Reference test_nufft.py:112-146 known answers, at the same 1e-8 bar."""
+    m = 8
+    plan = R.Nufft(q, m)
+    rng = np.random.default_rng(q)
+    pts = rng.uniform(-0.5, 0.4999, size=(10, q))
+    c = rng.normal(size=(m,) * q) + 1j * rng.normal(size=(m,) * q)
+    w = rng.normal(size=10) + 1j * rng.normal(size=10)
+    geom = R.Geometry(plan, pts)
+    ref2 = R.direct_type2(m, q, pts, c)
+    assert np.max(np.abs(R.type2(plan, geom, c) - ref2)) / np.max(np.abs(ref2)) <= 1e-8
+    ref1 = R.direct_type1(m, q, pts, w)
+    assert np.max(np.abs(R.type1(plan, geom, w) - ref1)) / np.max(np.abs(ref1)) <= 1e-8
+
+
+def test_oracle_dense_known_answer():
+    """Single point: K v = sigma_f^2 * P * v (reference test_kernels.py:46-51)."""
+    X = np.array([[0.01, -0.02, 0.03, 0.0, 0.1, -0.1]])
+    out = R.dense_matvec("gauss", 1.0, 2.0, [(0, 1, 2), (3, 4, 5)], X, np.array([3.0]))
+    assert abs(out[0] - 4.0 * 2 * 3.0) < 1e-12
