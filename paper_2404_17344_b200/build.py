@@ -17,7 +17,6 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libaddkern_b200.so"
 SOURCES = ["ak_lib.cu", "ak_probe.cu"]
-HEADERS = ["ak_common.cuh", "ak_kernels.cuh"]
 
 
 def _nvcc() -> str:
@@ -31,7 +30,7 @@ def _stale() -> bool:
     if not LIB.exists():
         return True
     t = LIB.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "addkern_b200.h", Path(__file__)]
+    deps = [CSRC / s for s in SOURCES] + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "addkern_b200.h", Path(__file__)]
     return any(d.stat().st_mtime > t for d in deps)
 
 

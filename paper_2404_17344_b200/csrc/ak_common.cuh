@@ -26,12 +26,11 @@ struct alignas(16) WorkItem {
 
 // Supercell edge (cells per axis) per window length.  A CTA accumulates one
 // supercell chunk into a (S+T-1)^q shared tile before flushing to HBM/L2.
+// (q = 3 uses a runtime edge of 2..4, see ak_geom::sedge and ak_q3.cuh.)
 template <int Q> struct SuperCell;
-template <> struct SuperCell<3> { static constexpr int S = 4;  };
 template <> struct SuperCell<2> { static constexpr int S = 16; };
 template <> struct SuperCell<1> { static constexpr int S = 32; };
 
-__host__ __device__ inline int supercell_edge(int q) { return q == 3 ? 4 : (q == 2 ? 16 : 32); }
 
 __device__ __forceinline__ int cell_axis(int32_t packed, int a) { return (packed >> (10 * a)) & 1023; }
 

@@ -21,6 +21,7 @@
 // several points of the same cell per step.
 #pragma once
 #include "ak_common.cuh"
+#include "ak_q3.cuh"
 
 namespace ak {
 
@@ -231,141 +232,9 @@ __device__ __forceinline__ void load_region(double* tile, const double* __restri
     }
 }
 
-__device__ __forceinline__ void store_out(double* __restrict__ out, int sum_windows, double v) {
-    if (sum_windows) red_add(out, v);
+__device__ __forceinline__ void store_out(double* __restrict__ out, int atomic_out, double v) {
+    if (atomic_out) red_add(out, v);
     else *out = v;
-}
-
-// Interp for q = 3: register-held footprint per cell, transposed reduction.
-// out(w, r)[idx] (+)= scale[w] * sum_taps w0 w1 w2 g
-template <int T>
-__global__ void __launch_bounds__(32)
-k_interp3_tile(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
-               const double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs,
-               int n, const ak_window_fn wf, const double* __restrict__ scale,
-               double* __restrict__ out, int64_t ldo, int sum_windows, int64_t wstride)
-{
-    constexpr int Q = 3;
-    using LY = Layout<3>;
-    constexpr int S = SuperCell<3>::S;
-    constexpr int R = S + T - 1;
-    constexpr int TILE = R * R * R;
-    constexpr int G0 = LY::G0, G1 = LY::G1, G2 = LY::G2;
-    constexpr int P0 = T / G0, P1 = T / G1, P2 = T / G2;
-    constexpr int WROW = Q * T;
-    static_assert(G0 * G1 * G2 == 32, "q=3 layout must use the full warp");
-
-    __shared__ double tile[TILE];
-    __shared__ __align__(16) double wst[32][WROW];
-    __shared__ int cst[32];
-    __shared__ int ist[32];
-
-    const WorkItem it = items[blockIdx.x];
-    const int r = blockIdx.y;
-    const int lane = threadIdx.x;
-    const int g0 = lane / (G1 * G2);
-    const int g1 = (lane / G2) % G1;
-    const int g2 = lane % G2;
-    const int sc0 = it.sc & 1023, sc1 = (it.sc >> 10) & 1023, sc2 = (it.sc >> 20) & 1023;
-
-    const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
-    load_region<3, T>(tile, g, n, sc0, sc1, sc2, lane);
-    const double sc = scale[it.window];
-    double* __restrict__ o = out + (sum_windows ? 0 : (int64_t)it.window * wstride) + (int64_t)r * ldo;
-
-    double tv[P0][P1][P2];
-    int cur = -1;
-    const int end = it.start + it.count;
-
-    for (int base = it.start; base < end; base += 32) {
-        const int nb = min(32, end - base);
-        __syncwarp();
-        if (lane < nb) {
-            const Point p = pts[base + lane];
-            double w[T];
-#pragma unroll
-            for (int ax = 0; ax < 3; ++ax) {
-                window_weights<T>(wf, p.s[ax], w);
-#pragma unroll
-                for (int a = 0; a < T; ++a) wst[lane][ax * T + a] = w[a];
-            }
-            const int l0 = cell_axis(p.cell, 0) - sc0 * S;
-            const int l1 = cell_axis(p.cell, 1) - sc1 * S;
-            const int l2 = cell_axis(p.cell, 2) - sc2 * S;
-            cst[lane] = l0 | (l1 << 8) | (l2 << 16);
-            ist[lane] = p.idx;
-        }
-        __syncwarp();
-        for (int grp = 0; grp < nb; grp += 8) {
-            double part[8];
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-                const int k = grp + kk;
-                part[kk] = 0.0;
-                if (k < nb) {
-                    const int cell = cst[k];
-                    if (cell != cur) {
-                        cur = cell;
-                        const int l0 = cell & 255, l1 = (cell >> 8) & 255, l2 = (cell >> 16) & 255;
-#pragma unroll
-                        for (int a = 0; a < P0; ++a)
-#pragma unroll
-                            for (int b = 0; b < P1; ++b)
-#pragma unroll
-                                for (int c = 0; c < P2; ++c)
-                                    tv[a][b][c] = tile[((l0 + g0 * P0 + a) * R + (l1 + g1 * P1 + b)) * R +
-                                                       (l2 + g2 * P2 + c)];
-                    }
-                    double w0[P0], w1[P1], w2[P2];
-#pragma unroll
-                    for (int a = 0; a < P0; ++a) w0[a] = wst[k][g0 * P0 + a];
-#pragma unroll
-                    for (int b = 0; b < P1; ++b) w1[b] = wst[k][T + g1 * P1 + b];
-#pragma unroll
-                    for (int c = 0; c < P2; ++c) w2[c] = wst[k][2 * T + g2 * P2 + c];
-                    double accb = 0.0;
-#pragma unroll
-                    for (int b = 0; b < P1; ++b) {
-                        double accc = 0.0;
-#pragma unroll
-                        for (int c = 0; c < P2; ++c) {
-                            double s = 0.0;
-#pragma unroll
-                            for (int a = 0; a < P0; ++a) s = fma(w0[a], tv[a][b][c], s);
-                            accc = fma(w2[c], s, accc);
-                        }
-                        accb = fma(w1[b], accc, accb);
-                    }
-                    part[kk] = accb;
-                }
-            }
-            // Transposed reduction: lane ends with the warp sum of part[lane & 7].
-            {
-                const bool hi4 = lane & 4;
-                double q4[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const double send = hi4 ? part[j] : part[j + 4];
-                    const double keep = hi4 ? part[j + 4] : part[j];
-                    q4[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-                }
-                const bool hi2 = lane & 2;
-                double q2[2];
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    const double send = hi2 ? q4[j] : q4[j + 2];
-                    const double keep = hi2 ? q4[j + 2] : q4[j];
-                    q2[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-                }
-                const bool hi1 = lane & 1;
-                const double send = hi1 ? q2[0] : q2[1];
-                double v = (hi1 ? q2[1] : q2[0]) + __shfl_xor_sync(0xffffffffu, send, 1);
-                v += __shfl_xor_sync(0xffffffffu, v, 8);
-                v += __shfl_xor_sync(0xffffffffu, v, 16);
-                if (lane < 8 && grp + lane < nb) store_out(o + ist[grp + lane], sum_windows, sc * v);
-            }
-        }
-    }
 }
 
 // Interp for q <= 2 (any T <= 16): one lane per point, footprint read from the
@@ -375,7 +244,7 @@ __global__ void __launch_bounds__(32)
 k_interp_lane(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
               const double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs,
               int n, const ak_window_fn wf, const double* __restrict__ scale,
-              double* __restrict__ out, int64_t ldo, int sum_windows, int64_t wstride)
+              double* __restrict__ out, int64_t ldo, int atomic_out, int64_t wstride)
 {
     constexpr int S = SuperCell<Q>::S;
     constexpr int R = S + T - 1;
@@ -390,7 +259,7 @@ k_interp_lane(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
     load_region<Q, T>(tile, g, n, sc0, sc1, 0, lane);
     __syncwarp();
     const double sc = scale[it.window];
-    double* __restrict__ o = out + (sum_windows ? 0 : (int64_t)it.window * wstride) + (int64_t)r * ldo;
+    double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * ldo;
     const int end = it.start + it.count;
     for (int j = it.start + lane; j < end; j += 32) {
         const Point p = pts[j];
@@ -413,7 +282,7 @@ k_interp_lane(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
                 acc = fma(w0[a], s, acc);
             }
         }
-        store_out(o + p.idx, sum_windows, sc * acc);
+        store_out(o + p.idx, atomic_out, sc * acc);
     }
 }
 

@@ -84,7 +84,15 @@ struct ak_geom {
     int64_t nitems = 0;
     int64_t item_begin[4] = {0, 0, 0, 0}, item_end[4] = {0, 0, 0, 0};
     std::vector<int> windows_of_q[4];   // window ids per q, canonical order
+    int sedge[4] = {0, 32, 16, 4};      // supercell edge (cells) per q
 };
+
+// Supercell edge for 3-D windows: 2, 3 or 4 cells (AK_SUPERCELL3 overrides the default).
+static int supercell3_default() {
+    const char* e = getenv("AK_SUPERCELL3");
+    const int v = e ? atoi(e) : 0;
+    return (v >= 2 && v <= 4) ? v : 4;
+}
 
 static int chunk_for_q(int q) { return q == 3 ? 1024 : (q == 2 ? 4096 : 8192); }
 
@@ -203,8 +211,9 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
     // item capacity
     int64_t cap = 0;
     int max_nsc_total = 1;
+    g->sedge[3] = supercell3_default();
     for (int w = 0; w < P; ++w) {
-        const int S = supercell_edge(g->q[w]);
+        const int S = g->sedge[g->q[w]];
         const int nsc = (n + S - 1) / S;
         const int tot = (int)ipow_rt(nsc, g->q[w]);
         max_nsc_total = std::max(max_nsc_total, tot);
@@ -237,7 +246,7 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
     for (int q = 3; q >= 1 && rc == AK_OK; --q) {
         g->item_begin[q] = host_counter;
         for (int w : g->windows_of_q[q]) {
-            const int S = supercell_edge(q);
+            const int S = g->sedge[q];
             const int nsc = (n + S - 1) / S;
             const int tot = (int)ipow_rt(nsc, q);
             int bits = 1;
@@ -447,6 +456,35 @@ static void launch_spread_tile(const ak_geom* g, int64_t i0, int64_t ni, const d
     k_spread_tile<Q, T><<<grid, 32, 0, st>>>(g->pts, g->items + i0, V, ldv, grids, g->canon_off_d, R, g->n, g->wf);
 }
 
+template <int T, int S>
+static void launch_spread3_ts(const ak_geom* g, int64_t i0, int64_t ni, const double* V, int R, int64_t ldv,
+                              double* grids, cudaStream_t st)
+{
+    dim3 grid((unsigned)ni, (unsigned)R);
+    k_spread3<T, S><<<grid, 32, 0, st>>>(g->pts, g->items + i0, V, ldv, grids, g->canon_off_d, R, g->n, g->wf);
+}
+
+template <int T>
+static void launch_spread3_t(const ak_geom* g, int64_t i0, int64_t ni, const double* V, int R, int64_t ldv,
+                             double* grids, cudaStream_t st)
+{
+    switch (g->sedge[3]) {
+        case 2: launch_spread3_ts<T, 2>(g, i0, ni, V, R, ldv, grids, st); break;
+        case 3: launch_spread3_ts<T, 3>(g, i0, ni, V, R, ldv, grids, st); break;
+        default: launch_spread3_ts<T, 4>(g, i0, ni, V, R, ldv, grids, st); break;
+    }
+}
+
+static void launch_spread3(const ak_geom* g, int64_t i0, int64_t ni, const double* V, int R, int64_t ldv,
+                           double* grids, cudaStream_t st)
+{
+    switch (g->wf.taps) {
+        case 12: launch_spread3_t<12>(g, i0, ni, V, R, ldv, grids, st); break;
+        case 8: launch_spread3_t<8>(g, i0, ni, V, R, ldv, grids, st); break;
+        default: launch_spread3_t<4>(g, i0, ni, V, R, ldv, grids, st); break;
+    }
+}
+
 static int spread_group(const ak_geom* g, int q, const double* V, int R, int64_t ldv, double* grids, cudaStream_t st) {
     const int64_t i0 = g->item_begin[q], ni = g->item_end[q] - g->item_begin[q];
     if (g->windows_of_q[q].empty() || g->N == 0) return AK_OK;
@@ -454,9 +492,7 @@ static int spread_group(const ak_geom* g, int q, const double* V, int R, int64_t
     bool done = false;
     if (!force_generic() && ni > 0) {
         done = true;
-        if (q == 3 && T == 12) launch_spread_tile<3, 12>(g, i0, ni, V, R, ldv, grids, st);
-        else if (q == 3 && T == 8) launch_spread_tile<3, 8>(g, i0, ni, V, R, ldv, grids, st);
-        else if (q == 3 && T == 4) launch_spread_tile<3, 4>(g, i0, ni, V, R, ldv, grids, st);
+        if (q == 3 && (T == 12 || T == 8 || T == 4)) launch_spread3(g, i0, ni, V, R, ldv, grids, st);
         else if (q == 2 && T == 12) launch_spread_tile<2, 12>(g, i0, ni, V, R, ldv, grids, st);
         else if (q == 2 && T == 8) launch_spread_tile<2, 8>(g, i0, ni, V, R, ldv, grids, st);
         else if (q == 2 && T == 16) launch_spread_tile<2, 16>(g, i0, ni, V, R, ldv, grids, st);
@@ -477,13 +513,36 @@ static int spread_group(const ak_geom* g, int q, const double* V, int R, int64_t
     return AK_OK;
 }
 
+template <int T, int S>
+static void launch_interp3_ts(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R,
+                              const double* scale, double* out, int64_t ldo, int atomic_out, int64_t wstride,
+                              cudaStream_t st)
+{
+    dim3 grid((unsigned)ni, (unsigned)R);
+    k_interp3<T, S><<<grid, 32, 0, st>>>(g->pts, g->items + i0, grids, g->canon_off_d, R, g->n, g->wf, scale, out,
+                                         ldo, atomic_out, wstride);
+}
+
 template <int T>
+static void launch_interp3_t(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R,
+                             const double* scale, double* out, int64_t ldo, int atomic_out, int64_t wstride,
+                             cudaStream_t st)
+{
+    switch (g->sedge[3]) {
+        case 2: launch_interp3_ts<T, 2>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
+        case 3: launch_interp3_ts<T, 3>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
+        default: launch_interp3_ts<T, 4>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
+    }
+}
+
 static void launch_interp3(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R, const double* scale,
                            double* out, int64_t ldo, int atomic_out, int64_t wstride, cudaStream_t st)
 {
-    dim3 grid((unsigned)ni, (unsigned)R);
-    k_interp3_tile<T><<<grid, 32, 0, st>>>(g->pts, g->items + i0, grids, g->canon_off_d, R, g->n, g->wf, scale, out,
-                                           ldo, atomic_out, wstride);
+    switch (g->wf.taps) {
+        case 12: launch_interp3_t<12>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
+        case 8: launch_interp3_t<8>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
+        default: launch_interp3_t<4>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
+    }
 }
 
 template <int Q, int T>
@@ -507,9 +566,8 @@ static int interp_group(const ak_geom* g, int q, const double* grids, int R, con
     bool done = false;
     if (!force_generic() && ni > 0) {
         done = true;
-        if (q == 3 && T == 12) launch_interp3<12>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, ws, st);
-        else if (q == 3 && T == 8) launch_interp3<8>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, ws, st);
-        else if (q == 3 && T == 4) launch_interp3<4>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, ws, st);
+        if (q == 3 && (T == 12 || T == 8 || T == 4))
+            launch_interp3(g, i0, ni, grids, R, scale, out, ldo, atomic_out, ws, st);
 #define AK_LANE(QQ, TT) \
         else if (q == QQ && T == TT) launch_interp_lane<QQ, TT>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, ws, st);
         AK_LANE(2, 4) AK_LANE(2, 6) AK_LANE(2, 8) AK_LANE(2, 10) AK_LANE(2, 12) AK_LANE(2, 14) AK_LANE(2, 16)
