@@ -55,31 +55,32 @@ __device__ __forceinline__ int64_t region_index(int i, int o0, int o1, int o2, i
     return ((int64_t)x * n + y) * n + z;
 }
 
-// One point of a spread cell run: FMAs with the current weights (w0 already
-// multiplied by the RHS value) while the next point's weights are loaded.
+// Load this lane's slice of one point's weights from its staging row.
 template <int T, int P0, int P1, int P2>
-__device__ __forceinline__ void spread_point(double (&acc)[P0][P1][P2], const double (&w0)[P0],
-                                             const double (&w1)[P1], const double (&w2)[P2],
-                                             double (&n0)[P0], double (&n1)[P1], double (&n2)[P2],
-                                             const double* __restrict__ nrow, int g0, int g1, int g2)
+__device__ __forceinline__ void load_w(double (&w0)[P0], double (&w1)[P1], double (&w2)[P2],
+                                       const double* __restrict__ row, int g0, int g1, int g2)
 {
-    double pbc[P1][P2];
+#pragma unroll
+    for (int a = 0; a < P0; ++a) w0[a] = row[g0 * P0 + a];
+#pragma unroll
+    for (int b = 0; b < P1; ++b) w1[b] = row[T + g1 * P1 + b];
+#pragma unroll
+    for (int c = 0; c < P2; ++c) w2[c] = row[2 * T + g2 * P2 + c];
+}
+
+// acc[a][b][c] += (v w0[a]) * (w1[b] w2[c]) for this lane's footprint slice.
+template <int P0, int P1, int P2>
+__device__ __forceinline__ void spread_fma(double (&acc)[P0][P1][P2], const double (&w0)[P0],
+                                           const double (&w1)[P1], const double (&w2)[P2])
+{
 #pragma unroll
     for (int b = 0; b < P1; ++b)
 #pragma unroll
-        for (int c = 0; c < P2; ++c) pbc[b][c] = w1[b] * w2[c];
+        for (int c = 0; c < P2; ++c) {
+            const double pbc = w1[b] * w2[c];
 #pragma unroll
-    for (int a = 0; a < P0; ++a) n0[a] = nrow[g0 * P0 + a];
-#pragma unroll
-    for (int b = 0; b < P1; ++b) n1[b] = nrow[T + g1 * P1 + b];
-#pragma unroll
-    for (int c = 0; c < P2; ++c) n2[c] = nrow[2 * T + g2 * P2 + c];
-#pragma unroll
-    for (int b = 0; b < P1; ++b)
-#pragma unroll
-        for (int c = 0; c < P2; ++c)
-#pragma unroll
-            for (int a = 0; a < P0; ++a) acc[a][b][c] = fma(w0[a], pbc[b][c], acc[a][b][c]);
+            for (int a = 0; a < P0; ++a) acc[a][b][c] = fma(w0[a], pbc, acc[a][b][c]);
+        }
 }
 
 template <int T, int S>
@@ -169,26 +170,26 @@ k_spread3(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
         const int prev = __shfl_up_sync(0xffffffffu, mycell, 1);
         const unsigned chg = __ballot_sync(0xffffffffu, lane < nb && (lane == 0 ? mycell != cur : mycell != prev));
 
-        // ping-pong register sets A/B: point k uses one set while k+1 loads into the other
-        double a0[P0], a1[P1], a2[P2], b0[P0], b1[P1], b2[P2];
-#pragma unroll
-        for (int a = 0; a < P0; ++a) a0[a] = wst[0][g0 * P0 + a];
-#pragma unroll
-        for (int b = 0; b < P1; ++b) a1[b] = wst[0][T + g1 * P1 + b];
-#pragma unroll
-        for (int c = 0; c < P2; ++c) a2[c] = wst[0][2 * T + g2 * P2 + c];
-        for (int k = 0; k < nb; k += 2) {
+        // Cell runs: the FMA loop of a run has no cell test; weights of the next
+        // point are loaded (register set B) before the FMAs of the current one (A).
+        for (int k = 0; k < nb;) {
             if ((chg >> k) & 1u) {
                 if (cur >= 0) flush(cur);
                 cur = cst[k];
             }
-            spread_point<T>(acc, a0, a1, a2, b0, b1, b2, &wst[k + 1 < nb ? k + 1 : k][0], g0, g1, g2);
-            if (k + 1 >= nb) break;
-            if ((chg >> (k + 1)) & 1u) {
-                if (cur >= 0) flush(cur);
-                cur = cst[k + 1];
+            const unsigned later = k < 31 ? chg & ~((2u << k) - 1u) : 0u;
+            const int kend = later ? min(__ffs(later) - 1, nb) : nb;
+            double a0[P0], a1[P1], a2[P2], b0[P0], b1[P1], b2[P2];
+            load_w<T>(a0, a1, a2, &wst[k][0], g0, g1, g2);
+            int j = k;
+            for (; j + 1 < kend; j += 2) {
+                load_w<T>(b0, b1, b2, &wst[j + 1][0], g0, g1, g2);
+                spread_fma(acc, a0, a1, a2);
+                load_w<T>(a0, a1, a2, &wst[j + 2 < kend ? j + 2 : j + 1][0], g0, g1, g2);
+                spread_fma(acc, b0, b1, b2);
             }
-            spread_point<T>(acc, b0, b1, b2, a0, a1, a2, &wst[k + 2 < nb ? k + 2 : k + 1][0], g0, g1, g2);
+            if (j < kend) spread_fma(acc, a0, a1, a2);
+            k = kend;
         }
     }
     if (cur >= 0) flush(cur);
