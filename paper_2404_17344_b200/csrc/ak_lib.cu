@@ -20,6 +20,7 @@
 
 #include "ak_common.cuh"
 #include "ak_kernels.cuh"
+#include "ak_q3w.cuh"
 
 using namespace ak;
 
@@ -85,13 +86,31 @@ struct ak_geom {
     int64_t item_begin[4] = {0, 0, 0, 0}, item_end[4] = {0, 0, 0, 0};
     std::vector<int> windows_of_q[4];   // window ids per q, canonical order
     int sedge[4] = {0, 32, 16, 4};      // supercell edge (cells) per q
+    // cached 3-D window weights (plan-time table, see ak_q3w.cuh)
+    bool cached = false;
+    int batch3 = 32;
+    double* W3 = nullptr;               // [P3][N][3T]
+    CellIdx* CI3 = nullptr;             // [P3][N]
+    int64_t* wshift_d = nullptr;        // per window: (w - rank3(w)) * N
 };
 
-// Supercell edge for 3-D windows: 2, 3 or 4 cells (AK_SUPERCELL3 overrides the default).
+// AK_WEIGHTS=horner disables the plan-time weight table (weights evaluated per pass).
+static bool weights_cached_default() {
+    const char* e = getenv("AK_WEIGHTS");
+    return !(e && strcmp(e, "horner") == 0);
+}
+// Points per staged batch of the cached-weight kernels (AK_BATCH3: 16 (default) or 32).
+static int batch3_default() {
+    const char* e = getenv("AK_BATCH3");
+    return (e && atoi(e) == 32) ? 32 : 16;
+}
+
+// Supercell edge for 3-D windows: 2, 3 or 4 cells (AK_SUPERCELL3 overrides the default 2;
+// measured on B200, config 4: 2 and 3 tie, 4 is ~7% slower).
 static int supercell3_default() {
     const char* e = getenv("AK_SUPERCELL3");
     const int v = e ? atoi(e) : 0;
-    return (v >= 2 && v <= 4) ? v : 4;
+    return (v >= 2 && v <= 4) ? v : 2;
 }
 
 static int chunk_for_q(int q) { return q == 3 ? 1024 : (q == 2 ? 4096 : 8192); }
@@ -186,6 +205,9 @@ extern "C" int ak_geom_destroy(ak_geom* g) {
     cudaFree(g->pts);
     cudaFree(g->items);
     cudaFree(g->canon_off_d);
+    cudaFree(g->W3);
+    cudaFree(g->CI3);
+    cudaFree(g->wshift_d);
     delete g;
     return AK_OK;
 }
@@ -291,6 +313,36 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
         g->item_end[q] = host_counter;
     }
     g->nitems = host_counter;
+    if (rc == AK_OK && g->wf.taps == 12 && !g->windows_of_q[3].empty() && N > 0 && weights_cached_default()) {
+        const int T = g->wf.taps;
+        const int64_t P3 = (int64_t)g->windows_of_q[3].size();
+        std::vector<int64_t> shift(P, 0);
+        if (cudaMalloc(&g->W3, sizeof(double) * P3 * N * 3 * T) == cudaSuccess &&
+            cudaMalloc(&g->CI3, sizeof(CellIdx) * P3 * N) == cudaSuccess &&
+            cudaMalloc(&g->wshift_d, sizeof(int64_t) * P) == cudaSuccess) {
+            int64_t rank = 0;
+            for (int w : g->windows_of_q[3]) {
+                shift[w] = ((int64_t)w - rank) * N;
+                k_weights3<12><<<(unsigned)((N + 127) / 128), 128, 0, st>>>(g->pts + (int64_t)w * N, N, g->wf,
+                                                                          g->W3 + rank * N * 3 * T,
+                                                                          g->CI3 + rank * N);
+                if ((rc = launched()) != AK_OK) break;
+                ++rank;
+            }
+            if (rc == AK_OK &&
+                cudaMemcpyAsync(g->wshift_d, shift.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice, st) == cudaSuccess)
+                g->cached = true;
+        } else {
+            cudaGetLastError();  // not enough memory for the table: evaluate weights per pass
+            cudaFree(g->W3);
+            cudaFree(g->CI3);
+            cudaFree(g->wshift_d);
+            g->W3 = nullptr;
+            g->CI3 = nullptr;
+            g->wshift_d = nullptr;
+        }
+        g->batch3 = batch3_default();
+    }
     cudaStreamSynchronize(st);
     cudaFree(keys);
     cudaFree(keys2);
@@ -464,10 +516,35 @@ static void launch_spread3_ts(const ak_geom* g, int64_t i0, int64_t ni, const do
     k_spread3<T, S><<<grid, 32, 0, st>>>(g->pts, g->items + i0, V, ldv, grids, g->canon_off_d, R, g->n, g->wf);
 }
 
+template <int S, int B>
+static void launch_spread3w_sb(const ak_geom* g, int64_t i0, int64_t ni, const double* V, int R, int64_t ldv,
+                               double* grids, cudaStream_t st)
+{
+    dim3 grid((unsigned)ni, (unsigned)R);
+    k_spread3w<12, S, B><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
+                                              g->canon_off_d, R, g->n);
+}
+
+template <int B>
+static void launch_spread3w_b(const ak_geom* g, int64_t i0, int64_t ni, const double* V, int R, int64_t ldv,
+                              double* grids, cudaStream_t st)
+{
+    switch (g->sedge[3]) {
+        case 2: launch_spread3w_sb<2, B>(g, i0, ni, V, R, ldv, grids, st); break;
+        case 3: launch_spread3w_sb<3, B>(g, i0, ni, V, R, ldv, grids, st); break;
+        default: launch_spread3w_sb<4, B>(g, i0, ni, V, R, ldv, grids, st); break;
+    }
+}
+
 template <int T>
 static void launch_spread3_t(const ak_geom* g, int64_t i0, int64_t ni, const double* V, int R, int64_t ldv,
                              double* grids, cudaStream_t st)
 {
+    if (T == 12 && g->cached) {
+        if (g->batch3 == 16) launch_spread3w_b<16>(g, i0, ni, V, R, ldv, grids, st);
+        else launch_spread3w_b<32>(g, i0, ni, V, R, ldv, grids, st);
+        return;
+    }
     switch (g->sedge[3]) {
         case 2: launch_spread3_ts<T, 2>(g, i0, ni, V, R, ldv, grids, st); break;
         case 3: launch_spread3_ts<T, 3>(g, i0, ni, V, R, ldv, grids, st); break;
@@ -523,11 +600,38 @@ static void launch_interp3_ts(const ak_geom* g, int64_t i0, int64_t ni, const do
                                          ldo, atomic_out, wstride);
 }
 
+template <int S, int B>
+static void launch_interp3w_sb(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R,
+                               const double* scale, double* out, int64_t ldo, int atomic_out, int64_t wstride,
+                               cudaStream_t st)
+{
+    dim3 grid((unsigned)ni, (unsigned)R);
+    k_interp3w<12, S, B><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids, g->canon_off_d, R,
+                                              g->n, scale, out, ldo, atomic_out, wstride);
+}
+
+template <int B>
+static void launch_interp3w_b(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R,
+                              const double* scale, double* out, int64_t ldo, int atomic_out, int64_t wstride,
+                              cudaStream_t st)
+{
+    switch (g->sedge[3]) {
+        case 2: launch_interp3w_sb<2, B>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
+        case 3: launch_interp3w_sb<3, B>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
+        default: launch_interp3w_sb<4, B>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
+    }
+}
+
 template <int T>
 static void launch_interp3_t(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R,
                              const double* scale, double* out, int64_t ldo, int atomic_out, int64_t wstride,
                              cudaStream_t st)
 {
+    if (T == 12 && g->cached) {
+        if (g->batch3 == 16) launch_interp3w_b<16>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st);
+        else launch_interp3w_b<32>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st);
+        return;
+    }
     switch (g->sedge[3]) {
         case 2: launch_interp3_ts<T, 2>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
         case 3: launch_interp3_ts<T, 3>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;

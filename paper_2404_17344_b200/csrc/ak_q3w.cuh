@@ -1,0 +1,360 @@
+// q = 3 spread / interpolation with plan-time window weights ("cached" mode).
+//
+// The window weights of a 3-D window depend only on the nodes, so the plan
+// tabulates them once (k_weights3: 3*T doubles per point, in bin-sorted
+// order, with the same per-tap polynomial the on-the-fly kernels use) and
+// the per-product kernels stream them instead of re-evaluating 36 window
+// polynomials per point per pass.  That removes ~12% of the FP64 work and the
+// latency-bound polynomial phase from every pass, at the price of 288 B of
+// HBM traffic per point per pass (~2 TB/s at the kernels' rate: the FP64 pipe
+// stays the bound).
+//
+// Pipeline per work item (one warp), batches of B points:
+//   - weight rows of batch b+1 arrive by a TMA bulk copy (cp.async.bulk,
+//     mbarrier completion) into the other half of a double buffer while batch
+//     b is processed;
+//   - (cell, row) records of batch b+2 and the gathered RHS values of batch
+//     b+1 arrive by cp.async;
+//   - spread multiplies the batch's axis-0 weights by the RHS values in shared
+//     memory (element-parallel, conflict-free), then runs the same register-
+//     tiled cell-run FMA loop as ak_q3.cuh.
+#pragma once
+#include "ak_common.cuh"
+#include "ak_q3.cuh"
+
+namespace ak {
+
+struct alignas(8) CellIdx {
+    int32_t cell;
+    int32_t idx;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "AK_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra AK_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// One elected lane: arm the barrier with `bytes` and start the bulk copy.
+__device__ __forceinline__ void tma_load_1d(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(smem)),
+        "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Plan time: weight rows (axis-major: w0[0..T), w1[0..T), w2[0..T)) and
+// (cell, row) records of the points of 3-D windows, compact per-window layout.
+template <int T>
+__global__ void k_weights3(const Point* __restrict__ pts, int64_t np, const ak_window_fn wf, double* __restrict__ W,
+                           CellIdx* __restrict__ CI)
+{
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= np) return;
+    const Point p = pts[j];
+    double w[T];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        window_weights<T>(wf, p.s[ax], w);
+#pragma unroll
+        for (int a = 0; a < T; ++a) W[j * 3 * T + ax * T + a] = w[a];
+    }
+    CI[j] = CellIdx{p.cell, p.idx};
+}
+
+template <int T, int S, int B>
+__global__ void __launch_bounds__(32, 8)
+k_spread3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
+           const WorkItem* __restrict__ items, const double* __restrict__ V, int64_t ldv,
+           double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
+{
+    using LN = Q3Lanes<T>;
+    constexpr int P0 = LN::P0, P1 = LN::P1, P2 = LN::P2;
+    constexpr int RW = 3 * T;
+    constexpr int R = S + T - 1;
+    constexpr int TILE = R * R * R;
+    static_assert(B <= 32, "batch must fit the change mask");
+
+    __shared__ double tile[TILE];
+    __shared__ __align__(128) double wbuf[2][B][RW];
+    __shared__ __align__(16) CellIdx cib[3][B];
+    __shared__ double vb[2][B];
+    __shared__ int cst[B];
+    __shared__ __align__(8) uint64_t bar[2];
+
+    const WorkItem it = items[blockIdx.x];
+    const int r = blockIdx.y;
+    const int lane = threadIdx.x;
+    const int g0 = lane >> 4, g1 = (lane >> 2) & 3, g2 = lane & 3;
+    const int sc0 = it.sc & 1023, sc1 = (it.sc >> 10) & 1023, sc2 = (it.sc >> 20) & 1023;
+    const double* __restrict__ Vr = V + (int64_t)r * ldv;
+    const int end = it.start + it.count;
+    const int nbatch = (it.count + B - 1) / B;
+    const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
+    const CellIdx* __restrict__ CIit = ci + (it.start - wshift[it.window]);
+
+    for (int i = lane; i < TILE; i += 32) tile[i] = 0.0;
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    if (lane == 0) tma_load_1d(&wbuf[0][0][0], Wit, (unsigned)(min(B, it.count) * RW * 8), &bar[0]);
+    if (lane < min(B, it.count)) cp_async8(&cib[0][lane], CIit + lane);
+    if (nbatch > 1 && lane < min(B, it.count - B)) cp_async8(&cib[1][lane], CIit + B + lane);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp();
+    if (lane < min(B, it.count)) cp_async8(&vb[0][lane], Vr + cib[0][lane].idx);
+    cp_async_commit();
+
+    double acc[P0][P1][P2];
+#pragma unroll
+    for (int a = 0; a < P0; ++a)
+#pragma unroll
+        for (int b = 0; b < P1; ++b)
+#pragma unroll
+            for (int c = 0; c < P2; ++c) acc[a][b][c] = 0.0;
+    int cur = -1;
+
+    auto flush = [&](int cell) {
+        const int l0 = cell & 255, l1 = (cell >> 8) & 255, l2 = (cell >> 16) & 255;
+#pragma unroll
+        for (int a = 0; a < P0; ++a)
+#pragma unroll
+            for (int b = 0; b < P1; ++b)
+#pragma unroll
+                for (int c = 0; c < P2; ++c) {
+                    double* t = &tile[((l0 + g0 * P0 + a) * R + (l1 + g1 * P1 + b)) * R + (l2 + g2 * P2 + c)];
+                    *t += acc[a][b][c];
+                    acc[a][b][c] = 0.0;
+                }
+        __syncwarp();
+    };
+
+    for (int bi = 0; bi < nbatch; ++bi) {
+        const int s = bi & 1;
+        const int off = bi * B;  // offset of this batch within the item
+        const int nb = min(B, it.count - off);
+        cp_async_wait_all();
+        mbar_wait(&bar[s], (bi >> 1) & 1);
+        __syncwarp();
+        if (bi + 1 < nbatch) {
+            const int nb1 = min(B, it.count - off - B);
+            if (lane == 0) {
+                fence_proxy_async();
+                tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + B) * RW, (unsigned)(nb1 * RW * 8), &bar[s ^ 1]);
+            }
+            if (lane < nb1) cp_async8(&vb[s ^ 1][lane], Vr + cib[(bi + 1) % 3][lane].idx);
+        }
+        if (bi + 2 < nbatch && lane < min(B, it.count - off - 2 * B))
+            cp_async8(&cib[(bi + 2) % 3][lane], CIit + off + 2 * B + lane);
+        cp_async_commit();
+        // axis-0 weights times the RHS value, element-parallel over the batch
+        for (int e = lane; e < nb * T; e += 32) {
+            const int row = e / T;
+            wbuf[s][row][e - row * T] *= vb[s][row];
+        }
+        if (lane < nb) {
+            const int c = cib[bi % 3][lane].cell;
+            cst[lane] = (cell_axis(c, 0) - sc0 * S) | ((cell_axis(c, 1) - sc1 * S) << 8) |
+                        ((cell_axis(c, 2) - sc2 * S) << 16);
+        }
+        __syncwarp();
+        const int mycell = lane < nb ? cst[lane] : -2;
+        const int prev = __shfl_up_sync(0xffffffffu, mycell, 1);
+        const unsigned chg = __ballot_sync(0xffffffffu, lane < nb && (lane == 0 ? mycell != cur : mycell != prev));
+        for (int k = 0; k < nb;) {
+            if ((chg >> k) & 1u) {
+                if (cur >= 0) flush(cur);
+                cur = cst[k];
+            }
+            const unsigned later = k < 31 ? chg & ~((2u << k) - 1u) : 0u;
+            const int kend = later ? min(__ffs(later) - 1, nb) : nb;
+            double a0[P0], a1[P1], a2[P2], b0[P0], b1[P1], b2[P2];
+            load_w<T>(a0, a1, a2, &wbuf[s][k][0], g0, g1, g2);
+            int j = k;
+            for (; j + 1 < kend; j += 2) {
+                load_w<T>(b0, b1, b2, &wbuf[s][j + 1][0], g0, g1, g2);
+                spread_fma(acc, a0, a1, a2);
+                load_w<T>(a0, a1, a2, &wbuf[s][j + 2 < kend ? j + 2 : j + 1][0], g0, g1, g2);
+                spread_fma(acc, b0, b1, b2);
+            }
+            if (j < kend) spread_fma(acc, a0, a1, a2);
+            k = kend;
+        }
+    }
+    if (cur >= 0) flush(cur);
+    __syncwarp();
+
+    double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
+    const int o0 = sc0 * S - (T / 2 - 1);
+    const int o1 = sc1 * S - (T / 2 - 1);
+    const int o2 = sc2 * S - (T / 2 - 1);
+    for (int i = lane; i < TILE; i += 32) {
+        const double val = tile[i];
+        if (val != 0.0) red_add(g + region_index<R>(i, o0, o1, o2, n), val);
+    }
+    (void)end;
+}
+
+template <int T, int S, int B>
+__global__ void __launch_bounds__(32, 8)
+k_interp3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
+           const WorkItem* __restrict__ items, const double* __restrict__ grids,
+           const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,
+           double* __restrict__ out, int64_t ldo, int atomic_out, int64_t wstride)
+{
+    using LN = Q3Lanes<T>;
+    constexpr int P0 = LN::P0, P1 = LN::P1, P2 = LN::P2;
+    constexpr int RW = 3 * T;
+    constexpr int R = S + T - 1;
+    constexpr int TILE = R * R * R;
+    static_assert(B % 8 == 0 && B <= 32, "batch: multiple of 8, at most 32");
+
+    __shared__ double tile[TILE];
+    __shared__ __align__(128) double wbuf[2][B][RW];
+    __shared__ __align__(16) CellIdx cib[2][B];
+    __shared__ int cst[B];
+    __shared__ __align__(8) uint64_t bar[2];
+
+    const WorkItem it = items[blockIdx.x];
+    const int r = blockIdx.y;
+    const int lane = threadIdx.x;
+    const int g0 = lane >> 4, g1 = (lane >> 2) & 3, g2 = lane & 3;
+    const int sc0 = it.sc & 1023, sc1 = (it.sc >> 10) & 1023, sc2 = (it.sc >> 20) & 1023;
+    const int nbatch = (it.count + B - 1) / B;
+    const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
+    const CellIdx* __restrict__ CIit = ci + (it.start - wshift[it.window]);
+
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    if (lane == 0) tma_load_1d(&wbuf[0][0][0], Wit, (unsigned)(min(B, it.count) * RW * 8), &bar[0]);
+    if (lane < min(B, it.count)) cp_async8(&cib[0][lane], CIit + lane);
+    cp_async_commit();
+    {
+        const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
+        const int o0 = sc0 * S - (T / 2 - 1);
+        const int o1 = sc1 * S - (T / 2 - 1);
+        const int o2 = sc2 * S - (T / 2 - 1);
+        for (int i = lane; i < TILE; i += 32) tile[i] = __ldg(g + region_index<R>(i, o0, o1, o2, n));
+    }
+    const double sc = scale[it.window];
+    double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * ldo;
+
+    double tv[P0][P1][P2];
+    int cur = -1;
+
+    for (int bi = 0; bi < nbatch; ++bi) {
+        const int s = bi & 1;
+        const int off = bi * B;
+        const int nb = min(B, it.count - off);
+        cp_async_wait_all();
+        mbar_wait(&bar[s], (bi >> 1) & 1);
+        __syncwarp();
+        if (bi + 1 < nbatch) {
+            const int nb1 = min(B, it.count - off - B);
+            if (lane == 0) {
+                fence_proxy_async();
+                tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + B) * RW, (unsigned)(nb1 * RW * 8), &bar[s ^ 1]);
+            }
+            if (lane < nb1) cp_async8(&cib[s ^ 1][lane], CIit + off + B + lane);
+        }
+        cp_async_commit();
+        if (lane < nb) {
+            const int c = cib[s][lane].cell;
+            cst[lane] = (cell_axis(c, 0) - sc0 * S) | ((cell_axis(c, 1) - sc1 * S) << 8) |
+                        ((cell_axis(c, 2) - sc2 * S) << 16);
+        }
+        __syncwarp();
+        const int mycell = lane < nb ? cst[lane] : -2;
+        const int prev = __shfl_up_sync(0xffffffffu, mycell, 1);
+        const unsigned chg = __ballot_sync(0xffffffffu, lane < nb && (lane == 0 ? mycell != cur : mycell != prev));
+
+        for (int grp = 0; grp < nb; grp += 8) {
+            double part[8];
+            if (grp + 8 <= nb && ((chg >> grp) & 0xffu) == 0u) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    part[kk] = footprint_dot<P0, P1, P2>(tv, &wbuf[s][grp + kk][0], g0, g1, g2);
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const int k = grp + kk;
+                    part[kk] = 0.0;
+                    if (k < nb) {
+                        if ((chg >> k) & 1u) {
+                            cur = cst[k];
+                            const int l0 = cur & 255, l1 = (cur >> 8) & 255, l2 = (cur >> 16) & 255;
+#pragma unroll
+                            for (int a = 0; a < P0; ++a)
+#pragma unroll
+                                for (int b = 0; b < P1; ++b)
+#pragma unroll
+                                    for (int c = 0; c < P2; ++c)
+                                        tv[a][b][c] = tile[((l0 + g0 * P0 + a) * R + (l1 + g1 * P1 + b)) * R +
+                                                           (l2 + g2 * P2 + c)];
+                        }
+                        part[kk] = footprint_dot<P0, P1, P2>(tv, &wbuf[s][k][0], g0, g1, g2);
+                    }
+                }
+            }
+            const bool hi4 = lane & 4;
+            double q4[4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const double send = hi4 ? part[jj] : part[jj + 4];
+                const double keep = hi4 ? part[jj + 4] : part[jj];
+                q4[jj] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+            }
+            const bool hi2 = lane & 2;
+            double q2[2];
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+                const double send = hi2 ? q4[jj] : q4[jj + 2];
+                const double keep = hi2 ? q4[jj + 2] : q4[jj];
+                q2[jj] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+            }
+            const bool hi1 = lane & 1;
+            const double send = hi1 ? q2[0] : q2[1];
+            double v = (hi1 ? q2[1] : q2[0]) + __shfl_xor_sync(0xffffffffu, send, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 16);
+            if (lane < 8 && grp + lane < nb) {
+                double* dst = o + cib[s][grp + lane].idx;
+                if (atomic_out) red_add(dst, sc * v);
+                else *dst = sc * v;
+            }
+        }
+    }
+}
+
+}  // namespace ak
