@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--n", type=int, default=1_000_000, help="points (default: the config's 1M)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip extras (for profilers)")
+    ap.add_argument("--shard", choices=["point", "window"], default="point",
+                    help="multi-GPU decomposition (N > 1): rows (default) or windows")
     return ap.parse_args()
 
 
@@ -210,14 +212,33 @@ def kernel_roofline(torch, plan, wl, peaks, reps=10):
     name, t = ("spread_q3", t_spread) if t_spread >= t_interp else ("interp_q3", t_interp)
     achieved = flops / (t * 1e-3) / 1e12
     alg_bytes = N * P3 * (24 + 8)  # coordinates + value (spread) / output (interp), compulsory
+    prof = profiled_traffic(name)
     return {
         "bound": "fp64", "kernel": name, "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
-        "frac": achieved / fp64, "traffic": None,
+        "frac": achieved / fp64, "traffic": prof["bytes"] if prof else None,
+        "traffic_source": (f"ncu --set full, {prof['source']} ({prof['kernel'][:40]}); includes the cached "
+                           "window-weight stream (288 B/point), see DESIGN.md") if prof else None,
         "peak_source": "ak_probe_fp64 DFMA microbenchmark in this run (MEASURED_PEAKS.json has no FP64 figure)",
         "flops_per_launch": flops, "ms_per_launch": t,
         "spread_ms": t_spread, "interp_ms": t_interp,
         "hbm_algorithmic_gbs": alg_bytes / (t * 1e-3) / 1e9, "hbm_peak_gbs": peaks.get("hbm_gbs"),
     }
+
+
+def profiled_traffic(kernel: str):
+    """dram read+write bytes per launch of `kernel` from the newest committed ncu
+    full capture summary (profiles/*_summary.json), or None."""
+    best = None
+    for f in sorted((ROOT / "profiles").glob("*_summary.json"), key=lambda p: p.stat().st_mtime):
+        try:
+            data = json.loads(f.read_text())
+        except (OSError, ValueError):
+            continue
+        key = "spread3" if kernel.startswith("spread") else "interp3"
+        for m in data.get("full", []):
+            if key in m.get("kernel", "") and m.get("dram_bytes_per_launch"):
+                best = {"bytes": m["dram_bytes_per_launch"], "source": f.name, "kernel": m["kernel"]}
+    return best
 
 
 def fp64_peak(torch):
@@ -274,15 +295,20 @@ def run_ours(args):
     wl = configs.config4(args.n)
     N = wl.data.n_rows
     wins = wl.window_set.windows
-    mine = tuple(w for i, w in enumerate(wins) if i % world == rank) if world > 1 else wins
-    ws = WindowSet(mine, d_max=3)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     t0 = time.perf_counter()
-    plan = build_plan(wl.spec, ws, "default", wl.data)
+    if world > 1:
+        from paper_2404_17344_b200.distributed import PointShardedPlan, WindowShardedPlan
+
+        cls = PointShardedPlan if args.shard == "point" else WindowShardedPlan
+        dplan = cls(wl.spec, wl.window_set, "default", wl.data)
+        plan = dplan.plan
+    else:
+        plan = build_plan(wl.spec, wl.window_set, "default", wl.data)
     torch.cuda.synchronize()
     plan_s = time.perf_counter() - t0
 
@@ -290,24 +316,25 @@ def run_ours(args):
     v_dev = torch.as_tensor(v_host, device="cuda")
 
     def step_dev():
-        out = fast_matvec(plan, v_dev)
         if world > 1:
-            dist.all_reduce(out)
-        return out
+            return dplan.matvec(v_dev)
+        return fast_matvec(plan, v_dev)
 
     def step_e2e():
         if world > 1:
-            out = fast_matvec(plan, torch.as_tensor(v_host).pin_memory().cuda(non_blocking=True))
-            dist.all_reduce(out)
+            out = dplan.matvec(torch.as_tensor(v_host).pin_memory().cuda(non_blocking=True))
             return out.cpu().numpy()
         return fast_matvec(plan, v_host)
 
     def step_deriv():
-        res = fast_matvecs(plan, v_dev, dell=True, dsigma=True)
         if world > 1:
-            for k in ("K", "dK_dell", "dK_dsigma"):
-                dist.all_reduce(res[k])
-        return res
+            fams = ("gauss", "der_gauss")
+            if args.shard == "point":
+                outs = dplan.matvecs_local(v_dev[dplan.lo:dplan.hi].reshape(1, -1), fams)
+            else:
+                outs = dplan.matvecs(v_dev.reshape(1, -1), fams)
+            return outs
+        return fast_matvecs(plan, v_dev, dell=True, dsigma=True)
 
     def timed(fn, steps, warmup):
         for _ in range(warmup):
@@ -341,7 +368,7 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "N": N, "windows": len(wins), "rhs": 1,
-                   "parallelism": f"window-shard x{world} + NCCL all-reduce" if world > 1 else "single GPU",
+                   "parallelism": (f"{args.shard}-shard x{world} + NCCL all-reduce" if world > 1 else "single GPU"),
                    "l2": "inputs larger than L2: per-step geometry stream 32 B x 1M x 10 windows = 320 MB"},
         "clocks": clocks, "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
         "plan_build_s": plan_s,

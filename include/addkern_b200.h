@@ -138,6 +138,16 @@ int ak_op_create(const ak_geom* spread_geom, const ak_geom* interp_geom,
                  int32_t m, int32_t R, int32_t C, void* stream, ak_op** out);
 int ak_op_destroy(ak_op* op);
 
+/* ak_op_apply flags */
+#define AK_APPLY_ACCUMULATE   1  /* add to the outputs instead of overwriting them            */
+#define AK_APPLY_SPREAD_ONLY  2  /* zero the op's grids, spread V, return (no FFT / interp)    */
+#define AK_APPLY_FROM_GRIDS   4  /* skip the spread: transform + interpolate the op's grids    */
+
+/* The op's spread grids (canonical layout, R right-hand sides): the exchange
+ * buffer of point-sharded multi-GPU products (spread locally, all-reduce the
+ * grids, then ak_op_apply(..., AK_APPLY_FROM_GRIDS)). */
+int ak_op_grids(ak_op* op, double** grids, int64_t* count);
+
 /*
  *   V          device double[R][ldv]
  *   H          DEVICE array [C*P] of device pointers to compact band multipliers
@@ -146,12 +156,13 @@ int ak_op_destroy(ak_op* op);
  *   outs       host array [C] of device output pointers;
  *              sum_windows[c]=1: out[c] is double[R][ldo] summed over windows
  *              sum_windows[c]=0: out[c] is double[P][R][ldo] (per-window products)
- *   accumulate 0: outputs are overwritten (zeroed first); 1: added to
+ *   flags      AK_APPLY_* bits; without AK_APPLY_ACCUMULATE the outputs are
+ *              overwritten (zeroed first)
  */
 int ak_op_apply(ak_op* op, const double* V, int64_t ldv,
                 const double* const* H, const double* scale,
                 double* const* outs, int64_t ldo, const int32_t* sum_windows,
-                int32_t accumulate, void* stream);
+                int32_t flags, void* stream);
 
 /*
  * Complex NUFFT building blocks (nufft_type1 / nufft_type2 API parity).

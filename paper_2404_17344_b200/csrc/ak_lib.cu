@@ -846,16 +846,32 @@ extern "C" int ak_op_create(const ak_geom* spread_geom, const ak_geom* interp_ge
     return AK_OK;
 }
 
+extern "C" int ak_op_grids(ak_op* op, double** grids, int64_t* count) {
+    if (!op || !grids || !count) return fail(AK_ERR_INVALID, "null argument");
+    *grids = op->grids;
+    *count = op->gs->canon_total * op->R;
+    return AK_OK;
+}
+
 extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double* const* H, const double* scale,
-                           double* const* outs, int64_t ldo, const int32_t* sum_windows, int32_t accumulate,
+                           double* const* outs, int64_t ldo, const int32_t* sum_windows, int32_t flags,
                            void* stream)
 {
-    if (!op || !H || !scale || !outs || !sum_windows) return fail(AK_ERR_INVALID, "null argument");
+    if (!op) return fail(AK_ERR_INVALID, "null argument");
     cudaStream_t st = (cudaStream_t)stream;
     const ak_geom* gs = op->gs;
     const ak_geom* gi = op->gi;
     const int R = op->R, P = gs->P;
-    if (ldo < gi->N || ldv < gs->N) return fail(AK_ERR_INVALID, "leading dimension too small");
+    const int accumulate = flags & AK_APPLY_ACCUMULATE;
+    if (!(flags & AK_APPLY_FROM_GRIDS)) {
+        if (ldv < gs->N || (gs->N > 0 && !V)) return fail(AK_ERR_INVALID, "bad right-hand sides");
+        AK_CUDA(cudaMemsetAsync(op->grids, 0, sizeof(double) * gs->canon_total * R, st));
+        if (gs->N > 0)
+            for (int q = 3; q >= 1; --q) AK_TRY(spread_group(gs, q, V, R, ldv, op->grids, st));
+    }
+    if (flags & AK_APPLY_SPREAD_ONLY) return AK_OK;
+    if (!H || !scale || !outs || !sum_windows) return fail(AK_ERR_INVALID, "null argument");
+    if (ldo < gi->N) return fail(AK_ERR_INVALID, "leading dimension too small");
     for (int c = 0; c < op->C; ++c) {
         if (!outs[c]) return fail(AK_ERR_INVALID, "null output");
         if (!accumulate) {
@@ -863,9 +879,7 @@ extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double
             AK_CUDA(cudaMemsetAsync(outs[c], 0, sizeof(double) * rows * ldo, st));
         }
     }
-    if (gs->N == 0 || gi->N == 0) return AK_OK;
-    AK_CUDA(cudaMemsetAsync(op->grids, 0, sizeof(double) * gs->canon_total * R, st));
-    for (int q = 3; q >= 1; --q) AK_TRY(spread_group(gs, q, V, R, ldv, op->grids, st));
+    if (gi->N == 0) return AK_OK;
     for (int q = 3; q >= 1; --q)
         if (op->has[q]) {
             AK_CUFFT(cufftSetStream(op->fwd[q], st));

@@ -1,0 +1,164 @@
+"""Multi-GPU fast summation: one process per GPU, NCCL through torch.distributed.
+
+The reference is single-process; its window loop
+(fastsum.py:156-159) is a sum of independent per-window products, and each
+window's product is linear in the spread grid, which gives two exact
+decompositions:
+
+* window sharding -- rank r owns a subset of the windows (longest-processing-
+  time assignment by per-point cost T^q), computes sum_{w in own} K_w v for
+  all N rows, and one all-reduce(sum) of the N x R products assembles K v on
+  every rank.  Balance is capped by the window granularity (10 windows on 8
+  GPUs: at most 5x).
+* point sharding -- rank r owns a contiguous block of rows.  It spreads only
+  its own nodes into every window's grid, the grids (sum_w n^q_w doubles per
+  RHS, 20 MB for config 4) are summed with one all-reduce, every rank runs the
+  tiny FFT/multiply stage redundantly and interpolates only its own rows.  The
+  result is row-sharded (all_gather for a replicated vector).  Balanced for
+  any window mix.
+
+Both reproduce the single-GPU product up to the order of floating-point sums.
+"""
+
+from __future__ import annotations
+
+import heapq
+
+import numpy as np
+
+from .dataset import Dataset
+from .windows import WindowSet
+
+WINDOW_TAPS = 12
+
+
+def window_cost(q: int, taps: int = WINDOW_TAPS) -> int:
+    """Per-point spread + interp cost of a window of length q (FMAs ~ taps^q)."""
+    return taps ** q
+
+
+def window_partition(lengths, world: int, taps: int = WINDOW_TAPS) -> list:
+    """Assign windows to ranks, longest-processing-time first (greedy LPT).
+
+    Returns world lists of window indices (ascending); ranks may be empty when
+    there are fewer windows than ranks.
+    """
+    order = sorted(range(len(lengths)), key=lambda w: (-window_cost(lengths[w], taps), w))
+    heap = [(0, r) for r in range(world)]
+    owned = [[] for _ in range(world)]
+    for w in order:
+        load, r = heapq.heappop(heap)
+        owned[r].append(w)
+        heapq.heappush(heap, (load + window_cost(lengths[w], taps), r))
+    return [sorted(o) for o in owned]
+
+
+def row_partition(n_rows: int, world: int) -> list:
+    """Contiguous, balanced row blocks [(lo, hi), ...] for point sharding."""
+    base, extra = divmod(n_rows, world)
+    out, lo = [], 0
+    for r in range(world):
+        hi = lo + base + (1 if r < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def _dist():
+    import torch.distributed as dist
+
+    return dist
+
+
+def _subset_rows(data: Dataset, lo: int, hi: int) -> Dataset:
+    from dataclasses import replace
+
+    return replace(data, features=data.features[lo:hi], targets=data.targets[lo:hi])
+
+
+class WindowShardedPlan:
+    """K v over all windows with the windows split across ranks."""
+
+    def __init__(self, spec, window_set: WindowSet, preset, data: Dataset, group=None, **kw):
+        from .fastsum import build_plan
+
+        dist = _dist()
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.owned = window_partition(window_set.lengths, self.world)[self.rank]
+        self.n_rows = data.n_rows
+        self.plan = None
+        if self.owned:
+            sub = WindowSet(tuple(window_set.windows[w] for w in self.owned), d_max=window_set.d_max)
+            self.plan = build_plan(spec, sub, preset, data, **kw)
+
+    def matvecs(self, V, families=None):
+        """(R, N) CUDA tensor -> list of (R, N) products (one per coefficient set), replicated."""
+        import torch
+
+        dist = _dist()
+        fams = families or ((self.plan.spec.family,) if self.plan else None)
+        R = V.shape[0]
+        outs = [torch.zeros((R, self.n_rows), dtype=torch.float64, device="cuda") for _ in fams]
+        if self.plan is not None:
+            self.plan._operator(tuple(fams), R).apply(V, outs, [True] * len(outs))
+        for o in outs:
+            dist.all_reduce(o, group=self.group)
+        return outs
+
+    def matvec(self, v):
+        return self.matvecs(v.reshape(1, -1))[0][0]
+
+
+class PointShardedPlan:
+    """K v with the rows split across ranks; the spread grids are all-reduced."""
+
+    def __init__(self, spec, window_set: WindowSet, preset, data: Dataset, group=None, **kw):
+        from .fastsum import build_plan
+
+        dist = _dist()
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.rows = row_partition(data.n_rows, self.world)
+        self.lo, self.hi = self.rows[self.rank]
+        self.n_rows = data.n_rows
+        self.plan = build_plan(spec, window_set, preset, _subset_rows(data, self.lo, self.hi), **kw)
+
+    def matvecs_local(self, V_local, families=None):
+        """(R, n_local) own-row RHS block -> list of (R, n_local) own-row products."""
+        import torch
+
+        dist = _dist()
+        fams = tuple(families or (self.plan.spec.family,))
+        R = V_local.shape[0]
+        op = self.plan._operator(fams, R)
+        op.spread_only(V_local)
+        dist.all_reduce(op.grids(), group=self.group)
+        from . import _native
+
+        outs = [torch.empty((R, self.hi - self.lo), dtype=torch.float64, device="cuda") for _ in fams]
+        op.apply(None, outs, [True] * len(outs), flags=_native.AK_APPLY_FROM_GRIDS)
+        return outs
+
+    def matvec(self, v, gather: bool = True):
+        """Full-length v (replicated) -> K v (replicated if gather, else own rows)."""
+        import torch
+
+        dist = _dist()
+        out = self.matvecs_local(v[self.lo:self.hi].reshape(1, -1))[0][0]
+        if not gather:
+            return out
+        sizes = [hi - lo for lo, hi in self.rows]
+        chunks = [torch.empty(s, dtype=torch.float64, device="cuda") for s in sizes]
+        if len(set(sizes)) == 1:
+            dist.all_gather(chunks, out, group=self.group)
+        else:
+            m = max(sizes)
+            pad = torch.zeros(m, dtype=torch.float64, device="cuda")
+            pad[: out.numel()] = out
+            bufs = [torch.empty(m, dtype=torch.float64, device="cuda") for _ in sizes]
+            dist.all_gather(bufs, pad, group=self.group)
+            chunks = [b[:s] for b, s in zip(bufs, sizes)]
+        return torch.cat(chunks)

@@ -142,16 +142,39 @@ class _Operator:
         rc = lib.ak_op_create(gs.handle, gi.handle, m, R, C, _stream_ptr(torch), ctypes.byref(self._handle))
         _native.check(rc, "ak_op_create")
 
-    def apply(self, V, outs: list, sum_windows: list, accumulate: bool = False) -> None:
+    def apply(self, V, outs: list, sum_windows: list, accumulate: bool = False, flags: int = 0) -> None:
+        """One product: spread V, transform, interpolate into outs (ak_op_apply)."""
         torch = _torch()
         C = self.C
         optrs = (ctypes.c_void_p * C)(*[o.data_ptr() for o in outs])
         sw = (ctypes.c_int32 * C)(*[1 if s else 0 for s in sum_windows])
         ldo = int(outs[0].shape[-1])
-        rc = self._lib.ak_op_apply(self._handle, V.data_ptr(), int(V.shape[-1]), self.hptr.data_ptr(),
-                                   self.scale.data_ptr(), optrs, ldo, sw, 1 if accumulate else 0,
-                                   _stream_ptr(torch))
+        f = flags | (_native.AK_APPLY_ACCUMULATE if accumulate else 0)
+        vptr = V.data_ptr() if V is not None else 0
+        ldv = int(V.shape[-1]) if V is not None else self.gs.n_points
+        rc = self._lib.ak_op_apply(self._handle, vptr, ldv, self.hptr.data_ptr(), self.scale.data_ptr(), optrs, ldo,
+                                   sw, f, _stream_ptr(torch))
         _native.check(rc, "ak_op_apply")
+
+    def spread_only(self, V) -> None:
+        """Zero the op's grids and spread V into them (first half of a point-sharded product)."""
+        torch = _torch()
+        rc = self._lib.ak_op_apply(self._handle, V.data_ptr(), int(V.shape[-1]), 0, 0, None, 0, None,
+                                   _native.AK_APPLY_SPREAD_ONLY, _stream_ptr(torch))
+        _native.check(rc, "ak_op_apply(spread only)")
+
+    def grids(self):
+        """The op's spread grids as a torch CUDA tensor view (all-reduce buffer)."""
+        torch = _torch()
+        ptr = ctypes.c_void_p()
+        count = ctypes.c_int64()
+        _native.check(self._lib.ak_op_grids(self._handle, ctypes.byref(ptr), ctypes.byref(count)), "ak_op_grids")
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (int(count.value),), "typestr": "<f8",
+                                        "data": (int(ptr.value or 0), False), "version": 3, "strides": None}
+
+        return torch.as_tensor(_View(), device="cuda")
 
     def __del__(self):
         h = getattr(self, "_handle", None)

@@ -193,3 +193,63 @@ def test_known_answers(cuda):
     out = nufft_type1(NufftPlan(dims=1, m=8), np.random.default_rng(0).uniform(-0.5, 0.5, size=(5, 1)),
                       np.zeros(5))
     np.testing.assert_array_equal(out, np.zeros(8, dtype=complex))
+
+
+def test_split_apply_and_grid_view(cuda):
+    """spread_only + FROM_GRIDS equals one apply; the grid view aliases the op's buffer
+    (the point-sharded multi-GPU path all-reduces exactly this view)."""
+    from paper_2404_17344_b200 import _native
+    from paper_2404_17344_b200.fastsum import build_plan
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    rng = np.random.default_rng(8)
+    X = rng.uniform(-0.25, 0.25, size=(3000, 6)) / math.sqrt(3)
+    ws = WindowSet(((1, 2, 3), (4, 5), (6,)), d_max=3)
+    plan = build_plan(KernelSpec("gauss", 0.4), ws, "default", _ds(X, 3))
+    V = cuda.as_tensor(rng.normal(size=(2, 3000)), device="cuda")
+    op = plan._operator(("gauss",), 2)
+    ref = cuda.empty((2, 3000), dtype=cuda.float64, device="cuda")
+    op.apply(V, [ref], [True])
+    op.spread_only(V)
+    g = op.grids()
+    assert g.numel() == plan.geometries.canon_total * 2 and float(g.abs().sum()) > 0
+    out = cuda.empty_like(ref)
+    op.apply(None, [out], [True], flags=_native.AK_APPLY_FROM_GRIDS)
+    assert rel(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-15
+    g.mul_(2.0)
+    op.apply(None, [out], [True], flags=_native.AK_APPLY_FROM_GRIDS)
+    assert rel(out.cpu().numpy(), 2.0 * ref.cpu().numpy()) <= 1e-15
+
+
+def test_sharded_plans_single_rank(cuda):
+    """World size 1 (NCCL): both multi-GPU plans reproduce the single-GPU product."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2404_17344_b200.distributed import PointShardedPlan, WindowShardedPlan
+    from paper_2404_17344_b200.fastsum import build_plan, fast_matvec
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        rng = np.random.default_rng(10)
+        X = rng.uniform(-0.25, 0.25, size=(5000, 7)) / math.sqrt(3)
+        ws = WindowSet(((1, 2, 3), (4, 5, 6), (6, 7), (2,)), d_max=3)
+        spec = KernelSpec("gauss", 0.5)
+        ds = _ds(X, 3)
+        v = rng.normal(size=5000)
+        ref = fast_matvec(build_plan(spec, ws, "default", ds), v)
+        vd = cuda.as_tensor(v, device="cuda")
+        for cls in (WindowShardedPlan, PointShardedPlan):
+            out = cls(spec, ws, "default", ds).matvec(vd)
+            assert rel(out.cpu().numpy(), ref) <= 1e-13, cls.__name__
+    finally:
+        dist.destroy_process_group()

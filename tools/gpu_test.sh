@@ -1,0 +1,2 @@
+timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+tail -15 gpurun_out/pytest_gpu.log
