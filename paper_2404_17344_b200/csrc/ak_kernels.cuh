@@ -228,8 +228,10 @@ __device__ __forceinline__ void load_region(double* tile, const double* __restri
         } else {
             gi = wrap(o0 + i, n);
         }
-        tile[i] = __ldg(g + gi);
+        cp_async8(&tile[i], g + gi);
     }
+    cp_async_commit();
+    cp_async_wait_all();
 }
 
 __device__ __forceinline__ void store_out(double* __restrict__ out, int atomic_out, double v) {

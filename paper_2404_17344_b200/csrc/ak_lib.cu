@@ -105,12 +105,12 @@ static int batch3_default() {
     return (e && atoi(e) == 32) ? 32 : 16;
 }
 
-// Supercell edge for 3-D windows: 2, 3 or 4 cells (AK_SUPERCELL3 overrides the default 2;
+// Supercell edge for 3-D windows: 2, 3 or 4 cells (AK_SUPERCELL3 overrides the default 3;
 // measured on B200, config 4: 2 and 3 tie, 4 is ~7% slower).
 static int supercell3_default() {
     const char* e = getenv("AK_SUPERCELL3");
     const int v = e ? atoi(e) : 0;
-    return (v >= 2 && v <= 4) ? v : 2;
+    return (v >= 2 && v <= 4) ? v : 3;
 }
 
 static int chunk_for_q(int q) { return q == 3 ? 1024 : (q == 2 ? 4096 : 8192); }

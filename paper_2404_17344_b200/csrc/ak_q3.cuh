@@ -267,7 +267,10 @@ k_interp3(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
         const int o0 = sc0 * S - (T / 2 - 1);
         const int o1 = sc1 * S - (T / 2 - 1);
         const int o2 = sc2 * S - (T / 2 - 1);
-        for (int i = lane; i < TILE; i += 32) tile[i] = __ldg(g + region_index<R>(i, o0, o1, o2, n));
+        for (int i = lane; i < TILE; i += 32) cp_async8(&tile[i], g + region_index<R>(i, o0, o1, o2, n));
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncwarp();
     }
     const double sc = scale[it.window];
     double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * ldo;

@@ -29,13 +29,6 @@ struct alignas(8) CellIdx {
     int32_t idx;
 };
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -175,9 +168,24 @@ k_spread3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
             cp_async8(&cib[(bi + 2) % 3][lane], CIit + off + 2 * B + lane);
         cp_async_commit();
         // axis-0 weights times the RHS value, element-parallel over the batch
-        for (int e = lane; e < nb * T; e += 32) {
-            const int row = e / T;
-            wbuf[s][row][e - row * T] *= vb[s][row];
+        {
+            constexpr int PER = (B * T + 31) / 32;  // elements of the batch's w0 block per lane
+            double x[PER], y[PER];
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int e = lane + 32 * i;
+                const int row = e / T;
+                if (row < nb) {
+                    x[i] = wbuf[s][row][e - row * T];
+                    y[i] = vb[s][row];
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int e = lane + 32 * i;
+                const int row = e / T;
+                if (row < nb) wbuf[s][row][e - row * T] = x[i] * y[i];
+            }
         }
         if (lane < nb) {
             const int c = cib[bi % 3][lane].cell;
@@ -261,11 +269,13 @@ k_interp3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     if (lane < min(B, it.count)) cp_async8(&cib[0][lane], CIit + lane);
     cp_async_commit();
     {
+        // region tile by cp.async (no register round trip: all loads in flight at once)
         const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
         const int o0 = sc0 * S - (T / 2 - 1);
         const int o1 = sc1 * S - (T / 2 - 1);
         const int o2 = sc2 * S - (T / 2 - 1);
-        for (int i = lane; i < TILE; i += 32) tile[i] = __ldg(g + region_index<R>(i, o0, o1, o2, n));
+        for (int i = lane; i < TILE; i += 32) cp_async8(&tile[i], g + region_index<R>(i, o0, o1, o2, n));
+        cp_async_commit();
     }
     const double sc = scale[it.window];
     double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * ldo;
