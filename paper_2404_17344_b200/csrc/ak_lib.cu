@@ -88,7 +88,8 @@ struct ak_geom {
     int sedge[4] = {0, 32, 16, 4};      // supercell edge (cells) per q
     // cached 3-D window weights (plan-time table, see ak_q3w.cuh)
     bool cached = false;
-    int batch3 = 32;
+    int batch3 = 16;
+    int iwarps = 1;                     // warps per CTA of the cached q=3 interp
     double* W3 = nullptr;               // [P3][N][3T]
     CellIdx* CI3 = nullptr;             // [P3][N]
     int64_t* wshift_d = nullptr;        // per window: (w - rank3(w)) * N
@@ -342,6 +343,8 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
             g->wshift_d = nullptr;
         }
         g->batch3 = batch3_default();
+        const char* iw = getenv("AK_IWARPS");
+        g->iwarps = (iw && atoi(iw) == 1) ? 1 : 2;
     }
     cudaStreamSynchronize(st);
     cudaFree(keys);
@@ -606,8 +609,20 @@ static void launch_interp3w_sb(const ak_geom* g, int64_t i0, int64_t ni, const d
                                cudaStream_t st)
 {
     dim3 grid((unsigned)ni, (unsigned)R);
-    k_interp3w<12, S, B><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids, g->canon_off_d, R,
-                                              g->n, scale, out, ldo, atomic_out, wstride);
+    if constexpr (B == 16) {
+        if (g->iwarps == 2) {
+            k_interp3w<12, S, B, 2><<<grid, 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids,
+                                                         g->canon_off_d, R, g->n, scale, out, ldo, atomic_out,
+                                                         wstride);
+            return;
+        }
+    }
+    if (false)
+        k_interp3w<12, S, B, 1><<<grid, 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids,
+                                                     g->canon_off_d, R, g->n, scale, out, ldo, atomic_out, wstride);
+    else
+        k_interp3w<12, S, B, 1><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids,
+                                                     g->canon_off_d, R, g->n, scale, out, ldo, atomic_out, wstride);
 }
 
 template <int B>

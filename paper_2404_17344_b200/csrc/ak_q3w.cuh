@@ -230,8 +230,10 @@ k_spread3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     (void)end;
 }
 
-template <int T, int S, int B>
-__global__ void __launch_bounds__(32, 8)
+// NW warps per CTA share the read-only region tile; warp w takes the batches
+// w, w+NW, w+2NW, ... of the item, each with its own weight double buffer.
+template <int T, int S, int B, int NW>
+__global__ void __launch_bounds__(32 * NW, 8 / NW)
 k_interp3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ grids,
            const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,
@@ -245,14 +247,19 @@ k_interp3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     static_assert(B % 8 == 0 && B <= 32, "batch: multiple of 8, at most 32");
 
     __shared__ double tile[TILE];
-    __shared__ __align__(128) double wbuf[2][B][RW];
-    __shared__ __align__(16) CellIdx cib[2][B];
-    __shared__ int cst[B];
-    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ __align__(128) double wbuf_all[NW][2][B][RW];
+    __shared__ __align__(16) CellIdx cib_all[NW][2][B];
+    __shared__ int cst_all[NW][B];
+    __shared__ __align__(8) uint64_t bar_all[NW][2];
 
     const WorkItem it = items[blockIdx.x];
     const int r = blockIdx.y;
-    const int lane = threadIdx.x;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    double (*wbuf)[B][RW] = wbuf_all[warp];
+    CellIdx (*cib)[B] = cib_all[warp];
+    int* cst = cst_all[warp];
+    uint64_t* bar = bar_all[warp];
     const int g0 = lane >> 4, g1 = (lane >> 2) & 3, g2 = lane & 3;
     const int sc0 = it.sc & 1023, sc1 = (it.sc >> 10) & 1023, sc2 = (it.sc >> 20) & 1023;
     const int nbatch = (it.count + B - 1) / B;
@@ -265,38 +272,43 @@ k_interp3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         mbar_fence_init();
     }
     __syncwarp();
-    if (lane == 0) tma_load_1d(&wbuf[0][0][0], Wit, (unsigned)(min(B, it.count) * RW * 8), &bar[0]);
-    if (lane < min(B, it.count)) cp_async8(&cib[0][lane], CIit + lane);
-    cp_async_commit();
+    if (warp < nbatch) {
+        const int cnt = min(B, it.count - warp * B);
+        if (lane == 0) tma_load_1d(&wbuf[0][0][0], Wit + (int64_t)warp * B * RW, (unsigned)(cnt * RW * 8), &bar[0]);
+        if (lane < cnt) cp_async8(&cib[0][lane], CIit + warp * B + lane);
+    }
     {
         // region tile by cp.async (no register round trip: all loads in flight at once)
         const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
         const int o0 = sc0 * S - (T / 2 - 1);
         const int o1 = sc1 * S - (T / 2 - 1);
         const int o2 = sc2 * S - (T / 2 - 1);
-        for (int i = lane; i < TILE; i += 32) cp_async8(&tile[i], g + region_index<R>(i, o0, o1, o2, n));
-        cp_async_commit();
+        for (int i = threadIdx.x; i < TILE; i += 32 * NW) cp_async8(&tile[i], g + region_index<R>(i, o0, o1, o2, n));
     }
+    cp_async_commit();
+    cp_async_wait_all();
+    if (NW > 1) __syncthreads();
     const double sc = scale[it.window];
     double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * ldo;
 
     double tv[P0][P1][P2];
     int cur = -1;
 
-    for (int bi = 0; bi < nbatch; ++bi) {
-        const int s = bi & 1;
+    for (int bi = warp, u = 0; bi < nbatch; bi += NW, ++u) {
+        const int s = u & 1;
         const int off = bi * B;
         const int nb = min(B, it.count - off);
         cp_async_wait_all();
-        mbar_wait(&bar[s], (bi >> 1) & 1);
+        mbar_wait(&bar[s], (u >> 1) & 1);
         __syncwarp();
-        if (bi + 1 < nbatch) {
-            const int nb1 = min(B, it.count - off - B);
+        if (bi + NW < nbatch) {
+            const int nb1 = min(B, it.count - off - NW * B);
             if (lane == 0) {
                 fence_proxy_async();
-                tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + B) * RW, (unsigned)(nb1 * RW * 8), &bar[s ^ 1]);
+                tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + NW * B) * RW, (unsigned)(nb1 * RW * 8),
+                            &bar[s ^ 1]);
             }
-            if (lane < nb1) cp_async8(&cib[s ^ 1][lane], CIit + off + B + lane);
+            if (lane < nb1) cp_async8(&cib[s ^ 1][lane], CIit + off + NW * B + lane);
         }
         cp_async_commit();
         if (lane < nb) {
