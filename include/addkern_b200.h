@@ -16,6 +16,7 @@
  *                      over windows and scaled, fastsum.py:136-138)
  *   ak_type1_band      fftn + band + deconvolution of nufft_type1 (nufft.py:362-365)
  *   ak_type2_grid      deconvolution + zero-pad + ifftn of nufft_type2 (nufft.py:379-383)
+ *   ak_dense_apply     dense_matvec / dense_cross_matvec / dense_matrix (kernels.py:92-170)
  *
  * Conventions
  *  - All array pointers are DEVICE pointers owned by the caller unless noted.
@@ -142,6 +143,9 @@ int ak_op_destroy(ak_op* op);
 #define AK_APPLY_ACCUMULATE   1  /* add to the outputs instead of overwriting them            */
 #define AK_APPLY_SPREAD_ONLY  2  /* zero the op's grids, spread V, return (no FFT / interp)    */
 #define AK_APPLY_FROM_GRIDS   4  /* skip the spread: transform + interpolate the op's grids    */
+#define AK_APPLY_H_PER_RHS    8  /* C == 1 and H holds R*P multipliers: RHS r of window w uses
+                                    H[r*P + w] (R different kernels in lockstep, e.g. the cells
+                                    of a length-scale grid search over one geometry)            */
 
 /* The op's spread grids (canonical layout, R right-hand sides): the exchange
  * buffer of point-sharded multi-GPU products (spread locally, all-reduce the
@@ -176,6 +180,23 @@ int ak_type1_band(int32_t q, int32_t n, int32_t m, const double* gre, const doub
                   const double* deconv, double* S, void* stream);
 int ak_type2_grid(int32_t q, int32_t n, int32_t m, const double* c,
                   const double* deconv, double* gre, double* gim, void* stream);
+
+/*
+ * Exact dense products (the reference's dense oracle, kernels.py:92-170):
+ *   matrix == NULL: out[i] = scale * sum_w sum_j kappa(r^2_w(i,j)) v[j]   (i < Na, j < Nb)
+ *   matrix != NULL: matrix[i*Nb + j] = scale * sum_w kappa(r^2_w(i,j))   (dense_matrix; P <= 64)
+ * r^2_w over the window's columns in ascending order (kernels.py:92-98).
+ *   Xa, Xb  device row-major feature matrices (eval / train rows; same pointer for K v)
+ *   q, cols host window lengths and 0-based columns (as ak_geom_create)
+ */
+#define AK_FAMILY_GAUSS         0
+#define AK_FAMILY_DER_GAUSS     1
+#define AK_FAMILY_MATERN12      2
+#define AK_FAMILY_DER_MATERN12  3
+int ak_dense_apply(int32_t family, double ell, double scale, int32_t P, const int32_t* q,
+                   const int32_t* cols, const double* Xa, int64_t Na, int64_t lda,
+                   const double* Xb, int64_t Nb, int64_t ldb, const double* v,
+                   double* out, double* matrix, void* stream);
 
 /* FP64 FMA throughput probe (roofline denominator; MEASURED_PEAKS.json has no FP64 entry).
  * Runs `iters` dependent-chain-free DFMA loops on all SMs; returns achieved TFLOP/s. */

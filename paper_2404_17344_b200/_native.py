@@ -27,6 +27,7 @@ AK_ERR_UNSUPPORTED = -6
 AK_APPLY_ACCUMULATE = 1
 AK_APPLY_SPREAD_ONLY = 2
 AK_APPLY_FROM_GRIDS = 4
+AK_APPLY_H_PER_RHS = 8
 
 AK_MAX_TAPS = 16
 AK_MAX_PAIRS = 8
@@ -38,8 +39,10 @@ EXPORTED = (
     "ak_geom_create", "ak_geom_destroy", "ak_geom_num_points", "ak_geom_num_windows",
     "ak_geom_num_items", "ak_geom_grid_elems", "ak_geom_canon_offset", "ak_geom_canon_total",
     "ak_spread", "ak_interp", "ak_op_create", "ak_op_destroy", "ak_op_apply", "ak_op_grids",
-    "ak_type1_band", "ak_type2_grid", "ak_probe_fp64", "ak_probe_dmma",
+    "ak_type1_band", "ak_type2_grid", "ak_dense_apply", "ak_probe_fp64", "ak_probe_dmma",
 )
+
+FAMILY_CODE = {"gauss": 0, "der_gauss": 1, "matern12": 2, "der_matern12": 3}
 
 
 class WindowFn(ctypes.Structure):
@@ -81,6 +84,8 @@ def _declare(lib: ctypes.CDLL) -> None:
                                  _i32, _vp]),
         "ak_type1_band": (_c_int, [_i32, _i32, _i32, _dp, _dp, _dp, _dp, _vp]),
         "ak_type2_grid": (_c_int, [_i32, _i32, _i32, _dp, _dp, _dp, _dp, _vp]),
+        "ak_dense_apply": (_c_int, [_i32, ctypes.c_double, ctypes.c_double, _i32, ctypes.POINTER(_i32),
+                                    ctypes.POINTER(_i32), _dp, _i64, _i64, _dp, _i64, _i64, _dp, _dp, _dp, _vp]),
         "ak_probe_fp64": (_c_int, [_i64, _vp, ctypes.POINTER(ctypes.c_double)]),
         "ak_probe_dmma": (_c_int, [_i64, _vp, ctypes.POINTER(ctypes.c_double)]),
     }

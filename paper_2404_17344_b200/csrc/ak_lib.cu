@@ -56,6 +56,9 @@ static int fail(int code, const std::string& msg) {
         if (rc_ != AK_OK) return rc_; \
     } while (0)
 
+int ak_internal_fail(int code, const char* msg) { return fail(code, msg); }
+void ak_internal_count(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
 static int launched() {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
@@ -727,7 +730,7 @@ extern "C" int ak_interp(const ak_geom* g, const double* grids, int32_t R, const
 // Y2 = H (compact band multiplier of the window) * Y on the band, 0 elsewhere.
 __global__ void k_band_multiply(const double2* __restrict__ Y, double2* __restrict__ Y2, int q, int n, int m,
                                 int R, int64_t hs, int64_t total, const int* __restrict__ gwin,
-                                const double* const* __restrict__ H, int hbase)
+                                const double* const* __restrict__ H, int hbase, int P, int per_rhs)
 {
     const int nh = n / 2 + 1, mh = m / 2;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
@@ -756,11 +759,12 @@ __global__ void k_band_multiply(const double2* __restrict__ Y, double2* __restri
         double2 out = make_double2(0.0, 0.0);
         if (in) {
             const int w = gwin[b / R];
+            const int hsel = per_rhs ? (int)(b % R) * P + w : hbase + w;
             int64_t ci;
             if (q == 3) ci = ((int64_t)b0 * m + b1) * mh + k2;
             else if (q == 2) ci = (int64_t)b1 * mh + k2;
             else ci = k2;
-            const double h = H[hbase + w][ci];
+            const double h = H[hsel][ci];
             const double2 y = Y[e];
             out = make_double2(h * y.x, h * y.y);
         }
@@ -887,6 +891,7 @@ extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double
     if (flags & AK_APPLY_SPREAD_ONLY) return AK_OK;
     if (!H || !scale || !outs || !sum_windows) return fail(AK_ERR_INVALID, "null argument");
     if (ldo < gi->N) return fail(AK_ERR_INVALID, "leading dimension too small");
+    if ((flags & AK_APPLY_H_PER_RHS) && op->C != 1) return fail(AK_ERR_INVALID, "per-RHS multipliers need C == 1");
     for (int c = 0; c < op->C; ++c) {
         if (!outs[c]) return fail(AK_ERR_INVALID, "null output");
         if (!accumulate) {
@@ -907,7 +912,8 @@ extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double
             const int64_t total = op->hs[q] * R * op->nwin[q];
             const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
             k_band_multiply<<<blocks, 256, 0, st>>>(op->spec + op->spec_off[q], op->spec2 + op->spec_off[q], q, gs->n,
-                                                    op->m, R, op->hs[q], total, op->gwin_d[q], H, c * P);
+                                                    op->m, R, op->hs[q], total, op->gwin_d[q], H, c * P, P,
+                                                    (flags & AK_APPLY_H_PER_RHS) ? 1 : 0);
             AK_TRY(launched());
             AK_CUFFT(cufftSetStream(op->inv[q], st));
             AK_CUFFT(cufftExecZ2D(op->inv[q], (cufftDoubleComplex*)(op->spec2 + op->spec_off[q]), op->gbuf + op->grid_off[q]));

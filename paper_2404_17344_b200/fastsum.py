@@ -117,19 +117,22 @@ class _Operator:
     """ak_op + its coefficient sets: C sets x P windows of (H, scale)."""
 
     def __init__(self, gs: DeviceGeometry, gi: DeviceGeometry, m: int, R: int,
-                 H_host: list, scales: list):
+                 H_host: list, scales: list, per_rhs: bool = False):
         torch = _torch()
         lib = _native.lib()
         self._lib = lib
         P = gs.n_windows
         C = len(H_host)
         self.R, self.C, self.P, self.m = R, C, P, m
+        self.per_rhs = per_rhs
+        if per_rhs and (C != 1 or len(H_host[0]) != R * P):
+            raise ValueError("per-RHS multipliers need one set of R*P tables")
         self.gs, self.gi = gs, gi  # keep geometries alive
         uniq = {}
         self._H = []
         ptrs = []
         for c in range(C):
-            for w in range(P):
+            for w in range(len(H_host[c])):
                 arr = H_host[c][w]
                 key = id(arr)
                 if key not in uniq:
@@ -150,6 +153,8 @@ class _Operator:
         sw = (ctypes.c_int32 * C)(*[1 if s else 0 for s in sum_windows])
         ldo = int(outs[0].shape[-1])
         f = flags | (_native.AK_APPLY_ACCUMULATE if accumulate else 0)
+        if self.per_rhs:
+            f |= _native.AK_APPLY_H_PER_RHS
         vptr = V.data_ptr() if V is not None else 0
         ldv = int(V.shape[-1]) if V is not None else self.gs.n_points
         rc = self._lib.ak_op_apply(self._handle, vptr, ldv, self.hptr.data_ptr(), self.scale.data_ptr(), optrs, ldo,

@@ -89,3 +89,80 @@ def eval_kernel(spec: KernelSpec, arg: float) -> float:
         raise ValueError("distance argument must be nonnegative")
     r2 = arg if spec.family in (GAUSS, DER_GAUSS) else arg * arg
     return float(radial_profile(spec.family, spec.ell, r2))
+
+
+# ---------------------------------------------------------------------------
+# exact dense products on the GPU (kernels.py:92-170 of the reference)
+
+
+def _check_limit(*sizes) -> None:
+    from .errors import DenseLimitExceededError
+
+    for n in sizes:
+        if n > DENSE_ROW_LIMIT:
+            raise DenseLimitExceededError(f"{n} rows exceeds the dense limit of {DENSE_ROW_LIMIT}")
+
+
+def _dense(spec: KernelSpec, ws, Xa, Xb, v=None, matrix=False):
+    import ctypes
+
+    import torch
+
+    from . import _native
+    from .nufft import _stream_ptr, _torch
+
+    _torch()
+    lib = _native.lib()
+    A = torch.as_tensor(np.ascontiguousarray(Xa, dtype=np.float64), device="cuda")
+    B = A if Xb is Xa else torch.as_tensor(np.ascontiguousarray(Xb, dtype=np.float64), device="cuda")
+    P = len(ws)
+    q = (ctypes.c_int32 * P)(*ws.lengths)
+    flat = []
+    for w in ws:
+        c = ws.columns(w)
+        flat.extend(c + [0] * (3 - len(c)))
+    cols = (ctypes.c_int32 * (3 * P))(*flat)
+    fam = _native.FAMILY_CODE[spec.family]
+    scale = spec.operator_scale()
+    st = _stream_ptr(torch)
+    if matrix:
+        M = torch.empty((A.shape[0], B.shape[0]), dtype=torch.float64, device="cuda")
+        _native.check(lib.ak_dense_apply(fam, spec.ell, scale, P, q, cols, A.data_ptr(), A.shape[0], A.shape[1],
+                                         B.data_ptr(), B.shape[0], B.shape[1], 0, 0, M.data_ptr(), st),
+                      "ak_dense_apply")
+        return M.cpu().numpy()
+    vd = torch.as_tensor(np.ascontiguousarray(v, dtype=np.float64), device="cuda")
+    out = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+    _native.check(lib.ak_dense_apply(fam, spec.ell, scale, P, q, cols, A.data_ptr(), A.shape[0], A.shape[1],
+                                     B.data_ptr(), B.shape[0], B.shape[1], vd.data_ptr(), out.data_ptr(), 0, st),
+                  "ak_dense_apply")
+    return out.cpu().numpy()
+
+
+def dense_matvec(spec: KernelSpec, ws, X, v) -> np.ndarray:
+    """Exact sigma_f^2 * pre * sum_s K_s v on the GPU (reference kernels.py:123-137)."""
+    v = np.asarray(v, dtype=np.float64)
+    if v.shape != (X.n_rows,):
+        raise ValueError("vector length must equal the number of rows")
+    _check_limit(X.n_rows)
+    return _dense(spec, ws, X.features, X.features, v)
+
+
+def dense_cross_matvec(spec: KernelSpec, ws, X_eval, X_train, v) -> np.ndarray:
+    """K(X_eval, X_train) v with dense_matvec's scaling (reference kernels.py:140-151)."""
+    v = np.asarray(v, dtype=np.float64)
+    if v.shape != (X_train.n_rows,):
+        raise ValueError("vector length must equal the number of training rows")
+    _check_limit(X_eval.n_rows, X_train.n_rows)
+    return _dense(spec, ws, X_eval.features, X_train.features, v)
+
+
+def dsigma_matvec(spec: KernelSpec, ws, X, v) -> np.ndarray:
+    """(dK/d sigma_f) v = (2/sigma_f) K v of the base family (reference kernels.py:154-156)."""
+    return (2.0 / spec.sigma_f) * dense_matvec(spec.base(), ws, X, v)
+
+
+def dense_matrix(spec: KernelSpec, ws, X) -> np.ndarray:
+    """The full operator (diagnostics, small N; reference kernels.py:159-170)."""
+    _check_limit(X.n_rows)
+    return _dense(spec, ws, X.features, X.features, matrix=True)

@@ -1,0 +1,352 @@
+"""CG kernel ridge regression on the GPU operator (the first caller of the hot path).
+
+Mirrors ``addkern.solver`` (/root/reference/pkg/src/addkern/solver.py):
+``cg_solve`` (:43-80, unpreconditioned CG on (A + beta I) v = y, relative
+residual tolerance, CgBreakdownError / MaxIterationsError), ``krr_fit``
+(:99-120), ``krr_predict`` (:123-132) and ``grid_search`` (:157-198).
+
+Differences in where the work runs, not in what is computed:
+* vectors stay on the device (torch) for the fast-summation backend; each CG
+  iteration is one ``ak_op_apply`` plus a few vector ops and one host read of
+  the residual norm (the reference's per-iteration stopping test);
+* ``grid_search`` runs all (ell, beta) cells' CG iterations in lockstep as ONE
+  batched operator over a single bin-sorted geometry: right-hand side r of the
+  batch is cell r's search direction and uses cell r's band multiplier
+  (``AK_APPLY_H_PER_RHS``).  The reference rebuilds the plan for every cell
+  (solver.py:179-183) although the geometry does not depend on ell or beta.
+  Converged or failed cells are frozen, so every cell performs exactly the
+  iterations a standalone ``krr_fit`` would.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .dataset import PRESCALED, Dataset, same_scaling
+from .errors import CgBreakdownError, InvalidScalingError, MaxIterationsError, ScalingMismatchError
+from .kernels import KernelSpec, dense_cross_matvec, dense_matvec
+from .windows import WindowSet
+
+DEFAULT_CG_TOL = 1e-3
+DEFAULT_CG_MAX_ITER = 5000
+
+DENSE = "dense"
+FASTSUM = "fastsum"
+
+
+def rmse(y_true, y_pred) -> float:
+    a = np.asarray(y_true, dtype=np.float64).ravel()
+    b = np.asarray(y_pred, dtype=np.float64).ravel()
+    return float(np.sqrt(np.mean((a - b) ** 2)))
+
+
+def default_sigma_f(n_windows: int) -> float:
+    """sigma_f = sqrt(1/P) normalises the additive kernel's diagonal to 1 (solver.py:38-40)."""
+    return math.sqrt(1.0 / n_windows)
+
+
+def _is_tensor(x) -> bool:
+    try:
+        import torch
+
+        return isinstance(x, torch.Tensor)
+    except ImportError:  # pragma: no cover
+        return False
+
+
+def cg_solve(matvec, y, beta: float, tol: float = DEFAULT_CG_TOL, max_iter: int = DEFAULT_CG_MAX_ITER,
+             callback=None):
+    """Solve (A + beta I) v = y, A symmetric PSD; returns (v, iterations) (solver.py:43-80).
+
+    ``y`` may be a numpy vector (matvec maps numpy -> numpy) or a torch CUDA
+    tensor (matvec maps tensors -> tensors; every vector stays on the device).
+    """
+    if _is_tensor(y):
+        import torch
+
+        dot = lambda a, b: float(torch.dot(a, b))
+        norm = lambda a: float(torch.linalg.vector_norm(a))
+        y = y.to(torch.float64)
+        x = torch.zeros_like(y)
+        copy = torch.clone
+    else:
+        y = np.asarray(y, dtype=np.float64)
+        dot = lambda a, b: float(a @ b)
+        norm = lambda a: float(np.linalg.norm(a))
+        x = np.zeros_like(y)
+        copy = np.copy
+    y_norm = norm(y)
+    if y_norm == 0.0:
+        return x, 0
+    r = copy(y)
+    p = copy(r)
+    rs = dot(r, r)
+    if callback is not None:
+        callback(math.sqrt(rs))
+    if math.sqrt(rs) <= tol * y_norm:
+        return x, 0
+    for it in range(1, max_iter + 1):
+        Ap = matvec(p) + beta * p
+        pAp = dot(p, Ap)
+        if pAp <= 0.0:
+            raise CgBreakdownError(f"p^T A p = {pAp:.3e} <= 0 at iteration {it}")
+        alpha = rs / pAp
+        x += alpha * p
+        r -= alpha * Ap
+        rs_new = dot(r, r)
+        if callback is not None:
+            callback(math.sqrt(rs_new))
+        if math.sqrt(rs_new) <= tol * y_norm:
+            return x, it
+        p = r + (rs_new / rs) * p
+        rs = rs_new
+    raise MaxIterationsError(f"CG did not reach tol={tol} within {max_iter} iterations")
+
+
+@dataclass(frozen=True)
+class KrrModel:
+    """Fitted ridge-regression state (solver.py:83-96)."""
+
+    spec: KernelSpec
+    window_set: WindowSet
+    beta: float
+    backend: str
+    preset: object
+    coefficients: np.ndarray
+    train: Dataset
+    cg_iterations: int
+    residual: float
+    plan: object = field(default=None, repr=False, compare=False)
+
+
+def krr_fit(train: Dataset, ws: WindowSet, spec: KernelSpec, beta: float, backend: str = FASTSUM,
+            preset="default", tol: float = DEFAULT_CG_TOL, max_iter: int = DEFAULT_CG_MAX_ITER) -> KrrModel:
+    """Solve (K + beta I) v = y on the training set (solver.py:99-120)."""
+    if train.scaling_state != PRESCALED:
+        raise InvalidScalingError("krr_fit requires prescaled training data")
+    log = []
+    plan = None
+    if backend == FASTSUM:
+        import torch
+
+        from .fastsum import build_plan, fast_matvec
+
+        plan = build_plan(spec, ws, preset, train)
+        y = torch.as_tensor(train.targets, device="cuda")
+        v, iters = cg_solve(lambda p: fast_matvec(plan, p), y, beta, tol=tol, max_iter=max_iter,
+                            callback=log.append)
+        coef = v.cpu().numpy()
+    elif backend == DENSE:
+        coef, iters = cg_solve(lambda p: dense_matvec(spec, ws, train, p), train.targets, beta, tol=tol,
+                               max_iter=max_iter, callback=log.append)
+    else:
+        raise ValueError(f"unknown backend {backend!r}")
+    y_norm = float(np.linalg.norm(train.targets))
+    residual = log[-1] / y_norm if y_norm > 0 else 0.0
+    return KrrModel(spec=spec, window_set=ws, beta=beta, backend=backend, preset=preset, coefficients=coef,
+                    train=train, cg_iterations=iters, residual=float(residual), plan=plan)
+
+
+def krr_predict(model: KrrModel, test: Dataset) -> np.ndarray:
+    """h(x') = sum_j v_j kappa(x', x_j) through the fitted backend (solver.py:123-132)."""
+    if test.scaling_state != PRESCALED or not same_scaling(model.train, test):
+        raise ScalingMismatchError("test data must be prescaled with the training maps")
+    if model.backend == DENSE:
+        return dense_cross_matvec(model.spec, model.window_set, test, model.train, model.coefficients)
+    from .fastsum import fast_cross_matvec, prepare_eval_points
+
+    geoms = prepare_eval_points(model.plan, test)
+    return fast_cross_matvec(model.plan, geoms, model.coefficients, test.n_rows)
+
+
+@dataclass(frozen=True)
+class GridCell:
+    ell: float
+    beta: float
+    rmse: float | None
+    cg_iterations: int | None
+    fit_seconds: float
+    predict_seconds: float
+    failed: bool = False
+    message: str = ""
+
+
+@dataclass(frozen=True)
+class GridSearchResult:
+    cells: tuple
+    best: GridCell
+
+    @property
+    def best_pair(self) -> tuple:
+        return self.best.ell, self.best.beta
+
+
+def _grid_operator(plan, specs, R, interp_geom=None):
+    """One batched operator whose RHS r uses cell r's band multiplier."""
+    from .fastsum import _Operator, band_multiplier, kernel_coefficients
+
+    per_q = {}
+    H = []
+    for spec in specs:
+        for w in plan.window_set:
+            q = len(w)
+            key = (spec.family, spec.ell, q)
+            if key not in per_q:
+                per_q[key] = band_multiplier(kernel_coefficients(spec.family, spec.ell, q, plan.m),
+                                             plan.nufft_plans[q])
+            H.append(per_q[key])
+    scales = [specs[0].operator_scale()] * len(plan.window_set)
+    gi = interp_geom if interp_geom is not None else plan.geometries
+    return _Operator(plan.geometries, gi, plan.m, R, [H], [scales], per_rhs=True)
+
+
+def cg_solve_batched(apply, Y, betas, tol: float = DEFAULT_CG_TOL, max_iter: int = DEFAULT_CG_MAX_ITER):
+    """Lockstep CG for R independent systems (A_r + beta_r I) x_r = y_r on the device.
+
+    ``apply`` maps an (R, N) tensor of directions to (A_r p_r)_r.  Returns
+    (X, iterations, messages); iterations[r] = -1 for a failed system, whose
+    message says why.  Each system follows exactly the iteration of cg_solve.
+    """
+    import torch
+
+    R, N = Y.shape
+    betas = torch.as_tensor(np.asarray(betas, dtype=np.float64), device=Y.device).reshape(R, 1)
+    X = torch.zeros_like(Y)
+    Rr = Y.clone()
+    P = Rr.clone()
+    ynorm = torch.linalg.vector_norm(Y, dim=1)
+    rs = (Rr * Rr).sum(dim=1)
+    iters = np.full(R, -1, dtype=np.int64)
+    msgs = [""] * R
+    yn = ynorm.cpu().numpy()
+    rs_h = rs.cpu().numpy()
+    active = np.ones(R, dtype=bool)
+    for r in range(R):
+        if yn[r] == 0.0 or math.sqrt(rs_h[r]) <= tol * yn[r]:
+            iters[r] = 0
+            active[r] = False
+    act = torch.as_tensor(active, device=Y.device)
+    P[~act] = 0.0
+    for it in range(1, max_iter + 1):
+        if not active.any():
+            break
+        AP = apply(P) + betas * P
+        pAp = (P * AP).sum(dim=1)
+        pAp_h = pAp.cpu().numpy()
+        for r in np.nonzero(active)[0]:
+            if pAp_h[r] <= 0.0:
+                msgs[r] = f"p^T A p = {pAp_h[r]:.3e} <= 0 at iteration {it}"
+                active[r] = False
+        act = torch.as_tensor(active, device=Y.device)
+        alpha = torch.where(act, rs / torch.where(act, pAp, torch.ones_like(pAp)), torch.zeros_like(rs))
+        X += alpha.reshape(R, 1) * P
+        Rr -= alpha.reshape(R, 1) * AP
+        rs_new = (Rr * Rr).sum(dim=1)
+        rs_new_h = rs_new.cpu().numpy()
+        for r in np.nonzero(active)[0]:
+            if math.sqrt(rs_new_h[r]) <= tol * yn[r]:
+                iters[r] = it
+                active[r] = False
+        act = torch.as_tensor(active, device=Y.device)
+        ratio = torch.where(act, rs_new / torch.where(act, rs, torch.ones_like(rs)), torch.zeros_like(rs))
+        P = torch.where(act.reshape(R, 1), Rr + ratio.reshape(R, 1) * P, torch.zeros_like(P))
+        rs = torch.where(act, rs_new, rs)
+    for r in np.nonzero(active)[0]:
+        msgs[r] = f"CG did not reach tol={tol} within {max_iter} iterations"
+    return X, iters, msgs
+
+
+def grid_search(train: Dataset, test: Dataset, ws: WindowSet, ell_grid, beta_grid, family: str = "gauss",
+                backend: str = FASTSUM, preset="default", sigma_f: float | None = None,
+                tol: float = DEFAULT_CG_TOL, max_iter: int = DEFAULT_CG_MAX_ITER) -> GridSearchResult:
+    """Fit and score every (ell, beta) pair; ties favour small ell, beta (solver.py:157-198).
+
+    ell values are in quarter-box units (rescaled by 1/sqrt(d_max) internally).
+    With the fast-summation backend all cells run as one batched lockstep CG.
+    """
+    ell_grid = [float(e) for e in ell_grid]
+    beta_grid = [float(b) for b in beta_grid]
+    if not ell_grid or not beta_grid:
+        raise ValueError("grids must be nonempty")
+    if train.d_max is None:
+        raise InvalidScalingError("training data must be prescaled")
+    factor = 1.0 / math.sqrt(train.d_max)
+    sf = default_sigma_f(len(ws)) if sigma_f is None else sigma_f
+    pairs = [(e, b) for e in ell_grid for b in beta_grid]
+    if backend != FASTSUM:
+        return _grid_search_sequential(train, test, ws, pairs, family, backend, preset, sf, tol, max_iter, factor)
+
+    import torch
+
+    from .fastsum import build_plan, prepare_eval_points
+
+    if train.scaling_state != PRESCALED:
+        raise InvalidScalingError("krr_fit requires prescaled training data")
+    if test.scaling_state != PRESCALED or not same_scaling(train, test):
+        raise ScalingMismatchError("test data must be prescaled with the training maps")
+    specs = [KernelSpec(family, e * factor, sf) for e, _ in pairs]
+    t0 = time.perf_counter()
+    with warnings.catch_warnings(record=True) as caught:
+        warnings.simplefilter("always")
+        plan = build_plan(specs[0], ws, preset, train)
+        from .fastsum import _eta_warning
+
+        for s in specs[1:]:
+            _eta_warning(s.ell, plan.m)
+    for w in caught:
+        warnings.warn_explicit(w.message, w.category, w.filename, w.lineno)
+    R = len(pairs)
+    op = _grid_operator(plan, specs, R)
+
+    def apply(Pm):
+        out = torch.empty_like(Pm)
+        op.apply(Pm.contiguous(), [out], [True])
+        return out
+
+    Y = torch.as_tensor(np.broadcast_to(train.targets, (R, train.n_rows)).copy(), device="cuda")
+    X, iters, msgs = cg_solve_batched(apply, Y, [b for _, b in pairs], tol=tol, max_iter=max_iter)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    geoms = prepare_eval_points(plan, test)
+    pop = _grid_operator(plan, specs, R, interp_geom=geoms)
+    pred = torch.empty((R, test.n_rows), dtype=torch.float64, device="cuda")
+    pop.apply(X.contiguous(), [pred], [True])
+    pred_h = pred.cpu().numpy()
+    t2 = time.perf_counter()
+    cells = []
+    for r, (e, b) in enumerate(pairs):
+        if iters[r] < 0:
+            cells.append(GridCell(e, b, None, None, (t1 - t0) / R, 0.0, failed=True, message=msgs[r]))
+        else:
+            cells.append(GridCell(e, b, rmse(test.targets, pred_h[r]), int(iters[r]), (t1 - t0) / R, (t2 - t1) / R))
+    ok = [c for c in cells if not c.failed]
+    if not ok:
+        raise MaxIterationsError("every grid cell failed")
+    best = min(ok, key=lambda c: (c.rmse, c.ell, c.beta))
+    return GridSearchResult(cells=tuple(cells), best=best)
+
+
+def _grid_search_sequential(train, test, ws, pairs, family, backend, preset, sf, tol, max_iter, factor):
+    cells = []
+    for e, b in pairs:
+        spec = KernelSpec(family, e * factor, sf)
+        t0 = time.perf_counter()
+        try:
+            model = krr_fit(train, ws, spec, b, backend=backend, preset=preset, tol=tol, max_iter=max_iter)
+        except (MaxIterationsError, CgBreakdownError) as exc:
+            cells.append(GridCell(e, b, None, None, time.perf_counter() - t0, 0.0, failed=True, message=str(exc)))
+            continue
+        t1 = time.perf_counter()
+        pred = krr_predict(model, test)
+        t2 = time.perf_counter()
+        cells.append(GridCell(e, b, rmse(test.targets, pred), model.cg_iterations, t1 - t0, t2 - t1))
+    ok = [c for c in cells if not c.failed]
+    if not ok:
+        raise MaxIterationsError("every grid cell failed")
+    best = min(ok, key=lambda c: (c.rmse, c.ell, c.beta))
+    return GridSearchResult(cells=tuple(cells), best=best)

@@ -1,0 +1,143 @@
+"""GPU: exact dense products (K5) and the CG / KRR / grid-search caller of the
+hot path against the reference's golden outputs."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel, windows_of
+
+pytestmark = pytest.mark.gpu
+
+
+def _ds(X, y, d_max):
+    from paper_2404_17344_b200.dataset import PRESCALED, Dataset
+
+    return Dataset(X, y, tuple(f"x{i + 1}" for i in range(X.shape[1])), scaling_state=PRESCALED, d_max=int(d_max))
+
+
+def _ws(g):
+    from paper_2404_17344_b200.windows import WindowSet
+
+    return WindowSet(tuple(tuple(int(c) for c in row[:q]) for row, q in zip(g["windows"], g["lengths"])),
+                     d_max=int(g["d_max"]))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c4"])
+def test_dense_matches_reference(cuda, name):
+    from paper_2404_17344_b200.kernels import KernelSpec, dense_matvec, dsigma_matvec
+
+    g = golden(name)
+    ds = _ds(g["X"], np.zeros(g["X"].shape[0]), g["d_max"])
+    spec = KernelSpec(str(g["families"][0]), float(g["ells"][0]), float(g["sigma_f"]))
+    assert rel(dense_matvec(spec, _ws(g), ds, g["V"][0]), g["K_dense"][0]) <= 1e-12
+    if "dK_dell_dense" in g:
+        dspec = KernelSpec("der_" + spec.family, spec.ell, spec.sigma_f)
+        assert rel(dense_matvec(dspec, _ws(g), ds, g["V"][0]), g["dK_dell_dense"][0]) <= 1e-12
+    assert rel(dsigma_matvec(spec, _ws(g), ds, g["V"][0]), (2.0 / spec.sigma_f) * g["K_dense"][0]) <= 1e-12
+
+
+def test_dense_cross_matrix_and_limits(cuda):
+    from paper_2404_17344_b200.errors import DenseLimitExceededError
+    from paper_2404_17344_b200.kernels import FAMILIES, KernelSpec, dense_cross_matvec, dense_matrix, dense_matvec
+
+    g = golden("cross")
+    ws = _ws({"windows": np.array([[1, 2, 0], [3, 4, 0]]), "lengths": np.array([2, 2]), "d_max": 2})
+    tr = _ds(g["Xtr"], np.zeros(150), 2)
+    te = _ds(g["Xte"], np.zeros(80), 2)
+    spec = KernelSpec("gauss", 1.0 / np.sqrt(2.0))
+    assert rel(dense_cross_matvec(spec, ws, te, tr, g["v"]), g["dense"]) <= 1e-12
+    for fam in FAMILIES:
+        s = KernelSpec(fam, 0.6)
+        K = dense_matrix(s, ws, tr)
+        np.testing.assert_array_equal(K, K.T)
+        assert rel(K @ g["v"], dense_matvec(s, ws, tr, g["v"])) <= 1e-13
+    big = _ds(np.zeros((20001, 2)), np.zeros(20001), 1)
+    with pytest.raises(DenseLimitExceededError):
+        dense_matvec(KernelSpec("gauss", 1.0), _ws({"windows": np.array([[1, 0, 0]]), "lengths": np.array([1]),
+                                                    "d_max": 1}), big, np.zeros(20001))
+
+
+def test_c2_full_size_fast_vs_dense(cuda):
+    """Config 2 at its full N = 20,000 (the dense limit): both fast products within the
+    Fourier error the reference shows for this setup (rel 3.2e-3 / 1.3e-2 measured in the survey)."""
+    from paper_2404_17344_b200 import configs
+    from paper_2404_17344_b200.fastsum import build_plan, fast_matvecs
+    from paper_2404_17344_b200.kernels import KernelSpec, dense_matvec
+
+    wl = configs.config2()
+    plan = build_plan(wl.spec, wl.window_set, "default", wl.data)
+    res = fast_matvecs(plan, wl.V[0], dell=True, dsigma=True)
+    dK = dense_matvec(wl.spec, wl.window_set, wl.data, wl.V[0])
+    ddK = dense_matvec(KernelSpec("der_matern12", wl.spec.ell, 1.0), wl.window_set, wl.data, wl.V[0])
+    assert rel(res["K"], dK) < 1e-2
+    assert rel(res["dK_dell"], ddK) < 5e-2
+    assert rel(res["dK_dsigma"], 2.0 * dK) < 1e-2
+
+
+def test_krr_fit_predict_match_reference(cuda):
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.solver import krr_fit, krr_predict
+    from paper_2404_17344_b200.windows import WindowSet
+
+    g = golden("solver")
+    tr = _ds(g["Xtr"], g["ytr"], 2)
+    te = _ds(g["Xte"], g["yte"], 2)
+    ws = WindowSet(((1, 2), (3, 4), (5, 6)), d_max=2)
+    spec = KernelSpec("gauss", 0.6 / math.sqrt(2), math.sqrt(1 / 3))
+    model = krr_fit(tr, ws, spec, 0.05)
+    # Same iteration count.  CG (ridge 0.05, 19 iterations) amplifies the ~1e-14
+    # run-to-run differences of atomically accumulated matvecs to 1e-7..1e-5 in
+    # the iterate, still two orders below the solve's own 1e-3 tolerance.
+    assert model.cg_iterations == int(g["iters"])
+    assert rel(model.coefficients, g["coef"]) <= 1e-4
+    assert model.residual <= 1e-3 and abs(model.residual / float(g["residual"]) - 1.0) < 0.05
+    # prediction is one cross product: with the reference's coefficients it matches tightly
+    from dataclasses import replace
+
+    ref_model = replace(model, coefficients=g["coef"])
+    assert rel(krr_predict(ref_model, te), g["pred"]) <= 1e-10
+    assert rel(krr_predict(model, te), g["pred"]) <= 1e-4
+    dense = krr_fit(tr, ws, spec, 0.05, backend="dense")
+    assert rel(dense.coefficients, model.coefficients) < 0.1
+
+
+def test_grid_search_batched_matches_reference(cuda):
+    from paper_2404_17344_b200.solver import grid_search
+    from paper_2404_17344_b200.windows import WindowSet
+
+    g = golden("solver")
+    tr = _ds(g["Xtr"], g["ytr"], 2)
+    te = _ds(g["Xte"], g["yte"], 2)
+    ws = WindowSet(((1, 2), (3, 4), (5, 6)), d_max=2)
+    res = grid_search(tr, te, ws, [0.5, 1.0, 2.0], [0.01, 0.1])
+    # long solves (56 iterations at ridge 0.01) may stop one iteration apart: the
+    # relative-residual test sits on a cancellation-dominated number (see krr test)
+    its = np.array([c.cg_iterations for c in res.cells])
+    assert np.all(np.abs(its - g["grid_iters"]) <= np.maximum(1, 0.02 * g["grid_iters"]))
+    np.testing.assert_allclose([c.rmse for c in res.cells], g["grid_rmse"], rtol=1e-3)
+    assert tuple(res.best_pair) == tuple(g["best"])
+
+
+def test_cg_solve_batched_equals_sequential(cuda):
+    import torch
+
+    from paper_2404_17344_b200.solver import cg_solve, cg_solve_batched
+
+    rng = np.random.default_rng(0)
+    A = rng.normal(size=(50, 50))
+    A = A @ A.T / 50
+    At = torch.as_tensor(A, device="cuda")
+    Y = torch.as_tensor(rng.normal(size=(3, 50)), device="cuda")
+    betas = [0.1, 1.0, 0.01]
+    X, iters, msgs = cg_solve_batched(lambda P: P @ At.T, Y, betas, tol=1e-8, max_iter=500)
+    for r in range(3):
+        x, it = cg_solve(lambda p: At @ p, Y[r], betas[r], tol=1e-8, max_iter=500)
+        # batched (GEMM) and single (GEMV) products round differently: allow one iteration
+        assert abs(it - iters[r]) <= 1 and msgs[r] == ""
+        xe = np.linalg.solve(A + betas[r] * np.eye(50), Y[r].cpu().numpy())
+        assert rel(X[r].cpu().numpy(), xe) <= 1e-6 and rel(x.cpu().numpy(), xe) <= 1e-6
+    # breakdown and iteration cap are reported per system, not raised
+    Xb, itb, mb = cg_solve_batched(lambda P: -P, Y[:2], [0.0, 0.0], tol=1e-8, max_iter=5)
+    assert list(itb) == [-1, -1] and all("<= 0" in m for m in mb)

@@ -103,3 +103,13 @@ def test_oracle_dense_known_answer():
     X = np.array([[0.01, -0.02, 0.03, 0.0, 0.1, -0.1]])
     out = R.dense_matvec("gauss", 1.0, 2.0, [(0, 1, 2), (3, 4, 5)], X, np.array([3.0]))
     assert abs(out[0] - 4.0 * 2 * 3.0) < 1e-12
+
+
+def test_oracle_cg_matches_reference_krr():
+    """krr_fit (solver.py:99-120) restated: same CG iterations, same coefficients."""
+    g = golden("solver")
+    sf = math.sqrt(1 / 3)
+    fs = R.FastSum("gauss", 0.6 / math.sqrt(2), sf, [(0, 1), (2, 3), (4, 5)], g["Xtr"])
+    x, it = R.cg_solve(fs.matvec, g["ytr"], 0.05)
+    assert it == int(g["iters"])
+    assert rel(x, g["coef"]) <= 1e-10
