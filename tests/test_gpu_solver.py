@@ -141,3 +141,25 @@ def test_cg_solve_batched_equals_sequential(cuda):
     # breakdown and iteration cap are reported per system, not raised
     Xb, itb, mb = cg_solve_batched(lambda P: -P, Y[:2], [0.0, 0.0], tol=1e-8, max_iter=5)
     assert list(itb) == [-1, -1] and all("<= 0" in m for m in mb)
+
+
+def test_gsi_matches_reference(cuda):
+    from paper_2404_17344_b200.fastsum import build_plan
+    from paper_2404_17344_b200.gsi import compute_gsi, gsi_pipeline, select_windows_by_gsi
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    g = golden("solver")
+    gg = golden("gsi")
+    tr = _ds(g["Xtr"], g["ytr"], 2)
+    ws = WindowSet(((1, 2), (3, 4), (5, 6)), d_max=2)
+    plan = build_plan(KernelSpec("gauss", 0.6 / math.sqrt(2), math.sqrt(1 / 3)), ws, "default", tr)
+    rep = compute_gsi(plan, g["coef"])
+    got = np.array([rep.thetas[tuple(int(x) for x in k.split(","))] for k in gg["keys"]])
+    assert rel(got, gg["thetas"]) <= 1e-10
+    assert abs(rep.total_variance / float(gg["total"]) - 1) <= 1e-10
+    assert abs(sum(rep.indices.values()) - 1.0) < 1e-12
+    sel, rep2 = gsi_pipeline(tr, 2, ell_init=1.0, beta_init=0.1, gsi_score=0.9)
+    assert [",".join(map(str, w)) for w in sel.windows] == list(gg["pipeline_windows"])
+    with pytest.raises(ValueError):
+        select_windows_by_gsi(rep, 1.0)

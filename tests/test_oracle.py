@@ -113,3 +113,27 @@ def test_oracle_cg_matches_reference_krr():
     x, it = R.cg_solve(fs.matvec, g["ytr"], 0.05)
     assert it == int(g["iters"])
     assert rel(x, g["coef"]) <= 1e-10
+
+
+def test_oracle_gsi_matches_reference():
+    """compute_gsi (gsi.py:72-102) restated on the oracle's type-1 transforms."""
+    from itertools import product
+
+    g = golden("solver")
+    gg = golden("gsi")
+    sf = math.sqrt(1 / 3)
+    wins = [(0, 1), (2, 3), (4, 5)]
+    fs = R.FastSum("gauss", 0.6 / math.sqrt(2), sf, wins, g["Xtr"])
+    thetas = {}
+    nz = R.freqs(32) != 0
+    for k, w in enumerate(wins):
+        S = np.conj(R.type1(fs.plans[2], fs.geoms[k], g["coef"]))
+        power = np.abs(fs.tables[2] * S) ** 2
+        for pat in product((0, 1), repeat=2):
+            if not any(pat):
+                continue
+            mask = (nz if pat[0] else ~nz)[:, None] & (nz if pat[1] else ~nz)[None, :]
+            key = ",".join(str(w[a] + 1) for a in range(2) if pat[a])
+            thetas[key] = thetas.get(key, 0.0) + float(power[mask].sum())
+    got = np.array([thetas[k] for k in gg["keys"]])
+    assert rel(got, gg["thetas"]) <= 1e-12
