@@ -322,8 +322,11 @@ def run_ours(args):
 
     def step_e2e():
         if world > 1:
-            out = dplan.matvec(torch.as_tensor(v_host).pin_memory().cuda(non_blocking=True))
-            return out.cpu().numpy()
+            out = dplan.matvec(torch.as_tensor(v_host).cuda())
+            host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+            host.copy_(out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return host.numpy()
         return fast_matvec(plan, v_host)
 
     def step_deriv():
