@@ -93,6 +93,8 @@ struct ak_geom {
     bool cached = false;
     int batch3 = 16;
     int iwarps = 1;                     // warps per CTA of the cached q=3 interp
+    int swarps = 1;                     // warps per CTA of the cached q=3 spread
+    bool vreg = false;                  // RHS value folded in registers (vs a scaling pass)
     double* W3 = nullptr;               // [P3][N][3T]
     CellIdx* CI3 = nullptr;             // [P3][N]
     int64_t* wshift_d = nullptr;        // per window: (w - rank3(w)) * N
@@ -103,6 +105,12 @@ static bool weights_cached_default() {
     const char* e = getenv("AK_WEIGHTS");
     return !(e && strcmp(e, "horner") == 0);
 }
+// Work items sorted by size, largest first (AK_SORT_ITEMS=0 keeps creation order).
+static bool items_sorted_default() {
+    const char* e = getenv("AK_SORT_ITEMS");
+    return !(e && e[0] == '0');
+}
+
 // Points per staged batch of the cached-weight kernels (AK_BATCH3: 16 (default) or 32).
 static int batch3_default() {
     const char* e = getenv("AK_BATCH3");
@@ -114,10 +122,18 @@ static int batch3_default() {
 static int supercell3_default() {
     const char* e = getenv("AK_SUPERCELL3");
     const int v = e ? atoi(e) : 0;
-    return (v >= 2 && v <= 4) ? v : 3;
+    return (v >= 2 && v <= 4) ? v : 2;
 }
 
-static int chunk_for_q(int q) { return q == 3 ? 1024 : (q == 2 ? 4096 : 8192); }
+// Maximum points per work item (AK_CHUNK3 overrides the 3-D value).
+static int chunk_for_q(int q) {
+    if (q == 3) {
+        const char* e = getenv("AK_CHUNK3");
+        const int v = e ? atoi(e) : 0;
+        return (v >= 64 && v <= 65536) ? v : 2048;
+    }
+    return q == 2 ? 4096 : 8192;
+}
 
 __global__ void k_keys(const double* __restrict__ X, int64_t ld, int q, int c0, int c1, int c2, int n, int S,
                        int nsc, int64_t N, uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
@@ -315,6 +331,25 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
         }
         host_counter = hf[1];
         g->item_end[q] = host_counter;
+        // Largest items first (blocks are dispatched in index order: LPT-like tail).
+        const int64_t ni = g->item_end[q] - g->item_begin[q];
+        if (ni > 1 && items_sorted_default()) {
+            std::vector<WorkItem> h((size_t)ni);
+            if (cudaMemcpy(h.data(), g->items + g->item_begin[q], sizeof(WorkItem) * ni, cudaMemcpyDeviceToHost) !=
+                cudaSuccess) {
+                rc = fail(AK_ERR_CUDA, "item copy failed");
+                break;
+            }
+            std::stable_sort(h.begin(), h.end(), [](const WorkItem& a, const WorkItem& b) {
+                if (a.count != b.count) return a.count > b.count;
+                return a.start < b.start;
+            });
+            if (cudaMemcpy(g->items + g->item_begin[q], h.data(), sizeof(WorkItem) * ni, cudaMemcpyHostToDevice) !=
+                cudaSuccess) {
+                rc = fail(AK_ERR_CUDA, "item copy failed");
+                break;
+            }
+        }
     }
     g->nitems = host_counter;
     if (rc == AK_OK && g->wf.taps == 12 && !g->windows_of_q[3].empty() && N > 0 && weights_cached_default()) {
@@ -348,6 +383,10 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
         g->batch3 = batch3_default();
         const char* iw = getenv("AK_IWARPS");
         g->iwarps = (iw && atoi(iw) == 1) ? 1 : 2;
+        const char* sw = getenv("AK_SWARPS");
+        g->swarps = (sw && atoi(sw) == 2) ? 2 : 1;
+        const char* vr = getenv("AK_VREG");
+        g->vreg = vr && vr[0] == '1';
     }
     cudaStreamSynchronize(st);
     cudaFree(keys);
@@ -527,8 +566,12 @@ static void launch_spread3w_sb(const ak_geom* g, int64_t i0, int64_t ni, const d
                                double* grids, cudaStream_t st)
 {
     dim3 grid((unsigned)ni, (unsigned)R);
-    k_spread3w<12, S, B><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
-                                              g->canon_off_d, R, g->n);
+    if (g->vreg)
+        k_spread3w<12, S, B, true><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
+                                                        g->canon_off_d, R, g->n);
+    else
+        k_spread3w<12, S, B, false><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
+                                                         g->canon_off_d, R, g->n);
 }
 
 template <int B>
@@ -546,6 +589,24 @@ template <int T>
 static void launch_spread3_t(const ak_geom* g, int64_t i0, int64_t ni, const double* V, int R, int64_t ldv,
                              double* grids, cudaStream_t st)
 {
+    if (T == 12 && g->cached && g->swarps == 2) {
+        dim3 grid((unsigned)ni, (unsigned)R);
+        switch (g->sedge[3]) {
+            case 2:
+                k_spread3w2<12, 2><<<grid, 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
+                                                        g->canon_off_d, R, g->n);
+                break;
+            case 3:
+                k_spread3w2<12, 3><<<grid, 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
+                                                        g->canon_off_d, R, g->n);
+                break;
+            default:
+                k_spread3w2<12, 4><<<grid, 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
+                                                        g->canon_off_d, R, g->n);
+                break;
+        }
+        return;
+    }
     if (T == 12 && g->cached) {
         if (g->batch3 == 16) launch_spread3w_b<16>(g, i0, ni, V, R, ldv, grids, st);
         else launch_spread3w_b<32>(g, i0, ni, V, R, ldv, grids, st);
