@@ -277,6 +277,41 @@ def cpu_baseline(wl, gpu_window_out):
     return base, err
 
 
+def extra_workloads(torch, steps=5, warmup=2):
+    """Batched-RHS / derivative configurations (BASELINE configs 3 and 5) on one GPU:
+    device time per step of the whole product set the config asks for."""
+    from paper_2404_17344_b200 import configs
+    from paper_2404_17344_b200.fastsum import build_mixed_plan, build_plan, fast_matvecs, mixed_matvecs
+
+    out = {}
+    for name in ("C3", "C5"):
+        wl = configs.CONFIGS[name]()
+        t0 = time.perf_counter()
+        if wl.mixed:
+            plan = build_mixed_plan(wl.specs, wl.window_set, "default", wl.data)
+            V = torch.as_tensor(wl.V, device="cuda")
+            fn = lambda: mixed_matvecs(plan, V, dell=True, dsigma=True)
+            n_products = V.shape[0] * (2 + len(wl.window_set))
+            what = "K V + dK/dl_w V (per window) + dK/ds V"
+        else:
+            plan = build_plan(wl.spec, wl.window_set, "default", wl.data)
+            V = torch.as_tensor(wl.V, device="cuda")
+            fn = lambda: fast_matvecs(plan, V, dell=wl.dell, dsigma=wl.dsigma)
+            n_products = V.shape[0] * (1 + int(wl.dell) + int(wl.dsigma))
+            what = "K V" + (" + dK/dl V" if wl.dell else "") + (" + dK/ds V" if wl.dsigma else "")
+        torch.cuda.synchronize()
+        plan_s = time.perf_counter() - t0
+        for _ in range(warmup):
+            fn()
+        ms = cuda_time(torch, fn, steps)
+        out[name] = {"N": wl.data.n_rows, "windows": list(wl.window_set.lengths), "rhs": int(V.shape[0]),
+                     "products": what, "ms_per_step": ms, "products_per_s": n_products * 1000.0 / ms,
+                     "plan_build_s": plan_s}
+        del plan, V
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -393,6 +428,7 @@ def run_ours(args):
             result["fp64_probe"] = {"dfma_tflops": fp64, "dmma_tflops": dmma}
             if world == 1:
                 result["roofline"] = kernel_roofline(torch, plan, wl, peaks)
+                result["extras"] = extra_workloads(torch)
             if world == 1 and not args.no_cpu_baseline:
                 one = build_plan(wl.spec, WindowSet((wins[0],), d_max=3), "default", wl.data)
                 gpu_w0 = fast_matvec(one, v_host)

@@ -159,7 +159,10 @@ __global__ void k_keys(const double* __restrict__ X, int64_t ld, int q, int c0, 
     for (int a = 0; a < q; ++a) sq *= S;
     keys[i] = (uint32_t)sc * (uint32_t)sq + (uint32_t)sub;
     vals[i] = (int32_t)i;
-    atomicAdd(&counts[sc], 1);
+    // warp-aggregated histogram update (clustered data puts many lanes in one supercell)
+    const unsigned active = __activemask();
+    const unsigned peers = __match_any_sync(active, sc);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&counts[sc], __popc(peers));
 }
 
 __global__ void k_points(const double* __restrict__ X, int64_t ld, int q, int c0, int c1, int c2, int n,
@@ -362,7 +365,7 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
             int64_t rank = 0;
             for (int w : g->windows_of_q[3]) {
                 shift[w] = ((int64_t)w - rank) * N;
-                k_weights3<12><<<(unsigned)((N + 127) / 128), 128, 0, st>>>(g->pts + (int64_t)w * N, N, g->wf,
+                k_weights3<12><<<(unsigned)((N * 36 + 255) / 256), 256, 0, st>>>(g->pts + (int64_t)w * N, N, g->wf,
                                                                           g->W3 + rank * N * 3 * T,
                                                                           g->CI3 + rank * N);
                 if ((rc = launched()) != AK_OK) break;

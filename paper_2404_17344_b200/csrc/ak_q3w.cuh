@@ -65,17 +65,14 @@ template <int T>
 __global__ void k_weights3(const Point* __restrict__ pts, int64_t np, const ak_window_fn wf, double* __restrict__ W,
                            CellIdx* __restrict__ CI)
 {
-    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= np) return;
-    const Point p = pts[j];
-    double w[T];
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-        window_weights<T>(wf, p.s[ax], w);
-#pragma unroll
-        for (int a = 0; a < T; ++a) W[j * 3 * T + ax * T + a] = w[a];
-    }
-    CI[j] = CellIdx{p.cell, p.idx};
+    // one thread per table entry: coalesced stores of the [np][3T] table
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= np * 3 * T) return;
+    const int64_t j = e / (3 * T);
+    const int k = (int)(e - j * 3 * T);
+    const int ax = k / T, t = k - ax * T;
+    W[e] = window_weight_rt(wf, pts[j].s[ax], t);
+    if (k == 0) CI[j] = CellIdx{pts[j].cell, pts[j].idx};
 }
 
 // acc += v * w0 (x) w1 (x) w2 with v folded into the w1 factor in registers
