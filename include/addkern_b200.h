@@ -146,11 +146,19 @@ int ak_op_destroy(ak_op* op);
 #define AK_APPLY_H_PER_RHS    8  /* C == 1 and H holds R*P multipliers: RHS r of window w uses
                                     H[r*P + w] (R different kernels in lockstep, e.g. the cells
                                     of a length-scale grid search over one geometry)            */
+#define AK_APPLY_SPECTRUM_ONLY 16 /* spread, forward FFT, pack the band of the half spectra into
+                                    the op's band buffer (ak_op_band), return                   */
+#define AK_APPLY_FROM_SPECTRUM 32 /* skip spread + forward FFT: unpack the band buffer, then
+                                    multiply, inverse FFT, interpolate                           */
 
 /* The op's spread grids (canonical layout, R right-hand sides): the exchange
  * buffer of point-sharded multi-GPU products (spread locally, all-reduce the
  * grids, then ak_op_apply(..., AK_APPLY_FROM_GRIDS)). */
 int ak_op_grids(ak_op* op, double** grids, int64_t* count);
+/* The op's compact band spectra (doubles = 2 * complex count): R * sum_w m^(q-1) * m/2
+ * complex values, 8x smaller than the grids at sigma = 2 -- the exchange buffer of
+ * point-sharded products with AK_APPLY_SPECTRUM_ONLY / AK_APPLY_FROM_SPECTRUM. */
+int ak_op_band(ak_op* op, double** band, int64_t* count);
 
 /*
  *   V          device double[R][ldv]

@@ -28,6 +28,8 @@ AK_APPLY_ACCUMULATE = 1
 AK_APPLY_SPREAD_ONLY = 2
 AK_APPLY_FROM_GRIDS = 4
 AK_APPLY_H_PER_RHS = 8
+AK_APPLY_SPECTRUM_ONLY = 16
+AK_APPLY_FROM_SPECTRUM = 32
 
 AK_MAX_TAPS = 16
 AK_MAX_PAIRS = 8
@@ -38,7 +40,7 @@ EXPORTED = (
     "ak_last_error", "ak_version", "ak_launch_count",
     "ak_geom_create", "ak_geom_destroy", "ak_geom_num_points", "ak_geom_num_windows",
     "ak_geom_num_items", "ak_geom_grid_elems", "ak_geom_canon_offset", "ak_geom_canon_total",
-    "ak_spread", "ak_interp", "ak_op_create", "ak_op_destroy", "ak_op_apply", "ak_op_grids",
+    "ak_spread", "ak_interp", "ak_op_create", "ak_op_destroy", "ak_op_apply", "ak_op_grids", "ak_op_band",
     "ak_type1_band", "ak_type2_grid", "ak_dense_apply", "ak_probe_fp64", "ak_probe_dmma",
 )
 
@@ -80,6 +82,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "ak_op_create": (_c_int, [_vp, _vp, _i32, _i32, _i32, _vp, ctypes.POINTER(_vp)]),
         "ak_op_destroy": (_c_int, [_vp]),
         "ak_op_grids": (_c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_i64)]),
+        "ak_op_band": (_c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_i64)]),
         "ak_op_apply": (_c_int, [_vp, _dp, _i64, _dp, _dp, ctypes.POINTER(_vp), _i64, ctypes.POINTER(_i32),
                                  _i32, _vp]),
         "ak_type1_band": (_c_int, [_i32, _i32, _i32, _dp, _dp, _dp, _dp, _vp]),

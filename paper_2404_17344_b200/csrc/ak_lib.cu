@@ -836,6 +836,35 @@ __global__ void k_band_multiply(const double2* __restrict__ Y, double2* __restri
     }
 }
 
+// Band of the half spectra <-> compact exchange buffer (same compact indexing as H):
+// dir = 0 packs spec -> band, dir = 1 unpacks band -> spec (band entries only).
+__global__ void k_band_pack(double2* __restrict__ spec, double2* __restrict__ band, int q, int n, int m, int64_t hs,
+                            int64_t bs, int64_t total, int dir)
+{
+    const int nh = n / 2 + 1, mh = m / 2;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = e / bs;
+        const int64_t k = e - b * bs;
+        const int k2 = (int)(k % mh);
+        const int64_t rest = k / mh;
+        int64_t lin;
+        if (q == 3) {
+            const int b1 = (int)(rest % m), b0 = (int)(rest / m);
+            const int k0 = b0 < mh ? b0 : b0 + (n - m), k1 = b1 < mh ? b1 : b1 + (n - m);
+            lin = ((int64_t)k0 * n + k1) * nh + k2;
+        } else if (q == 2) {
+            const int b1 = (int)rest;
+            const int k1 = b1 < mh ? b1 : b1 + (n - m);
+            lin = (int64_t)k1 * nh + k2;
+        } else {
+            lin = k2;
+        }
+        if (dir == 0) band[e] = spec[b * hs + lin];
+        else spec[b * hs + lin] = band[e];
+    }
+}
+
 struct ak_op {
     const ak_geom* gs = nullptr;
     const ak_geom* gi = nullptr;
@@ -845,6 +874,10 @@ struct ak_op {
     double2* spec = nullptr;
     double2* spec2 = nullptr;
     int64_t spec_off[4] = {0, 0, 0, 0};   // complex elements, per q group
+    double2* band = nullptr;              // compact band spectra (multi-GPU exchange buffer)
+    int64_t band_off[4] = {0, 0, 0, 0};
+    int64_t bs[4] = {0, 0, 0, 0};         // band elements per grid
+    int64_t band_total = 0;
     int64_t hs[4] = {0, 0, 0, 0};         // half-spectrum elements per grid
     int64_t grid_off[4] = {0, 0, 0, 0};   // doubles, per q group (R units applied)
     int nwin[4] = {0, 0, 0, 0};
@@ -866,6 +899,7 @@ extern "C" int ak_op_destroy(ak_op* op) {
     cudaFree(op->gbuf);
     cudaFree(op->spec);
     cudaFree(op->spec2);
+    cudaFree(op->band);
     delete op;
     return AK_OK;
 }
@@ -896,6 +930,14 @@ static int op_build(ak_op* op, cudaStream_t st) {
         }
         op->has[q] = true;
     }
+    int64_t boff = 0;
+    for (int q = 3; q >= 1; --q) {
+        op->bs[q] = ipow_rt(op->m, q - 1) * (op->m / 2);
+        op->band_off[q] = boff;
+        boff += op->bs[q] * op->R * op->nwin[q];
+    }
+    op->band_total = boff;
+    AK_CUDA(cudaMalloc(&op->band, sizeof(double2) * std::max<int64_t>(boff, 1)));
     AK_CUDA(cudaMalloc(&op->spec, sizeof(double2) * std::max<int64_t>(soff, 1)));
     AK_CUDA(cudaMalloc(&op->spec2, sizeof(double2) * std::max<int64_t>(soff, 1)));
     AK_CUDA(cudaStreamSynchronize(st));
@@ -936,6 +978,13 @@ extern "C" int ak_op_grids(ak_op* op, double** grids, int64_t* count) {
     return AK_OK;
 }
 
+extern "C" int ak_op_band(ak_op* op, double** band, int64_t* count) {
+    if (!op || !band || !count) return fail(AK_ERR_INVALID, "null argument");
+    *band = reinterpret_cast<double*>(op->band);
+    *count = 2 * op->band_total;
+    return AK_OK;
+}
+
 extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double* const* H, const double* scale,
                            double* const* outs, int64_t ldo, const int32_t* sum_windows, int32_t flags,
                            void* stream)
@@ -946,13 +995,28 @@ extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double
     const ak_geom* gi = op->gi;
     const int R = op->R, P = gs->P;
     const int accumulate = flags & AK_APPLY_ACCUMULATE;
-    if (!(flags & AK_APPLY_FROM_GRIDS)) {
+    if (!(flags & (AK_APPLY_FROM_GRIDS | AK_APPLY_FROM_SPECTRUM))) {
         if (ldv < gs->N || (gs->N > 0 && !V)) return fail(AK_ERR_INVALID, "bad right-hand sides");
         AK_CUDA(cudaMemsetAsync(op->grids, 0, sizeof(double) * gs->canon_total * R, st));
         if (gs->N > 0)
             for (int q = 3; q >= 1; --q) AK_TRY(spread_group(gs, q, V, R, ldv, op->grids, st));
     }
     if (flags & AK_APPLY_SPREAD_ONLY) return AK_OK;
+    if (flags & AK_APPLY_SPECTRUM_ONLY) {
+        for (int q = 3; q >= 1; --q)
+            if (op->has[q]) {
+                AK_CUFFT(cufftSetStream(op->fwd[q], st));
+                AK_CUFFT(cufftExecD2Z(op->fwd[q], op->grids + op->grid_off[q],
+                                      (cufftDoubleComplex*)(op->spec + op->spec_off[q])));
+                g_launches.fetch_add(1);
+                const int64_t total = op->bs[q] * R * op->nwin[q];
+                k_band_pack<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(
+                    op->spec + op->spec_off[q], op->band + op->band_off[q], q, gs->n, op->m, op->hs[q], op->bs[q],
+                    total, 0);
+                AK_TRY(launched());
+            }
+        return AK_OK;
+    }
     if (!H || !scale || !outs || !sum_windows) return fail(AK_ERR_INVALID, "null argument");
     if (ldo < gi->N) return fail(AK_ERR_INVALID, "leading dimension too small");
     if ((flags & AK_APPLY_H_PER_RHS) && op->C != 1) return fail(AK_ERR_INVALID, "per-RHS multipliers need C == 1");
@@ -966,6 +1030,14 @@ extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double
     if (gi->N == 0) return AK_OK;
     for (int q = 3; q >= 1; --q)
         if (op->has[q]) {
+            if (flags & AK_APPLY_FROM_SPECTRUM) {
+                const int64_t total = op->bs[q] * R * op->nwin[q];
+                k_band_pack<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(
+                    op->spec + op->spec_off[q], op->band + op->band_off[q], q, gs->n, op->m, op->hs[q], op->bs[q],
+                    total, 1);
+                AK_TRY(launched());
+                continue;
+            }
             AK_CUFFT(cufftSetStream(op->fwd[q], st));
             AK_CUFFT(cufftExecD2Z(op->fwd[q], op->grids + op->grid_off[q], (cufftDoubleComplex*)(op->spec + op->spec_off[q])));
             g_launches.fetch_add(1);

@@ -11,11 +11,14 @@ decompositions:
   every rank.  Balance is capped by the window granularity (10 windows on 8
   GPUs: at most 5x).
 * point sharding -- rank r owns a contiguous block of rows.  It spreads only
-  its own nodes into every window's grid, the grids (sum_w n^q_w doubles per
-  RHS, 20 MB for config 4) are summed with one all-reduce, every rank runs the
-  tiny FFT/multiply stage redundantly and interpolates only its own rows.  The
-  result is row-sharded (all_gather for a replicated vector).  Balanced for
-  any window mix.
+  its own nodes into every window's grid and transforms it; the band of the
+  half spectra (R * sum_w m^(q-1) m/2 complex values: 2.6 MB for config 4,
+  8x less than the 20 MB of grids) is summed with one all-reduce, every rank
+  runs the multiply / inverse FFT redundantly and interpolates only its own
+  rows.  The spread and the FFT are linear, so the summed band equals the band
+  of the summed grid.  The result is row-sharded (all_gather for a replicated
+  vector).  Balanced for any window mix.  ``exchange="grid"`` all-reduces the
+  grids instead (before the FFT).
 
 Both reproduce the single-GPU product up to the order of floating-point sums.
 """
@@ -112,12 +115,16 @@ class WindowShardedPlan:
 
 
 class PointShardedPlan:
-    """K v with the rows split across ranks; the spread grids are all-reduced."""
+    """K v with the rows split across ranks; band spectra (or grids) are all-reduced."""
 
-    def __init__(self, spec, window_set: WindowSet, preset, data: Dataset, group=None, **kw):
+    def __init__(self, spec, window_set: WindowSet, preset, data: Dataset, group=None, exchange: str = "band",
+                 **kw):
         from .fastsum import build_plan
 
+        if exchange not in ("band", "grid"):
+            raise ValueError("exchange must be 'band' or 'grid'")
         dist = _dist()
+        self.exchange = exchange
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -133,13 +140,19 @@ class PointShardedPlan:
         dist = _dist()
         fams = tuple(families or (self.plan.spec.family,))
         R = V_local.shape[0]
-        op = self.plan._operator(fams, R)
-        op.spread_only(V_local)
-        dist.all_reduce(op.grids(), group=self.group)
         from . import _native
 
+        op = self.plan._operator(fams, R)
+        if self.exchange == "band":
+            op.spectrum_only(V_local)
+            dist.all_reduce(op.band(), group=self.group)
+            flag = _native.AK_APPLY_FROM_SPECTRUM
+        else:
+            op.spread_only(V_local)
+            dist.all_reduce(op.grids(), group=self.group)
+            flag = _native.AK_APPLY_FROM_GRIDS
         outs = [torch.empty((R, self.hi - self.lo), dtype=torch.float64, device="cuda") for _ in fams]
-        op.apply(None, outs, [True] * len(outs), flags=_native.AK_APPLY_FROM_GRIDS)
+        op.apply(None, outs, [True] * len(outs), flags=flag)
         return outs
 
     def matvec(self, v, gather: bool = True):

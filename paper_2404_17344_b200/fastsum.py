@@ -168,12 +168,26 @@ class _Operator:
                                    _native.AK_APPLY_SPREAD_ONLY, _stream_ptr(torch))
         _native.check(rc, "ak_op_apply(spread only)")
 
+    def spectrum_only(self, V) -> None:
+        """Spread V, forward FFT, pack the band spectra into the op's band buffer."""
+        torch = _torch()
+        rc = self._lib.ak_op_apply(self._handle, V.data_ptr(), int(V.shape[-1]), 0, 0, None, 0, None,
+                                   _native.AK_APPLY_SPECTRUM_ONLY, _stream_ptr(torch))
+        _native.check(rc, "ak_op_apply(spectrum only)")
+
+    def band(self):
+        """The op's compact band spectra (float64 view of complex values): all-reduce buffer."""
+        return self._view(self._lib.ak_op_band, "ak_op_band")
+
     def grids(self):
         """The op's spread grids as a torch CUDA tensor view (all-reduce buffer)."""
+        return self._view(self._lib.ak_op_grids, "ak_op_grids")
+
+    def _view(self, fn, what):
         torch = _torch()
         ptr = ctypes.c_void_p()
         count = ctypes.c_int64()
-        _native.check(self._lib.ak_op_grids(self._handle, ctypes.byref(ptr), ctypes.byref(count)), "ak_op_grids")
+        _native.check(fn(self._handle, ctypes.byref(ptr), ctypes.byref(count)), what)
 
         class _View:
             __cuda_array_interface__ = {"shape": (int(count.value),), "typestr": "<f8",

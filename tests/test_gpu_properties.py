@@ -220,6 +220,16 @@ def test_split_apply_and_grid_view(cuda):
     g.mul_(2.0)
     op.apply(None, [out], [True], flags=_native.AK_APPLY_FROM_GRIDS)
     assert rel(out.cpu().numpy(), 2.0 * ref.cpu().numpy()) <= 1e-15
+    # band-spectrum exchange path (8x smaller all-reduce buffer)
+    op.spectrum_only(V)
+    b = op.band()
+    m = plan.m
+    assert b.numel() == 2 * 2 * (m * m * (m // 2) + m * (m // 2) + m // 2)
+    op.apply(None, [out], [True], flags=_native.AK_APPLY_FROM_SPECTRUM)
+    assert rel(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-15
+    b.mul_(3.0)
+    op.apply(None, [out], [True], flags=_native.AK_APPLY_FROM_SPECTRUM)
+    assert rel(out.cpu().numpy(), 3.0 * ref.cpu().numpy()) <= 1e-14
 
 
 def test_sharded_plans_single_rank(cuda):
@@ -248,8 +258,11 @@ def test_sharded_plans_single_rank(cuda):
         v = rng.normal(size=5000)
         ref = fast_matvec(build_plan(spec, ws, "default", ds), v)
         vd = cuda.as_tensor(v, device="cuda")
-        for cls in (WindowShardedPlan, PointShardedPlan):
-            out = cls(spec, ws, "default", ds).matvec(vd)
-            assert rel(out.cpu().numpy(), ref) <= 1e-13, cls.__name__
+        for make in (lambda: WindowShardedPlan(spec, ws, "default", ds),
+                     lambda: PointShardedPlan(spec, ws, "default", ds),
+                     lambda: PointShardedPlan(spec, ws, "default", ds, exchange="grid")):
+            p = make()
+            out = p.matvec(vd)
+            assert rel(out.cpu().numpy(), ref) <= 1e-13, type(p).__name__
     finally:
         dist.destroy_process_group()

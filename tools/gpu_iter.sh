@@ -1,3 +1,3 @@
-for c in 2048 4096 8192; do
-  echo "chunk=$c"; AK_CHUNK3=$c AK_SUPERCELL3=2 timeout 300 python tools/kbench.py
-done
+for v in 0 1; do for b in 16 32; do
+  echo "vreg=$v batch=$b"; AK_VREG=$v AK_BATCH3=$b timeout 300 python tools/kbench.py
+done; done
