@@ -21,6 +21,7 @@
 #include "ak_common.cuh"
 #include "ak_kernels.cuh"
 #include "ak_q3w.cuh"
+#include "ak_q3m.cuh"
 
 using namespace ak;
 
@@ -95,6 +96,7 @@ struct ak_geom {
     int iwarps = 1;                     // warps per CTA of the cached q=3 interp
     int swarps = 1;                     // warps per CTA of the cached q=3 spread
     bool vreg = false;                  // RHS value folded in registers (vs a scaling pass)
+    bool imma = true;                   // q=3 interp on FP64 tensor cores (mma.sync m8n8k4; AK_IMMA=0: DFMA)
     double* W3 = nullptr;               // [P3][N][3T]
     CellIdx* CI3 = nullptr;             // [P3][N]
     int64_t* wshift_d = nullptr;        // per window: (w - rank3(w)) * N
@@ -385,9 +387,11 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
         }
         g->batch3 = batch3_default();
         const char* iw = getenv("AK_IWARPS");
-        g->iwarps = (iw && atoi(iw) == 1) ? 1 : 2;
+        g->iwarps = (iw && atoi(iw) == 2) ? 2 : 1;
         const char* sw = getenv("AK_SWARPS");
         g->swarps = (sw && atoi(sw) == 2) ? 2 : 1;
+        const char* im = getenv("AK_IMMA");
+        g->imma = !(im && im[0] == '0');
         const char* vr = getenv("AK_VREG");
         g->vreg = vr && vr[0] == '1';
     }
@@ -676,6 +680,15 @@ static void launch_interp3w_sb(const ak_geom* g, int64_t i0, int64_t ni, const d
                                cudaStream_t st)
 {
     dim3 grid((unsigned)ni, (unsigned)R);
+    if (g->imma) {
+        if (g->iwarps == 2 && B == 16)
+            k_interp3m<S, 16, 2><<<grid, 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids,
+                                                      g->canon_off_d, R, g->n, scale, out, ldo, atomic_out, wstride);
+        else
+            k_interp3m<S, B, 1><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids,
+                                                     g->canon_off_d, R, g->n, scale, out, ldo, atomic_out, wstride);
+        return;
+    }
     if constexpr (B == 16) {
         if (g->iwarps == 2) {
             k_interp3w<12, S, B, 2><<<grid, 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids,

@@ -1,0 +1,200 @@
+// q = 3 interpolation on the FP64 tensor cores (mma.sync m8n8k4 f64), T = 12.
+//
+// For the points of one cell the interpolation is a small GEMM followed by two
+// cheap contractions:
+//   U[j, (a,b)] = sum_c w2_j[c] G[a,b,c]          (8 points x 144 pairs, K = 12 = 3 k-steps)
+//   out_j       = sum_a w0_j[a] sum_b w1_j[b] U[j, (a,b)]
+// The first stage (1728 FMA per point, 90% of the work) runs as 54 DMMA per 8
+// points: A = w2 of the 8 points (row-major 8x4 fragment), B = the cell's
+// footprint G (col-major 4x8 fragments, held in registers while the cell
+// lasts, 54 doubles per lane), C = U (18 tiles, 36 doubles per lane).  The
+// B columns are permuted so that lane quad q (lane % 4) holds exactly the
+// pairs (a, b) with b in {3q, 3q+1, 3q+2}, which makes the second stage a
+// compile-time-indexed 48-FMA contraction per lane followed by a 2-step quad
+// shuffle.  DMMA and DFMA share the FP64 datapath (37 TF/s either way on
+// B200), so the gain is not peak rate but issue pressure: ~135 instructions
+// per 8 points per lane instead of ~700, and 1920 instead of 2144 FP64 slots
+// per point.  Partially filled groups (run ends) are padded with zero rows.
+#pragma once
+#include "ak_q3w.cuh"
+
+namespace ak {
+
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// Footprint fragments of the cell at local coordinates (l0, l1, l2):
+// gf[t][ks] = G[a][b][c] with c = 4 ks + lane%4 and column n = lane/4 of tile t
+// mapped to pair i = 2t + (n & 1), quad n >> 1: a = i / 3, b = 3 (n >> 1) + i % 3.
+template <int R>
+__device__ __forceinline__ void load_fragments(double (&gf)[18][3], const double* tile, int cell, int lane) {
+    const int l0 = cell & 255, l1 = (cell >> 8) & 255, l2 = (cell >> 16) & 255;
+    const int n = lane >> 2, kk = lane & 3;
+    const int qq = n >> 1, e = n & 1;
+#pragma unroll
+    for (int t = 0; t < 18; ++t) {
+        const int i = 2 * t + e;
+        const int a = i / 3, b = 3 * qq + i % 3;
+        const double* row = tile + ((l0 + a) * R + (l1 + b)) * R + l2 + kk;
+#pragma unroll
+        for (int ks = 0; ks < 3; ++ks) gf[t][ks] = row[4 * ks];
+    }
+}
+
+// One group of up to 8 points (rows k0 .. k0+cnt-1 of the staged batch), all in the
+// cell whose fragments are in gf.  Returns this lane's quad-partial for point
+// k0 + lane/4 (summed over the quad by the caller).
+template <int RW>
+__device__ __forceinline__ double interp_group_mma(const double (&gf)[18][3], const double (*wrow)[RW], int k0,
+                                                   int cnt, int lane)
+{
+    const int pj = lane >> 2, q = lane & 3;
+    const bool valid = pj < cnt;
+    const double* w = wrow[k0 + (valid ? pj : 0)];
+    double af[3];
+#pragma unroll
+    for (int ks = 0; ks < 3; ++ks) af[ks] = valid ? w[24 + 4 * ks + q] : 0.0;
+    double C[18][2];
+#pragma unroll
+    for (int t = 0; t < 18; ++t) {
+        C[t][0] = 0.0;
+        C[t][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 3; ++ks) dmma_8x8x4(C[t][0], C[t][1], af[ks], gf[t][ks]);
+    }
+    // lane (pj, q) holds U[pj][(a, b)] for a = i/3, b = 3q + i%3, i = 2t + e
+    double w0[12], w1[3];
+#pragma unroll
+    for (int a = 0; a < 12; ++a) w0[a] = w[a];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) w1[b] = w[12 + 3 * q + b];
+    double acc = 0.0;
+#pragma unroll
+    for (int a = 0; a < 12; ++a) {
+        double sa = 0.0;
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb) {
+            const int i = 3 * a + bb;
+            sa = fma(w1[bb], C[i >> 1][i & 1], sa);
+        }
+        acc = fma(w0[a], sa, acc);
+    }
+    return valid ? acc : 0.0;
+}
+
+template <int S, int B, int NW>
+__global__ void __launch_bounds__(32 * NW, 8 / NW)
+k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
+           const WorkItem* __restrict__ items, const double* __restrict__ grids,
+           const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,
+           double* __restrict__ out, int64_t ldo, int atomic_out, int64_t wstride)
+{
+    constexpr int T = 12;
+    constexpr int RW = 3 * T;
+    constexpr int R = S + T - 1;
+    constexpr int TILE = R * R * R;
+    static_assert(B % 8 == 0 && B <= 32, "batch: multiple of 8, at most 32");
+
+    __shared__ double tile[TILE];
+    __shared__ __align__(128) double wbuf_all[NW][2][B][RW];
+    __shared__ __align__(16) CellIdx cib_all[NW][2][B];
+    __shared__ int cst_all[NW][B];
+    __shared__ int widx[3][R];
+    __shared__ __align__(8) uint64_t bar_all[NW][2];
+
+    const WorkItem it = items[blockIdx.x];
+    const int r = blockIdx.y;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    double (*wbuf)[B][RW] = wbuf_all[warp];
+    CellIdx (*cib)[B] = cib_all[warp];
+    int* cst = cst_all[warp];
+    uint64_t* bar = bar_all[warp];
+    const int sc0 = it.sc & 1023, sc1 = (it.sc >> 10) & 1023, sc2 = (it.sc >> 20) & 1023;
+    const int nbatch = (it.count + B - 1) / B;
+    const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
+    const CellIdx* __restrict__ CIit = ci + (it.start - wshift[it.window]);
+
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    if (warp < nbatch) {
+        const int cnt = min(B, it.count - warp * B);
+        if (lane == 0) tma_load_1d(&wbuf[0][0][0], Wit + (int64_t)warp * B * RW, (unsigned)(cnt * RW * 8), &bar[0]);
+        if (lane < cnt) cp_async8(&cib[0][lane], CIit + warp * B + lane);
+    }
+    {
+        const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
+        region_axes<R>(widx, sc0 * S - (T / 2 - 1), sc1 * S - (T / 2 - 1), sc2 * S - (T / 2 - 1), n, threadIdx.x,
+                       32 * NW);
+        if (NW > 1) __syncthreads();
+        else __syncwarp();
+        for (int i = threadIdx.x; i < TILE; i += 32 * NW) cp_async8(&tile[i], g + region_index_s<R>(widx, i, n));
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    if (NW > 1) __syncthreads();
+    else __syncwarp();
+    const double sc = scale[it.window];
+    double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * ldo;
+
+    double gf[18][3];
+    int cur = -1;
+
+    for (int bi = warp, u = 0; bi < nbatch; bi += NW, ++u) {
+        const int s = u & 1;
+        const int off = bi * B;
+        const int nb = min(B, it.count - off);
+        cp_async_wait_all();
+        mbar_wait(&bar[s], (u >> 1) & 1);
+        __syncwarp();
+        if (bi + NW < nbatch) {
+            const int nb1 = min(B, it.count - off - NW * B);
+            if (lane == 0) {
+                fence_proxy_async();
+                tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + NW * B) * RW, (unsigned)(nb1 * RW * 8),
+                            &bar[s ^ 1]);
+            }
+            if (lane < nb1) cp_async8(&cib[s ^ 1][lane], CIit + off + NW * B + lane);
+        }
+        cp_async_commit();
+        if (lane < nb) {
+            const int c = cib[s][lane].cell;
+            cst[lane] = (cell_axis(c, 0) - sc0 * S) | ((cell_axis(c, 1) - sc1 * S) << 8) |
+                        ((cell_axis(c, 2) - sc2 * S) << 16);
+        }
+        __syncwarp();
+        const int mycell = lane < nb ? cst[lane] : -2;
+        const int prev = __shfl_up_sync(0xffffffffu, mycell, 1);
+        const unsigned chg = __ballot_sync(0xffffffffu, lane < nb && (lane == 0 ? mycell != cur : mycell != prev));
+        for (int k = 0; k < nb;) {
+            if ((chg >> k) & 1u) {
+                cur = cst[k];
+                load_fragments<R>(gf, tile, cur, lane);
+            }
+            const unsigned later = k < 31 ? chg & ~((2u << k) - 1u) : 0u;
+            const int kend = later ? min(__ffs(later) - 1, nb) : nb;
+            for (int k0 = k; k0 < kend; k0 += 8) {
+                const int cnt = min(8, kend - k0);
+                double v = interp_group_mma<RW>(gf, wbuf[s], k0, cnt, lane);
+                v += __shfl_xor_sync(0xffffffffu, v, 1);
+                v += __shfl_xor_sync(0xffffffffu, v, 2);
+                const int pj = lane >> 2;
+                if ((lane & 3) == 0 && pj < cnt) {
+                    double* dst = o + cib[s][k0 + pj].idx;
+                    if (atomic_out) red_add(dst, sc * v);
+                    else *dst = sc * v;
+                }
+            }
+            k = kend;
+        }
+    }
+}
+
+}  // namespace ak
