@@ -59,30 +59,30 @@ __device__ __forceinline__ double interp_group_mma(const double (&gf)[18][3], co
     for (int ks = 0; ks < 3; ++ks) af[ks] = valid ? w[24 + 4 * ks + q] : 0.0;
     double C[18][2];
 #pragma unroll
-    for (int t = 0; t < 18; ++t) {
-        C[t][0] = 0.0;
-        C[t][1] = 0.0;
+    for (int t = 0; t < 18; ++t) C[t][0] = C[t][1] = 0.0;
+    // k-step outer: 18 independent accumulators between dependent DMMAs
 #pragma unroll
-        for (int ks = 0; ks < 3; ++ks) dmma_8x8x4(C[t][0], C[t][1], af[ks], gf[t][ks]);
-    }
+    for (int ks = 0; ks < 3; ++ks)
+#pragma unroll
+        for (int t = 0; t < 18; ++t) dmma_8x8x4(C[t][0], C[t][1], af[ks], gf[t][ks]);
     // lane (pj, q) holds U[pj][(a, b)] for a = i/3, b = 3q + i%3, i = 2t + e
     double w0[12], w1[3];
 #pragma unroll
     for (int a = 0; a < 12; ++a) w0[a] = w[a];
 #pragma unroll
     for (int b = 0; b < 3; ++b) w1[b] = w[12 + 3 * q + b];
-    double acc = 0.0;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};  // 4 independent chains (FMA latency)
 #pragma unroll
     for (int a = 0; a < 12; ++a) {
-        double sa = 0.0;
+        double sa = w1[0] * C[(3 * a) >> 1][(3 * a) & 1];
 #pragma unroll
-        for (int bb = 0; bb < 3; ++bb) {
+        for (int bb = 1; bb < 3; ++bb) {
             const int i = 3 * a + bb;
             sa = fma(w1[bb], C[i >> 1][i & 1], sa);
         }
-        acc = fma(w0[a], sa, acc);
+        acc[a & 3] = fma(w0[a], sa, acc[a & 3]);
     }
-    return valid ? acc : 0.0;
+    return valid ? (acc[0] + acc[1]) + (acc[2] + acc[3]) : 0.0;
 }
 
 template <int S, int B, int NW>
