@@ -367,7 +367,7 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
             int64_t rank = 0;
             for (int w : g->windows_of_q[3]) {
                 shift[w] = ((int64_t)w - rank) * N;
-                k_weights3<12><<<(unsigned)((N * 36 + 255) / 256), 256, 0, st>>>(g->pts + (int64_t)w * N, N, g->wf,
+                k_weights3<12><<<(unsigned)((N + 127) / 128), 128, 0, st>>>(g->pts + (int64_t)w * N, N, g->wf,
                                                                           g->W3 + rank * N * 3 * T,
                                                                           g->CI3 + rank * N);
                 if ((rc = launched()) != AK_OK) break;

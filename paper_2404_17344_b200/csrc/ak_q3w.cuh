@@ -62,17 +62,28 @@ __device__ __forceinline__ void tma_load_1d(void* smem, const void* gmem, unsign
 // Plan time: weight rows (axis-major: w0[0..T), w1[0..T), w2[0..T)) and
 // (cell, row) records of the points of 3-D windows, compact per-window layout.
 template <int T>
-__global__ void k_weights3(const Point* __restrict__ pts, int64_t np, const ak_window_fn wf, double* __restrict__ W,
-                           CellIdx* __restrict__ CI)
+__global__ void __launch_bounds__(128) k_weights3(const Point* __restrict__ pts, int64_t np, const ak_window_fn wf,
+                                                 double* __restrict__ W, CellIdx* __restrict__ CI)
 {
-    // one thread per table entry: coalesced stores of the [np][3T] table
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= np * 3 * T) return;
-    const int64_t j = e / (3 * T);
-    const int k = (int)(e - j * 3 * T);
-    const int ax = k / T, t = k - ax * T;
-    W[e] = window_weight_rt(wf, pts[j].s[ax], t);
-    if (k == 0) CI[j] = CellIdx{pts[j].cell, pts[j].idx};
+    // 128 points per block: weights evaluated per thread (unrolled polynomials) into
+    // shared memory, then the block's contiguous [128][3T] slice is stored coalesced.
+    __shared__ double st[128 * 3 * T];
+    const int64_t p0 = (int64_t)blockIdx.x * 128;
+    const int64_t j = p0 + threadIdx.x;
+    if (j < np) {
+        const Point p = pts[j];
+        double w[T];
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            window_weights<T>(wf, p.s[ax], w);
+#pragma unroll
+            for (int a = 0; a < T; ++a) st[threadIdx.x * 3 * T + ax * T + a] = w[a];
+        }
+        CI[j] = CellIdx{p.cell, p.idx};
+    }
+    __syncthreads();
+    const int64_t cnt = (np - p0 < 128 ? np - p0 : 128) * 3 * T;
+    for (int64_t e = threadIdx.x; e < cnt; e += 128) W[p0 * 3 * T + e] = st[e];
 }
 
 // acc += v * w0 (x) w1 (x) w2 with v folded into the w1 factor in registers

@@ -169,3 +169,26 @@ def test_native_library_is_what_runs(cuda):
     before = _native.launch_count()
     fast_matvec(plan, g["V"][0])
     assert _native.launch_count() > before
+
+
+@pytest.mark.parametrize("variant", [
+    {"AK_IMMA": "0"},                       # DFMA interp (transposed warp reduction)
+    {"AK_WEIGHTS": "horner"},               # weights evaluated per pass (no plan-time table)
+    {"AK_SWARPS": "2"},                     # two-warp spread CTAs with barrier-serialised flushes
+    {"AK_IWARPS": "2"},                     # two-warp interp CTAs sharing the region tile
+    {"AK_SUPERCELL3": "4", "AK_CHUNK3": "256", "AK_SORT_ITEMS": "0"},
+    {"AK_BATCH3": "32", "AK_VREG": "1"},
+])
+def test_kernel_variants_match_reference(cuda, monkeypatch, variant):
+    """Every tuned kernel variant (selected at plan time) reproduces the reference."""
+    from paper_2404_17344_b200.fastsum import fast_matvecs
+
+    for k, v in variant.items():
+        monkeypatch.setenv(k, v)
+    for name in ("c3", "c4"):
+        g = golden(name)
+        plan = _plan(g)
+        res = fast_matvecs(plan, g["V"], dell="dK_dell_default" in g)
+        assert rel(res["K"], g["K_default"]) <= TOL, (variant, name)
+        if "dK_dell_default" in g:
+            assert rel(res["dK_dell"], g["dK_dell_default"]) <= TOL, (variant, name)
