@@ -28,8 +28,8 @@ struct alignas(16) WorkItem {
 // supercell chunk into a (S+T-1)^q shared tile before flushing to HBM/L2.
 // (q = 3 uses a runtime edge of 2..4, see ak_geom::sedge and ak_q3.cuh.)
 template <int Q> struct SuperCell;
-template <> struct SuperCell<2> { static constexpr int S = 16; };
-template <> struct SuperCell<1> { static constexpr int S = 32; };
+template <> struct SuperCell<2> { static constexpr int S = 8; };
+template <> struct SuperCell<1> { static constexpr int S = 16; };
 
 
 __device__ __forceinline__ int cell_axis(int32_t packed, int a) { return (packed >> (10 * a)) & 1023; }

@@ -89,7 +89,7 @@ struct ak_geom {
     int64_t nitems = 0;
     int64_t item_begin[4] = {0, 0, 0, 0}, item_end[4] = {0, 0, 0, 0};
     std::vector<int> windows_of_q[4];   // window ids per q, canonical order
-    int sedge[4] = {0, 32, 16, 4};      // supercell edge (cells) per q
+    int sedge[4] = {0, 16, 8, 4};       // supercell edge (cells) per q (must match SuperCell<q>)
     // cached 3-D window weights (plan-time table, see ak_q3w.cuh)
     bool cached = false;
     int batch3 = 16;
@@ -134,7 +134,7 @@ static int chunk_for_q(int q) {
         const int v = e ? atoi(e) : 0;
         return (v >= 64 && v <= 65536) ? v : 2048;
     }
-    return q == 2 ? 4096 : 8192;
+    return q == 2 ? 1024 : 2048;
 }
 
 __global__ void k_keys(const double* __restrict__ X, int64_t ld, int q, int c0, int c1, int c2, int n, int S,
