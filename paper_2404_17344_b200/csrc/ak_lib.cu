@@ -22,6 +22,7 @@
 #include "ak_kernels.cuh"
 #include "ak_q3w.cuh"
 #include "ak_q3m.cuh"
+#include "ak_q3c.cuh"
 
 using namespace ak;
 
@@ -113,18 +114,35 @@ static bool items_sorted_default() {
     return !(e && e[0] == '0');
 }
 
-// Points per staged batch of the cached-weight kernels (AK_BATCH3: 16 (default) or 32).
-static int batch3_default() {
+// Points per staged batch of the cached-weight kernels (AK_BATCH3: 16 or 32; default
+// 32 for single-cell items, whose shared memory is only the weight buffer, else 16).
+static int batch3_default(int sedge3) {
     const char* e = getenv("AK_BATCH3");
-    return (e && atoi(e) == 32) ? 32 : 16;
+    if (e && (atoi(e) == 16 || atoi(e) == 32)) return atoi(e);
+    return sedge3 == 1 ? 32 : 16;
 }
 
 // Supercell edge for 3-D windows: 2, 3 or 4 cells (AK_SUPERCELL3 overrides the default 3;
 // measured on B200, config 4: 2 and 3 tie, 4 is ~7% slower).
+// Returns 0 when unset: the plan then chooses 1 (single-cell items) for densely
+// occupied cells and 2 otherwise.
 static int supercell3_default() {
     const char* e = getenv("AK_SUPERCELL3");
     const int v = e ? atoi(e) : 0;
-    return (v >= 2 && v <= 4) ? v : 2;
+    return (v >= 1 && v <= 4) ? v : 0;
+}
+
+// Mean points per occupied cell above which 3-D windows use single-cell work items.
+static double dense_cell_threshold() {
+    const char* e = getenv("AK_DENSE_CELLS");
+    return e ? atof(e) : 64.0;
+}
+
+__global__ void k_count_nonzero(const int* __restrict__ counts, int total, int* __restrict__ nz) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool on = i < total && counts[i] > 0;
+    const unsigned b = __ballot_sync(0xffffffffu, on);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(nz, __popc(b));
 }
 
 // Maximum points per work item (AK_CHUNK3 overrides the 3-D value).
@@ -258,7 +276,40 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
     // item capacity
     int64_t cap = 0;
     int max_nsc_total = 1;
-    g->sedge[3] = supercell3_default();
+    const bool cached = g->wf.taps == 12 && N > 0 && weights_cached_default();
+    int s3 = supercell3_default();
+    if (s3 == 1 && !cached) s3 = 2;  // single-cell kernels exist for the cached-weight path only
+    if (s3 == 0) {
+        s3 = 2;
+        if (cached && !g->windows_of_q[3].empty()) {
+            // occupancy probe on the first 3-D window: bin by cell, count occupied cells
+            const int w = g->windows_of_q[3][0];
+            const int tot = n * n * n;
+            int *cnt = nullptr, *aux = nullptr;
+            uint32_t* kk = nullptr;
+            int32_t* vv = nullptr;
+            if (cudaMalloc(&cnt, sizeof(int) * tot) == cudaSuccess && cudaMalloc(&aux, sizeof(int) * 2) == cudaSuccess &&
+                cudaMalloc(&kk, sizeof(uint32_t) * N) == cudaSuccess && cudaMalloc(&vv, sizeof(int32_t) * N) == cudaSuccess) {
+                cudaMemsetAsync(cnt, 0, sizeof(int) * tot, st);
+                cudaMemsetAsync(aux, 0, sizeof(int) * 2, st);
+                k_keys<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(X, ld, 3, cols[3 * w], cols[3 * w + 1],
+                                                                     cols[3 * w + 2], n, 1, n, N, kk, vv, cnt, aux);
+                k_count_nonzero<<<(tot + 255) / 256, 256, 0, st>>>(cnt, tot, aux + 1);
+                g_launches.fetch_add(2);
+                int h[2] = {0, 0};
+                if (cudaMemcpyAsync(h, aux, sizeof(h), cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+                    cudaStreamSynchronize(st) == cudaSuccess && h[1] > 0 &&
+                    (double)N / h[1] >= dense_cell_threshold())
+                    s3 = 1;
+            }
+            cudaGetLastError();
+            cudaFree(cnt);
+            cudaFree(aux);
+            cudaFree(kk);
+            cudaFree(vv);
+        }
+    }
+    g->sedge[3] = s3;
     for (int w = 0; w < P; ++w) {
         const int S = g->sedge[g->q[w]];
         const int nsc = (n + S - 1) / S;
@@ -385,7 +436,7 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
             g->CI3 = nullptr;
             g->wshift_d = nullptr;
         }
-        g->batch3 = batch3_default();
+        g->batch3 = batch3_default(g->sedge[3]);
         const char* iw = getenv("AK_IWARPS");
         g->iwarps = (iw && atoi(iw) == 2) ? 2 : 1;
         const char* sw = getenv("AK_SWARPS");
@@ -596,6 +647,16 @@ template <int T>
 static void launch_spread3_t(const ak_geom* g, int64_t i0, int64_t ni, const double* V, int R, int64_t ldv,
                              double* grids, cudaStream_t st)
 {
+    if (T == 12 && g->cached && g->sedge[3] == 1) {
+        dim3 grid((unsigned)ni, (unsigned)R);
+        if (g->batch3 == 32)
+            k_spread3c<32><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
+                                                g->canon_off_d, R, g->n);
+        else
+            k_spread3c<16><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
+                                                g->canon_off_d, R, g->n);
+        return;
+    }
     if (T == 12 && g->cached && g->swarps == 2) {
         dim3 grid((unsigned)ni, (unsigned)R);
         switch (g->sedge[3]) {
@@ -722,6 +783,16 @@ static void launch_interp3_t(const ak_geom* g, int64_t i0, int64_t ni, const dou
                              const double* scale, double* out, int64_t ldo, int atomic_out, int64_t wstride,
                              cudaStream_t st)
 {
+    if (T == 12 && g->cached && g->sedge[3] == 1) {
+        dim3 grid((unsigned)ni, (unsigned)R);
+        if (g->batch3 == 32)
+            k_interp3c<32><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids, g->canon_off_d, R,
+                                                g->n, scale, out, ldo, atomic_out, wstride);
+        else
+            k_interp3c<16><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids, g->canon_off_d, R,
+                                                g->n, scale, out, ldo, atomic_out, wstride);
+        return;
+    }
     if (T == 12 && g->cached) {
         if (g->batch3 == 16) launch_interp3w_b<16>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st);
         else launch_interp3w_b<32>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st);

@@ -1,0 +1,223 @@
+// q = 3 kernels for single-cell work items (supercell edge S = 1).
+//
+// When cells are densely populated (config 4: 395 points per occupied cell on
+// average) every work item can be one cell (or a chunk of one): the warp's
+// register tile IS the item's footprint, so there is no shared region tile, no
+// cell-run bookkeeping, no shared-memory flushes:
+//   spread : register-tiled FMAs over all points of the item, then 54 RED.F64
+//            per lane straight from registers to the grid;
+//   interp : the footprint fragments are loaded once per item from the grid
+//            (L2) and every batch is processed in groups of 8 points on the
+//            FP64 tensor cores (ak_q3m.cuh).
+// Shared memory shrinks to the double-buffered weight rows, which allows more
+// warps per SM.  The plan picks these kernels when the mean occupancy of the
+// occupied cells is high (ak_lib.cu: geom_build).
+#pragma once
+#include "ak_q3m.cuh"
+
+namespace ak {
+
+template <int B>
+__global__ void __launch_bounds__(32, 8)
+k_spread3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
+           const WorkItem* __restrict__ items, const double* __restrict__ V, int64_t ldv,
+           double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
+{
+    constexpr int T = 12;
+    using LN = Q3Lanes<T>;
+    constexpr int P0 = LN::P0, P1 = LN::P1, P2 = LN::P2;
+    constexpr int RW = 3 * T;
+    static_assert(B <= 32, "batch");
+
+    __shared__ __align__(128) double wbuf[2][B][RW];
+    __shared__ __align__(16) CellIdx cib[3][B];
+    __shared__ double vb[2][B];
+    __shared__ __align__(8) uint64_t bar[2];
+
+    const WorkItem it = items[blockIdx.x];
+    const int r = blockIdx.y;
+    const int lane = threadIdx.x;
+    const int g0 = lane >> 4, g1 = (lane >> 2) & 3, g2 = lane & 3;
+    const double* __restrict__ Vr = V + (int64_t)r * ldv;
+    const int nbatch = (it.count + B - 1) / B;
+    const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
+    const CellIdx* __restrict__ CIit = ci + (it.start - wshift[it.window]);
+
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    if (lane == 0) tma_load_1d(&wbuf[0][0][0], Wit, (unsigned)(min(B, it.count) * RW * 8), &bar[0]);
+    if (lane < min(B, it.count)) cp_async8(&cib[0][lane], CIit + lane);
+    if (nbatch > 1 && lane < min(B, it.count - B)) cp_async8(&cib[1][lane], CIit + B + lane);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp();
+    if (lane < min(B, it.count)) cp_async8(&vb[0][lane], Vr + cib[0][lane].idx);
+    cp_async_commit();
+
+    double acc[P0][P1][P2];
+#pragma unroll
+    for (int a = 0; a < P0; ++a)
+#pragma unroll
+        for (int b = 0; b < P1; ++b)
+#pragma unroll
+            for (int c = 0; c < P2; ++c) acc[a][b][c] = 0.0;
+
+    for (int bi = 0; bi < nbatch; ++bi) {
+        const int s = bi & 1;
+        const int off = bi * B;
+        const int nb = min(B, it.count - off);
+        cp_async_wait_all();
+        mbar_wait(&bar[s], (bi >> 1) & 1);
+        __syncwarp();
+        if (bi + 1 < nbatch) {
+            const int nb1 = min(B, it.count - off - B);
+            if (lane == 0) {
+                fence_proxy_async();
+                tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + B) * RW, (unsigned)(nb1 * RW * 8), &bar[s ^ 1]);
+            }
+            if (lane < nb1) cp_async8(&vb[s ^ 1][lane], Vr + cib[(bi + 1) % 3][lane].idx);
+        }
+        if (bi + 2 < nbatch && lane < min(B, it.count - off - 2 * B))
+            cp_async8(&cib[(bi + 2) % 3][lane], CIit + off + 2 * B + lane);
+        cp_async_commit();
+        {
+            constexpr int PER = (B * T + 31) / 32;
+            double x[PER], y[PER];
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int e = lane + 32 * i;
+                const int row = e / T;
+                if (row < nb) {
+                    x[i] = wbuf[s][row][e - row * T];
+                    y[i] = vb[s][row];
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int e = lane + 32 * i;
+                const int row = e / T;
+                if (row < nb) wbuf[s][row][e - row * T] = x[i] * y[i];
+            }
+        }
+        __syncwarp();
+        double a0[P0], a1[P1], a2[P2], b0[P0], b1[P1], b2[P2];
+        load_w<T>(a0, a1, a2, &wbuf[s][0][0], g0, g1, g2);
+        int j = 0;
+        for (; j + 1 < nb; j += 2) {
+            load_w<T>(b0, b1, b2, &wbuf[s][j + 1][0], g0, g1, g2);
+            spread_fma(acc, a0, a1, a2);
+            load_w<T>(a0, a1, a2, &wbuf[s][j + 2 < nb ? j + 2 : j + 1][0], g0, g1, g2);
+            spread_fma(acc, b0, b1, b2);
+        }
+        if (j < nb) spread_fma(acc, a0, a1, a2);
+    }
+
+    // flush the register tile straight to the grid
+    const int c0 = it.sc & 1023, c1 = (it.sc >> 10) & 1023, c2 = (it.sc >> 20) & 1023;
+    double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
+    int x0[P0], x1[P1], x2[P2];
+#pragma unroll
+    for (int a = 0; a < P0; ++a) x0[a] = wrap(c0 - (T / 2 - 1) + g0 * P0 + a, n);
+#pragma unroll
+    for (int b = 0; b < P1; ++b) x1[b] = wrap(c1 - (T / 2 - 1) + g1 * P1 + b, n);
+#pragma unroll
+    for (int c = 0; c < P2; ++c) x2[c] = wrap(c2 - (T / 2 - 1) + g2 * P2 + c, n);
+#pragma unroll
+    for (int a = 0; a < P0; ++a)
+#pragma unroll
+        for (int b = 0; b < P1; ++b)
+#pragma unroll
+            for (int c = 0; c < P2; ++c)
+                red_add(g + ((int64_t)x0[a] * n + x1[b]) * n + x2[c], acc[a][b][c]);
+}
+
+template <int B>
+__global__ void __launch_bounds__(32, 8)
+k_interp3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
+           const WorkItem* __restrict__ items, const double* __restrict__ grids,
+           const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,
+           double* __restrict__ out, int64_t ldo, int atomic_out, int64_t wstride)
+{
+    constexpr int T = 12;
+    constexpr int RW = 3 * T;
+    static_assert(B % 8 == 0 && B <= 32, "batch");
+
+    __shared__ __align__(128) double wbuf[2][B][RW];
+    __shared__ __align__(16) CellIdx cib[2][B];
+    __shared__ __align__(8) uint64_t bar[2];
+
+    const WorkItem it = items[blockIdx.x];
+    const int r = blockIdx.y;
+    const int lane = threadIdx.x;
+    const int nbatch = (it.count + B - 1) / B;
+    const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
+    const CellIdx* __restrict__ CIit = ci + (it.start - wshift[it.window]);
+
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    if (lane == 0) tma_load_1d(&wbuf[0][0][0], Wit, (unsigned)(min(B, it.count) * RW * 8), &bar[0]);
+    if (lane < min(B, it.count)) cp_async8(&cib[0][lane], CIit + lane);
+    cp_async_commit();
+
+    // footprint fragments straight from the grid (same permuted layout as load_fragments)
+    double gf[18][3];
+    {
+        const int c0 = it.sc & 1023, c1 = (it.sc >> 10) & 1023, c2 = (it.sc >> 20) & 1023;
+        const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
+        const int nn = lane >> 2, kk = lane & 3;
+        const int qq = nn >> 1, e = nn & 1;
+        int z[3];
+#pragma unroll
+        for (int ks = 0; ks < 3; ++ks) z[ks] = wrap(c2 - (T / 2 - 1) + 4 * ks + kk, n);
+#pragma unroll
+        for (int t = 0; t < 18; ++t) {
+            const int i = 2 * t + e;
+            const int a = i / 3, b = 3 * qq + i % 3;
+            const int64_t rowb = ((int64_t)wrap(c0 - (T / 2 - 1) + a, n) * n + wrap(c1 - (T / 2 - 1) + b, n)) * n;
+#pragma unroll
+            for (int ks = 0; ks < 3; ++ks) gf[t][ks] = __ldg(g + rowb + z[ks]);
+        }
+    }
+    const double sc = scale[it.window];
+    double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * ldo;
+
+    for (int bi = 0; bi < nbatch; ++bi) {
+        const int s = bi & 1;
+        const int off = bi * B;
+        const int nb = min(B, it.count - off);
+        cp_async_wait_all();
+        mbar_wait(&bar[s], (bi >> 1) & 1);
+        __syncwarp();
+        if (bi + 1 < nbatch) {
+            const int nb1 = min(B, it.count - off - B);
+            if (lane == 0) {
+                fence_proxy_async();
+                tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + B) * RW, (unsigned)(nb1 * RW * 8), &bar[s ^ 1]);
+            }
+            if (lane < nb1) cp_async8(&cib[s ^ 1][lane], CIit + off + B + lane);
+        }
+        cp_async_commit();
+        for (int k0 = 0; k0 < nb; k0 += 8) {
+            const int cnt = min(8, nb - k0);
+            double v = interp_group_mma<RW>(gf, wbuf[s], k0, cnt, lane);
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            const int pj = lane >> 2;
+            if ((lane & 3) == 0 && pj < cnt) {
+                double* dst = o + cib[s][k0 + pj].idx;
+                if (atomic_out) red_add(dst, sc * v);
+                else *dst = sc * v;
+            }
+        }
+    }
+}
+
+}  // namespace ak

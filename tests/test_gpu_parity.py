@@ -178,6 +178,8 @@ def test_native_library_is_what_runs(cuda):
     {"AK_IWARPS": "2"},                     # two-warp interp CTAs sharing the region tile
     {"AK_SUPERCELL3": "4", "AK_CHUNK3": "256", "AK_SORT_ITEMS": "0"},
     {"AK_BATCH3": "32", "AK_VREG": "1"},
+    {"AK_SUPERCELL3": "1"},                 # single-cell work items (auto-selected for dense data)
+    {"AK_SUPERCELL3": "1", "AK_BATCH3": "16", "AK_CHUNK3": "100"},
 ])
 def test_kernel_variants_match_reference(cuda, monkeypatch, variant):
     """Every tuned kernel variant (selected at plan time) reproduces the reference."""
