@@ -127,12 +127,15 @@ k_spread3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
 #pragma unroll
     for (int c = 0; c < P2; ++c) x2[c] = wrap(c2 - (T / 2 - 1) + g2 * P2 + c, n);
 #pragma unroll
-    for (int a = 0; a < P0; ++a)
+    for (int a = 0; a < P0; ++a) {
+        const double* plane = g + (int64_t)x0[a] * n * n;
 #pragma unroll
-        for (int b = 0; b < P1; ++b)
+        for (int b = 0; b < P1; ++b) {
+            double* row = const_cast<double*>(plane) + x1[b] * n;
 #pragma unroll
-            for (int c = 0; c < P2; ++c)
-                red_add(g + ((int64_t)x0[a] * n + x1[b]) * n + x2[c], acc[a][b][c]);
+            for (int c = 0; c < P2; ++c) red_add(row + x2[c], acc[a][b][c]);
+        }
+    }
 }
 
 template <int B>
