@@ -23,6 +23,7 @@
 #include "ak_q3w.cuh"
 #include "ak_q3m.cuh"
 #include "ak_q3c.cuh"
+#include "ak_q2c.cuh"
 
 using namespace ak;
 
@@ -100,7 +101,10 @@ struct ak_geom {
     bool imma = true;                   // q=3 interp on FP64 tensor cores (mma.sync m8n8k4; AK_IMMA=0: DFMA)
     double* W3 = nullptr;               // [P3][N][3T]
     CellIdx* CI3 = nullptr;             // [P3][N]
-    int64_t* wshift_d = nullptr;        // per window: (w - rank3(w)) * N
+    bool cached2 = false;               // 2-D weight table present (ak_q2c.cuh kernels)
+    double* W2 = nullptr;               // [P2][N][2T]
+    CellIdx* CI2 = nullptr;             // [P2][N]
+    int64_t* wshift_d = nullptr;        // per window: (w - rank_q(w)) * N, rank among windows of its q
 };
 
 // AK_WEIGHTS=horner disables the plan-time weight table (weights evaluated per pass).
@@ -136,6 +140,20 @@ static int supercell3_default() {
 static double dense_cell_threshold() {
     const char* e = getenv("AK_DENSE_CELLS");
     return e ? atof(e) : 64.0;
+}
+
+// Supercell edge for 2-D windows: AK_SUPERCELL2=1 forces single-cell items (tensor-core
+// kernels, ak_q2c.cuh), 8 the lane-per-point kernels; unset: chosen by occupancy
+// (mean points per occupied cell >= AK_DENSE_CELLS2, default 2; config 2 at ~5 per cell
+// is 2.6x faster with single-cell items).
+static int supercell2_default() {
+    const char* e = getenv("AK_SUPERCELL2");
+    const int v = e ? atoi(e) : 0;
+    return (v == 1 || v == 8) ? v : 0;
+}
+static double dense_cell_threshold2() {
+    const char* e = getenv("AK_DENSE_CELLS2");
+    return e ? atof(e) : 2.0;
 }
 
 __global__ void k_count_nonzero(const int* __restrict__ counts, int total, int* __restrict__ nz) {
@@ -250,9 +268,41 @@ extern "C" int ak_geom_destroy(ak_geom* g) {
     cudaFree(g->canon_off_d);
     cudaFree(g->W3);
     cudaFree(g->CI3);
+    cudaFree(g->W2);
+    cudaFree(g->CI2);
     cudaFree(g->wshift_d);
     delete g;
     return AK_OK;
+}
+
+// Mean points per occupied cell of window w (bins at S = 1); -1 when the probe fails.
+static double mean_occupancy(const double* X, int64_t ld, const int32_t* cols, int w, int q, int n, int64_t N,
+                             cudaStream_t st)
+{
+    const int tot = (int)ipow_rt(n, q);
+    int *cnt = nullptr, *aux = nullptr;
+    uint32_t* kk = nullptr;
+    int32_t* vv = nullptr;
+    double mean = -1.0;
+    if (cudaMalloc(&cnt, sizeof(int) * tot) == cudaSuccess && cudaMalloc(&aux, sizeof(int) * 2) == cudaSuccess &&
+        cudaMalloc(&kk, sizeof(uint32_t) * N) == cudaSuccess && cudaMalloc(&vv, sizeof(int32_t) * N) == cudaSuccess) {
+        cudaMemsetAsync(cnt, 0, sizeof(int) * tot, st);
+        cudaMemsetAsync(aux, 0, sizeof(int) * 2, st);
+        k_keys<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(X, ld, q, cols[3 * w], cols[3 * w + 1], cols[3 * w + 2],
+                                                             n, 1, n, N, kk, vv, cnt, aux);
+        k_count_nonzero<<<(tot + 255) / 256, 256, 0, st>>>(cnt, tot, aux + 1);
+        g_launches.fetch_add(2);
+        int h[2] = {0, 0};
+        if (cudaMemcpyAsync(h, aux, sizeof(h), cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+            cudaStreamSynchronize(st) == cudaSuccess && h[1] > 0)
+            mean = (double)N / h[1];
+    }
+    cudaGetLastError();
+    cudaFree(cnt);
+    cudaFree(aux);
+    cudaFree(kk);
+    cudaFree(vv);
+    return mean;
 }
 
 static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t ld, cudaStream_t st) {
@@ -276,39 +326,48 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
     // item capacity
     int64_t cap = 0;
     int max_nsc_total = 1;
-    const bool cached = g->wf.taps == 12 && N > 0 && weights_cached_default();
+    bool cached = g->wf.taps == 12 && N > 0 && weights_cached_default();
+    if (cached) {
+        // plan-time weight tables (filled once the points are sorted, below)
+        const int64_t P3 = (int64_t)g->windows_of_q[3].size(), P2 = (int64_t)g->windows_of_q[2].size();
+        const int T = g->wf.taps;
+        bool ok = cudaMalloc(&g->wshift_d, sizeof(int64_t) * P) == cudaSuccess;
+        if (ok && P3 > 0)
+            ok = cudaMalloc(&g->W3, sizeof(double) * P3 * N * 3 * T) == cudaSuccess &&
+                 cudaMalloc(&g->CI3, sizeof(CellIdx) * P3 * N) == cudaSuccess;
+        if (ok && P2 > 0)
+            ok = cudaMalloc(&g->W2, sizeof(double) * P2 * N * 2 * T) == cudaSuccess &&
+                 cudaMalloc(&g->CI2, sizeof(CellIdx) * P2 * N) == cudaSuccess;
+        if (!ok) {
+            cudaGetLastError();  // not enough memory for the tables: evaluate weights per pass
+            cudaFree(g->W3);
+            cudaFree(g->CI3);
+            cudaFree(g->W2);
+            cudaFree(g->CI2);
+            cudaFree(g->wshift_d);
+            g->W3 = g->W2 = nullptr;
+            g->CI3 = g->CI2 = nullptr;
+            g->wshift_d = nullptr;
+            cached = false;
+        }
+    }
     int s3 = supercell3_default();
     if (s3 == 1 && !cached) s3 = 2;  // single-cell kernels exist for the cached-weight path only
     if (s3 == 0) {
         s3 = 2;
-        if (cached && !g->windows_of_q[3].empty()) {
-            // occupancy probe on the first 3-D window: bin by cell, count occupied cells
-            const int w = g->windows_of_q[3][0];
-            const int tot = n * n * n;
-            int *cnt = nullptr, *aux = nullptr;
-            uint32_t* kk = nullptr;
-            int32_t* vv = nullptr;
-            if (cudaMalloc(&cnt, sizeof(int) * tot) == cudaSuccess && cudaMalloc(&aux, sizeof(int) * 2) == cudaSuccess &&
-                cudaMalloc(&kk, sizeof(uint32_t) * N) == cudaSuccess && cudaMalloc(&vv, sizeof(int32_t) * N) == cudaSuccess) {
-                cudaMemsetAsync(cnt, 0, sizeof(int) * tot, st);
-                cudaMemsetAsync(aux, 0, sizeof(int) * 2, st);
-                k_keys<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(X, ld, 3, cols[3 * w], cols[3 * w + 1],
-                                                                     cols[3 * w + 2], n, 1, n, N, kk, vv, cnt, aux);
-                k_count_nonzero<<<(tot + 255) / 256, 256, 0, st>>>(cnt, tot, aux + 1);
-                g_launches.fetch_add(2);
-                int h[2] = {0, 0};
-                if (cudaMemcpyAsync(h, aux, sizeof(h), cudaMemcpyDeviceToHost, st) == cudaSuccess &&
-                    cudaStreamSynchronize(st) == cudaSuccess && h[1] > 0 &&
-                    (double)N / h[1] >= dense_cell_threshold())
-                    s3 = 1;
-            }
-            cudaGetLastError();
-            cudaFree(cnt);
-            cudaFree(aux);
-            cudaFree(kk);
-            cudaFree(vv);
-        }
+        if (cached && !g->windows_of_q[3].empty() &&
+            mean_occupancy(X, ld, cols, g->windows_of_q[3][0], 3, n, N, st) >= dense_cell_threshold())
+            s3 = 1;
     }
+    int s2 = supercell2_default();
+    if (s2 == 1 && !cached) s2 = 8;
+    if (s2 == 0) {
+        s2 = 8;
+        if (cached && !g->windows_of_q[2].empty() &&
+            mean_occupancy(X, ld, cols, g->windows_of_q[2][0], 2, n, N, st) >= dense_cell_threshold2())
+            s2 = 1;
+    }
+    g->sedge[2] = s2;
     g->sedge[3] = s3;
     for (int w = 0; w < P; ++w) {
         const int S = g->sedge[g->q[w]];
@@ -408,33 +467,32 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
         }
     }
     g->nitems = host_counter;
-    if (rc == AK_OK && g->wf.taps == 12 && !g->windows_of_q[3].empty() && N > 0 && weights_cached_default()) {
+    if (rc == AK_OK && cached) {
         const int T = g->wf.taps;
-        const int64_t P3 = (int64_t)g->windows_of_q[3].size();
         std::vector<int64_t> shift(P, 0);
-        if (cudaMalloc(&g->W3, sizeof(double) * P3 * N * 3 * T) == cudaSuccess &&
-            cudaMalloc(&g->CI3, sizeof(CellIdx) * P3 * N) == cudaSuccess &&
-            cudaMalloc(&g->wshift_d, sizeof(int64_t) * P) == cudaSuccess) {
+        for (int q = 3; q >= 2 && rc == AK_OK; --q) {
             int64_t rank = 0;
-            for (int w : g->windows_of_q[3]) {
+            for (int w : g->windows_of_q[q]) {
                 shift[w] = ((int64_t)w - rank) * N;
-                k_weights3<12><<<(unsigned)((N + 127) / 128), 128, 0, st>>>(g->pts + (int64_t)w * N, N, g->wf,
-                                                                          g->W3 + rank * N * 3 * T,
-                                                                          g->CI3 + rank * N);
+                const unsigned nb = (unsigned)((N + 127) / 128);
+                if (q == 3)
+                    k_weights<3, 12><<<nb, 128, 0, st>>>(g->pts + (int64_t)w * N, N, g->wf, g->W3 + rank * N * 3 * T,
+                                                         g->CI3 + rank * N);
+                else
+                    k_weights<2, 12><<<nb, 128, 0, st>>>(g->pts + (int64_t)w * N, N, g->wf, g->W2 + rank * N * 2 * T,
+                                                         g->CI2 + rank * N);
                 if ((rc = launched()) != AK_OK) break;
                 ++rank;
             }
-            if (rc == AK_OK &&
-                cudaMemcpyAsync(g->wshift_d, shift.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice, st) == cudaSuccess)
-                g->cached = true;
-        } else {
-            cudaGetLastError();  // not enough memory for the table: evaluate weights per pass
-            cudaFree(g->W3);
-            cudaFree(g->CI3);
-            cudaFree(g->wshift_d);
-            g->W3 = nullptr;
-            g->CI3 = nullptr;
-            g->wshift_d = nullptr;
+        }
+        if (rc == AK_OK) {
+            if (cudaMemcpyAsync(g->wshift_d, shift.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice, st) ==
+                cudaSuccess) {
+                g->cached = g->W3 != nullptr;
+                g->cached2 = g->W2 != nullptr;
+            } else {
+                rc = fail(AK_ERR_CUDA, "weight table setup failed");
+            }
         }
         g->batch3 = batch3_default(g->sedge[3]);
         const char* iw = getenv("AK_IWARPS");
@@ -648,7 +706,7 @@ static void launch_spread3_t(const ak_geom* g, int64_t i0, int64_t ni, const dou
                              double* grids, cudaStream_t st)
 {
     if (T == 12 && g->cached && g->sedge[3] == 1) {
-        dim3 grid((unsigned)ni, (unsigned)R);
+        const unsigned grid = (unsigned)(ni * R);  // item-major, RHS fastest
         if (g->batch3 == 32)
             k_spread3c<32><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
                                                 g->canon_off_d, R, g->n);
@@ -705,6 +763,9 @@ static int spread_group(const ak_geom* g, int q, const double* V, int R, int64_t
     if (!force_generic() && ni > 0) {
         done = true;
         if (q == 3 && (T == 12 || T == 8 || T == 4)) launch_spread3(g, i0, ni, V, R, ldv, grids, st);
+        else if (q == 2 && T == 12 && g->cached2 && g->sedge[2] == 1)
+            k_spread2c<32><<<(unsigned)(ni * R), 32, 0, st>>>(g->CI2, g->W2, g->wshift_d, g->items + i0, V,
+                                                                           ldv, grids, g->canon_off_d, R, g->n);
         else if (q == 2 && T == 12) launch_spread_tile<2, 12>(g, i0, ni, V, R, ldv, grids, st);
         else if (q == 2 && T == 8) launch_spread_tile<2, 8>(g, i0, ni, V, R, ldv, grids, st);
         else if (q == 2 && T == 16) launch_spread_tile<2, 16>(g, i0, ni, V, R, ldv, grids, st);
@@ -784,7 +845,7 @@ static void launch_interp3_t(const ak_geom* g, int64_t i0, int64_t ni, const dou
                              cudaStream_t st)
 {
     if (T == 12 && g->cached && g->sedge[3] == 1) {
-        dim3 grid((unsigned)ni, (unsigned)R);
+        const unsigned grid = (unsigned)(ni * R);  // item-major, RHS fastest
         if (g->batch3 == 32)
             k_interp3c<32><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids, g->canon_off_d, R,
                                                 g->n, scale, out, ldo, atomic_out, wstride);
@@ -838,6 +899,10 @@ static int interp_group(const ak_geom* g, int q, const double* grids, int R, con
         done = true;
         if (q == 3 && (T == 12 || T == 8 || T == 4))
             launch_interp3(g, i0, ni, grids, R, scale, out, ldo, atomic_out, ws, st);
+        else if (q == 2 && T == 12 && g->cached2 && g->sedge[2] == 1)
+            k_interp2c<32><<<(unsigned)(ni * R), 32, 0, st>>>(g->CI2, g->W2, g->wshift_d, g->items + i0,
+                                                                           grids, g->canon_off_d, R, g->n, scale, out,
+                                                                           ldo, atomic_out, ws);
 #define AK_LANE(QQ, TT) \
         else if (q == QQ && T == TT) launch_interp_lane<QQ, TT>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, ws, st);
         AK_LANE(2, 4) AK_LANE(2, 6) AK_LANE(2, 8) AK_LANE(2, 10) AK_LANE(2, 12) AK_LANE(2, 14) AK_LANE(2, 16)
@@ -855,8 +920,16 @@ static int interp_group(const ak_geom* g, int q, const double* grids, int R, con
     return AK_OK;
 }
 
+// Launch-shape limits: RHS on grid.y (<= 65535) or folded into grid.x with the items.
+static int check_rhs(const ak_geom* g, int R) {
+    if (R > 65535 || g->nitems * (int64_t)R >= ((int64_t)1 << 31))
+        return fail(AK_ERR_UNSUPPORTED, "too many right-hand sides for one call (R <= 65535, items x R < 2^31)");
+    return AK_OK;
+}
+
 extern "C" int ak_spread(const ak_geom* g, const double* V, int32_t R, int64_t ldv, double* grids, void* stream) {
     if (!g || R < 1 || (g->N > 0 && (!V || !grids))) return fail(AK_ERR_INVALID, "bad spread arguments");
+    AK_TRY(check_rhs(g, R));
     cudaStream_t st = (cudaStream_t)stream;
     for (int q = 3; q >= 1; --q) AK_TRY(spread_group(g, q, V, R, ldv, grids, st));
     return AK_OK;
@@ -866,6 +939,7 @@ extern "C" int ak_interp(const ak_geom* g, const double* grids, int32_t R, const
                          int64_t ldo, int32_t sum_windows, int64_t wstride, void* stream)
 {
     if (!g || R < 1 || !scale || (g->N > 0 && (!grids || !out))) return fail(AK_ERR_INVALID, "bad interp arguments");
+    AK_TRY(check_rhs(g, R));
     cudaStream_t st = (cudaStream_t)stream;
     for (int q = 3; q >= 1; --q)
         AK_TRY(interp_group(g, q, grids, R, scale, out, ldo, sum_windows, sum_windows ? 1 : 0, wstride, st));
@@ -1038,6 +1112,8 @@ extern "C" int ak_op_create(const ak_geom* spread_geom, const ak_geom* interp_ge
     if (m < 2 || m % 2 || m > spread_geom->n) return fail(AK_ERR_INVALID, "m must be even, 2 <= m <= n");
     if (interp_geom->n != spread_geom->n || interp_geom->q != spread_geom->q)
         return fail(AK_ERR_INVALID, "spread and interp geometries must share windows and n");
+    AK_TRY(check_rhs(spread_geom, R));
+    AK_TRY(check_rhs(interp_geom, R));
     ak_op* op = new ak_op();
     op->gs = spread_geom;
     op->gi = interp_geom;

@@ -1,33 +1,33 @@
-// q = 3 kernels for single-cell work items (supercell edge S = 1).
+// q = 2 kernels for single-cell work items on the FP64 tensor cores (T = 12).
 //
-// When cells are densely populated (config 4: 395 points per occupied cell on
-// average) every work item can be one cell (or a chunk of one): the warp's
-// register tile IS the item's footprint, so there is no shared region tile, no
-// cell-run bookkeeping, no shared-memory flushes:
-//   spread : register-tiled FMAs over all points of the item, then 54 RED.F64
-//            per lane straight from registers to the grid;
-//   interp : the footprint fragments are loaded once per item from the grid
-//            (L2) and every batch is processed in groups of 8 points on the
-//            FP64 tensor cores (ak_q3m.cuh).
-// Shared memory shrinks to the double-buffered weight rows, which allows more
-// warps per SM.  The plan picks these kernels when the mean occupancy of the
-// occupied cells is high (ak_lib.cu: geom_build).
+// A 2-D footprint is a 12 x 12 tile; per cell both directions are small GEMMs
+// over the cell's points j (weights w0_j, w1_j from the plan-time table, rows of
+// 24 doubles: [w0 | w1]):
+//   spread : G[a][b] += sum_j (v_j w0_j[a]) w1_j[b]      M = a, N = b, K = points
+//            4 DMMA (m8n8k4: 2 row tiles x 2 column tiles, 16 x 16 padded) per 4
+//            points; C (8 doubles per lane) is flushed with RED.F64 at the end.
+//   interp : U[j][a] = sum_b w1_j[b] G[a][b]           M = points, N = a, K = b
+//            6 DMMA (2 column tiles x 3 k-steps) per 8 points; the columns are
+//            permuted so lane quad q holds a in {3q, 3q+1, 3q+2}, and
+//            out_j = sum_a w0_j[a] U[j][a] is 3 FMAs + a 2-step quad shuffle.
+// Compared with the lane-per-point kernels (ak_kernels.cuh) this removes the
+// per-point window polynomials (~180 FP64 ops, more than the 144 useful FMAs)
+// and almost all instruction issue: the tensor pipe does the contraction.
+// Padding costs 25% (interp) / 44% (spread) of the DMMA slots.
 #pragma once
 #include "ak_q3m.cuh"
 
 namespace ak {
 
 template <int B>
-__global__ void __launch_bounds__(32, 8)
-k_spread3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
+__global__ void __launch_bounds__(32, 16)
+k_spread2c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ V, int64_t ldv,
            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
 {
     constexpr int T = 12;
-    using LN = Q3Lanes<T>;
-    constexpr int P0 = LN::P0, P1 = LN::P1, P2 = LN::P2;
-    constexpr int RW = 3 * T;
-    static_assert(B <= 32, "batch");
+    constexpr int RW = 2 * T;
+    static_assert(B % 4 == 0 && B <= 32, "batch");
 
     __shared__ __align__(128) double wbuf[2][B][RW];
     __shared__ __align__(16) CellIdx cib[3][B];
@@ -38,7 +38,6 @@ k_spread3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     const WorkItem it = items[blockIdx.x / nrhs];
     const int r = blockIdx.x % nrhs;
     const int lane = threadIdx.x;
-    const int g0 = lane >> 4, g1 = (lane >> 2) & 3, g2 = lane & 3;
     const double* __restrict__ Vr = V + (int64_t)r * ldv;
     const int nbatch = (it.count + B - 1) / B;
     const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
@@ -59,13 +58,12 @@ k_spread3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     if (lane < min(B, it.count)) cp_async8(&vb[0][lane], Vr + cib[0][lane].idx);
     cp_async_commit();
 
-    double acc[P0][P1][P2];
+    const int rn = lane >> 2, kq = lane & 3;
+    double C[2][2][2];
 #pragma unroll
-    for (int a = 0; a < P0; ++a)
+    for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int b = 0; b < P1; ++b)
-#pragma unroll
-            for (int c = 0; c < P2; ++c) acc[a][b][c] = 0.0;
+        for (int nt = 0; nt < 2; ++nt) C[mt][nt][0] = C[mt][nt][1] = 0.0;
 
     for (int bi = 0; bi < nbatch; ++bi) {
         const int s = bi & 1;
@@ -85,69 +83,50 @@ k_spread3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         if (bi + 2 < nbatch && lane < min(B, it.count - off - 2 * B))
             cp_async8(&cib[(bi + 2) % 3][lane], CIit + off + 2 * B + lane);
         cp_async_commit();
-        {
-            constexpr int PER = (B * T + 31) / 32;
-            double x[PER], y[PER];
-#pragma unroll
-            for (int i = 0; i < PER; ++i) {
-                const int e = lane + 32 * i;
-                const int row = e / T;
-                if (row < nb) {
-                    x[i] = wbuf[s][row][e - row * T];
-                    y[i] = vb[s][row];
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < PER; ++i) {
-                const int e = lane + 32 * i;
-                const int row = e / T;
-                if (row < nb) wbuf[s][row][e - row * T] = x[i] * y[i];
-            }
+#pragma unroll 4
+        for (int k0 = 0; k0 < nb; k0 += 4) {
+            const int j = k0 + kq;
+            const bool valid = j < nb;
+            const double* w = wbuf[s][valid ? j : 0];
+            const double v = valid ? vb[s][j] : 0.0;    // zero rows pad the last k-step
+            const double a0 = v * w[rn];
+            const double a1 = rn < 4 ? v * w[8 + rn] : 0.0;
+            const double b0 = w[T + rn];
+            const double b1 = rn < 4 ? w[T + 8 + rn] : 0.0;
+            dmma_8x8x4(C[0][0][0], C[0][0][1], a0, b0);
+            dmma_8x8x4(C[0][1][0], C[0][1][1], a0, b1);
+            dmma_8x8x4(C[1][0][0], C[1][0][1], a1, b0);
+            dmma_8x8x4(C[1][1][0], C[1][1][1], a1, b1);
         }
-        __syncwarp();
-        double a0[P0], a1[P1], a2[P2], b0[P0], b1[P1], b2[P2];
-        load_w<T>(a0, a1, a2, &wbuf[s][0][0], g0, g1, g2);
-        int j = 0;
-        for (; j + 1 < nb; j += 2) {
-            load_w<T>(b0, b1, b2, &wbuf[s][j + 1][0], g0, g1, g2);
-            spread_fma(acc, a0, a1, a2);
-            load_w<T>(a0, a1, a2, &wbuf[s][j + 2 < nb ? j + 2 : j + 1][0], g0, g1, g2);
-            spread_fma(acc, b0, b1, b2);
-        }
-        if (j < nb) spread_fma(acc, a0, a1, a2);
     }
 
-    // flush the register tile straight to the grid
-    const int c0 = it.sc & 1023, c1 = (it.sc >> 10) & 1023, c2 = (it.sc >> 20) & 1023;
-    double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
-    int x0[P0], x1[P1], x2[P2];
+    // lane holds G[a = rn + 8 mt][b = 2 kq + e + 8 nt]
+    const int c0 = it.sc & 1023, c1 = (it.sc >> 10) & 1023;
+    double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n;
 #pragma unroll
-    for (int a = 0; a < P0; ++a) x0[a] = wrap(c0 - (T / 2 - 1) + g0 * P0 + a, n);
+    for (int mt = 0; mt < 2; ++mt) {
+        const int a = rn + 8 * mt;
+        if (a >= T) continue;
+        double* row = g + (int64_t)wrap(c0 - (T / 2 - 1) + a, n) * n;
 #pragma unroll
-    for (int b = 0; b < P1; ++b) x1[b] = wrap(c1 - (T / 2 - 1) + g1 * P1 + b, n);
+        for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-    for (int c = 0; c < P2; ++c) x2[c] = wrap(c2 - (T / 2 - 1) + g2 * P2 + c, n);
-#pragma unroll
-    for (int a = 0; a < P0; ++a) {
-        const double* plane = g + (int64_t)x0[a] * n * n;
-#pragma unroll
-        for (int b = 0; b < P1; ++b) {
-            double* row = const_cast<double*>(plane) + x1[b] * n;
-#pragma unroll
-            for (int c = 0; c < P2; ++c) red_add(row + x2[c], acc[a][b][c]);
-        }
+            for (int e = 0; e < 2; ++e) {
+                const int b = 2 * kq + e + 8 * nt;
+                if (b < T) red_add(row + wrap(c1 - (T / 2 - 1) + b, n), C[mt][nt][e]);
+            }
     }
 }
 
 template <int B>
-__global__ void __launch_bounds__(32, 8)
-k_interp3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
+__global__ void __launch_bounds__(32, 16)
+k_interp2c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ grids,
            const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,
            double* __restrict__ out, int64_t ldo, int atomic_out, int64_t wstride)
 {
     constexpr int T = 12;
-    constexpr int RW = 3 * T;
+    constexpr int RW = 2 * T;
     static_assert(B % 8 == 0 && B <= 32, "batch");
 
     __shared__ __align__(128) double wbuf[2][B][RW];
@@ -172,27 +151,28 @@ k_interp3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     if (lane < min(B, it.count)) cp_async8(&cib[0][lane], CIit + lane);
     cp_async_commit();
 
-    // footprint fragments straight from the grid (same permuted layout as load_fragments)
-    double gf[18][3];
+    // B fragments: column n = lane/4 of tile t is a = 3 (n >> 1) + 2 t + (n & 1) (invalid: 2t + (n&1) = 3),
+    // row k = lane%4 of k-step ks is b = 4 ks + k
+    double gf[2][3];
     {
-        const int c0 = it.sc & 1023, c1 = (it.sc >> 10) & 1023, c2 = (it.sc >> 20) & 1023;
-        const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
+        const int c0 = it.sc & 1023, c1 = (it.sc >> 10) & 1023;
+        const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n;
         const int nn = lane >> 2, kk = lane & 3;
-        const int qq = nn >> 1, e = nn & 1;
         int z[3];
 #pragma unroll
-        for (int ks = 0; ks < 3; ++ks) z[ks] = wrap(c2 - (T / 2 - 1) + 4 * ks + kk, n);
+        for (int ks = 0; ks < 3; ++ks) z[ks] = wrap(c1 - (T / 2 - 1) + 4 * ks + kk, n);
 #pragma unroll
-        for (int t = 0; t < 18; ++t) {
-            const int i = 2 * t + e;
-            const int a = i / 3, b = 3 * qq + i % 3;
-            const int64_t rowb = ((int64_t)wrap(c0 - (T / 2 - 1) + a, n) * n + wrap(c1 - (T / 2 - 1) + b, n)) * n;
+        for (int t = 0; t < 2; ++t) {
+            const int i = 2 * t + (nn & 1);
+            const int a = 3 * (nn >> 1) + i;
+            const double* row = g + (int64_t)wrap(c0 - (T / 2 - 1) + (i < 3 ? a : 0), n) * n;
 #pragma unroll
-            for (int ks = 0; ks < 3; ++ks) gf[t][ks] = __ldg(g + rowb + z[ks]);
+            for (int ks = 0; ks < 3; ++ks) gf[t][ks] = i < 3 ? __ldg(row + z[ks]) : 0.0;
         }
     }
     const double sc = scale[it.window];
     double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * ldo;
+    const int pj = lane >> 2, q = lane & 3;
 
     for (int bi = 0; bi < nbatch; ++bi) {
         const int s = bi & 1;
@@ -210,13 +190,25 @@ k_interp3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
             if (lane < nb1) cp_async8(&cib[s ^ 1][lane], CIit + off + B + lane);
         }
         cp_async_commit();
+#pragma unroll 2
         for (int k0 = 0; k0 < nb; k0 += 8) {
             const int cnt = min(8, nb - k0);
-            double v = interp_group_mma<RW>(gf, wbuf[s], k0, cnt, lane);
+            const bool valid = pj < cnt;
+            const double* w = wbuf[s][k0 + (valid ? pj : 0)];
+            double C[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+            for (int ks = 0; ks < 3; ++ks) {
+                const double af = valid ? w[T + 4 * ks + q] : 0.0;
+                dmma_8x8x4(C[0][0], C[0][1], af, gf[0][ks]);
+                dmma_8x8x4(C[1][0], C[1][1], af, gf[1][ks]);
+            }
+            // lane (pj, q) holds U[pj][3q + i], i = 2t + e (i = 3 is padding)
+            double v = w[3 * q] * C[0][0];
+            v = fma(w[3 * q + 1], C[0][1], v);
+            v = fma(w[3 * q + 2], C[1][0], v);
             v += __shfl_xor_sync(0xffffffffu, v, 1);
             v += __shfl_xor_sync(0xffffffffu, v, 2);
-            const int pj = lane >> 2;
-            if ((lane & 3) == 0 && pj < cnt) {
+            if (q == 0 && valid) {
                 double* dst = o + cib[s][k0 + pj].idx;
                 if (atomic_out) red_add(dst, sc * v);
                 else *dst = sc * v;

@@ -1,7 +1,7 @@
 // q = 3 spread / interpolation with plan-time window weights ("cached" mode).
 //
 // The window weights of a 3-D window depend only on the nodes, so the plan
-// tabulates them once (k_weights3: 3*T doubles per point, in bin-sorted
+// tabulates them once (k_weights: q*T doubles per point, in bin-sorted
 // order, with the same per-tap polynomial the on-the-fly kernels use) and
 // the per-product kernels stream them instead of re-evaluating 36 window
 // polynomials per point per pass.  That removes ~12% of the FP64 work and the
@@ -60,30 +60,30 @@ __device__ __forceinline__ void tma_load_1d(void* smem, const void* gmem, unsign
 }
 
 // Plan time: weight rows (axis-major: w0[0..T), w1[0..T), w2[0..T)) and
-// (cell, row) records of the points of 3-D windows, compact per-window layout.
-template <int T>
-__global__ void __launch_bounds__(128) k_weights3(const Point* __restrict__ pts, int64_t np, const ak_window_fn wf,
-                                                 double* __restrict__ W, CellIdx* __restrict__ CI)
+// (cell, row) records of the points of 2-D / 3-D windows, compact per-window layout.
+template <int Q, int T>
+__global__ void __launch_bounds__(128) k_weights(const Point* __restrict__ pts, int64_t np, const ak_window_fn wf,
+                                                double* __restrict__ W, CellIdx* __restrict__ CI)
 {
     // 128 points per block: weights evaluated per thread (unrolled polynomials) into
-    // shared memory, then the block's contiguous [128][3T] slice is stored coalesced.
-    __shared__ double st[128 * 3 * T];
+    // shared memory, then the block's contiguous [128][Q T] slice is stored coalesced.
+    __shared__ double st[128 * Q * T];
     const int64_t p0 = (int64_t)blockIdx.x * 128;
     const int64_t j = p0 + threadIdx.x;
     if (j < np) {
         const Point p = pts[j];
         double w[T];
 #pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
+        for (int ax = 0; ax < Q; ++ax) {
             window_weights<T>(wf, p.s[ax], w);
 #pragma unroll
-            for (int a = 0; a < T; ++a) st[threadIdx.x * 3 * T + ax * T + a] = w[a];
+            for (int a = 0; a < T; ++a) st[threadIdx.x * Q * T + ax * T + a] = w[a];
         }
         CI[j] = CellIdx{p.cell, p.idx};
     }
     __syncthreads();
-    const int64_t cnt = (np - p0 < 128 ? np - p0 : 128) * 3 * T;
-    for (int64_t e = threadIdx.x; e < cnt; e += 128) W[p0 * 3 * T + e] = st[e];
+    const int64_t cnt = (np - p0 < 128 ? np - p0 : 128) * Q * T;
+    for (int64_t e = threadIdx.x; e < cnt; e += 128) W[p0 * Q * T + e] = st[e];
 }
 
 // acc += v * w0 (x) w1 (x) w2 with v folded into the w1 factor in registers

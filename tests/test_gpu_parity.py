@@ -194,3 +194,30 @@ def test_kernel_variants_match_reference(cuda, monkeypatch, variant):
         assert rel(res["K"], g["K_default"]) <= TOL, (variant, name)
         if "dK_dell_default" in g:
             assert rel(res["dK_dell"], g["dK_dell_default"]) <= TOL, (variant, name)
+
+
+@pytest.mark.parametrize("sc2", ["1", "8"])
+def test_q2_item_kernels_match_reference(cuda, monkeypatch, sc2):
+    """2-D windows through the single-cell tensor-core kernels (AK_SUPERCELL2=1) and the
+    lane-per-point kernels (8): configs 2 and 5 and the q = 2 NUFFT goldens."""
+    from paper_2404_17344_b200.fastsum import build_mixed_plan, fast_matvecs, mixed_matvecs
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.nufft import NufftPlan, nufft_type1, nufft_type2, prepare_points
+
+    monkeypatch.setenv("AK_SUPERCELL2", sc2)
+    g = golden("c2")
+    res = fast_matvecs(_plan(g), g["V"], dell=True)
+    assert rel(res["K"], g["K_default"]) <= TOL
+    assert rel(res["dK_dell"], g["dK_dell_default"]) <= TOL
+    g = golden("c5")
+    specs = [KernelSpec(str(f), float(l), 1.0) for f, l in zip(g["families"], g["ells"])]
+    res = mixed_matvecs(build_mixed_plan(specs, _ws(g), "default", _ds(g["X"], g["d_max"])), g["V"])
+    assert rel(res["K"], g["K_default"]) <= TOL
+    for w in range(len(specs)):
+        assert rel(res["dK_dell"][w], g["dK_dell_default"][w]) <= TOL
+    g = golden("nufft")
+    for m in (8, 16):
+        plan = NufftPlan(dims=2, m=m)
+        geom = prepare_points(plan, g[f"q2_m{m}_pts"])
+        assert rel(nufft_type1(plan, geom, g[f"q2_m{m}_w"]), g[f"q2_m{m}_type1"]) <= TOL
+        assert rel(nufft_type2(plan, geom, g[f"q2_m{m}_c"]), g[f"q2_m{m}_type2"]) <= TOL

@@ -100,8 +100,12 @@ def test_single_point(cuda):
     assert out.shape == (1,)
 
 
-def test_points_on_the_box_boundary_and_wraparound(cuda):
+@pytest.mark.parametrize("items", ["auto", "single_cell"])
+def test_points_on_the_box_boundary_and_wraparound(cuda, monkeypatch, items):
     """Nodes at -1/2, just below +1/2 and on cell boundaries: footprints wrap."""
+    if items == "single_cell":
+        monkeypatch.setenv("AK_SUPERCELL2", "1")
+        monkeypatch.setenv("AK_SUPERCELL3", "1")
     rng = np.random.default_rng(1)
     X = rng.uniform(-0.5, 0.5, size=(600, 6))
     X[:50] = -0.5
@@ -110,8 +114,12 @@ def test_points_on_the_box_boundary_and_wraparound(cuda):
     _oracle_check(X, [(0, 1, 2), (3, 4), (5,)], rng.normal(size=600), ell=0.2)
 
 
-def test_all_points_in_one_cell(cuda):
+@pytest.mark.parametrize("items", ["auto", "single_cell"])
+def test_all_points_in_one_cell(cuda, monkeypatch, items):
     """One heavy cell: exercises work-item chunking (several chunks per supercell)."""
+    if items == "single_cell":
+        monkeypatch.setenv("AK_SUPERCELL2", "1")
+        monkeypatch.setenv("AK_SUPERCELL3", "1")
     rng = np.random.default_rng(2)
     X = 0.001 + 1e-5 * rng.random(size=(5000, 3))
     _oracle_check(X, [(0, 1, 2), (0, 1), (2,)], rng.normal(size=5000))
@@ -122,6 +130,18 @@ def test_clustered_data_many_chunks(cuda):
     X = np.concatenate([0.02 * rng.normal(size=(20000, 3)), rng.uniform(-0.14, 0.14, size=(3000, 3))])
     X = np.clip(X, -0.49, 0.49)
     _oracle_check(X, [(0, 1, 2)], rng.normal(size=X.shape[0]), ell=0.5)
+
+
+def test_dense_2d_windows_tensor_core_items(cuda, monkeypatch):
+    """300k nodes in 2-D windows (mean occupancy ~70 per cell: single-cell tensor-core items
+    chosen automatically) against the oracle and against the lane-per-point kernels."""
+    rng = np.random.default_rng(7)
+    X = rng.uniform(-0.5, 0.5, size=(300_000, 4))
+    v = rng.normal(size=300_000)
+    auto, _ = _oracle_check(X, [(0, 1), (2, 3), (1, 2)], v, family="matern12", ell=0.3)
+    monkeypatch.setenv("AK_SUPERCELL2", "8")
+    lane, _ = _oracle_check(X, [(0, 1), (2, 3), (1, 2)], v, family="matern12", ell=0.3)
+    assert rel(auto, lane) <= 1e-13
 
 
 @pytest.mark.parametrize("preset", ["rough", "fine", 48])
