@@ -14,7 +14,8 @@ from pathlib import Path
 from .errors import NativeLibraryError, PointOutOfDomainError
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libaddkern_b200.so"
+# AK_LIB_PATH: load a variant build instead (tuning experiments, tools/build_variant.py)
+LIB_PATH = Path(os.environ["AK_LIB_PATH"]) if os.environ.get("AK_LIB_PATH") else _PKG / "libaddkern_b200.so"
 
 AK_OK = 0
 AK_ERR_INVALID = -1

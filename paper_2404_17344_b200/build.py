@@ -34,8 +34,10 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines=()) -> Path:
+    """Compile the library (out/defines: variant builds for tuning experiments)."""
+    target = Path(out) if out else LIB
+    if out is None and not force and not _stale():
         return LIB
     cuda_home = Path(_nvcc()).resolve().parent.parent
     cmd = [
@@ -47,15 +49,16 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         *[str(CSRC / s) for s in SOURCES],
         "-L", str(cuda_home / "lib64"), "-lcufft",
         "-Xlinker", f"-rpath,{cuda_home / 'lib64'}",
-        "-o", str(LIB) + ".tmp",
+        *[f"-D{d}" for d in defines],
+        "-o", str(target) + ".tmp",
     ]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode})")
-    os.replace(str(LIB) + ".tmp", LIB)
-    return LIB
+    os.replace(str(target) + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

@@ -68,7 +68,15 @@ __device__ __forceinline__ double window_weight_rt(const ak_window_fn& wf, doubl
     return mirror ? fma(-s, o, e) : fma(s, o, e);
 }
 
+// Periodic grid index.  Every index the kernels form (footprints and supercell
+// regions: S <= 16, T <= 16) lies in [-7, n + 22], so for n >= 32 one conditional
+// add/subtract suffices (a few integer ops instead of a ~20-instruction integer
+// division); n is warp-uniform, the branch does not diverge.
 __device__ __forceinline__ int wrap(int i, int n) {
+    if (n >= 32) {
+        i += i < 0 ? n : 0;
+        return i >= n ? i - n : i;
+    }
     i %= n;
     return i < 0 ? i + n : i;
 }

@@ -17,8 +17,11 @@
 
 namespace ak {
 
+#ifndef AK_SPREAD3C_MINB
+#define AK_SPREAD3C_MINB 8
+#endif
 template <int B>
-__global__ void __launch_bounds__(32, 8)
+__global__ void __launch_bounds__(32, AK_SPREAD3C_MINB)
 k_spread3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ V, int64_t ldv,
            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
@@ -117,24 +120,27 @@ k_spread3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         if (j < nb) spread_fma(acc, a0, a1, a2);
     }
 
-    // flush the register tile straight to the grid
     const int c0 = it.sc & 1023, c1 = (it.sc >> 10) & 1023, c2 = (it.sc >> 20) & 1023;
     double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
-    int x0[P0], x1[P1], x2[P2];
+    {
+        // flush the register tile straight to the grid (a shared-memory staged, row-
+        // coalesced flush measured 3% slower on B200)
+        int x0[P0], x1[P1], x2[P2];
 #pragma unroll
-    for (int a = 0; a < P0; ++a) x0[a] = wrap(c0 - (T / 2 - 1) + g0 * P0 + a, n);
+        for (int a = 0; a < P0; ++a) x0[a] = wrap(c0 - (T / 2 - 1) + g0 * P0 + a, n);
 #pragma unroll
-    for (int b = 0; b < P1; ++b) x1[b] = wrap(c1 - (T / 2 - 1) + g1 * P1 + b, n);
+        for (int b = 0; b < P1; ++b) x1[b] = wrap(c1 - (T / 2 - 1) + g1 * P1 + b, n);
 #pragma unroll
-    for (int c = 0; c < P2; ++c) x2[c] = wrap(c2 - (T / 2 - 1) + g2 * P2 + c, n);
+        for (int c = 0; c < P2; ++c) x2[c] = wrap(c2 - (T / 2 - 1) + g2 * P2 + c, n);
 #pragma unroll
-    for (int a = 0; a < P0; ++a) {
-        const double* plane = g + (int64_t)x0[a] * n * n;
+        for (int a = 0; a < P0; ++a) {
+            double* plane = g + (int64_t)x0[a] * n * n;
 #pragma unroll
-        for (int b = 0; b < P1; ++b) {
-            double* row = const_cast<double*>(plane) + x1[b] * n;
+            for (int b = 0; b < P1; ++b) {
+                double* row = plane + x1[b] * n;
 #pragma unroll
-            for (int c = 0; c < P2; ++c) red_add(row + x2[c], acc[a][b][c]);
+                for (int c = 0; c < P2; ++c) red_add(row + x2[c], acc[a][b][c]);
+            }
         }
     }
 }

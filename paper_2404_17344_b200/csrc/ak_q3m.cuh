@@ -10,10 +10,10 @@
 // lasts, 54 doubles per lane), C = U (18 tiles, 36 doubles per lane).  The
 // B columns are permuted so that lane quad q (lane % 4) holds exactly the
 // pairs (a, b) with b in {3q, 3q+1, 3q+2}, which makes the second stage a
-// compile-time-indexed 48-FMA contraction per lane followed by a 2-step quad
+// compile-time-indexed 39-op contraction per lane followed by a 2-step quad
 // shuffle.  DMMA and DFMA share the FP64 datapath (37 TF/s either way on
 // B200), so the gain is not peak rate but issue pressure: ~135 instructions
-// per 8 points per lane instead of ~700, and 1920 instead of 2144 FP64 slots
+// per 8 points per lane instead of ~700, and 1884 instead of 2144 FP64 slots
 // per point.  Partially filled groups (run ends) are padded with zero rows.
 #pragma once
 #include "ak_q3w.cuh"
@@ -65,24 +65,23 @@ __device__ __forceinline__ double interp_group_mma(const double (&gf)[18][3], co
     for (int ks = 0; ks < 3; ++ks)
 #pragma unroll
         for (int t = 0; t < 18; ++t) dmma_8x8x4(C[t][0], C[t][1], af[ks], gf[t][ks]);
-    // lane (pj, q) holds U[pj][(a, b)] for a = i/3, b = 3q + i%3, i = 2t + e
-    double w0[12], w1[3];
+    // lane (pj, q) holds U[pj][(a, b)] for a = i/3, b = 3q + i%3, i = 2t + e:
+    // out = sum_b w1[b] (sum_a w0[a] U[a][b]) -- 3 chains of 12 FMAs, then 3 more
+    double s[3];
 #pragma unroll
-    for (int a = 0; a < 12; ++a) w0[a] = w[a];
+    for (int bb = 0; bb < 3; ++bb) s[bb] = w[0] * C[bb >> 1][bb & 1];
 #pragma unroll
-    for (int b = 0; b < 3; ++b) w1[b] = w[12 + 3 * q + b];
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};  // 4 independent chains (FMA latency)
+    for (int a = 1; a < 12; ++a) {
+        const double w0a = w[a];
 #pragma unroll
-    for (int a = 0; a < 12; ++a) {
-        double sa = w1[0] * C[(3 * a) >> 1][(3 * a) & 1];
-#pragma unroll
-        for (int bb = 1; bb < 3; ++bb) {
+        for (int bb = 0; bb < 3; ++bb) {
             const int i = 3 * a + bb;
-            sa = fma(w1[bb], C[i >> 1][i & 1], sa);
+            s[bb] = fma(w0a, C[i >> 1][i & 1], s[bb]);
         }
-        acc[a & 3] = fma(w0[a], sa, acc[a & 3]);
     }
-    return valid ? (acc[0] + acc[1]) + (acc[2] + acc[3]) : 0.0;
+    const double* w1 = w + 12 + 3 * q;
+    const double v = fma(w1[2], s[2], fma(w1[1], s[1], w1[0] * s[0]));
+    return valid ? v : 0.0;
 }
 
 template <int S, int B, int NW>
