@@ -229,7 +229,8 @@ def profiled_traffic(kernel: str):
     """dram read+write bytes per launch of `kernel` from the newest committed ncu
     full capture summary (profiles/*_summary.json), or None."""
     best = None
-    for f in sorted((ROOT / "profiles").glob("*_summary.json"), key=lambda p: p.stat().st_mtime):
+    # round tags sort by name: r1 < r1b < ... < r1e < r2
+    for f in sorted((ROOT / "profiles").glob("*_summary.json"), key=lambda p: p.name):
         try:
             data = json.loads(f.read_text())
         except (OSError, ValueError):
