@@ -134,7 +134,7 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
                        32 * NW);
         if (NW > 1) __syncthreads();
         else __syncwarp();
-        for (int i = threadIdx.x; i < TILE; i += 32 * NW) cp_async8(&tile[i], g + region_index_s<R>(widx, i, n));
+        for_region_rows<R>(widx, n, threadIdx.x, 32 * NW, [&](int i, int64_t gi) { cp_async8(&tile[i], g + gi); });
     }
     cp_async_commit();
     cp_async_wait_all();

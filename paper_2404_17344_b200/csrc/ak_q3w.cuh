@@ -115,10 +115,24 @@ __device__ __forceinline__ void region_axes(int (*widx)[R], int o0, int o1, int 
     }
 }
 
-template <int R>
-__device__ __forceinline__ int64_t region_index_s(const int (*widx)[R], int i, int n) {
-    const int i2 = i % R, i1 = (i / R) % R, i0 = i / (R * R);
-    return ((int64_t)widx[0][i0] * n + widx[1][i1]) * n + widx[2][i2];
+// Visit the R^3 region tile row by row: a warp pass covers 32 / R whole rows (lane
+// = row-in-pass x element), so the per-element index work is two shared loads and
+// an add instead of three constant divisions.  f(tile index, grid index).
+// Measured on sparse data (config 3, ~15 points per cell): the element-wise loop
+// was a quarter of the spread time.
+template <int R, typename F>
+__device__ __forceinline__ void for_region_rows(const int (*widx)[R], int n, int tid, int nthreads, F&& f) {
+    static_assert(R <= 32, "region row must fit a warp");
+    constexpr int RPP = 32 / R;
+    const int lane = tid & 31;
+    const int sub = lane / R, k = lane - sub * R;
+    if (sub >= RPP) return;
+    const int z = widx[2][k];
+    const int step = (nthreads >> 5) * RPP;
+    for (int row = (tid >> 5) * RPP + sub; row < R * R; row += step) {
+        const int i0 = row / R, i1 = row - i0 * R;
+        f(row * R + k, ((int64_t)widx[0][i0] * n + widx[1][i1]) * n + z);
+    }
 }
 
 template <int T, int S, int B, bool VREG = false>
@@ -282,10 +296,10 @@ k_spread3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
     region_axes<R>(widx, sc0 * S - (T / 2 - 1), sc1 * S - (T / 2 - 1), sc2 * S - (T / 2 - 1), n, lane, 32);
     __syncwarp();
-    for (int i = lane; i < TILE; i += 32) {
+    for_region_rows<R>(widx, n, lane, 32, [&](int i, int64_t gi) {
         const double val = tile[i];
-        if (val != 0.0) red_add(g + region_index_s<R>(widx, i, n), val);
-    }
+        if (val != 0.0) red_add(g + gi, val);
+    });
     (void)end;
 }
 
@@ -520,7 +534,7 @@ k_interp3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
                        32 * NW);
         if (NW > 1) __syncthreads();
         else __syncwarp();
-        for (int i = threadIdx.x; i < TILE; i += 32 * NW) cp_async8(&tile[i], g + region_index_s<R>(widx, i, n));
+        for_region_rows<R>(widx, n, threadIdx.x, 32 * NW, [&](int i, int64_t gi) { cp_async8(&tile[i], g + gi); });
     }
     cp_async_commit();
     cp_async_wait_all();
