@@ -137,3 +137,20 @@ def test_oracle_gsi_matches_reference():
             thetas[key] = thetas.get(key, 0.0) + float(power[mask].sum())
     got = np.array([thetas[k] for k in gg["keys"]])
     assert rel(got, gg["thetas"]) <= 1e-12
+
+
+def test_chunked_oracle_equals_plain():
+    """The bench reference arm's row-chunked, thread-pooled product equals the plain oracle."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import restate as R
+
+    rng = np.random.default_rng(11)
+    X = rng.uniform(-0.14, 0.14, size=(700, 6))
+    v = rng.normal(size=700)
+    windows = [(0, 1, 2), (3, 4), (5,)]
+    plain = R.FastSum("gauss", 0.3, 1.0, windows, X).matvec(v)
+    chunked = R.ChunkedFastSum("gauss", 0.3, 1.0, windows, X, chunks=3)
+    with ThreadPoolExecutor(4) as pool:
+        out = chunked.matvec_pool(v, pool)
+    assert np.linalg.norm(out - plain) <= 1e-13 * np.linalg.norm(plain)
