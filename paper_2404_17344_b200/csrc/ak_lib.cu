@@ -450,8 +450,9 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
         const int64_t ni = g->item_end[q] - g->item_begin[q];
         if (ni > 1 && items_sorted_default()) {
             std::vector<WorkItem> h((size_t)ni);
-            if (cudaMemcpy(h.data(), g->items + g->item_begin[q], sizeof(WorkItem) * ni, cudaMemcpyDeviceToHost) !=
-                cudaSuccess) {
+            if (cudaMemcpyAsync(h.data(), g->items + g->item_begin[q], sizeof(WorkItem) * ni, cudaMemcpyDeviceToHost,
+                                st) != cudaSuccess ||
+                cudaStreamSynchronize(st) != cudaSuccess) {
                 rc = fail(AK_ERR_CUDA, "item copy failed");
                 break;
             }
@@ -459,8 +460,10 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
                 if (a.count != b.count) return a.count > b.count;
                 return a.start < b.start;
             });
-            if (cudaMemcpy(g->items + g->item_begin[q], h.data(), sizeof(WorkItem) * ni, cudaMemcpyHostToDevice) !=
-                cudaSuccess) {
+            // stream-ordered upload; wait for it before `h` goes out of scope
+            if (cudaMemcpyAsync(g->items + g->item_begin[q], h.data(), sizeof(WorkItem) * ni, cudaMemcpyHostToDevice,
+                                st) != cudaSuccess ||
+                cudaStreamSynchronize(st) != cudaSuccess) {
                 rc = fail(AK_ERR_CUDA, "item copy failed");
                 break;
             }
@@ -1226,16 +1229,21 @@ extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double
 // ---------------------------------------------------------------------------
 // complex NUFFT building blocks
 
+// Plans are cached per (shape, type, stream): a cuFFT plan owns one work area, so
+// one plan must not execute on two streams at once.
 struct PlanKey {
     int q, n, type;
-    bool operator<(const PlanKey& o) const { return std::tie(q, n, type) < std::tie(o.q, o.n, o.type); }
+    cudaStream_t stream;
+    bool operator<(const PlanKey& o) const {
+        return std::tie(q, n, type, stream) < std::tie(o.q, o.n, o.type, o.stream);
+    }
 };
 static std::mutex g_plan_mu;
 static std::map<PlanKey, cufftHandle> g_plans;
 
-static int cached_plan(int q, int n, cufftType type, cufftHandle* out) {
+static int cached_plan(int q, int n, cufftType type, cudaStream_t st, cufftHandle* out) {
     std::lock_guard<std::mutex> lk(g_plan_mu);
-    PlanKey k{q, n, (int)type};
+    PlanKey k{q, n, (int)type, st};
     auto it = g_plans.find(k);
     if (it != g_plans.end()) {
         *out = it->second;
@@ -1244,6 +1252,10 @@ static int cached_plan(int q, int n, cufftType type, cufftHandle* out) {
     int dims[3] = {n, n, n};
     cufftHandle h;
     AK_CUFFT(cufftPlanMany(&h, q, dims, nullptr, 1, 0, nullptr, 1, 0, type, 1));
+    if (cufftSetStream(h, st) != CUFFT_SUCCESS) {
+        cufftDestroy(h);
+        return fail(AK_ERR_CUFFT, "cufftSetStream failed");
+    }
     g_plans[k] = h;
     *out = h;
     return AK_OK;
@@ -1288,20 +1300,23 @@ extern "C" int ak_type1_band(int32_t q, int32_t n, int32_t m, const double* gre,
     if (q < 1 || q > 3 || m < 2 || m > n || !gre || !gim || !deconv || !S) return fail(AK_ERR_INVALID, "bad type1 args");
     cudaStream_t st = (cudaStream_t)stream;
     cufftHandle h;
-    AK_TRY(cached_plan(q, n, CUFFT_D2Z, &h));
+    AK_TRY(cached_plan(q, n, CUFFT_D2Z, st, &h));
     const int64_t hs = ipow_rt(n, q - 1) * (n / 2 + 1);
     double2* Y = nullptr;
     AK_CUDA(cudaMallocAsync(&Y, sizeof(double2) * hs * 2, st));
+    int rc = AK_OK;
     {
         std::lock_guard<std::mutex> lk(g_plan_mu);
-        AK_CUFFT(cufftSetStream(h, st));
-        AK_CUFFT(cufftExecD2Z(h, const_cast<double*>(gre), (cufftDoubleComplex*)Y));
-        AK_CUFFT(cufftExecD2Z(h, const_cast<double*>(gim), (cufftDoubleComplex*)(Y + hs)));
+        if (cufftExecD2Z(h, const_cast<double*>(gre), (cufftDoubleComplex*)Y) != CUFFT_SUCCESS ||
+            cufftExecD2Z(h, const_cast<double*>(gim), (cufftDoubleComplex*)(Y + hs)) != CUFFT_SUCCESS)
+            rc = fail(AK_ERR_CUFFT, "cufftExecD2Z failed");
     }
-    g_launches.fetch_add(2);
-    const int64_t tot = ipow_rt(m, q);
-    k_type1_extract<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(Y, Y + hs, q, n, m, deconv, (double2*)S);
-    int rc = launched();
+    if (rc == AK_OK) {
+        g_launches.fetch_add(2);
+        const int64_t tot = ipow_rt(m, q);
+        k_type1_extract<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(Y, Y + hs, q, n, m, deconv, (double2*)S);
+        rc = launched();
+    }
     cudaFreeAsync(Y, st);
     return rc;
 }
@@ -1343,22 +1358,28 @@ extern "C" int ak_type2_grid(int32_t q, int32_t n, int32_t m, const double* c, c
     if (q < 1 || q > 3 || m < 2 || m > n || !c || !deconv || !gre || !gim) return fail(AK_ERR_INVALID, "bad type2 args");
     cudaStream_t st = (cudaStream_t)stream;
     cufftHandle h;
-    AK_TRY(cached_plan(q, n, CUFFT_Z2Z, &h));
+    AK_TRY(cached_plan(q, n, CUFFT_Z2Z, st, &h));
     const int64_t tot = ipow_rt(n, q);
     double2* G = nullptr;
     AK_CUDA(cudaMallocAsync(&G, sizeof(double2) * tot, st));
-    AK_CUDA(cudaMemsetAsync(G, 0, sizeof(double2) * tot, st));
-    const int64_t tm = ipow_rt(m, q);
-    k_type2_pad<<<(unsigned)((tm + 255) / 256), 256, 0, st>>>((const double2*)c, q, n, m, deconv, G);
-    AK_TRY(launched());
-    {
-        std::lock_guard<std::mutex> lk(g_plan_mu);
-        AK_CUFFT(cufftSetStream(h, st));
-        AK_CUFFT(cufftExecZ2Z(h, (cufftDoubleComplex*)G, (cufftDoubleComplex*)G, CUFFT_INVERSE));
+    int rc = cudaMemsetAsync(G, 0, sizeof(double2) * tot, st) == cudaSuccess ? AK_OK
+                                                                               : fail(AK_ERR_CUDA, "memset failed");
+    if (rc == AK_OK) {
+        const int64_t tm = ipow_rt(m, q);
+        k_type2_pad<<<(unsigned)((tm + 255) / 256), 256, 0, st>>>((const double2*)c, q, n, m, deconv, G);
+        rc = launched();
     }
-    g_launches.fetch_add(1);
-    k_split<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(G, tot, gre, gim);
-    int rc = launched();
+    if (rc == AK_OK) {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        if (cufftExecZ2Z(h, (cufftDoubleComplex*)G, (cufftDoubleComplex*)G, CUFFT_INVERSE) != CUFFT_SUCCESS)
+            rc = fail(AK_ERR_CUFFT, "cufftExecZ2Z failed");
+        else
+            g_launches.fetch_add(1);
+    }
+    if (rc == AK_OK) {
+        k_split<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(G, tot, gre, gim);
+        rc = launched();
+    }
     cudaFreeAsync(G, st);
     return rc;
 }

@@ -113,6 +113,23 @@ def band_multiplier(table: CoefficientTable, nplan: NufftPlan) -> np.ndarray:
 # device operator
 
 
+#: operators (device workspace: R x the grids, spectra and band buffers) kept per plan
+OPERATOR_CACHE_LIMIT = 8
+
+
+def _cached_operator(cache: dict, key, make):
+    """Most-recently-used cache of a plan's operators, at most OPERATOR_CACHE_LIMIT
+    (each holds R x ~2 grids of device memory; evicted ones are destroyed)."""
+    op = cache.pop(key, None)
+    if op is None:
+        op = make()
+        keys = [k for k in cache if isinstance(k, tuple) and k and k[0] == "op"]
+        while len(keys) >= OPERATOR_CACHE_LIMIT:
+            del cache[keys.pop(0)]
+    cache[key] = op
+    return op
+
+
 class _Operator:
     """ak_op + its coefficient sets: C sets x P windows of (H, scale)."""
 
@@ -293,13 +310,12 @@ class FastsumPlan:
 
     def _operator(self, families: tuple, R: int, interp_geom: DeviceGeometry | None = None) -> _Operator:
         gi = interp_geom if interp_geom is not None else self.geometries
-        key = ("op", families, R, id(gi))
-        op = self._cache.get(key)
-        if op is None:
+
+        def make():
             sets = [self._family_set(f) for f in families]
-            op = _Operator(self.geometries, gi, self.m, R, [s[0] for s in sets], [s[1] for s in sets])
-            self._cache[key] = op
-        return op
+            return _Operator(self.geometries, gi, self.m, R, [s[0] for s in sets], [s[1] for s in sets])
+
+        return _cached_operator(self._cache, ("op", families, R, id(gi)), make)
 
 
 def _check_prescaled(data: Dataset, window_set: WindowSet) -> None:
@@ -449,15 +465,13 @@ class MixedKernelPlan:
         return hit
 
     def _operator(self, R: int, dell: bool) -> _Operator:
-        key = ("op", R, dell)
-        op = self._cache.get(key)
-        if op is None:
+        def make():
             (Hk, sk), (Hd, sd) = self._sets()
             H = [Hk, Hd] if dell else [Hk]
             S = [sk, sd] if dell else [sk]
-            op = _Operator(self.geometries, self.geometries, self.m, R, H, S)
-            self._cache[key] = op
-        return op
+            return _Operator(self.geometries, self.geometries, self.m, R, H, S)
+
+        return _cached_operator(self._cache, ("op", R, dell), make)
 
 
 def build_mixed_plan(specs, window_set: WindowSet, preset, data: Dataset, cutoff: int = 6,

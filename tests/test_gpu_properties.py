@@ -286,3 +286,30 @@ def test_sharded_plans_single_rank(cuda):
             assert rel(out.cpu().numpy(), ref) <= 1e-13, type(p).__name__
     finally:
         dist.destroy_process_group()
+
+
+def test_side_stream_and_operator_cache(cuda):
+    """Plan build and products on a non-default (non-blocking) stream match the default
+    stream; the per-plan operator cache stays bounded."""
+    import torch
+
+    from paper_2404_17344_b200.fastsum import OPERATOR_CACHE_LIMIT, build_plan, fast_matvec, fast_matvecs
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    rng = np.random.default_rng(8)
+    X = rng.uniform(-0.14, 0.14, size=(3000, 5))
+    v = rng.normal(size=3000)
+    ws = WindowSet(((1, 2, 3), (4, 5), (2,)), d_max=3)
+    spec = KernelSpec("gauss", 0.3)
+    ref = fast_matvec(build_plan(spec, ws, "default", _ds(X, 3)), v)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        plan = build_plan(spec, ws, "default", _ds(X, 3))
+        out = fast_matvec(plan, v)
+        for R in range(1, OPERATOR_CACHE_LIMIT + 4):
+            res = fast_matvecs(plan, np.tile(v, (R, 1)))
+            assert rel(res["K"][-1], ref) <= 1e-13
+    s.synchronize()
+    assert rel(out, ref) <= 1e-13
+    assert sum(1 for k in plan._cache if isinstance(k, tuple) and k[0] == "op") <= OPERATOR_CACHE_LIMIT
