@@ -313,3 +313,22 @@ def test_side_stream_and_operator_cache(cuda):
     s.synchronize()
     assert rel(out, ref) <= 1e-13
     assert sum(1 for k in plan._cache if isinstance(k, tuple) and k[0] == "op") <= OPERATOR_CACHE_LIMIT
+
+
+def test_q2_many_rhs(cuda):
+    """2-D single-cell kernels with R = 11 right-hand sides: K V and dK/dl V rows equal
+    the oracle's single products."""
+    from oracle import restate as R
+    from paper_2404_17344_b200.fastsum import build_plan, fast_matvecs
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    rng = np.random.default_rng(9)
+    X = rng.uniform(-0.1, 0.1, size=(20000, 4))
+    V = rng.normal(size=(11, 20000))
+    plan = build_plan(KernelSpec("matern12", 0.3), WindowSet(((1, 2), (3, 4)), d_max=2), "default", _ds(X, 2))
+    res = fast_matvecs(plan, V, dell=True)
+    for fam, key in (("matern12", "K"), ("der_matern12", "dK_dell")):
+        fs = R.FastSum(fam, 0.3, 1.0, [(0, 1), (2, 3)], X)
+        for r in (0, 7, 10):
+            assert rel(res[key][r], fs.matvec(V[r])) <= 1e-8, (key, r)
