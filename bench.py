@@ -21,8 +21,11 @@ n = 64, cutoff 6, Kaiser-Bessel).  A step is one full K v over all windows.
 * ``cpu_baseline``: the CPU oracle port (oracle/, serial C loops + numpy FFT,
   the reference's algorithm and cost structure) timed on one window at full N.
 
-Multi-GPU (torchrun): windows are sharded over ranks and the partial K v is
-summed with one NCCL all-reduce; timing is the max over ranks.
+Multi-GPU (torchrun): point sharding by default (each rank spreads its own
+rows into every window's grid; one NCCL all-reduce of the band spectra, then
+every rank interpolates its rows; --shard window: windows split over ranks
+and the partial K v all-reduced).  Timing is the max over ranks; the roofline
+is rank 0's local kernels.
 """
 
 from __future__ import annotations
@@ -193,10 +196,10 @@ def kernel_roofline(torch, plan, wl, peaks, reps=10):
 
     lib = _native.lib()
     geom = plan.geometries
-    N = wl.data.n_rows
-    P3 = sum(1 for w in wl.window_set if len(w) == 3)
+    N = plan.n_rows  # this rank's rows (all of them on one GPU)
+    P3 = sum(1 for w in plan.window_set if len(w) == 3)
     T = plan.nufft_plans[3].taps
-    V = torch.as_tensor(wl.V[:1], device="cuda").contiguous()
+    V = torch.as_tensor(np.ascontiguousarray(wl.V[:1, :N]), device="cuda").contiguous()
     grids = torch.zeros(geom.canon_total, dtype=torch.float64, device="cuda")
     out = torch.zeros(N, dtype=torch.float64, device="cuda")
     scale = torch.ones(geom.n_windows, dtype=torch.float64, device="cuda")
@@ -433,8 +436,9 @@ def run_ours(args):
             fp64, dmma = fp64_peak(torch)
             peaks["fp64_tflops"] = fp64
             result["fp64_probe"] = {"dfma_tflops": fp64, "dmma_tflops": dmma}
-            if world == 1:
+            if plan is not None and 3 in plan.nufft_plans:
                 result["roofline"] = kernel_roofline(torch, plan, wl, peaks)
+            if world == 1:
                 result["extras"] = extra_workloads(torch)
             if world == 1 and not args.no_cpu_baseline:
                 one = build_plan(wl.spec, WindowSet((wins[0],), d_max=3), "default", wl.data)
