@@ -221,3 +221,27 @@ def test_q2_item_kernels_match_reference(cuda, monkeypatch, sc2):
         geom = prepare_points(plan, g[f"q2_m{m}_pts"])
         assert rel(nufft_type1(plan, geom, g[f"q2_m{m}_w"]), g[f"q2_m{m}_type1"]) <= TOL
         assert rel(nufft_type2(plan, geom, g[f"q2_m{m}_c"]), g[f"q2_m{m}_type2"]) <= TOL
+
+
+def test_plan_options_match_reference(cuda):
+    """build_plan(cutoff, oversampling, window, explicit m) on mixed window lengths, and the
+    dense-cell regime (single-cell tensor-core items) for all four families."""
+    from paper_2404_17344_b200.fastsum import build_plan, fast_matvec
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    g = golden("plan_options")
+    ws = WindowSet(((1, 2, 3), (4, 5), (6,)), d_max=3)
+    ds = _ds(g["X"], 3)
+    opts = {"cut3": dict(cutoff=3), "cut4": dict(cutoff=4), "cut5": dict(cutoff=5), "cut8": dict(cutoff=8),
+            "os1p5": dict(oversampling=1.5), "os3": dict(oversampling=3.0),
+            "gaussw": dict(window="gaussian_window"), "gaussw_cut4": dict(window="gaussian_window", cutoff=4)}
+    for fam in ("gauss", "matern12"):
+        spec = KernelSpec(fam, 0.35, 0.8)
+        for key, kw in opts.items():
+            assert rel(fast_matvec(build_plan(spec, ws, "default", ds, **kw), g["v"]), g[f"{fam}_{key}"]) <= TOL, key
+        assert rel(fast_matvec(build_plan(spec, ws, 24, ds), g["v"]), g[f"{fam}_m24"]) <= TOL
+    dsd = _ds(g["Xd"], 3)
+    for fam in ("gauss", "der_gauss", "matern12", "der_matern12"):
+        plan = build_plan(KernelSpec(fam, 0.3, 1.0), ws, "default", dsd)
+        assert rel(fast_matvec(plan, g["vd"]), g[f"dense_{fam}"]) <= TOL, fam

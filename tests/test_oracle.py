@@ -154,3 +154,22 @@ def test_chunked_oracle_equals_plain():
     with ThreadPoolExecutor(4) as pool:
         out = chunked.matvec_pool(v, pool)
     assert np.linalg.norm(out - plain) <= 1e-13 * np.linalg.norm(plain)
+
+
+def test_oracle_plan_options_match_reference():
+    """cutoff / oversampling / Gaussian window / explicit m, and densely occupied cells."""
+    from oracle import restate as R
+
+    g = golden("plan_options")
+    wins = [(0, 1, 2), (3, 4), (5,)]
+    opts = {"cut3": dict(cutoff=3), "cut4": dict(cutoff=4), "cut5": dict(cutoff=5), "cut8": dict(cutoff=8),
+            "os1p5": dict(oversampling=1.5), "os3": dict(oversampling=3.0),
+            "gaussw": dict(window="gaussian_window"), "gaussw_cut4": dict(window="gaussian_window", cutoff=4)}
+    for fam in ("gauss", "matern12"):
+        for key, kw in opts.items():
+            out = R.FastSum(fam, 0.35, 0.8, wins, g["X"], **kw).matvec(g["v"])
+            assert rel(out, g[f"{fam}_{key}"]) <= 1e-13, (fam, key)
+        assert rel(R.FastSum(fam, 0.35, 0.8, wins, g["X"], m=24).matvec(g["v"]), g[f"{fam}_m24"]) <= 1e-13
+    for fam in ("gauss", "der_gauss", "matern12", "der_matern12"):
+        out = R.FastSum(fam, 0.3, 1.0, wins, g["Xd"]).matvec(g["vd"])
+        assert rel(out, g[f"dense_{fam}"]) <= 1e-13, fam
