@@ -245,3 +245,15 @@ def test_plan_options_match_reference(cuda):
     for fam in ("gauss", "der_gauss", "matern12", "der_matern12"):
         plan = build_plan(KernelSpec(fam, 0.3, 1.0), ws, "default", dsd)
         assert rel(fast_matvec(plan, g["vd"]), g[f"dense_{fam}"]) <= TOL, fam
+
+
+def test_nufft_dense_boundary_cells(cuda):
+    """Densely occupied cells on the periodic boundary: single-cell items, wrapping footprints."""
+    from paper_2404_17344_b200.nufft import NufftPlan, nufft_type1, nufft_type2, prepare_points
+
+    g = golden("nufft_dense")
+    for q in (2, 3):
+        plan = NufftPlan(dims=q, m=32)
+        geom = prepare_points(plan, g[f"q{q}_pts"])
+        assert rel(nufft_type1(plan, geom, g[f"q{q}_w"]), g[f"q{q}_type1"]) <= TOL
+        assert rel(nufft_type2(plan, geom, g[f"q{q}_c"]), g[f"q{q}_type2"]) <= TOL

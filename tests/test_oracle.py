@@ -173,3 +173,14 @@ def test_oracle_plan_options_match_reference():
     for fam in ("gauss", "der_gauss", "matern12", "der_matern12"):
         out = R.FastSum(fam, 0.3, 1.0, wins, g["Xd"]).matvec(g["vd"])
         assert rel(out, g[f"dense_{fam}"]) <= 1e-13, fam
+
+
+def test_oracle_nufft_dense_boundary_cells():
+    from oracle import restate as R
+
+    g = golden("nufft_dense")
+    for q in (2, 3):
+        plan = R.Nufft(q, 32)
+        geom = R.Geometry(plan, g[f"q{q}_pts"])
+        assert rel(R.type1(plan, geom, g[f"q{q}_w"]), g[f"q{q}_type1"]) <= 1e-13
+        assert rel(R.type2(plan, geom, g[f"q{q}_c"]), g[f"q{q}_type2"]) <= 1e-13
