@@ -806,6 +806,15 @@ static void launch_interp3w_sb(const ak_geom* g, int64_t i0, int64_t ni, const d
 {
     dim3 grid((unsigned)ni, (unsigned)R);
     if (g->imma) {
+        // B fragments read from the shared region tile inside the DMMA loop (default;
+        // AK_IMMA_SMEM=0: 54 fragment registers per lane loaded per cell run)
+        const char* sb = getenv("AK_IMMA_SMEM");
+        if (!(sb && sb[0] == '0') && g->iwarps == 1) {
+            k_interp3m<S, B, 1, true><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids,
+                                                           g->canon_off_d, R, g->n, scale, out, ldo, atomic_out,
+                                                           wstride);
+            return;
+        }
         if (g->iwarps == 2 && B == 16)
             k_interp3m<S, 16, 2><<<grid, 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids,
                                                       g->canon_off_d, R, g->n, scale, out, ldo, atomic_out, wstride);

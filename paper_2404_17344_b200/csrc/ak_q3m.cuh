@@ -84,8 +84,57 @@ __device__ __forceinline__ double interp_group_mma(const double (&gf)[18][3], co
     return valid ? v : 0.0;
 }
 
-template <int S, int B, int NW>
-__global__ void __launch_bounds__(32 * NW, 8 / NW)
+// Per-lane tile offsets of the 18 permuted B-fragment columns (same mapping as
+// load_fragments): column n = lane/4 of tile t is pair i = 2t + (n & 1) of quad n >> 1.
+template <int R>
+__device__ __forceinline__ void fragment_offsets(int (&off)[18], int lane) {
+    const int n = lane >> 2, kk = lane & 3;
+    const int qq = n >> 1, e = n & 1;
+#pragma unroll
+    for (int t = 0; t < 18; ++t) {
+        const int i = 2 * t + e;
+        off[t] = ((i / 3) * R + 3 * qq + i % 3) * R + kk;
+    }
+}
+
+// interp_group_mma with the B fragments read from the shared region tile inside the
+// DMMA loop (cell origin `cb`), instead of 54 registers per lane loaded per cell.
+template <int R, int RW>
+__device__ __forceinline__ double interp_group_mma_s(const double* cb, const int (&off)[18],
+                                                     const double (*wrow)[RW], int k0, int cnt, int lane)
+{
+    const int pj = lane >> 2, q = lane & 3;
+    const bool valid = pj < cnt;
+    const double* w = wrow[k0 + (valid ? pj : 0)];
+    double af[3];
+#pragma unroll
+    for (int ks = 0; ks < 3; ++ks) af[ks] = valid ? w[24 + 4 * ks + q] : 0.0;
+    double C[18][2];
+#pragma unroll
+    for (int t = 0; t < 18; ++t) C[t][0] = C[t][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 3; ++ks)
+#pragma unroll
+        for (int t = 0; t < 18; ++t) dmma_8x8x4(C[t][0], C[t][1], af[ks], cb[off[t] + 4 * ks]);
+    double s[3];
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) s[bb] = w[0] * C[bb >> 1][bb & 1];
+#pragma unroll
+    for (int a = 1; a < 12; ++a) {
+        const double w0a = w[a];
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb) {
+            const int i = 3 * a + bb;
+            s[bb] = fma(w0a, C[i >> 1][i & 1], s[bb]);
+        }
+    }
+    const double* w1 = w + 12 + 3 * q;
+    const double v = fma(w1[2], s[2], fma(w1[1], s[1], w1[0] * s[0]));
+    return valid ? v : 0.0;
+}
+
+template <int S, int B, int NW, bool SMEMB = false>
+__global__ void __launch_bounds__(32 * NW, (SMEMB ? 12 : 8) / NW)
 k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ grids,
            const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,
@@ -143,7 +192,10 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     const double sc = scale[it.window];
     double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * ldo;
 
-    double gf[18][3];
+    double gf[SMEMB ? 1 : 18][3];
+    int foff[18];
+    if constexpr (SMEMB) fragment_offsets<R>(foff, lane);
+    const double* cb = tile;
     int cur = -1;
 
     for (int bi = warp, u = 0; bi < nbatch; bi += NW, ++u) {
@@ -175,13 +227,18 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         for (int k = 0; k < nb;) {
             if ((chg >> k) & 1u) {
                 cur = cst[k];
-                load_fragments<R>(gf, tile, cur, lane);
+                if constexpr (SMEMB)
+                    cb = tile + ((cur & 255) * R + ((cur >> 8) & 255)) * R + ((cur >> 16) & 255);
+                else
+                    load_fragments<R>(reinterpret_cast<double (&)[18][3]>(gf), tile, cur, lane);
             }
             const unsigned later = k < 31 ? chg & ~((2u << k) - 1u) : 0u;
             const int kend = later ? min(__ffs(later) - 1, nb) : nb;
             for (int k0 = k; k0 < kend; k0 += 8) {
                 const int cnt = min(8, kend - k0);
-                double v = interp_group_mma<RW>(gf, wbuf[s], k0, cnt, lane);
+                double v;
+                if constexpr (SMEMB) v = interp_group_mma_s<R, RW>(cb, foff, wbuf[s], k0, cnt, lane);
+                else v = interp_group_mma<RW>(reinterpret_cast<double (&)[18][3]>(gf), wbuf[s], k0, cnt, lane);
                 v += __shfl_xor_sync(0xffffffffu, v, 1);
                 v += __shfl_xor_sync(0xffffffffu, v, 2);
                 const int pj = lane >> 2;

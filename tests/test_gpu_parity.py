@@ -173,6 +173,7 @@ def test_native_library_is_what_runs(cuda):
 
 @pytest.mark.parametrize("variant", [
     {"AK_IMMA": "0"},                       # DFMA interp (transposed warp reduction)
+    {"AK_IMMA_SMEM": "0", "AK_SUPERCELL3": "2"},  # DMMA interp, fragments in registers per cell run
     {"AK_WEIGHTS": "horner"},               # weights evaluated per pass (no plan-time table)
     {"AK_SWARPS": "2"},                     # two-warp spread CTAs with barrier-serialised flushes
     {"AK_IWARPS": "2"},                     # two-warp interp CTAs sharing the region tile
