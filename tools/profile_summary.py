@@ -29,6 +29,10 @@ METRICS = {
     "grid_size": "launch__grid_size",
     "issue_active_pct": "sm__inst_issued.avg.pct_of_peak_sustained_active",
     "l2_hit_pct": "lts__t_sector_hit_rate.pct",
+    "l2_throughput_pct": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "red_sectors_to_l2": "l1tex__m_l1tex2xbar_write_sectors_mem_global_op_red.sum",
+    "smem_wavefronts": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "dram_throughput_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
 }
 STALLS = "smsp__average_warps_issue_stalled_"
 
