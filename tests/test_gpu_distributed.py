@@ -1,0 +1,80 @@
+"""GPU: the multi-GPU decompositions (distributed.py) with two ranks on the one
+available device, exchanging through gloo (host-side collectives; the ranks'
+kernels never wait on each other).  Checks the real sharded code paths --
+SPECTRUM_ONLY spread + band all-reduce + FROM_SPECTRUM interpolation (point
+sharding) and the LPT window split + all-reduce (window sharding) -- against the
+single-process product."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, X, V, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2404_17344_b200.dataset import PRESCALED, Dataset
+        from paper_2404_17344_b200.distributed import PointShardedPlan, WindowShardedPlan
+        from paper_2404_17344_b200.fastsum import build_plan, fast_matvecs
+        from paper_2404_17344_b200.kernels import KernelSpec
+        from paper_2404_17344_b200.windows import WindowSet
+
+        ds = Dataset(X, np.zeros(X.shape[0]), tuple(f"x{i}" for i in range(X.shape[1])), scaling_state=PRESCALED,
+                     d_max=3)
+        ws = WindowSet(((1, 2, 3), (4, 5, 6), (2, 5), (7,)), d_max=3)
+        spec = KernelSpec("gauss", 0.3, 0.9)
+        ref = fast_matvecs(build_plan(spec, ws, "default", ds), V, dell=True)
+        Vd = torch.as_tensor(V, device="cuda")
+        errs = {}
+        for exchange in ("band", "grid"):
+            pp = PointShardedPlan(spec, ws, "default", ds, exchange=exchange)
+            k_rows = pp.matvec(Vd[0]).cpu().numpy()
+            errs[f"point_{exchange}_K"] = np.linalg.norm(k_rows - ref["K"][0]) / np.linalg.norm(ref["K"][0])
+            local = pp.matvecs_local(Vd[:, pp.lo:pp.hi].contiguous(), ("gauss", "der_gauss"))
+            for name, o in zip(("K", "dK_dell"), local):
+                r = ref[name][:, pp.lo:pp.hi]
+                errs[f"point_{exchange}_local_{name}"] = np.linalg.norm(o.cpu().numpy() - r) / np.linalg.norm(r)
+        wp = WindowShardedPlan(spec, ws, "default", ds)
+        outs = wp.matvecs(Vd, ("gauss", "der_gauss"))
+        for name, o in zip(("K", "dK_dell"), outs):
+            errs[f"window_{name}"] = np.linalg.norm(o.cpu().numpy() - ref[name]) / np.linalg.norm(ref[name])
+        q.put((rank, errs))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_on_one_device_match_single_process(cuda):
+    import torch.multiprocessing as mp
+
+    rng = np.random.default_rng(21)
+    X = rng.uniform(-0.14, 0.14, size=(5001, 7))   # odd N: unequal row blocks
+    V = rng.normal(size=(3, 5001))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, X, V, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, errs in results:
+        for key, err in errs.items():
+            assert err <= 1e-12, (rank, key, err)
