@@ -92,9 +92,13 @@ struct ak_geom {
     int64_t item_begin[4] = {0, 0, 0, 0}, item_end[4] = {0, 0, 0, 0};
     std::vector<int> windows_of_q[4];   // window ids per q, canonical order
     int sedge[4] = {0, 16, 8, 4};       // supercell edge (cells) per q (must match SuperCell<q>)
+    int sedge_i3 = 4;                   // supercell edge of the 3-D interpolation items
+    int chunk[4] = {0, 2048, 1024, 2048};  // maximum points per work item, per q
+    int64_t iitem_begin3 = 0, iitem_end3 = 0;  // 3-D interpolation items (== spread items unless split)
     // cached 3-D window weights (plan-time table, see ak_q3w.cuh)
     bool cached = false;
-    int batch3 = 16;
+    int batch3 = 16;                    // spread batch (q = 3)
+    int batch3i = 16;                   // interpolation batch (q = 3)
     int iwarps = 1;                     // warps per CTA of the cached q=3 interp
     int swarps = 1;                     // warps per CTA of the cached q=3 spread
     bool vreg = false;                  // RHS value folded in registers (vs a scaling pass)
@@ -136,9 +140,14 @@ static int supercell3_default() {
     return (v >= 1 && v <= 4) ? v : 0;
 }
 
-// Mean points per occupied cell above which 3-D windows use single-cell work items.
+// Mean points per occupied cell above which the 3-D spread / interpolation use
+// single-cell work items (measured on B200 with config-4 data at 125k..2M points).
 static double dense_cell_threshold() {
     const char* e = getenv("AK_DENSE_CELLS");
+    return e ? atof(e) : 300.0;
+}
+static double dense_cell_threshold_interp() {
+    const char* e = getenv("AK_DENSE_CELLS_INTERP");
     return e ? atof(e) : 64.0;
 }
 
@@ -163,14 +172,28 @@ __global__ void k_count_nonzero(const int* __restrict__ counts, int total, int* 
     if ((threadIdx.x & 31) == 0 && b) atomicAdd(nz, __popc(b));
 }
 
-// Maximum points per work item (AK_CHUNK3 overrides the 3-D value).
-static int chunk_for_q(int q) {
+// Maximum points per work item.  Items are processed one per CTA in largest-first
+// order, so the largest item bounds the tail: the cap is half the average work per
+// resident CTA slot (SMs x 8), within [64, 2048] (q = 3) / [64, 1024] (q = 2);
+// 2048 for q = 1.  Measured on clustered config-4 data at 30k nodes: the fixed 2048
+// cap left a few 800-point supercell items as the tail (spread 0.140 -> 0.097 ms,
+// interp 0.157 -> 0.082 ms with the adaptive cap).  AK_CHUNK3 overrides q = 3.
+static int chunk_for(int q, int64_t point_windows) {
+    if (q == 1) return 2048;
     if (q == 3) {
         const char* e = getenv("AK_CHUNK3");
         const int v = e ? atoi(e) : 0;
-        return (v >= 64 && v <= 65536) ? v : 2048;
+        if (v >= 64 && v <= 65536) return v;
     }
-    return q == 2 ? 1024 : 2048;
+    static int slots = 0;
+    if (!slots) {
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        slots = std::max(1, sms) * 8;
+    }
+    const int64_t hi = q == 3 ? 2048 : 1024;
+    return (int)std::max<int64_t>(64, std::min<int64_t>(hi, point_windows / (2 * (int64_t)slots)));
 }
 
 __global__ void k_keys(const double* __restrict__ X, int64_t ld, int q, int c0, int c1, int c2, int n, int S,
@@ -257,6 +280,45 @@ __global__ void k_items(const int* __restrict__ counts, const int* __restrict__ 
     }
 }
 
+// Run boundaries of the sorted keys: a key's run is [kstart, kend) (0/0 when absent).
+__global__ void k_key_bounds(const uint32_t* __restrict__ keys, int64_t N, int* __restrict__ kstart,
+                             int* __restrict__ kend)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const uint32_t k = keys[i];
+    if (i == 0 || keys[i - 1] != k) kstart[k] = (int)i;
+    if (i == N - 1 || keys[i + 1] != k) kend[k] = (int)(i + 1);
+}
+
+// Single-cell work items (3-D) from the run of each key of a (supercell, cell) sort:
+// key = supercell * S^3 + (u0 * S + u1) * S + u2, cell = supercell digit * S + u.
+__global__ void k_items_cells(const int* __restrict__ kstart, const int* __restrict__ kend, int64_t nkeys, int S,
+                              int nsc, int chunk, int64_t pt_base, int w, int* __restrict__ counter,
+                              WorkItem* __restrict__ items)
+{
+    const int64_t key = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (key >= nkeys) return;
+    const int cnt = kend[key] - kstart[key];
+    if (cnt <= 0) return;
+    const int S3 = S * S * S;
+    const int sc = (int)(key / S3), sub = (int)(key - (int64_t)sc * S3);
+    const int s0 = sc / (nsc * nsc), s1 = (sc / nsc) % nsc, s2 = sc % nsc;
+    const int u0 = sub / (S * S), u1 = (sub / S) % S, u2 = sub % S;
+    const int packed = (s0 * S + u0) | ((s1 * S + u1) << 10) | ((s2 * S + u2) << 20);
+    const int k = (cnt + chunk - 1) / chunk;
+    const int size = (cnt + k - 1) / k;
+    const int base = atomicAdd(counter, k);
+    for (int j = 0; j < k; ++j) {
+        WorkItem it;
+        it.window = w;
+        it.sc = packed;
+        it.start = (int)(pt_base + kstart[key] + (int64_t)j * size);
+        it.count = min(size, cnt - j * size);
+        items[base + j] = it;
+    }
+}
+
 extern "C" const char* ak_last_error(void) { return g_err.c_str(); }
 extern "C" const char* ak_version(void) { return "addkern_b200 0.1.0 (sm_100a)"; }
 extern "C" int64_t ak_launch_count(void) { return g_launches.load(); }
@@ -305,6 +367,21 @@ static double mean_occupancy(const double* X, int64_t ld, const int32_t* cols, i
     return mean;
 }
 
+// Device scratch released when it goes out of scope (every return path of geom_build).
+struct Scratch {
+    std::vector<void*> bufs;
+    ~Scratch() {
+        for (void* b : bufs) cudaFree(b);
+    }
+    template <typename T>
+    cudaError_t alloc(T** p, size_t bytes) {
+        *p = nullptr;
+        const cudaError_t e = cudaMalloc(p, bytes);
+        if (e == cudaSuccess) bufs.push_back(*p);
+        return e;
+    }
+};
+
 static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t ld, cudaStream_t st) {
     const int n = g->n, P = g->P;
     const int64_t N = g->N;
@@ -323,8 +400,6 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
     AK_CUDA(cudaMemcpyAsync(g->canon_off_d, g->canon_off.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice, st));
 
     AK_CUDA(cudaMalloc(&g->pts, sizeof(Point) * (size_t)std::max<int64_t>(1, N * P)));
-    // item capacity
-    int64_t cap = 0;
     int max_nsc_total = 1;
     bool cached = g->wf.taps == 12 && N > 0 && weights_cached_default();
     if (cached) {
@@ -351,14 +426,24 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
             cached = false;
         }
     }
+    // Supercell edges.  3-D windows: the spread and the interpolation may use different
+    // work items over the same sorted points: single-cell items pay off for the
+    // interpolation from ~64 points per occupied cell, for the spread only from ~300
+    // (below that its per-cell register flush costs more than the supercell tile;
+    // config-4 data: 210 points per cell at 500k nodes, 427 at 1M).
     int s3 = supercell3_default();
     if (s3 == 1 && !cached) s3 = 2;  // single-cell kernels exist for the cached-weight path only
+    int si3 = s3;
     if (s3 == 0) {
-        s3 = 2;
-        if (cached && !g->windows_of_q[3].empty() &&
-            mean_occupancy(X, ld, cols, g->windows_of_q[3][0], 3, n, N, st) >= dense_cell_threshold())
-            s3 = 1;
+        s3 = si3 = 2;
+        if (cached && !g->windows_of_q[3].empty()) {
+            const double occ = mean_occupancy(X, ld, cols, g->windows_of_q[3][0], 3, n, N, st);
+            if (occ >= dense_cell_threshold()) s3 = 1;
+            if (occ >= dense_cell_threshold_interp()) si3 = 1;
+        }
     }
+    if (s3 == 1) si3 = 1;
+    const bool split3 = (si3 == 1 && s3 != 1);
     int s2 = supercell2_default();
     if (s2 == 1 && !cached) s2 = 8;
     if (s2 == 0) {
@@ -369,39 +454,80 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
     }
     g->sedge[2] = s2;
     g->sedge[3] = s3;
+    g->sedge_i3 = si3;
+    for (int q = 1; q <= 3; ++q) g->chunk[q] = chunk_for(q, N * (int64_t)g->windows_of_q[q].size());
+    int64_t tcap = 1;     // per-window item capacity of the staging buffer
+    int64_t keyspace = 1; // 3-D sort-key space (cells in supercell order) when split
     for (int w = 0; w < P; ++w) {
         const int S = g->sedge[g->q[w]];
         const int nsc = (n + S - 1) / S;
         const int tot = (int)ipow_rt(nsc, g->q[w]);
         max_nsc_total = std::max(max_nsc_total, tot);
-        cap += (N + chunk_for_q(g->q[w]) - 1) / chunk_for_q(g->q[w]) + tot;
+        const int ch = g->chunk[g->q[w]];
+        tcap = std::max<int64_t>(tcap, (N + ch - 1) / ch + tot);
+        if (g->q[w] == 3 && split3) {
+            keyspace = std::max<int64_t>(keyspace, (int64_t)tot * S * S * S);
+            tcap = std::max<int64_t>(tcap, (N + ch - 1) / ch + std::min<int64_t>(N, (int64_t)tot * S * S * S));
+        }
     }
-    AK_CUDA(cudaMalloc(&g->items, sizeof(WorkItem) * (size_t)std::max<int64_t>(1, cap)));
 
+    Scratch scratch;  // plan-time buffers, released on every return path
     uint32_t *keys = nullptr, *keys2 = nullptr;
     int32_t *vals = nullptr, *vals2 = nullptr;
-    int *counts = nullptr, *starts = nullptr, *dflags = nullptr;
+    int *counts = nullptr, *starts = nullptr, *dflags = nullptr, *kstart = nullptr, *kend = nullptr;
+    WorkItem* titems = nullptr;
     void* temp = nullptr;
     size_t temp_bytes = 0, need = 0;
     const int64_t NN = std::max<int64_t>(N, 1);
-    AK_CUDA(cudaMalloc(&keys, sizeof(uint32_t) * NN));
-    AK_CUDA(cudaMalloc(&keys2, sizeof(uint32_t) * NN));
-    AK_CUDA(cudaMalloc(&vals, sizeof(int32_t) * NN));
-    AK_CUDA(cudaMalloc(&vals2, sizeof(int32_t) * NN));
-    AK_CUDA(cudaMalloc(&counts, sizeof(int) * max_nsc_total));
-    AK_CUDA(cudaMalloc(&starts, sizeof(int) * max_nsc_total));
-    AK_CUDA(cudaMalloc(&dflags, sizeof(int) * 2));  // [0] bad, [1] item counter
+    AK_CUDA(scratch.alloc(&keys, sizeof(uint32_t) * NN));
+    AK_CUDA(scratch.alloc(&keys2, sizeof(uint32_t) * NN));
+    AK_CUDA(scratch.alloc(&vals, sizeof(int32_t) * NN));
+    AK_CUDA(scratch.alloc(&vals2, sizeof(int32_t) * NN));
+    AK_CUDA(scratch.alloc(&counts, sizeof(int) * max_nsc_total));
+    AK_CUDA(scratch.alloc(&starts, sizeof(int) * max_nsc_total));
+    AK_CUDA(scratch.alloc(&dflags, sizeof(int) * 2));  // [0] bad, [1] item counter
+    AK_CUDA(scratch.alloc(&titems, sizeof(WorkItem) * tcap));
+    if (split3) {
+        AK_CUDA(scratch.alloc(&kstart, sizeof(int) * keyspace));
+        AK_CUDA(scratch.alloc(&kend, sizeof(int) * keyspace));
+    }
     AK_CUDA(cudaMemsetAsync(dflags, 0, sizeof(int) * 2, st));
     cub::DeviceRadixSort::SortPairs(nullptr, need, keys, keys2, vals, vals2, (int)N, 0, 32, st);
     temp_bytes = need;
     cub::DeviceScan::ExclusiveSum(nullptr, need, counts, starts, max_nsc_total, st);
     temp_bytes = std::max(temp_bytes, need);
-    AK_CUDA(cudaMalloc(&temp, std::max<size_t>(temp_bytes, 16)));
+    AK_CUDA(scratch.alloc(&temp, std::max<size_t>(temp_bytes, 16)));
 
     int rc = AK_OK;
-    int host_counter = 0;
+    std::vector<WorkItem> all;  // final order: q=3 spread | q=3 interp (split) | q=2 | q=1
+    // staged items of one window -> host (the counter is reset per window)
+    auto take = [&](std::vector<WorkItem>& dst) -> int {
+        int cnt = 0;
+        if (cudaMemcpyAsync(&cnt, dflags + 1, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return fail(AK_ERR_CUDA, "item count read failed");
+        const size_t at = dst.size();
+        dst.resize(at + (size_t)cnt);
+        if (cnt > 0 && (cudaMemcpyAsync(dst.data() + at, titems, sizeof(WorkItem) * cnt, cudaMemcpyDeviceToHost, st) !=
+                            cudaSuccess ||
+                        cudaStreamSynchronize(st) != cudaSuccess))
+            return fail(AK_ERR_CUDA, "item copy failed");
+        if (cudaMemsetAsync(dflags + 1, 0, sizeof(int), st) != cudaSuccess) return fail(AK_ERR_CUDA, "memset failed");
+        return AK_OK;
+    };
+    // Largest items first (blocks are dispatched in index order: LPT-like tail).
+    auto append_sorted = [&](std::vector<WorkItem>& v, int64_t& begin, int64_t& end) {
+        if (v.size() > 1 && items_sorted_default())
+            std::stable_sort(v.begin(), v.end(), [](const WorkItem& a, const WorkItem& b) {
+                if (a.count != b.count) return a.count > b.count;
+                return a.start < b.start;
+            });
+        begin = (int64_t)all.size();
+        all.insert(all.end(), v.begin(), v.end());
+        end = (int64_t)all.size();
+    };
     for (int q = 3; q >= 1 && rc == AK_OK; --q) {
-        g->item_begin[q] = host_counter;
+        std::vector<WorkItem> spread_items, cell_items;
         for (int w : g->windows_of_q[q]) {
             const int S = g->sedge[q];
             const int nsc = (n + S - 1) / S;
@@ -429,47 +555,55 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
                 break;
             }
             g_launches.fetch_add(1);
-            k_items<<<(tot + 255) / 256, 256, 0, st>>>(counts, starts, tot, q, nsc, chunk_for_q(q), (int64_t)w * N, w,
-                                                       dflags + 1, g->items);
-            if ((rc = launched()) != AK_OK) break;
+            k_items<<<(tot + 255) / 256, 256, 0, st>>>(counts, starts, tot, q, nsc, g->chunk[q], (int64_t)w * N, w,
+                                                       dflags + 1, titems);
+            if ((rc = launched()) != AK_OK || (rc = take(spread_items)) != AK_OK) break;
+            if (q == 3 && split3) {
+                // single-cell items over the same (supercell, cell)-sorted points: each cell is
+                // one run of equal keys
+                const int64_t nk = (int64_t)tot * S * S * S;
+                cudaMemsetAsync(kstart, 0, sizeof(int) * nk, st);
+                cudaMemsetAsync(kend, 0, sizeof(int) * nk, st);
+                k_key_bounds<<<nblk, tb, 0, st>>>(keys2, N, kstart, kend);
+                if ((rc = launched()) != AK_OK) break;
+                k_items_cells<<<(unsigned)((nk + 255) / 256), 256, 0, st>>>(kstart, kend, nk, S, nsc, g->chunk[3],
+                                                                            (int64_t)w * N, w, dflags + 1, titems);
+                if ((rc = launched()) != AK_OK || (rc = take(cell_items)) != AK_OK) break;
+            }
         }
         if (rc != AK_OK) break;
-        int hf[2];
-        if (cudaMemcpyAsync(hf, dflags, sizeof(hf), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        int bad = 0;
+        if (cudaMemcpyAsync(&bad, dflags, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
             cudaStreamSynchronize(st) != cudaSuccess) {
             rc = fail(AK_ERR_CUDA, "geometry sync failed");
             break;
         }
-        if (hf[0]) {
+        if (bad) {
             rc = fail(AK_ERR_DOMAIN, "points must lie in [-1/2, 1/2)");
             break;
         }
-        host_counter = hf[1];
-        g->item_end[q] = host_counter;
-        // Largest items first (blocks are dispatched in index order: LPT-like tail).
-        const int64_t ni = g->item_end[q] - g->item_begin[q];
-        if (ni > 1 && items_sorted_default()) {
-            std::vector<WorkItem> h((size_t)ni);
-            if (cudaMemcpyAsync(h.data(), g->items + g->item_begin[q], sizeof(WorkItem) * ni, cudaMemcpyDeviceToHost,
-                                st) != cudaSuccess ||
-                cudaStreamSynchronize(st) != cudaSuccess) {
-                rc = fail(AK_ERR_CUDA, "item copy failed");
-                break;
-            }
-            std::stable_sort(h.begin(), h.end(), [](const WorkItem& a, const WorkItem& b) {
-                if (a.count != b.count) return a.count > b.count;
-                return a.start < b.start;
-            });
-            // stream-ordered upload; wait for it before `h` goes out of scope
-            if (cudaMemcpyAsync(g->items + g->item_begin[q], h.data(), sizeof(WorkItem) * ni, cudaMemcpyHostToDevice,
-                                st) != cudaSuccess ||
-                cudaStreamSynchronize(st) != cudaSuccess) {
-                rc = fail(AK_ERR_CUDA, "item copy failed");
-                break;
+        append_sorted(spread_items, g->item_begin[q], g->item_end[q]);
+        if (q == 3) {
+            if (split3) {
+                append_sorted(cell_items, g->iitem_begin3, g->iitem_end3);
+            } else {
+                g->iitem_begin3 = g->item_begin[3];
+                g->iitem_end3 = g->item_end[3];
             }
         }
     }
-    g->nitems = host_counter;
+    if (rc == AK_OK) {
+        if (cudaMalloc(&g->items, sizeof(WorkItem) * std::max<size_t>(1, all.size())) != cudaSuccess) {
+            cudaGetLastError();
+            rc = fail(AK_ERR_ALLOC, "item allocation failed");
+        } else if (!all.empty() &&
+                   (cudaMemcpyAsync(g->items, all.data(), sizeof(WorkItem) * all.size(), cudaMemcpyHostToDevice, st) !=
+                        cudaSuccess ||
+                    cudaStreamSynchronize(st) != cudaSuccess)) {
+            rc = fail(AK_ERR_CUDA, "item upload failed");
+        }
+    }
+    g->nitems = (int64_t)all.size();
     if (rc == AK_OK && cached) {
         const int T = g->wf.taps;
         std::vector<int64_t> shift(P, 0);
@@ -498,6 +632,7 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
             }
         }
         g->batch3 = batch3_default(g->sedge[3]);
+        g->batch3i = batch3_default(g->sedge_i3);
         const char* iw = getenv("AK_IWARPS");
         g->iwarps = (iw && atoi(iw) == 2) ? 2 : 1;
         const char* sw = getenv("AK_SWARPS");
@@ -508,14 +643,6 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
         g->vreg = vr && vr[0] == '1';
     }
     cudaStreamSynchronize(st);
-    cudaFree(keys);
-    cudaFree(keys2);
-    cudaFree(vals);
-    cudaFree(vals2);
-    cudaFree(counts);
-    cudaFree(starts);
-    cudaFree(dflags);
-    cudaFree(temp);
     return rc;
 }
 
@@ -856,9 +983,9 @@ static void launch_interp3_t(const ak_geom* g, int64_t i0, int64_t ni, const dou
                              const double* scale, double* out, int64_t ldo, int atomic_out, int64_t wstride,
                              cudaStream_t st)
 {
-    if (T == 12 && g->cached && g->sedge[3] == 1) {
+    if (T == 12 && g->cached && g->sedge_i3 == 1) {
         const unsigned grid = (unsigned)(ni * R);  // item-major, RHS fastest
-        if (g->batch3 == 32)
+        if (g->batch3i == 32)
             k_interp3c<32><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids, g->canon_off_d, R,
                                                 g->n, scale, out, ldo, atomic_out, wstride);
         else
@@ -902,7 +1029,9 @@ static void launch_interp_lane(const ak_geom* g, int64_t i0, int64_t ni, const d
 static int interp_group(const ak_geom* g, int q, const double* grids, int R, const double* scale, double* out,
                         int64_t ldo, int sum_windows, int atomic_out, int64_t wstride, cudaStream_t st)
 {
-    const int64_t i0 = g->item_begin[q], ni = g->item_end[q] - g->item_begin[q];
+    // 3-D windows may interpolate over their own (single-cell) item list
+    const int64_t i0 = q == 3 ? g->iitem_begin3 : g->item_begin[q];
+    const int64_t ni = q == 3 ? g->iitem_end3 - g->iitem_begin3 : g->item_end[q] - g->item_begin[q];
     if (g->windows_of_q[q].empty() || g->N == 0) return AK_OK;
     const int T = g->wf.taps;
     const int64_t ws = sum_windows ? 0 : wstride;

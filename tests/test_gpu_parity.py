@@ -181,6 +181,9 @@ def test_native_library_is_what_runs(cuda):
     {"AK_BATCH3": "32", "AK_VREG": "1"},
     {"AK_SUPERCELL3": "1"},                 # single-cell work items (auto-selected for dense data)
     {"AK_SUPERCELL3": "1", "AK_BATCH3": "16", "AK_CHUNK3": "100"},
+    # split items: supercell spread, single-cell interpolation over the same sorted points
+    {"AK_DENSE_CELLS": "1e9", "AK_DENSE_CELLS_INTERP": "0"},
+    {"AK_DENSE_CELLS": "1e9", "AK_DENSE_CELLS_INTERP": "0", "AK_CHUNK3": "100"},
 ])
 def test_kernel_variants_match_reference(cuda, monkeypatch, variant):
     """Every tuned kernel variant (selected at plan time) reproduces the reference."""
