@@ -23,6 +23,8 @@ METRICS = {
     "dram_read_bytes": "dram__bytes_read.sum",
     "dram_write_bytes": "dram__bytes_write.sum",
     "fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    # DMMA (mma.sync f64) issues to the tensor pipe, not the fp64 pipe counter above
+    "dmma_pipe_pct": "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
     "warps_active_per_sm": "sm__warps_active.avg.per_cycle_active",
     "registers_per_thread": "launch__registers_per_thread",
     "smem_per_block": "launch__shared_mem_per_block_static",
