@@ -21,11 +21,13 @@ n = 64, cutoff 6, Kaiser-Bessel).  A step is one full K v over all windows.
 * ``cpu_baseline``: the CPU oracle port (oracle/, serial C loops + numpy FFT,
   the reference's algorithm and cost structure) timed on one window at full N.
 
-Multi-GPU (torchrun): point sharding by default (each rank spreads its own
-rows into every window's grid; one NCCL all-reduce of the band spectra, then
-every rank interpolates its rows; --shard window: windows split over ranks
-and the partial K v all-reduced).  Timing is the max over ranks; the roofline
-is rank 0's local kernels.
+Multi-GPU (torchrun): --shard hybrid (default) splits the ranks into G window
+groups x Q row blocks (G from distributed.hybrid_layout: 2 x 4 on 8 GPUs for
+config 4); each rank spreads its rows into its windows' grids, the band
+spectra are all-reduced within the window group, each rank interpolates its
+rows, and the row partials are all-reduced across window groups.  --shard
+point (G = 1) / window (Q = 1) are the two pure decompositions.  Timing is the
+max over ranks; the roofline is rank 0's local kernels.
 """
 
 from __future__ import annotations
@@ -60,7 +62,10 @@ def parse():
     ap.add_argument("--n", type=int, default=1_000_000, help="points (default: the config's 1M)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip extras (for profilers)")
-    ap.add_argument("--shard", choices=["point", "window"], default="point",
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo: functional check of the multi-rank path with several ranks on one device "
+                         "(host-side collectives; its timings are not bench values)")
+    ap.add_argument("--shard", choices=["hybrid", "point", "window"], default="hybrid",
                     help="multi-GPU decomposition (N > 1): rows (default) or windows")
     return ap.parse_args()
 
@@ -322,6 +327,13 @@ def extra_workloads(torch, steps=5, warmup=2):
     return out
 
 
+def _parallelism(shard, dplan, world):
+    if shard == "hybrid":
+        return (f"hybrid x{world}: {dplan.G} window groups x {dplan.Q} row blocks; NCCL all-reduce of band "
+                f"spectra within a window group, of row partials across groups")
+    return f"{shard}-shard x{world} + NCCL all-reduce"
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -329,9 +341,14 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dist_backend == "gloo":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2404_17344_b200 import _native, configs
     from paper_2404_17344_b200.fastsum import build_plan, fast_matvec, fast_matvecs
@@ -347,9 +364,9 @@ def run_ours(args):
 
     t0 = time.perf_counter()
     if world > 1:
-        from paper_2404_17344_b200.distributed import PointShardedPlan, WindowShardedPlan
+        from paper_2404_17344_b200.distributed import HybridShardedPlan, PointShardedPlan, WindowShardedPlan
 
-        cls = PointShardedPlan if args.shard == "point" else WindowShardedPlan
+        cls = {"hybrid": HybridShardedPlan, "point": PointShardedPlan, "window": WindowShardedPlan}[args.shard]
         dplan = cls(wl.spec, wl.window_set, "default", wl.data)
         plan = dplan.plan
     else:
@@ -377,7 +394,7 @@ def run_ours(args):
     def step_deriv():
         if world > 1:
             fams = ("gauss", "der_gauss")
-            if args.shard == "point":
+            if args.shard != "window":
                 outs = dplan.matvecs_local(v_dev[dplan.lo:dplan.hi].reshape(1, -1), fams)
             else:
                 outs = dplan.matvecs(v_dev.reshape(1, -1), fams)
@@ -416,7 +433,7 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "N": N, "windows": len(wins), "rhs": 1,
-                   "parallelism": (f"{args.shard}-shard x{world} + NCCL all-reduce" if world > 1 else "single GPU"),
+                   "parallelism": (_parallelism(args.shard, dplan, world) if world > 1 else "single GPU"),
                    "l2": "inputs larger than L2: per-step geometry stream 32 B x 1M x 10 windows = 320 MB"},
         "clocks": clocks, "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
         "plan_build_s": plan_s,

@@ -175,3 +175,109 @@ class PointShardedPlan:
             dist.all_gather(bufs, pad, group=self.group)
             chunks = [b[:s] for b, s in zip(bufs, sizes)]
         return torch.cat(chunks)
+
+
+def hybrid_layout(lengths, world: int, taps: int = WINDOW_TAPS, tolerance: float = 0.1) -> int:
+    """Number of window groups for HybridShardedPlan: the largest g in {world, ..., 2}
+    dividing world whose LPT window partition is balanced within `tolerance`
+    (max group cost <= (1 + tolerance) * mean), else 1 (pure point sharding)."""
+    total = sum(window_cost(q, taps) for q in lengths)
+    for g in range(min(world, len(lengths)), 1, -1):
+        if world % g:
+            continue
+        parts = window_partition(lengths, g, taps)
+        worst = max(sum(window_cost(lengths[w], taps) for w in p) for p in parts)
+        if worst <= (1.0 + tolerance) * total / g:
+            return g
+    return 1
+
+
+class HybridShardedPlan:
+    """Window groups x point groups (the two exact decompositions combined).
+
+    world = G x Q ranks: window group gi = rank // Q owns an LPT share of the
+    windows, point group position pj = rank % Q owns a contiguous row block.
+    Each rank spreads its rows into its windows' grids; the band spectra are
+    all-reduced among the Q ranks of its window group; each rank interpolates
+    its own rows for its own windows; the partial products of a row block are
+    all-reduced across the G window groups.  G = 1 is point sharding, Q = 1 is
+    window sharding.  Per rank: 1/world of the gridding work and 1/G of the
+    FFTs (point sharding repeats all FFTs on every rank), with one small
+    collective per stage: band (R * sum_w m^(q-1) m/2 complex over own
+    windows) and rows (R * N/Q doubles).
+    """
+
+    def __init__(self, spec, window_set: WindowSet, preset, data: Dataset, window_groups: int | None = None,
+                 group=None, **kw):
+        from .fastsum import build_plan
+
+        dist = _dist()
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        G = window_groups or hybrid_layout(window_set.lengths, world)
+        if world % G:
+            raise ValueError("window_groups must divide the world size")
+        Q = world // G
+        self.world, self.rank, self.G, self.Q = world, rank, G, Q
+        self.gi, self.pj = rank // Q, rank % Q
+        base = dist.get_process_group_ranks(group) if group is not None else list(range(world))
+        # every rank creates every subgroup (new_group is collective)
+        self.band_group = self.row_group = None
+        for g in range(G):
+            members = [base[g * Q + j] for j in range(Q)]
+            pg = dist.new_group(members) if Q > 1 else None
+            if g == self.gi:
+                self.band_group = pg
+        for j in range(Q):
+            members = [base[g * Q + j] for g in range(G)]
+            pg = dist.new_group(members) if G > 1 else None
+            if j == self.pj:
+                self.row_group = pg
+        self.owned = window_partition(window_set.lengths, G)[self.gi]
+        self.rows = row_partition(data.n_rows, Q)
+        self.lo, self.hi = self.rows[self.pj]
+        self.n_rows = data.n_rows
+        sub = WindowSet(tuple(window_set.windows[w] for w in self.owned), d_max=window_set.d_max)
+        self.plan = build_plan(spec, sub, preset, _subset_rows(data, self.lo, self.hi), **kw)
+
+    def matvecs_local(self, V_local, families=None):
+        """(R, n_local) own-row RHS block -> list of (R, n_local) own-row products (all windows)."""
+        import torch
+
+        from . import _native
+
+        dist = _dist()
+        fams = tuple(families or (self.plan.spec.family,))
+        R = V_local.shape[0]
+        op = self.plan._operator(fams, R)
+        if self.Q > 1:
+            op.spectrum_only(V_local)
+            dist.all_reduce(op.band(), group=self.band_group)
+            flag = _native.AK_APPLY_FROM_SPECTRUM
+            V_arg = None
+        else:
+            flag, V_arg = 0, V_local
+        outs = [torch.empty((R, self.hi - self.lo), dtype=torch.float64, device="cuda") for _ in fams]
+        op.apply(V_arg, outs, [True] * len(outs), flags=flag)
+        if self.G > 1:
+            for o in outs:
+                dist.all_reduce(o, group=self.row_group)
+        return outs
+
+    def matvec(self, v, gather: bool = True):
+        """Full-length v (replicated) -> K v (replicated if gather, else own rows)."""
+        import torch
+
+        dist = _dist()
+        out = self.matvecs_local(v[self.lo:self.hi].reshape(1, -1))[0][0]
+        if not gather:
+            return out
+        if self.Q == 1:
+            return out
+        sizes = [hi - lo for lo, hi in self.rows]
+        m = max(sizes)
+        pad = torch.zeros(m, dtype=torch.float64, device="cuda")
+        pad[: out.numel()] = out
+        bufs = [torch.empty(m, dtype=torch.float64, device="cuda") for _ in sizes]
+        dist.all_gather(bufs, pad, group=self.band_group)
+        return torch.cat([b[:s] for b, s in zip(bufs, sizes)])

@@ -103,3 +103,13 @@ def test_two_rank_decompositions_match_single_process():
     for rank, err_w, err_p in res:
         assert err_w <= 1e-13, (rank, err_w)
         assert err_p <= 1e-12, (rank, err_p)
+
+
+def test_hybrid_layout():
+    from paper_2404_17344_b200.distributed import hybrid_layout
+
+    assert hybrid_layout([3] * 10, 8) == 2      # 5 + 5 windows, 4 point groups each
+    assert hybrid_layout([3] * 10, 1) == 1
+    assert hybrid_layout([3, 3, 3, 3], 8) == 4  # one window per group
+    assert hybrid_layout([3, 3, 3], 2) == 1     # 2 + 1 is not balanced: point sharding
+    assert hybrid_layout([3, 3, 3, 3, 3, 3, 2, 2, 1, 1], 8) == 2

@@ -3,7 +3,8 @@ available device, exchanging through gloo (host-side collectives; the ranks'
 kernels never wait on each other).  Checks the real sharded code paths --
 SPECTRUM_ONLY spread + band all-reduce + FROM_SPECTRUM interpolation (point
 sharding) and the LPT window split + all-reduce (window sharding) -- against the
-single-process product."""
+single-process product; with 4 ranks also the 2 x 2 hybrid (window groups x
+point groups)."""
 
 import os
 import socket
@@ -30,7 +31,7 @@ def _worker(rank, world, port, X, V, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2404_17344_b200.dataset import PRESCALED, Dataset
-        from paper_2404_17344_b200.distributed import PointShardedPlan, WindowShardedPlan
+        from paper_2404_17344_b200.distributed import HybridShardedPlan, PointShardedPlan, WindowShardedPlan
         from paper_2404_17344_b200.fastsum import build_plan, fast_matvecs
         from paper_2404_17344_b200.kernels import KernelSpec
         from paper_2404_17344_b200.windows import WindowSet
@@ -50,16 +51,26 @@ def _worker(rank, world, port, X, V, q):
             for name, o in zip(("K", "dK_dell"), local):
                 r = ref[name][:, pp.lo:pp.hi]
                 errs[f"point_{exchange}_local_{name}"] = np.linalg.norm(o.cpu().numpy() - r) / np.linalg.norm(r)
-        wp = WindowShardedPlan(spec, ws, "default", ds)
-        outs = wp.matvecs(Vd, ("gauss", "der_gauss"))
-        for name, o in zip(("K", "dK_dell"), outs):
-            errs[f"window_{name}"] = np.linalg.norm(o.cpu().numpy() - ref[name]) / np.linalg.norm(ref[name])
+        if world == 2:
+            wp = WindowShardedPlan(spec, ws, "default", ds)
+            outs = wp.matvecs(Vd, ("gauss", "der_gauss"))
+            for name, o in zip(("K", "dK_dell"), outs):
+                errs[f"window_{name}"] = np.linalg.norm(o.cpu().numpy() - ref[name]) / np.linalg.norm(ref[name])
+        for G in sorted({1, 2, world}):
+            hp = HybridShardedPlan(spec, ws, "default", ds, window_groups=G)
+            k_rows = hp.matvec(Vd[0]).cpu().numpy()
+            errs[f"hybrid{G}_K"] = np.linalg.norm(k_rows - ref["K"][0]) / np.linalg.norm(ref["K"][0])
+            local = hp.matvecs_local(Vd[:, hp.lo:hp.hi].contiguous(), ("gauss", "der_gauss"))
+            for name, o in zip(("K", "dK_dell"), local):
+                r = ref[name][:, hp.lo:hp.hi]
+                errs[f"hybrid{G}_local_{name}"] = np.linalg.norm(o.cpu().numpy() - r) / np.linalg.norm(r)
         q.put((rank, errs))
     finally:
         dist.destroy_process_group()
 
 
-def test_two_ranks_on_one_device_match_single_process(cuda):
+@pytest.mark.parametrize("world", [2, 4])
+def test_ranks_on_one_device_match_single_process(cuda, world):
     import torch.multiprocessing as mp
 
     rng = np.random.default_rng(21)
@@ -68,7 +79,7 @@ def test_two_ranks_on_one_device_match_single_process(cuda):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, X, V, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, X, V, q)) for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=300) for _ in procs]
