@@ -215,8 +215,8 @@ class HybridShardedPlan:
         world = dist.get_world_size(group)
         rank = dist.get_rank(group)
         G = window_groups or hybrid_layout(window_set.lengths, world)
-        if world % G:
-            raise ValueError("window_groups must divide the world size")
+        if G < 1 or world % G or G > len(window_set):
+            raise ValueError("window_groups must divide the world size and not exceed the number of windows")
         Q = world // G
         self.world, self.rank, self.G, self.Q = world, rank, G, Q
         self.gi, self.pj = rank // Q, rank % Q
