@@ -35,6 +35,23 @@ __global__ void __launch_bounds__(32, 8) k(long iters, double* io) {
     double acc[P0][P1][P2];
     for (int a = 0; a < P0; ++a) for (int b = 0; b < P1; ++b) for (int c = 0; c < P2; ++c) acc[a][b][c] = 0;
     const int nb = 32;
+    if (V == 2) {
+        // no shared-memory loads: two register weight sets, made opaque every point so the
+        // w1*w2 products are recomputed (same FP64 instruction mix as the real loop)
+        double a0[P0], a1[P1], a2[P2], b0[P0], b1[P1], b2[P2];
+        load_w<T>(a0, a1, a2, &wbuf[0][0], g0, g1, g2);
+        load_w<T>(b0, b1, b2, &wbuf[1][0], g0, g1, g2);
+        for (long it = 0; it < iters; ++it) {
+            for (int j = 0; j < nb; j += 2) {
+#pragma unroll
+                for (int i = 0; i < P1; ++i) asm volatile("" : "+d"(a1[i]), "+d"(a2[i]));
+                spread_fma(acc, a0, a1, a2);
+#pragma unroll
+                for (int i = 0; i < P1; ++i) asm volatile("" : "+d"(b1[i]), "+d"(b2[i]));
+                spread_fma(acc, b0, b1, b2);
+            }
+        }
+    } else
     for (long it = 0; it < iters; ++it) {
         double a0[P0], a1[P1], a2[P2], b0[P0], b1[P1], b2[P2];
         load_w<T>(a0, a1, a2, &wbuf[0][0], g0, g1, g2);
@@ -63,7 +80,7 @@ void run(int wpsm, int sms, double* io) {
 int main() {
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     double* io; cudaMalloc(&io, 4096 * 8); cudaMemset(io, 0, 4096 * 8);
-    for (int w : {8, 16}) { run<0>(w, sms, io); run<1>(w, sms, io); }
+    for (int w : {8, 16}) { run<0>(w, sms, io); run<1>(w, sms, io); run<2>(w, sms, io); }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
