@@ -1,0 +1,94 @@
+"""GPU: seeded random configurations against the CPU oracle (robustness sweep).
+
+Each case draws N (1 .. 20k, log-uniform), 1-4 windows of length 1-3 over 6
+features, a preset or explicit m, a kernel family, a node distribution
+(uniform box, clustered, hugging the periodic boundary, all in one cell), R
+right-hand sides and plan knobs (supercell edge, item cap), and checks K V
+(and dK/dl V for base families) against the oracle at the north_star
+tolerance.  The cases are fixed by their seeds, so failures reproduce."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-8
+N_CASES = 64
+
+
+def _case(seed):
+    rng = np.random.default_rng(10_000 + seed)
+    lo = 0.0 if rng.random() < 0.25 else math.log(100)
+    N = int(round(math.exp(rng.uniform(lo, math.log(20_000)))))
+    P = int(rng.integers(1, 5))
+    windows = []
+    for _ in range(P):
+        q = int(rng.integers(1, 4))
+        w = tuple(sorted(int(c) for c in rng.choice(6, size=q, replace=False)))
+        if w not in windows:
+            windows.append(w)
+    preset = rng.choice(["rough", "default", "fine", "explicit"])
+    if preset == "explicit":
+        preset = int(rng.integers(4, 25)) * 2
+    family = str(rng.choice(["gauss", "der_gauss", "matern12", "der_matern12"]))
+    ell = float(math.exp(rng.uniform(math.log(0.05), math.log(3.0))))
+    dist = rng.choice(["uniform", "cluster", "boundary", "onecell"])
+    if dist == "uniform":
+        X = rng.uniform(-0.25, 0.25, size=(N, 6)) / math.sqrt(3.0)
+    elif dist == "cluster":
+        X = np.clip(rng.normal(scale=0.02, size=(N, 6)) + rng.uniform(-0.1, 0.1, size=(1, 6)), -0.49, 0.49)
+    elif dist == "boundary":
+        X = np.where(rng.random((N, 6)) < 0.5, rng.uniform(-0.5, -0.47, (N, 6)), rng.uniform(0.47, 0.5, (N, 6)))
+        X = np.minimum(X, np.nextafter(0.5, 0.0))
+    else:
+        X = 0.003 + 1e-4 * rng.random((N, 6))
+    R = int(rng.choice([1, 2, 5]))
+    V = rng.normal(size=(R, N))
+    knobs = {}
+    k = rng.integers(0, 4)
+    if k == 1:
+        knobs["AK_SUPERCELL3"] = "1"
+    elif k == 2:
+        knobs["AK_SUPERCELL3"] = "2"
+    elif k == 3:
+        knobs["AK_DENSE_CELLS"] = "1e9"
+        knobs["AK_DENSE_CELLS_INTERP"] = "0"
+    if rng.random() < 0.3:
+        knobs["AK_CHUNK3"] = str(int(rng.choice([64, 100, 333])))
+    return dict(N=N, windows=windows, preset=preset, family=family, ell=ell, dist=str(dist), X=X, V=V,
+                knobs=knobs)
+
+
+@pytest.mark.parametrize("seed", range(N_CASES))
+def test_random_configuration_matches_oracle(cuda, monkeypatch, seed):
+    from oracle import restate as R
+    from paper_2404_17344_b200.dataset import PRESCALED, Dataset
+    from paper_2404_17344_b200.fastsum import PRESETS, build_plan, fast_matvecs
+    from paper_2404_17344_b200.kernels import DERIVATIVE_PREFACTOR, KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    c = _case(seed)
+    for k, v in c["knobs"].items():
+        monkeypatch.setenv(k, v)
+    ds = Dataset(c["X"], np.zeros(c["N"]), tuple(f"x{i}" for i in range(6)), scaling_state=PRESCALED, d_max=3)
+    ws = WindowSet(tuple(tuple(col + 1 for col in w) for w in c["windows"]), d_max=3)
+    spec = KernelSpec(c["family"], c["ell"], 0.7)
+    import warnings
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")  # AccuracyWarning for small ell * m is expected here
+        plan = build_plan(spec, ws, c["preset"], ds)
+    base = DERIVATIVE_PREFACTOR[c["family"]] is None
+    res = fast_matvecs(plan, c["V"], dell=base)
+    m = PRESETS.get(c["preset"], c["preset"])
+    fs = R.FastSum(c["family"], c["ell"], 0.7, c["windows"], c["X"], m=m)
+    for r in range(c["V"].shape[0]):
+        ref = fs.matvec(c["V"][r])
+        assert rel(res["K"][r], ref) <= TOL, (seed, c["dist"], c["knobs"], r)
+    if base:
+        der = R.FastSum("der_" + c["family"], c["ell"], 0.7, c["windows"], c["X"], m=m)
+        assert rel(res["dK_dell"][0], der.matvec(c["V"][0])) <= TOL, (seed, "dK")
