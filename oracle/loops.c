@@ -11,6 +11,13 @@
  * (nufft.py:169-191), row-major grid with the last axis fastest, and the
  * same loop nesting / accumulation order, so results agree with the
  * reference to rounding.
+ *
+ * One deliberate difference: the reference wraps a tap index with a single
+ * `if (i >= n) i -= n` (nufft.py:204-206 and the other loops), which indexes
+ * out of bounds when the grid is smaller than the window (n < 2*cutoff, e.g.
+ * m <= 4 at cutoff 6) -- undefined behaviour in the numba kernels.  Here the
+ * wrap is a loop (full periodic wrap), identical whenever the reference is
+ * defined; the CUDA kernels wrap the same way.
  */
 #include <stdint.h>
 
@@ -31,7 +38,7 @@ void oracle_spread(int q, int64_t N, int T, int64_t n,
         const double vr = values[2 * j], vi = values[2 * j + 1];
         for (int a = 0; a < T; ++a) {
             int64_t ia = f0[j] + a;
-            if (ia >= n) ia -= n;
+            while (ia >= n) ia -= n;
             const double ar = vr * w0[j * T + a], ai = vi * w0[j * T + a];
             if (q == 1) {
                 grid[2 * ia] += ar;
@@ -41,7 +48,7 @@ void oracle_spread(int q, int64_t N, int T, int64_t n,
             const int64_t plane = ia * n;
             for (int b = 0; b < T; ++b) {
                 int64_t ib = f1[j] + b;
-                if (ib >= n) ib -= n;
+                while (ib >= n) ib -= n;
                 const double br = ar * w1[j * T + b], bi = ai * w1[j * T + b];
                 if (q == 2) {
                     grid[2 * (plane + ib)] += br;
@@ -51,7 +58,7 @@ void oracle_spread(int q, int64_t N, int T, int64_t n,
                 const int64_t row = (plane + ib) * n;
                 for (int c = 0; c < T; ++c) {
                     int64_t ic = f2[j] + c;
-                    if (ic >= n) ic -= n;
+                    while (ic >= n) ic -= n;
                     grid[2 * (row + ic)] += br * w2[j * T + c];
                     grid[2 * (row + ic) + 1] += bi * w2[j * T + c];
                 }
@@ -76,7 +83,7 @@ void oracle_interp(int q, int64_t N, int T, int64_t n,
         double accr = 0.0, acci = 0.0;
         for (int a = 0; a < T; ++a) {
             int64_t ia = f0[j] + a;
-            if (ia >= n) ia -= n;
+            while (ia >= n) ia -= n;
             double sar, sai;
             if (q == 1) {
                 sar = grid[2 * ia];
@@ -87,7 +94,7 @@ void oracle_interp(int q, int64_t N, int T, int64_t n,
                 sai = 0.0;
                 for (int b = 0; b < T; ++b) {
                     int64_t ib = f1[j] + b;
-                    if (ib >= n) ib -= n;
+                    while (ib >= n) ib -= n;
                     double sbr, sbi;
                     if (q == 2) {
                         sbr = grid[2 * (plane + ib)];
@@ -98,7 +105,7 @@ void oracle_interp(int q, int64_t N, int T, int64_t n,
                         sbi = 0.0;
                         for (int c = 0; c < T; ++c) {
                             int64_t ic = f2[j] + c;
-                            if (ic >= n) ic -= n;
+                            while (ic >= n) ic -= n;
                             sbr += grid[2 * (row + ic)] * w2[j * T + c];
                             sbi += grid[2 * (row + ic) + 1] * w2[j * T + c];
                         }

@@ -92,3 +92,31 @@ def test_random_configuration_matches_oracle(cuda, monkeypatch, seed):
     if base:
         der = R.FastSum("der_" + c["family"], c["ell"], 0.7, c["windows"], c["X"], m=m)
         assert rel(res["dK_dell"][0], der.matvec(c["V"][0])) <= TOL, (seed, "dK")
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_nufft_matches_oracle(cuda, seed):
+    """Type-1 / type-2 NUFFTs: random q, m (even, 2..64), N (0..5000), node distribution."""
+    from oracle import restate as R
+    from paper_2404_17344_b200.nufft import NufftPlan, nufft_type1, nufft_type2, prepare_points
+
+    rng = np.random.default_rng(20_000 + seed)
+    q = int(rng.integers(1, 4))
+    m = int(rng.integers(1, 33)) * 2 if q < 3 else int(rng.integers(1, 17)) * 2
+    N = int(rng.integers(0, 5001))
+    if rng.random() < 0.5:
+        pts = rng.uniform(-0.5, 0.5, size=(N, q))
+    else:
+        pts = np.clip(rng.normal(scale=0.01, size=(N, q)) + rng.uniform(-0.5, 0.5, size=(1, q)), -0.5, 0.4999)
+    pts = np.minimum(pts, np.nextafter(0.5, 0.0))
+    w = rng.normal(size=N) + 1j * rng.normal(size=N)
+    c = rng.normal(size=(m,) * q) + 1j * rng.normal(size=(m,) * q)
+    plan = NufftPlan(dims=q, m=m)
+    oplan = R.Nufft(q, m)
+    if N == 0:
+        assert np.all(nufft_type1(plan, pts, w) == 0)
+        return
+    geom = prepare_points(plan, pts)
+    ogeom = R.Geometry(oplan, pts)
+    assert rel(nufft_type1(plan, geom, w), R.type1(oplan, ogeom, w)) <= TOL, (seed, q, m, N)
+    assert rel(nufft_type2(plan, geom, c), R.type2(oplan, ogeom, c)) <= TOL, (seed, q, m, N)
