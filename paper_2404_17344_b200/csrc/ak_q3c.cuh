@@ -17,11 +17,13 @@
 
 namespace ak {
 
-#ifndef AK_SPREAD3C_MINB
-#define AK_SPREAD3C_MINB 8
+// 222 registers (no spills) -> 9 warps per SM; __launch_bounds__(32, 8) let ptxas use
+// 240 (8 warps): 1.551 vs 1.569 ms on config 4.  Tighter caps spill (200: 1.69 ms).
+#ifndef AK_SPREAD3C_BOUNDS
+#define AK_SPREAD3C_BOUNDS __maxnreg__(224)
 #endif
 template <int B>
-__global__ void __launch_bounds__(32, AK_SPREAD3C_MINB)
+__global__ void AK_SPREAD3C_BOUNDS
 k_spread3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ V, int64_t ldv,
            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
@@ -145,6 +147,7 @@ k_spread3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     }
 }
 
+// (__maxnreg__ 184/200/208 for 10-11 warps per SM: no gain, 1.353-1.369 vs 1.351 ms)
 template <int B>
 __global__ void __launch_bounds__(32, 8)
 k_interp3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
