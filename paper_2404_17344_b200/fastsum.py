@@ -117,6 +117,12 @@ def band_multiplier(table: CoefficientTable, nplan: NufftPlan) -> np.ndarray:
 OPERATOR_CACHE_LIMIT = 8
 
 
+def _stream_key() -> int:
+    """The current CUDA stream: an operator owns mutable workspace (grids, spectra), so
+    products issued on different streams get different operators (ak_op: one per stream)."""
+    return _torch().cuda.current_stream().cuda_stream
+
+
 def _cached_operator(cache: dict, key, make):
     """Most-recently-used cache of a plan's operators, at most OPERATOR_CACHE_LIMIT
     (each holds R x ~2 grids of device memory; evicted ones are destroyed)."""
@@ -315,7 +321,7 @@ class FastsumPlan:
             sets = [self._family_set(f) for f in families]
             return _Operator(self.geometries, gi, self.m, R, [s[0] for s in sets], [s[1] for s in sets])
 
-        return _cached_operator(self._cache, ("op", families, R, id(gi)), make)
+        return _cached_operator(self._cache, ("op", families, R, id(gi), _stream_key()), make)
 
 
 def _check_prescaled(data: Dataset, window_set: WindowSet) -> None:
@@ -471,7 +477,7 @@ class MixedKernelPlan:
             S = [sk, sd] if dell else [sk]
             return _Operator(self.geometries, self.geometries, self.m, R, H, S)
 
-        return _cached_operator(self._cache, ("op", R, dell), make)
+        return _cached_operator(self._cache, ("op", R, dell, _stream_key()), make)
 
 
 def build_mixed_plan(specs, window_set: WindowSet, preset, data: Dataset, cutoff: int = 6,

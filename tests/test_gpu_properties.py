@@ -332,3 +332,42 @@ def test_q2_many_rhs(cuda):
         fs = R.FastSum(fam, 0.3, 1.0, [(0, 1), (2, 3)], X)
         for r in (0, 7, 10):
             assert rel(res[key][r], fs.matvec(V[r])) <= 1e-8, (key, r)
+
+
+def test_concurrent_streams_share_a_plan(cuda):
+    """Two host threads, each on its own CUDA stream, run products on one plan at the
+    same time: each stream gets its own operator workspace (results stay exact)."""
+    import threading
+
+    import torch
+
+    from paper_2404_17344_b200.fastsum import build_plan, fast_matvec
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    rng = np.random.default_rng(12)
+    X = rng.uniform(-0.14, 0.14, size=(20000, 6))
+    plan = build_plan(KernelSpec("gauss", 0.3), WindowSet(((1, 2, 3), (4, 5, 6)), d_max=3), "default", _ds(X, 3))
+    vs = [torch.as_tensor(rng.normal(size=20000), device="cuda") for _ in range(2)]
+    refs = [fast_matvec(plan, v).clone() for v in vs]
+    torch.cuda.synchronize()
+    outs, errors = [None, None], []
+
+    def run(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(20):
+                    outs[k] = fast_matvec(plan, vs[k])
+            s.synchronize()
+        except Exception as exc:  # pragma: no cover - reported below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=run, args=(k,)) for k in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for k in range(2):
+        assert rel(outs[k].cpu().numpy(), refs[k].cpu().numpy()) <= 1e-13
