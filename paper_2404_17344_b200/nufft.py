@@ -153,10 +153,19 @@ class NufftPlan:
         return 1.0 / self.window_transform(freqs(self.m)) ** 2
 
     def window_fn(self) -> "_native.WindowFn":
-        """Per-tap polynomial table of the window for the CUDA kernels (cached)."""
+        """Per-tap polynomial table of the window for the CUDA kernels (cached).
+
+        Tap counts without specialised kernels are padded with one zero tap on
+        each side (the window is zero there: identical sums): 6 -> 8 and
+        10 -> 12 taps, so cutoffs 3 and 5 run on the tuned 8- and 12-tap kernels
+        (12: tensor-core interpolation, plan-time weight tables) instead of the
+        one-thread-per-point fallback.
+        """
         cached = _WINDOW_CACHE.get(self._wkey())
         if cached is None:
             cached = _fit_window(self)
+            if cached.taps in PADDED_TAPS:
+                cached = _pad_window(cached, PADDED_TAPS[cached.taps])
             _WINDOW_CACHE[self._wkey()] = cached
         return cached
 
@@ -165,6 +174,24 @@ class NufftPlan:
 
 
 _WINDOW_CACHE: dict = {}
+
+#: kernel tap count used for window tap counts that have no specialised kernels
+PADDED_TAPS = {6: 8, 10: 12}
+
+
+def _pad_window(wf: "_native.WindowFn", taps: int) -> "_native.WindowFn":
+    """The same window on `taps` >= wf.taps kernel taps: (taps - wf.taps) / 2 zero taps on
+    each side.  Pair a of the padded table (taps a and taps-1-a) is pair a - k of the
+    original, k = (taps - wf.taps) / 2; the outer k pairs are zero."""
+    k = (taps - wf.taps) // 2
+    out = _native.WindowFn()
+    out.taps = taps
+    out.ncoef = wf.ncoef
+    for a in range(taps // 2):
+        for j in range(_native.AK_NCOEF):
+            out.ce[a][j] = wf.ce[a - k][j] if a >= k else 0.0
+            out.co[a][j] = wf.co[a - k][j] if a >= k else 0.0
+    return out
 
 
 def _fit_window(plan: NufftPlan) -> "_native.WindowFn":

@@ -123,14 +123,20 @@ def test_window_polynomial_accuracy(cutoff, window):
     wf = p.window_fn()
     o = R.Nufft(2, 16, cutoff=cutoff, window=window)
     T = 2 * cutoff
+    Tk = wf.taps                 # kernel taps: T, or T + 2 (zero outer taps, see PADDED_TAPS)
+    k = (Tk - T) // 2
+    assert Tk == NU.PADDED_TAPS.get(T, T)
     frac = np.linspace(0.0, 1.0, 1001, endpoint=False)
     s = 2 * frac - 1
-    for a in range(T):
-        pair = a if a < T // 2 else T - 1 - a
+    for a in range(Tk):
+        pair = a if a < Tk // 2 else Tk - 1 - a
         e = np.polyval(np.array(wf.ce[pair][:]), s * s)
         od = np.polyval(np.array(wf.co[pair][:]), s * s)
-        val = e + s * od if a < T // 2 else e - s * od
-        exact = o.window_values(frac + cutoff - 1 - a)
+        val = e + s * od if a < Tk // 2 else e - s * od
+        if not k <= a < T + k:
+            assert np.all(val == 0.0)  # padding tap: the reference has no tap there
+            continue
+        exact = o.window_values(frac + cutoff - 1 - (a - k))
         # ~1e-14 of the peak at the default cutoff 6; the 4-tap window is the roughest
         assert np.max(np.abs(val - exact)) < (NU.WINDOW_FIT_TOL_SMALL_CUTOFF if cutoff < 4 else 3e-14)
 
