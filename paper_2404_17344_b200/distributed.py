@@ -27,8 +27,6 @@ from __future__ import annotations
 
 import heapq
 
-import numpy as np
-
 from .dataset import Dataset
 from .windows import WindowSet
 

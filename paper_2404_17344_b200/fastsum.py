@@ -42,7 +42,7 @@ import numpy as np
 from . import _native
 from .dataset import PRESCALED, Dataset, same_scaling
 from .errors import InvalidScalingError, ScalingMismatchError
-from .kernels import BASE_FAMILY, DERIVATIVE_FAMILY, DERIVATIVE_PREFACTOR, KernelSpec, radial_profile
+from .kernels import DERIVATIVE_FAMILY, DERIVATIVE_PREFACTOR, KernelSpec, radial_profile
 from .nufft import (CoefficientTable, DeviceGeometry, NufftPlan, _stream_ptr, _torch,
                     grid_fft_coefficients, grid_positions)
 from .windows import WindowSet

@@ -1,7 +1,6 @@
 """Shared fixtures.  GPU tests carry @pytest.mark.gpu (run on the B200 box);
 everything else runs on the CPU-only build container."""
 
-import os
 import sys
 from pathlib import Path
 

@@ -8,12 +8,11 @@ rounding and the ~1e-14 window polynomial.
 """
 
 import math
-import os
 
 import numpy as np
 import pytest
 
-from conftest import golden, rel, windows_of
+from conftest import golden, rel
 
 pytestmark = pytest.mark.gpu
 

@@ -6,7 +6,7 @@ import math
 import numpy as np
 import pytest
 
-from conftest import golden, rel, windows_of
+from conftest import golden, rel
 
 pytestmark = pytest.mark.gpu
 

@@ -3,13 +3,11 @@ the scaling pipeline and the window polynomial used by the CUDA kernels."""
 
 import json
 import math
-import re
-from pathlib import Path
 
 import numpy as np
 import pytest
 
-from conftest import ROOT, golden, rel
+from conftest import golden
 from oracle import restate as R
 from paper_2404_17344_b200 import dataset as D
 from paper_2404_17344_b200 import kernels as K

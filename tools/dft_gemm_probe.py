@@ -1,8 +1,6 @@
 """Band-pruned 3-D transforms as GEMMs (cuBLAS, FP64): time of the forward
 (grid -> band) and inverse (band -> grid) for 10 windows of 64^3 vs cuFFT D2Z/Z2D."""
 import math
-import sys
-import time
 
 import torch
 

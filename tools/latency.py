@@ -4,7 +4,7 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import torch
 from paper_2404_17344_b200 import configs
-from paper_2404_17344_b200.fastsum import build_plan, fast_matvec, fast_matvecs
+from paper_2404_17344_b200.fastsum import build_plan, fast_matvec
 for name in ("C1", "C2", "C3", "C4"):
     wl = configs.CONFIGS[name]()
     plan = build_plan(wl.spec, wl.window_set, "default", wl.data)
