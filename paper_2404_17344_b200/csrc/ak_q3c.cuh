@@ -23,8 +23,16 @@ namespace ak {
 #define AK_SPREAD3C_BOUNDS __maxnreg__(224)
 #endif
 template <int B>
-__global__ void AK_SPREAD3C_BOUNDS
-k_spread3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
+struct alignas(128) Spread3cSmem {
+    double wbuf[2][B][36];
+    CellIdx cib[3][B];
+    double vb[2][B];
+    uint64_t bar[2];
+};
+
+// One (item, RHS) unit of the single-cell spread (the body of k_spread3c).
+template <int B>
+__device__ __forceinline__ void spread3c_unit(Spread3cSmem<B>& sm, int unit, const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ V, int64_t ldv,
            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
 {
@@ -34,14 +42,14 @@ k_spread3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     constexpr int RW = 3 * T;
     static_assert(B <= 32, "batch");
 
-    __shared__ __align__(128) double wbuf[2][B][RW];
-    __shared__ __align__(16) CellIdx cib[3][B];
-    __shared__ double vb[2][B];
-    __shared__ __align__(8) uint64_t bar[2];
+    auto& wbuf = sm.wbuf;
+    auto& cib = sm.cib;
+    auto& vb = sm.vb;
+    auto& bar = sm.bar;
 
     // the RHS index runs fastest: the nrhs CTAs of one item share its weight rows in L2
-    const WorkItem it = items[blockIdx.x / nrhs];
-    const int r = blockIdx.x % nrhs;
+    const WorkItem it = items[unit / nrhs];
+    const int r = unit % nrhs;
     const int lane = threadIdx.x;
     const int g0 = lane >> 4, g1 = (lane >> 2) & 3, g2 = lane & 3;
     const double* __restrict__ Vr = V + (int64_t)r * ldv;
@@ -147,10 +155,26 @@ k_spread3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     }
 }
 
-// (__maxnreg__ 184/200/208 for 10-11 warps per SM: no gain, 1.353-1.369 vs 1.351 ms)
 template <int B>
-__global__ void __launch_bounds__(32, 8)
-k_interp3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
+__global__ void AK_SPREAD3C_BOUNDS
+k_spread3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
+           const WorkItem* __restrict__ items, const double* __restrict__ V, int64_t ldv,
+           double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
+{
+    __shared__ Spread3cSmem<B> sm;
+    spread3c_unit<B>(sm, blockIdx.x, ci, W, wshift, items, V, ldv, grids, canon_off, nrhs, n);
+}
+
+template <int B>
+struct alignas(128) Interp3cSmem {
+    double wbuf[2][B][36];
+    CellIdx cib[2][B];
+    uint64_t bar[2];
+};
+
+// One (item, RHS) unit of the single-cell interpolation (the body of k_interp3c).
+template <int B>
+__device__ __forceinline__ void interp3c_unit(Interp3cSmem<B>& sm, int unit, const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ grids,
            const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,
            double* __restrict__ out, int64_t ldo, int atomic_out, int64_t wstride)
@@ -159,13 +183,13 @@ k_interp3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     constexpr int RW = 3 * T;
     static_assert(B % 8 == 0 && B <= 32, "batch");
 
-    __shared__ __align__(128) double wbuf[2][B][RW];
-    __shared__ __align__(16) CellIdx cib[2][B];
-    __shared__ __align__(8) uint64_t bar[2];
+    auto& wbuf = sm.wbuf;
+    auto& cib = sm.cib;
+    auto& bar = sm.bar;
 
     // the RHS index runs fastest: the nrhs CTAs of one item share its weight rows in L2
-    const WorkItem it = items[blockIdx.x / nrhs];
-    const int r = blockIdx.x % nrhs;
+    const WorkItem it = items[unit / nrhs];
+    const int r = unit % nrhs;
     const int lane = threadIdx.x;
     const int nbatch = (it.count + B - 1) / B;
     const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
@@ -232,6 +256,19 @@ k_interp3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
             }
         }
     }
+}
+
+// (__maxnreg__ 184/200/208 for 10-11 warps per SM: no gain, 1.353-1.369 vs 1.351 ms)
+template <int B>
+__global__ void __launch_bounds__(32, 8)
+k_interp3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
+           const WorkItem* __restrict__ items, const double* __restrict__ grids,
+           const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,
+           double* __restrict__ out, int64_t ldo, int atomic_out, int64_t wstride)
+{
+    __shared__ Interp3cSmem<B> sm;
+    interp3c_unit<B>(sm, blockIdx.x, ci, W, wshift, items, grids, canon_off, nrhs, n, scale, out, ldo, atomic_out,
+                     wstride);
 }
 
 }  // namespace ak
