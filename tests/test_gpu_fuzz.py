@@ -120,3 +120,41 @@ def test_random_nufft_matches_oracle(cuda, seed):
     ogeom = R.Geometry(oplan, pts)
     assert rel(nufft_type1(plan, geom, w), R.type1(oplan, ogeom, w)) <= TOL, (seed, q, m, N)
     assert rel(nufft_type2(plan, geom, c), R.type2(oplan, ogeom, c)) <= TOL, (seed, q, m, N)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_cross_matvec_matches_oracle(cuda, seed):
+    """K(eval, train) v with train / eval sets of different size and density (their own
+    item lists: the eval geometry may pick other supercell edges than the train one)."""
+    from oracle import restate as R
+    from paper_2404_17344_b200.dataset import PRESCALED, Dataset
+    from paper_2404_17344_b200.fastsum import build_plan, fast_cross_matvec, prepare_eval_points
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    rng = np.random.default_rng(30_000 + seed)
+    windows = [(0, 1, 2), (3, 4)] if seed % 2 else [(0, 1, 2), (2, 3, 4), (5,)]
+    Ntr = int(rng.integers(50, 20000))
+    Nte = int(rng.integers(1, 20000))
+    spread_tr = float(rng.choice([0.01, 0.05, 0.14]))
+    spread_te = float(rng.choice([0.01, 0.05, 0.14]))
+    Xtr = rng.uniform(-spread_tr, spread_tr, size=(Ntr, 6))
+    Xte = rng.uniform(-spread_te, spread_te, size=(Nte, 6))
+    v = rng.normal(size=Ntr)
+    fam = str(rng.choice(["gauss", "matern12", "der_gauss"]))
+    ell = float(rng.uniform(0.1, 1.0))
+
+    def ds(X):
+        return Dataset(X, np.zeros(X.shape[0]), tuple(f"x{i}" for i in range(6)), scaling_state=PRESCALED, d_max=3)
+
+    plan = build_plan(KernelSpec(fam, ell, 0.8), WindowSet(tuple(tuple(c + 1 for c in w) for w in windows), d_max=3),
+                      "default", ds(Xtr))
+    out = fast_cross_matvec(plan, prepare_eval_points(plan, ds(Xte)), v, Nte)
+    # oracle composition of fastsum.py:180-191: spread at train, interp at eval, per window
+    acc = np.zeros(Nte, dtype=np.complex128)
+    for w in windows:
+        nplan = R.Nufft(len(w), 32)
+        S = R.type1(nplan, R.Geometry(nplan, Xtr[:, list(w)]), v)
+        acc += R.type2(nplan, R.Geometry(nplan, Xte[:, list(w)]), R.kernel_coefficients(fam, ell, len(w), 32) * S)
+    ref = R.operator_scale(fam, ell, 0.8) * acc.real
+    assert rel(out, ref) <= TOL, (seed, Ntr, Nte, spread_tr, spread_te)
