@@ -158,3 +158,43 @@ def test_random_cross_matvec_matches_oracle(cuda, seed):
         acc += R.type2(nplan, R.Geometry(nplan, Xte[:, list(w)]), R.kernel_coefficients(fam, ell, len(w), 32) * S)
     ref = R.operator_scale(fam, ell, 0.8) * acc.real
     assert rel(out, ref) <= TOL, (seed, Ntr, Nte, spread_tr, spread_te)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_mixed_plan_matches_oracle(cuda, seed):
+    """Per-window family and length-scale (MixedKernelPlan): K V, the per-window dK/dl_w V
+    and dK/dsigma_f V against sums of single-window oracle products."""
+    from oracle import restate as R
+    from paper_2404_17344_b200.dataset import PRESCALED, Dataset
+    from paper_2404_17344_b200.fastsum import build_mixed_plan, mixed_matvecs
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    rng = np.random.default_rng(40_000 + seed)
+    P = int(rng.integers(2, 6))
+    windows = []
+    while len(windows) < P:
+        q = int(rng.integers(1, 4))
+        w = tuple(sorted(int(c) for c in rng.choice(7, size=q, replace=False)))
+        if w not in windows:
+            windows.append(w)
+    N = int(rng.integers(100, 8000))
+    X = np.clip(rng.normal(scale=float(rng.choice([0.01, 0.05])), size=(N, 7)), -0.49, 0.49)
+    R_ = int(rng.choice([1, 3]))
+    V = rng.normal(size=(R_, N))
+    fams = [str(rng.choice(["gauss", "matern12"])) for _ in windows]
+    ells = [float(rng.uniform(0.1, 1.5)) for _ in windows]
+    sf = 0.9
+    ds = Dataset(X, np.zeros(N), tuple(f"x{i}" for i in range(7)), scaling_state=PRESCALED, d_max=3)
+    specs = [KernelSpec(f, l, sf) for f, l in zip(fams, ells)]
+    plan = build_mixed_plan(specs, WindowSet(tuple(tuple(c + 1 for c in w) for w in windows), d_max=3), "default", ds)
+    res = mixed_matvecs(plan, V)
+    for r in range(R_):
+        K = np.zeros(N)
+        for w, (win, f, l) in enumerate(zip(windows, fams, ells)):
+            Kw = R.FastSum(f, l, sf, [win], X).matvec(V[r])
+            dKw = R.FastSum("der_" + f, l, sf, [win], X).matvec(V[r])
+            K += Kw
+            assert rel(res["dK_dell"][w][r], dKw) <= TOL, (seed, w, r)
+        assert rel(res["K"][r], K) <= TOL, (seed, r)
+        assert rel(res["dK_dsigma"][r], (2.0 / sf) * K) <= TOL, (seed, r)
