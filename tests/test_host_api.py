@@ -204,3 +204,12 @@ def test_configs_shapes():
     w5 = configs.config5(200, rhs=2)
     assert w5.window_set.lengths == configs.C5_LENGTHS and w5.mixed
     assert [s.family for s in w5.specs] == ["gauss"] * 6 + ["matern12"] * 4
+
+
+def test_empty_dataset_rejected_like_the_reference():
+    """An empty training set never reaches the device: Dataset raises EmptyDatasetError
+    (reference dataset.py, same check)."""
+    from paper_2404_17344_b200.errors import EmptyDatasetError
+
+    with pytest.raises(EmptyDatasetError):
+        D.Dataset(np.zeros((0, 5)), np.zeros(0), tuple(f"x{i}" for i in range(5)), scaling_state=D.PRESCALED, d_max=3)
