@@ -436,19 +436,21 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
     int si3 = s3;
     if (s3 == 0) {
         s3 = si3 = 2;
-        if (cached && !g->windows_of_q[3].empty()) {
+        // (the probe and the split item lists keep one int per cell: only for grids up to 256^3)
+        if (cached && !g->windows_of_q[3].empty() && n <= 256) {
             const double occ = mean_occupancy(X, ld, cols, g->windows_of_q[3][0], 3, n, N, st);
             if (occ >= dense_cell_threshold()) s3 = 1;
             if (occ >= dense_cell_threshold_interp()) si3 = 1;
         }
     }
     if (s3 == 1) si3 = 1;
+    if (n > 256) si3 = s3;  // no split item lists for huge grids (see above)
     const bool split3 = (si3 == 1 && s3 != 1);
     int s2 = supercell2_default();
     if (s2 == 1 && !cached) s2 = 8;
     if (s2 == 0) {
         s2 = 8;
-        if (cached && !g->windows_of_q[2].empty() &&
+        if (cached && !g->windows_of_q[2].empty() && n <= 4096 &&
             mean_occupancy(X, ld, cols, g->windows_of_q[2][0], 2, n, N, st) >= dense_cell_threshold2())
             s2 = 1;
     }
