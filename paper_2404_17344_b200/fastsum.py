@@ -184,6 +184,14 @@ class _Operator:
                                    sw, f, _stream_ptr(torch))
         _native.check(rc, "ak_op_apply")
 
+    def set_rhs_multipliers(self, ptrs) -> None:
+        """Replace the per-RHS multiplier table (int64 device tensor of R * P device
+        pointers, RHS-major) -- e.g. to re-point a batched operator at a subset of
+        cells.  The pointed-to tables must outlive the products that use them."""
+        if not self.per_rhs or ptrs.numel() != self.R * self.P:
+            raise ValueError("need R * P multiplier pointers of a per-RHS operator")
+        self.hptr = ptrs.contiguous()
+
     def spread_only(self, V) -> None:
         """Zero the op's grids and spread V into them (first half of a point-sharded product)."""
         torch = _torch()

@@ -205,12 +205,54 @@ def _grid_operator(plan, specs, R, interp_geom=None):
     return _Operator(plan.geometries, gi, plan.m, R, [H], [scales], per_rhs=True)
 
 
-def cg_solve_batched(apply, Y, betas, tol: float = DEFAULT_CG_TOL, max_iter: int = DEFAULT_CG_MAX_ITER):
+def _subset_applier(plan, specs, full_op):
+    """apply_subset for cg_solve_batched over a per-RHS grid operator: products for the
+    active cells only, on operators of power-of-two batch size (cached; padding rows
+    are zero directions) whose per-RHS multiplier tables are re-pointed at the active
+    cells' tables of `full_op` (which keeps them alive)."""
+    import torch
+
+    R, P = full_op.R, full_op.P
+    table = full_op.hptr.reshape(R, P)
+    ops = {R: full_op}
+
+    def bucket(n):
+        b = 1
+        while b < n:
+            b *= 2
+        return min(b, R)
+
+    def apply_subset(Pa, idx):
+        n = len(idx)
+        B = bucket(n)
+        op = ops.get(B)
+        if op is None:
+            op = _grid_operator(plan, specs[:B], B)
+            ops[B] = op
+        rows = np.concatenate([idx, np.full(B - n, idx[0])]) if B > n else idx
+        op.set_rhs_multipliers(table[torch.as_tensor(rows, device=table.device)].reshape(-1))
+        if B > n:
+            Pp = torch.zeros((B, Pa.shape[1]), dtype=Pa.dtype, device=Pa.device)
+            Pp[:n] = Pa
+        else:
+            Pp = Pa
+        out = torch.empty_like(Pp)
+        op.apply(Pp, [out], [True])
+        return out[:n]
+
+    return apply_subset
+
+
+def cg_solve_batched(apply, Y, betas, tol: float = DEFAULT_CG_TOL, max_iter: int = DEFAULT_CG_MAX_ITER,
+                     apply_subset=None):
     """Lockstep CG for R independent systems (A_r + beta_r I) x_r = y_r on the device.
 
-    ``apply`` maps an (R, N) tensor of directions to (A_r p_r)_r.  Returns
-    (X, iterations, messages); iterations[r] = -1 for a failed system, whose
-    message says why.  Each system follows exactly the iteration of cg_solve.
+    ``apply`` maps an (R, N) tensor of directions to (A_r p_r)_r.  If
+    ``apply_subset(P_active, idx)`` is given, only the still-active systems are
+    multiplied ((R_active, N) -> (R_active, N), idx = their indices), so
+    converged systems stop costing products.  Returns (X, iterations,
+    messages); iterations[r] = -1 for a failed system, whose message says why.
+    Each system follows exactly the iteration of cg_solve.
     """
     import torch
 
@@ -235,7 +277,14 @@ def cg_solve_batched(apply, Y, betas, tol: float = DEFAULT_CG_TOL, max_iter: int
     for it in range(1, max_iter + 1):
         if not active.any():
             break
-        AP = apply(P) + betas * P
+        if apply_subset is not None:
+            idx = np.nonzero(active)[0]
+            idx_d = torch.as_tensor(idx, device=Y.device)
+            AP = torch.zeros_like(P)
+            AP[idx_d] = apply_subset(P[idx_d].contiguous(), idx)
+            AP += betas * P
+        else:
+            AP = apply(P) + betas * P
         pAp = (P * AP).sum(dim=1)
         pAp_h = pAp.cpu().numpy()
         for r in np.nonzero(active)[0]:
@@ -302,6 +351,7 @@ def grid_search(train: Dataset, test: Dataset, ws: WindowSet, ell_grid, beta_gri
         warnings.warn_explicit(w.message, w.category, w.filename, w.lineno)
     R = len(pairs)
     op = _grid_operator(plan, specs, R)
+    apply_subset = _subset_applier(plan, specs, op)
 
     def apply(Pm):
         out = torch.empty_like(Pm)
@@ -309,7 +359,8 @@ def grid_search(train: Dataset, test: Dataset, ws: WindowSet, ell_grid, beta_gri
         return out
 
     Y = torch.as_tensor(np.broadcast_to(train.targets, (R, train.n_rows)).copy(), device="cuda")
-    X, iters, msgs = cg_solve_batched(apply, Y, [b for _, b in pairs], tol=tol, max_iter=max_iter)
+    X, iters, msgs = cg_solve_batched(apply, Y, [b for _, b in pairs], tol=tol, max_iter=max_iter,
+                                      apply_subset=apply_subset)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     geoms = prepare_eval_points(plan, test)
