@@ -163,3 +163,28 @@ def test_gsi_matches_reference(cuda):
     assert [",".join(map(str, w)) for w in sel.windows] == list(gg["pipeline_windows"])
     with pytest.raises(ValueError):
         select_windows_by_gsi(rep, 1.0)
+
+
+def test_cg_solve_batched_active_subset(cuda):
+    """Products restricted to the still-active systems give the same solves."""
+    import torch
+
+    from paper_2404_17344_b200.solver import cg_solve_batched
+
+    rng = np.random.default_rng(5)
+    A = rng.normal(size=(60, 60))
+    A = A @ A.T / 60
+    At = torch.as_tensor(A, device="cuda")
+    Y = torch.as_tensor(rng.normal(size=(5, 60)), device="cuda")
+    betas = [0.01, 10.0, 0.1, 1.0, 0.001]
+    calls = []
+
+    def subset(Pa, idx):
+        calls.append(len(idx))
+        return Pa @ At.T
+
+    X1, it1, _ = cg_solve_batched(lambda P: P @ At.T, Y, betas, tol=1e-8, max_iter=500)
+    X2, it2, _ = cg_solve_batched(None, Y, betas, tol=1e-8, max_iter=500, apply_subset=subset)
+    assert list(it1) == list(it2)
+    assert rel(X2.cpu().numpy(), X1.cpu().numpy()) <= 1e-12
+    assert calls[0] == 5 and calls[-1] < 5  # converged systems left the batch
