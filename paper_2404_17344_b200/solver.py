@@ -34,6 +34,9 @@ from .windows import WindowSet
 
 DEFAULT_CG_TOL = 1e-3
 DEFAULT_CG_MAX_ITER = 5000
+#: krr_fit replays each CG iteration as a captured CUDA graph (falls back to eager launches
+#: if the product cannot be captured)
+GRAPHED_CG = True
 
 DENSE = "dense"
 FASTSUM = "fastsum"
@@ -67,13 +70,7 @@ def cg_solve(matvec, y, beta: float, tol: float = DEFAULT_CG_TOL, max_iter: int 
     tensor (matvec maps tensors -> tensors; every vector stays on the device).
     """
     if _is_tensor(y):
-        import torch
-
-        dot = lambda a, b: float(torch.dot(a, b))
-        norm = lambda a: float(torch.linalg.vector_norm(a))
-        y = y.to(torch.float64)
-        x = torch.zeros_like(y)
-        copy = torch.clone
+        return _cg_solve_device(matvec, y, beta, tol, max_iter, callback)
     else:
         y = np.asarray(y, dtype=np.float64)
         dot = lambda a, b: float(a @ b)
@@ -108,6 +105,103 @@ def cg_solve(matvec, y, beta: float, tol: float = DEFAULT_CG_TOL, max_iter: int 
     raise MaxIterationsError(f"CG did not reach tol={tol} within {max_iter} iterations")
 
 
+def _cg_solve_graphed(matvec, y, beta, tol, max_iter, callback):
+    """_cg_solve_device with one CG iteration captured as a CUDA graph and replayed:
+    the ~10 launches of an iteration (the product's memsets, kernels and cuFFT
+    executions, the vector updates and dots) cost one graph launch, so the host
+    time between iterations (the one read of p^T A p and ||r||^2 per iteration)
+    no longer exposes per-launch Python overhead.  Same arithmetic, same
+    iterations.  Returns None if the product cannot be captured (caller falls back)."""
+    import torch
+
+    y = y.to(torch.float64)
+    x = torch.zeros_like(y)
+    y_norm = float(torch.linalg.vector_norm(y))
+    if y_norm == 0.0:
+        return x, 0
+    r = y.clone()
+    p = r.clone()
+    rs = torch.dot(r, r).reshape(1)
+    rs_h = float(rs)
+    if callback is not None:
+        callback(math.sqrt(rs_h))
+    if math.sqrt(rs_h) <= tol * y_norm:
+        return x, 0
+    stats = torch.empty(2, dtype=torch.float64, device=y.device)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    try:
+        with torch.cuda.stream(s):
+            matvec(p)                         # warm-up: operators / cuFFT plans exist before capture
+            torch.cuda.current_stream().synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=s):
+                Ap = matvec(p) + beta * p
+                pAp = torch.dot(p, Ap).reshape(1)
+                alpha = rs / pAp
+                x.add_(alpha * p)
+                r.sub_(alpha * Ap)
+                rs_new = torch.dot(r, r).reshape(1)
+                stats.copy_(torch.cat([pAp, rs_new]))
+                p.mul_(rs_new / rs).add_(r)
+                rs.copy_(rs_new)
+    except Exception:  # pragma: no cover - capture unsupported for this product
+        torch.cuda.current_stream().wait_stream(s)
+        return None
+    torch.cuda.current_stream().wait_stream(s)
+    for it in range(1, max_iter + 1):
+        graph.replay()
+        pAp_h, rs_new_h = stats.tolist()
+        if pAp_h <= 0.0:
+            raise CgBreakdownError(f"p^T A p = {pAp_h:.3e} <= 0 at iteration {it}")
+        if callback is not None:
+            callback(math.sqrt(rs_new_h))
+        if math.sqrt(rs_new_h) <= tol * y_norm:
+            return x, it
+    raise MaxIterationsError(f"CG did not reach tol={tol} within {max_iter} iterations")
+
+
+def _cg_solve_device(matvec, y, beta, tol, max_iter, callback):
+    """cg_solve on CUDA tensors with the scalars kept on the device: one host read per
+    iteration (p^T A p and the new residual norm together) instead of two, and no
+    host round trip between the vector updates.  Same arithmetic as the host loop:
+    alpha = rs / pAp, x += alpha p, r -= alpha Ap, p = r + (rs_new / rs) p.  On a
+    breakdown the (discarded) update of that iteration is computed before the
+    check; the error is raised exactly where the reference raises it."""
+    import torch
+
+    y = y.to(torch.float64)
+    x = torch.zeros_like(y)
+    y_norm = float(torch.linalg.vector_norm(y))
+    if y_norm == 0.0:
+        return x, 0
+    r = y.clone()
+    p = r.clone()
+    rs = torch.dot(r, r)
+    rs_h = float(rs)
+    if callback is not None:
+        callback(math.sqrt(rs_h))
+    if math.sqrt(rs_h) <= tol * y_norm:
+        return x, 0
+    for it in range(1, max_iter + 1):
+        Ap = matvec(p) + beta * p
+        pAp = torch.dot(p, Ap)
+        alpha = rs / pAp
+        x.add_(alpha * p)
+        r.sub_(alpha * Ap)
+        rs_new = torch.dot(r, r)
+        pAp_h, rs_new_h = torch.stack([pAp, rs_new]).tolist()
+        if pAp_h <= 0.0:
+            raise CgBreakdownError(f"p^T A p = {pAp_h:.3e} <= 0 at iteration {it}")
+        if callback is not None:
+            callback(math.sqrt(rs_new_h))
+        if math.sqrt(rs_new_h) <= tol * y_norm:
+            return x, it
+        p.mul_(rs_new / rs).add_(r)
+        rs = rs_new
+    raise MaxIterationsError(f"CG did not reach tol={tol} within {max_iter} iterations")
+
+
 @dataclass(frozen=True)
 class KrrModel:
     """Fitted ridge-regression state (solver.py:83-96)."""
@@ -138,8 +232,14 @@ def krr_fit(train: Dataset, ws: WindowSet, spec: KernelSpec, beta: float, backen
 
         plan = build_plan(spec, ws, preset, train)
         y = torch.as_tensor(train.targets, device="cuda")
-        v, iters = cg_solve(lambda p: fast_matvec(plan, p), y, beta, tol=tol, max_iter=max_iter,
-                            callback=log.append)
+        res = None
+        if GRAPHED_CG:
+            res = _cg_solve_graphed(lambda p: fast_matvec(plan, p), y, beta, tol, max_iter, log.append)
+            if res is None:
+                log.clear()
+        if res is None:
+            res = cg_solve(lambda p: fast_matvec(plan, p), y, beta, tol=tol, max_iter=max_iter, callback=log.append)
+        v, iters = res
         coef = v.cpu().numpy()
     elif backend == DENSE:
         coef, iters = cg_solve(lambda p: dense_matvec(spec, ws, train, p), train.targets, beta, tol=tol,
@@ -286,19 +386,18 @@ def cg_solve_batched(apply, Y, betas, tol: float = DEFAULT_CG_TOL, max_iter: int
         else:
             AP = apply(P) + betas * P
         pAp = (P * AP).sum(dim=1)
-        pAp_h = pAp.cpu().numpy()
+        act = torch.as_tensor(active, device=Y.device)
+        ok = act & (pAp > 0.0)                      # breakdown: frozen before the update
+        alpha = torch.where(ok, rs / torch.where(ok, pAp, torch.ones_like(pAp)), torch.zeros_like(rs))
+        X += alpha.reshape(R, 1) * P
+        Rr -= alpha.reshape(R, 1) * AP
+        rs_new = (Rr * Rr).sum(dim=1)
+        pAp_h, rs_new_h = torch.stack([pAp, rs_new]).cpu().numpy()   # one host read per iteration
         for r in np.nonzero(active)[0]:
             if pAp_h[r] <= 0.0:
                 msgs[r] = f"p^T A p = {pAp_h[r]:.3e} <= 0 at iteration {it}"
                 active[r] = False
-        act = torch.as_tensor(active, device=Y.device)
-        alpha = torch.where(act, rs / torch.where(act, pAp, torch.ones_like(pAp)), torch.zeros_like(rs))
-        X += alpha.reshape(R, 1) * P
-        Rr -= alpha.reshape(R, 1) * AP
-        rs_new = (Rr * Rr).sum(dim=1)
-        rs_new_h = rs_new.cpu().numpy()
-        for r in np.nonzero(active)[0]:
-            if math.sqrt(rs_new_h[r]) <= tol * yn[r]:
+            elif math.sqrt(rs_new_h[r]) <= tol * yn[r]:
                 iters[r] = it
                 active[r] = False
         act = torch.as_tensor(active, device=Y.device)
