@@ -371,3 +371,51 @@ def test_concurrent_streams_share_a_plan(cuda):
     assert not errors, errors
     for k in range(2):
         assert rel(outs[k].cpu().numpy(), refs[k].cpu().numpy()) <= 1e-13
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_full_size_config_vs_oracle(cuda, name):
+    """Configs 2 and 3 at their full BASELINE sizes (20k and 100k nodes) against the oracle:
+    K and dK/dl for the first RHS, every window."""
+    from oracle import restate as R
+    from paper_2404_17344_b200 import configs
+    from paper_2404_17344_b200.fastsum import build_plan, fast_matvecs
+
+    wl = configs.CONFIGS[name]()
+    plan = build_plan(wl.spec, wl.window_set, "default", wl.data)
+    res = fast_matvecs(plan, wl.V, dell=True)
+    cols = [wl.window_set.columns(w) for w in wl.window_set]
+    for fam, key in ((wl.spec.family, "K"), ("der_" + wl.spec.family, "dK_dell")):
+        ref = R.FastSum(fam, wl.spec.ell, wl.spec.sigma_f, cols, wl.data.features).matvec(wl.V[0], threads=8)
+        assert rel(res[key][0], ref) <= 1e-8, (name, key)
+
+
+def test_c5_full_size_properties(cuda):
+    """Config 5 at its full size (4M nodes, 16 RHS, mixed windows and kernels):
+    linearity across RHS, the per-window derivative outputs against single-window
+    plans, operator symmetry, and dK/dsigma_f = 2/sigma_f K."""
+    import torch
+
+    from paper_2404_17344_b200 import configs
+    from paper_2404_17344_b200.fastsum import build_mixed_plan, build_plan, fast_matvecs, mixed_matvecs
+    from paper_2404_17344_b200.windows import WindowSet
+
+    wl = configs.config5()
+    plan = build_mixed_plan(wl.specs, wl.window_set, "default", wl.data)
+    V = torch.as_tensor(wl.V, device="cuda")
+    res = mixed_matvecs(plan, V)
+    K = res["K"]
+    # linearity: K(V0 - 2 V1) = K V0 - 2 K V1
+    lin = mixed_matvecs(plan, (V[0] - 2.0 * V[1]).reshape(1, -1), dell=False, dsigma=False)["K"][0]
+    scale = float(torch.max(torch.abs(K[0])))
+    assert float(torch.max(torch.abs(lin - (K[0] - 2.0 * K[1])))) <= 1e-10 * scale
+    # symmetry <K v0, v1> = <v0, K v1>
+    lhs = float(torch.dot(K[0], V[1]))
+    rhs_ = float(torch.dot(V[0], K[1]))
+    assert abs(lhs - rhs_) <= 1e-8 * float(torch.linalg.vector_norm(V[0]) * torch.linalg.vector_norm(V[1]))
+    assert rel(res["dK_dsigma"].cpu().numpy(), (2.0 / wl.specs[0].sigma_f) * K.cpu().numpy()) <= 1e-14
+    # window 7 (2-D, Matern) and window 9 (1-D): per-window dK/dl against a single-window base plan
+    for w in (6, 8):
+        one = build_plan(wl.specs[w], WindowSet((wl.window_set.windows[w],), d_max=3), "default", wl.data)
+        single = fast_matvecs(one, V[:2], dell=True)["dK_dell"]
+        assert rel(res["dK_dell"][w][:2].cpu().numpy(), single.cpu().numpy()) <= 1e-12, w
