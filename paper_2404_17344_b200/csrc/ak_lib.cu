@@ -93,6 +93,7 @@ struct ak_geom {
     std::vector<int> windows_of_q[4];   // window ids per q, canonical order
     int sedge[4] = {0, 16, 8, 4};       // supercell edge (cells) per q (must match SuperCell<q>)
     int sedge_i3 = 4;                   // supercell edge of the 3-D interpolation items
+    bool trim3 = false;                 // 12-tap table whose outer tap pair is zero (a padded 10-tap window)
     int chunk[4] = {0, 2048, 1024, 2048};  // maximum points per work item, per q
     int64_t iitem_begin3 = 0, iitem_end3 = 0;  // 3-D interpolation items (== spread items unless split)
     // cached 3-D window weights (plan-time table, see ak_q3w.cuh)
@@ -670,6 +671,11 @@ extern "C" int ak_geom_create(int32_t n, int32_t P, const int32_t* q, const int3
     g->N = N;
     g->q.assign(q, q + P);
     g->wf = *wf;
+    if (wf->taps == 12) {
+        bool zero = true;
+        for (int k = 0; k < AK_NCOEF; ++k) zero = zero && wf->ce[0][k] == 0.0 && wf->co[0][k] == 0.0;
+        g->trim3 = zero;  // taps 0 and 11 vanish: the single-cell q = 3 kernels skip them on axis 0
+    }
     int rc = geom_build(g, cols, X, ld, (cudaStream_t)stream);
     if (rc != AK_OK) {
         std::string keep = g_err;
@@ -839,7 +845,10 @@ static void launch_spread3_t(const ak_geom* g, int64_t i0, int64_t ni, const dou
 {
     if (T == 12 && g->cached && g->sedge[3] == 1) {
         const unsigned grid = (unsigned)(ni * R);  // item-major, RHS fastest
-        if (g->batch3 == 32)
+        if (g->batch3 == 32 && g->trim3)
+            k_spread3c<32, 10><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
+                                                    g->canon_off_d, R, g->n);
+        else if (g->batch3 == 32)
             k_spread3c<32><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
                                                 g->canon_off_d, R, g->n);
         else
@@ -987,7 +996,10 @@ static void launch_interp3_t(const ak_geom* g, int64_t i0, int64_t ni, const dou
 {
     if (T == 12 && g->cached && g->sedge_i3 == 1) {
         const unsigned grid = (unsigned)(ni * R);  // item-major, RHS fastest
-        if (g->batch3i == 32)
+        if (g->batch3i == 32 && g->trim3)
+            k_interp3c<32, 10><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids,
+                                                    g->canon_off_d, R, g->n, scale, out, ldo, atomic_out, wstride);
+        else if (g->batch3i == 32)
             k_interp3c<32><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids, g->canon_off_d, R,
                                                 g->n, scale, out, ldo, atomic_out, wstride);
         else

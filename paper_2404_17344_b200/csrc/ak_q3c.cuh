@@ -30,15 +30,17 @@ struct alignas(128) Spread3cSmem {
     uint64_t bar[2];
 };
 
-// One (item, RHS) unit of the single-cell spread (the body of k_spread3c).
-template <int B>
+// One (item, RHS) unit of the single-cell spread (the body of k_spread3c).  A = active
+// taps on axis 0: 12, or 10 for a zero-padded 10-tap window (cutoff 5: the lane tile
+// skips the zero taps 0 and 11, 5 x 3 x 3 instead of 6 x 3 x 3 accumulators).
+template <int B, int A = 12>
 __device__ __forceinline__ void spread3c_unit(Spread3cSmem<B>& sm, int unit, const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ V, int64_t ldv,
            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
 {
     constexpr int T = 12;
     using LN = Q3Lanes<T>;
-    constexpr int P0 = LN::P0, P1 = LN::P1, P2 = LN::P2;
+    constexpr int P0 = A / 2, P1 = LN::P1, P2 = LN::P2, AO = (T - A) / 2;
     constexpr int RW = 3 * T;
     static_assert(B <= 32, "batch");
 
@@ -119,12 +121,20 @@ __device__ __forceinline__ void spread3c_unit(Spread3cSmem<B>& sm, int unit, con
         }
         __syncwarp();
         double a0[P0], a1[P1], a2[P2], b0[P0], b1[P1], b2[P2];
-        load_w<T>(a0, a1, a2, &wbuf[s][0][0], g0, g1, g2);
+        auto load = [&](double (&w0)[P0], double (&w1)[P1], double (&w2)[P2], const double* row) {
+#pragma unroll
+            for (int a = 0; a < P0; ++a) w0[a] = row[AO + g0 * P0 + a];
+#pragma unroll
+            for (int b = 0; b < P1; ++b) w1[b] = row[T + g1 * P1 + b];
+#pragma unroll
+            for (int c = 0; c < P2; ++c) w2[c] = row[2 * T + g2 * P2 + c];
+        };
+        load(a0, a1, a2, &wbuf[s][0][0]);
         int j = 0;
         for (; j + 1 < nb; j += 2) {
-            load_w<T>(b0, b1, b2, &wbuf[s][j + 1][0], g0, g1, g2);
+            load(b0, b1, b2, &wbuf[s][j + 1][0]);
             spread_fma(acc, a0, a1, a2);
-            load_w<T>(a0, a1, a2, &wbuf[s][j + 2 < nb ? j + 2 : j + 1][0], g0, g1, g2);
+            load(a0, a1, a2, &wbuf[s][j + 2 < nb ? j + 2 : j + 1][0]);
             spread_fma(acc, b0, b1, b2);
         }
         if (j < nb) spread_fma(acc, a0, a1, a2);
@@ -137,7 +147,7 @@ __device__ __forceinline__ void spread3c_unit(Spread3cSmem<B>& sm, int unit, con
         // coalesced flush measured 3% slower on B200)
         int x0[P0], x1[P1], x2[P2];
 #pragma unroll
-        for (int a = 0; a < P0; ++a) x0[a] = wrap(c0 - (T / 2 - 1) + g0 * P0 + a, n);
+        for (int a = 0; a < P0; ++a) x0[a] = wrap(c0 - (T / 2 - 1) + AO + g0 * P0 + a, n);
 #pragma unroll
         for (int b = 0; b < P1; ++b) x1[b] = wrap(c1 - (T / 2 - 1) + g1 * P1 + b, n);
 #pragma unroll
@@ -155,14 +165,14 @@ __device__ __forceinline__ void spread3c_unit(Spread3cSmem<B>& sm, int unit, con
     }
 }
 
-template <int B>
+template <int B, int A = 12>
 __global__ void AK_SPREAD3C_BOUNDS
 k_spread3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ V, int64_t ldv,
            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
 {
     __shared__ Spread3cSmem<B> sm;
-    spread3c_unit<B>(sm, blockIdx.x, ci, W, wshift, items, V, ldv, grids, canon_off, nrhs, n);
+    spread3c_unit<B, A>(sm, blockIdx.x, ci, W, wshift, items, V, ldv, grids, canon_off, nrhs, n);
 }
 
 template <int B>
@@ -172,8 +182,9 @@ struct alignas(128) Interp3cSmem {
     uint64_t bar[2];
 };
 
-// One (item, RHS) unit of the single-cell interpolation (the body of k_interp3c).
-template <int B>
+// One (item, RHS) unit of the single-cell interpolation (the body of k_interp3c);
+// A as for spread3c_unit (10: 15 fragment tiles instead of 18).
+template <int B, int A = 12>
 __device__ __forceinline__ void interp3c_unit(Interp3cSmem<B>& sm, int unit, const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ grids,
            const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,
@@ -206,7 +217,8 @@ __device__ __forceinline__ void interp3c_unit(Interp3cSmem<B>& sm, int unit, con
     cp_async_commit();
 
     // footprint fragments straight from the grid (same permuted layout as load_fragments)
-    double gf[18][3];
+    constexpr int NT = 3 * A / 2, AO = (T - A) / 2;
+    double gf[NT][3];
     {
         const int c0 = it.sc & 1023, c1 = (it.sc >> 10) & 1023, c2 = (it.sc >> 20) & 1023;
         const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
@@ -216,9 +228,9 @@ __device__ __forceinline__ void interp3c_unit(Interp3cSmem<B>& sm, int unit, con
 #pragma unroll
         for (int ks = 0; ks < 3; ++ks) z[ks] = wrap(c2 - (T / 2 - 1) + 4 * ks + kk, n);
 #pragma unroll
-        for (int t = 0; t < 18; ++t) {
+        for (int t = 0; t < NT; ++t) {
             const int i = 2 * t + e;
-            const int a = i / 3, b = 3 * qq + i % 3;
+            const int a = AO + i / 3, b = 3 * qq + i % 3;
             const int64_t rowb = ((int64_t)wrap(c0 - (T / 2 - 1) + a, n) * n + wrap(c1 - (T / 2 - 1) + b, n)) * n;
 #pragma unroll
             for (int ks = 0; ks < 3; ++ks) gf[t][ks] = __ldg(g + rowb + z[ks]);
@@ -245,7 +257,7 @@ __device__ __forceinline__ void interp3c_unit(Interp3cSmem<B>& sm, int unit, con
         cp_async_commit();
         for (int k0 = 0; k0 < nb; k0 += 8) {
             const int cnt = min(8, nb - k0);
-            double v = interp_group_mma<RW>(gf, wbuf[s], k0, cnt, lane);
+            double v = interp_group_mma<RW, A>(gf, wbuf[s], k0, cnt, lane);
             v += __shfl_xor_sync(0xffffffffu, v, 1);
             v += __shfl_xor_sync(0xffffffffu, v, 2);
             const int pj = lane >> 2;
@@ -259,7 +271,7 @@ __device__ __forceinline__ void interp3c_unit(Interp3cSmem<B>& sm, int unit, con
 }
 
 // (__maxnreg__ 184/200/208 for 10-11 warps per SM: no gain, 1.353-1.369 vs 1.351 ms)
-template <int B>
+template <int B, int A = 12>
 __global__ void __launch_bounds__(32, 8)
 k_interp3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ grids,
@@ -267,7 +279,7 @@ k_interp3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
            double* __restrict__ out, int64_t ldo, int atomic_out, int64_t wstride)
 {
     __shared__ Interp3cSmem<B> sm;
-    interp3c_unit<B>(sm, blockIdx.x, ci, W, wshift, items, grids, canon_off, nrhs, n, scale, out, ldo, atomic_out,
+    interp3c_unit<B, A>(sm, blockIdx.x, ci, W, wshift, items, grids, canon_off, nrhs, n, scale, out, ldo, atomic_out,
                      wstride);
 }
 

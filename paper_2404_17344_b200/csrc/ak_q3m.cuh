@@ -46,33 +46,35 @@ __device__ __forceinline__ void load_fragments(double (&gf)[18][3], const double
 
 // One group of up to 8 points (rows k0 .. k0+cnt-1 of the staged batch), all in the
 // cell whose fragments are in gf.  Returns this lane's quad-partial for point
-// k0 + lane/4 (summed over the quad by the caller).
-template <int RW>
-__device__ __forceinline__ double interp_group_mma(const double (&gf)[18][3], const double (*wrow)[RW], int k0,
-                                                   int cnt, int lane)
+// k0 + lane/4 (summed over the quad by the caller).  A = active taps on axis 0
+// (12, or 10 for a zero-padded 10-tap window: taps 1..10, 15 instead of 18 tiles).
+template <int RW, int A = 12>
+__device__ __forceinline__ double interp_group_mma(const double (&gf)[3 * A / 2][3], const double (*wrow)[RW],
+                                                   int k0, int cnt, int lane)
 {
+    constexpr int NT = 3 * A / 2, AO = (12 - A) / 2;
     const int pj = lane >> 2, q = lane & 3;
     const bool valid = pj < cnt;
     const double* w = wrow[k0 + (valid ? pj : 0)];
     double af[3];
 #pragma unroll
     for (int ks = 0; ks < 3; ++ks) af[ks] = valid ? w[24 + 4 * ks + q] : 0.0;
-    double C[18][2];
+    double C[NT][2];
 #pragma unroll
-    for (int t = 0; t < 18; ++t) C[t][0] = C[t][1] = 0.0;
-    // k-step outer: 18 independent accumulators between dependent DMMAs
+    for (int t = 0; t < NT; ++t) C[t][0] = C[t][1] = 0.0;
+    // k-step outer: NT independent accumulators between dependent DMMAs
 #pragma unroll
     for (int ks = 0; ks < 3; ++ks)
 #pragma unroll
-        for (int t = 0; t < 18; ++t) dmma_8x8x4(C[t][0], C[t][1], af[ks], gf[t][ks]);
-    // lane (pj, q) holds U[pj][(a, b)] for a = i/3, b = 3q + i%3, i = 2t + e:
-    // out = sum_b w1[b] (sum_a w0[a] U[a][b]) -- 3 chains of 12 FMAs, then 3 more
+        for (int t = 0; t < NT; ++t) dmma_8x8x4(C[t][0], C[t][1], af[ks], gf[t][ks]);
+    // lane (pj, q) holds U[pj][(a, b)] for a = AO + i/3, b = 3q + i%3, i = 2t + e:
+    // out = sum_b w1[b] (sum_a w0[a] U[a][b]) -- 3 chains of A FMAs, then 3 more
     double s[3];
 #pragma unroll
-    for (int bb = 0; bb < 3; ++bb) s[bb] = w[0] * C[bb >> 1][bb & 1];
+    for (int bb = 0; bb < 3; ++bb) s[bb] = w[AO] * C[bb >> 1][bb & 1];
 #pragma unroll
-    for (int a = 1; a < 12; ++a) {
-        const double w0a = w[a];
+    for (int a = 1; a < A; ++a) {
+        const double w0a = w[AO + a];
 #pragma unroll
         for (int bb = 0; bb < 3; ++bb) {
             const int i = 3 * a + bb;

@@ -260,3 +260,25 @@ def test_nufft_dense_boundary_cells(cuda):
         geom = prepare_points(plan, g[f"q{q}_pts"])
         assert rel(nufft_type1(plan, geom, g[f"q{q}_w"]), g[f"q{q}_type1"]) <= TOL
         assert rel(nufft_type2(plan, geom, g[f"q{q}_c"]), g[f"q{q}_type2"]) <= TOL
+
+
+@pytest.mark.parametrize("cutoff", [5, 6])
+def test_dense_cells_cutoff(cuda, cutoff):
+    """Densely occupied cells (single-cell kernels) at cutoff 5 -- a 10-tap window padded to
+    the 12-tap kernels, whose lane tiles then skip the zero taps -- and at the default 6,
+    against the oracle with the same cutoff."""
+    from oracle import restate as R
+    from paper_2404_17344_b200.fastsum import build_plan, fast_matvecs
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    rng = np.random.default_rng(31)
+    X = rng.uniform(-0.01, 0.01, size=(4000, 6))
+    V = rng.normal(size=(2, 4000))
+    ws = WindowSet(((1, 2, 3), (4, 5, 6)), d_max=3)
+    plan = build_plan(KernelSpec("gauss", 0.3), ws, "default", _ds(X, 3), cutoff=cutoff)
+    res = fast_matvecs(plan, V, dell=True)
+    for fam, key in (("gauss", "K"), ("der_gauss", "dK_dell")):
+        fs = R.FastSum(fam, 0.3, 1.0, [(0, 1, 2), (3, 4, 5)], X, cutoff=cutoff)
+        for r in range(2):
+            assert rel(res[key][r], fs.matvec(V[r])) <= TOL, (cutoff, key, r)
