@@ -236,6 +236,7 @@ def kernel_roofline(torch, plan, wl, peaks, reps=10):
         "flops_per_launch": flops, "ms_per_launch": t,
         "spread_ms": t_spread, "interp_ms": t_interp,
         "hbm_algorithmic_gbs": alg_bytes / (t * 1e-3) / 1e9, "hbm_peak_gbs": peaks.get("hbm_gbs"),
+        "ncu": ncu_evidence(prof),
     }
 
 
@@ -252,8 +253,25 @@ def profiled_traffic(kernel: str):
         key = "spread3" if kernel.startswith("spread") else "interp3"
         for m in data.get("full", []):
             if key in m.get("kernel", "") and m.get("dram_bytes_per_launch"):
-                best = {"bytes": m["dram_bytes_per_launch"], "source": f.name, "kernel": m["kernel"]}
+                best = {"bytes": m["dram_bytes_per_launch"], "source": f.name, "kernel": m["kernel"], "metrics": m}
     return best
+
+
+def ncu_evidence(prof):
+    """Memory-side evidence of the dominant kernel from the same committed ncu capture
+    (the north_star asks for achieved HBM GB/s and L2/atomic throughput)."""
+    if not prof:
+        return None
+    m = prof["metrics"]
+    dur = m.get("duration_s") or 0.0
+    out = {"source": prof["source"], "duration_ms": dur * 1e3 if dur else None,
+           "dram_gbs": prof["bytes"] / dur / 1e9 if dur else None,
+           "l2_throughput_pct": m.get("l2_throughput_pct"), "dram_throughput_pct": m.get("dram_throughput_pct"),
+           "fp64_pipe_pct": m.get("fp64_pipe_pct"), "dmma_pipe_pct": m.get("dmma_pipe_pct")}
+    red = m.get("red_sectors_to_l2")
+    if red is not None and dur:
+        out["red_sectors_per_s"] = red / dur
+    return out
 
 
 def fp64_peak(torch):
