@@ -188,3 +188,34 @@ def test_cg_solve_batched_active_subset(cuda):
     assert list(it1) == list(it2)
     assert rel(X2.cpu().numpy(), X1.cpu().numpy()) <= 1e-12
     assert calls[0] == 5 and calls[-1] < 5  # converged systems left the batch
+
+
+@pytest.mark.parametrize("preset", ["rough", "default", "fine"])
+def test_fast_vs_dense_within_measured_ceiling(cuda, preset):
+    """The reference's paper-bound check (test_fastsum.py:60-82) on the GPU path: the
+    fast product's distance to the exact dense product stays below the per-entry bound
+    ||v||_1 * sigma_f^2 * pre * P * ||kappa_ERR||_inf, with the measured Fourier
+    ceiling ||kappa_ERR||_inf of the kernel table (all four families, ell 0.1 / 1 / 10)."""
+    from oracle import restate as R
+    from paper_2404_17344_b200.fastsum import PRESETS, build_plan, fast_matvec
+    from paper_2404_17344_b200.kernels import DERIVATIVE_PREFACTOR, KernelSpec, dense_matvec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    g = golden("family_grid")
+    N = g["X"].shape[0]
+    ds = _ds(g["X"], np.zeros(N), 3)
+    ws = WindowSet(((1, 2, 3), (4, 5, 6)), d_max=3)
+    v = g["v"]
+    m = PRESETS[preset]
+    for fam in ("gauss", "der_gauss", "matern12", "der_matern12"):
+        for ell in (0.1, 1.0, 10.0):
+            spec = KernelSpec(fam, ell, math.sqrt(0.5))
+            fast = fast_matvec(build_plan(spec, ws, preset, ds), v)
+            dense = dense_matvec(spec, ws, ds, v)
+            denom = np.linalg.norm(dense)
+            err = np.linalg.norm(fast - dense) / denom
+            pre = DERIVATIVE_PREFACTOR[fam]
+            scale = spec.sigma_f ** 2 * (1.0 if pre is None else pre / ell)
+            ceiling = R.worst_case_kernel_error(fam, ell, 3, m, seed=1)
+            bound = math.sqrt(N) * np.abs(v).sum() * scale * len(ws) * ceiling / denom
+            assert err <= bound + 1e-6, (fam, ell, preset, err, bound)
