@@ -219,3 +219,80 @@ def test_fast_vs_dense_within_measured_ceiling(cuda, preset):
             ceiling = R.worst_case_kernel_error(fam, ell, 3, m, seed=1)
             bound = math.sqrt(N) * np.abs(v).sum() * scale * len(ws) * ceiling / denom
             assert err <= bound + 1e-6, (fam, ell, preset, err, bound)
+
+
+def _prescaled(n, d, seed):
+    rng = np.random.default_rng(seed)
+    X = rng.uniform(-0.25, 0.25, size=(n, d)) / math.sqrt(2)
+    y = np.sin(4 * X[:, 0]) + 0.1 * rng.normal(size=n)
+    return _ds(X, y, 2)
+
+
+def test_krr_fast_backend_edge_cases(cuda):
+    """Reference test_solver.py:113-130 on the fast backend: zero targets give exact zero
+    coefficients (0 iterations); a huge ridge gives v ~ y / beta."""
+    from paper_2404_17344_b200.dataset import PRESCALED, Dataset
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.solver import default_sigma_f, krr_fit
+    from paper_2404_17344_b200.windows import WindowSet
+
+    ds = _prescaled(300, 4, 6)
+    ws = WindowSet(((1, 2), (3, 4)), d_max=2)
+    zero = Dataset(ds.features, np.zeros(300), ds.feature_names, scaling_state=PRESCALED, d_max=2)
+    m = krr_fit(zero, ws, KernelSpec("gauss", 0.5), 1.0)
+    assert m.cg_iterations == 0
+    np.testing.assert_array_equal(m.coefficients, np.zeros(300))
+    beta = 1e6
+    m = krr_fit(ds, ws, KernelSpec("gauss", 0.5, default_sigma_f(2)), beta, tol=1e-8)
+    ref = ds.targets / beta
+    assert np.linalg.norm(m.coefficients - ref) <= 0.01 * np.linalg.norm(ref)
+
+
+def test_fast_and_dense_backends_agree(cuda):
+    """Reference test_solver.py:167-177: predictions of the fast and dense backends agree.
+    (The ridge solve amplifies the Fourier approximation error of the kernel; with this
+    data a length-scale of 0.15 keeps it at ~2e-4 in the oracle, 1/sqrt(2) would not.)"""
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.solver import default_sigma_f, krr_fit, krr_predict
+    from paper_2404_17344_b200.windows import WindowSet
+
+    ds = _prescaled(200, 4, 8)
+    te = _prescaled(200, 4, 9)
+    ws = WindowSet(((1, 2), (3, 4)), d_max=2)
+    spec = KernelSpec("gauss", 0.15, default_sigma_f(2))
+    fast = krr_fit(ds, ws, spec, 0.1, tol=1e-6)
+    dense = krr_fit(ds, ws, spec, 0.1, backend="dense", tol=1e-6)
+    pd, pf = krr_predict(dense, te), krr_predict(fast, te)
+    assert np.linalg.norm(pd - pf) / np.linalg.norm(pd) <= 1e-3
+
+
+def test_grid_search_records_failures_and_single_cell(cuda):
+    """Reference test_solver.py:191-220 on the batched fast backend."""
+    from paper_2404_17344_b200.solver import grid_search
+    from paper_2404_17344_b200.windows import WindowSet
+
+    tr, te = _prescaled(200, 4, 13), _prescaled(100, 4, 14)
+    ws = WindowSet(((1, 2), (3, 4)), d_max=2)
+    res = grid_search(tr, te, ws, [1.0], [0.1])
+    assert len(res.cells) == 1 and res.best_pair == (1.0, 0.1) and res.best.rmse is not None
+    res = grid_search(tr, te, ws, [1.0, 0.5], [1e-8, 1e3], tol=1e-3, max_iter=2)
+    assert any(c.failed for c in res.cells) and not all(c.failed for c in res.cells)
+    assert all(c.message for c in res.cells if c.failed)
+
+
+def test_fast_dell_matches_central_difference(cuda):
+    """dK/dl v from the fast path equals the central difference of the fast K v in the
+    prescaled length-scale (reference test_kernels.py:121-143 for the dense case)."""
+    from paper_2404_17344_b200.fastsum import build_plan, fast_matvec, fast_matvecs
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    ds = _prescaled(800, 4, 21)
+    ws = WindowSet(((1, 2), (3, 4), (1, 4)), d_max=2)
+    v = np.random.default_rng(22).normal(size=800)
+    for fam, ell in (("gauss", 0.3), ("matern12", 0.4)):
+        d = fast_matvecs(build_plan(KernelSpec(fam, ell), ws, "fine", ds), v, dell=True)["dK_dell"]
+        h = 1e-5
+        kp = fast_matvec(build_plan(KernelSpec(fam, ell + h), ws, "fine", ds), v)
+        km = fast_matvec(build_plan(KernelSpec(fam, ell - h), ws, "fine", ds), v)
+        assert rel(d, (kp - km) / (2 * h)) < 1e-6, fam
