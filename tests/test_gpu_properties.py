@@ -419,3 +419,36 @@ def test_c5_full_size_properties(cuda):
         one = build_plan(wl.specs[w], WindowSet((wl.window_set.windows[w],), d_max=3), "default", wl.data)
         single = fast_matvecs(one, V[:2], dell=True)["dK_dell"]
         assert rel(res["dK_dell"][w][:2].cpu().numpy(), single.cpu().numpy()) <= 1e-12, w
+
+
+def test_plans_release_device_memory(cuda):
+    """Building and dropping plans (geometry, weight tables, operators, cuFFT plans) in a
+    loop does not accumulate device memory."""
+    import gc
+
+    import torch
+
+    from paper_2404_17344_b200.fastsum import build_plan, fast_matvecs
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    rng = np.random.default_rng(17)
+    X = rng.uniform(-0.05, 0.05, size=(50000, 6))
+    V = rng.normal(size=(3, 50000))
+    ws = WindowSet(((1, 2, 3), (4, 5), (6,)), d_max=3)
+
+    def cycle():
+        plan = build_plan(KernelSpec("gauss", 0.3), ws, "default", _ds(X, 3))
+        fast_matvecs(plan, V, dell=True)
+        del plan
+        gc.collect()
+        torch.cuda.synchronize()
+
+    cycle()
+    torch.cuda.empty_cache()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(10):
+        cycle()
+    torch.cuda.empty_cache()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 < 64 * 2**20, (free0 - free1) / 2**20
