@@ -1393,9 +1393,15 @@ struct PlanKey {
 static std::mutex g_plan_mu;
 static std::map<PlanKey, cufftHandle> g_plans;
 
-static int cached_plan(int q, int n, cufftType type, cudaStream_t st, cufftHandle* out) {
+// At most kMaxCachedPlans (shape, type, stream) plans are kept; beyond that (a process
+// cycling through many streams) a call gets a temporary plan that the caller destroys
+// after synchronising its stream.
+static constexpr size_t kMaxCachedPlans = 64;
+
+static int cached_plan(int q, int n, cufftType type, cudaStream_t st, cufftHandle* out, bool* temporary) {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     PlanKey k{q, n, (int)type, st};
+    *temporary = false;
     auto it = g_plans.find(k);
     if (it != g_plans.end()) {
         *out = it->second;
@@ -1408,9 +1414,17 @@ static int cached_plan(int q, int n, cufftType type, cudaStream_t st, cufftHandl
         cufftDestroy(h);
         return fail(AK_ERR_CUFFT, "cufftSetStream failed");
     }
-    g_plans[k] = h;
+    if (g_plans.size() < kMaxCachedPlans) g_plans[k] = h;
+    else *temporary = true;
     *out = h;
     return AK_OK;
+}
+
+// Release a plan obtained with *temporary set, once the work queued on `st` is done.
+static void release_plan(cufftHandle h, bool temporary, cudaStream_t st) {
+    if (!temporary) return;
+    cudaStreamSynchronize(st);
+    cufftDestroy(h);
 }
 
 __global__ void k_type1_extract(const double2* __restrict__ Yr, const double2* __restrict__ Yi, int q, int n, int m,
@@ -1452,10 +1466,15 @@ extern "C" int ak_type1_band(int32_t q, int32_t n, int32_t m, const double* gre,
     if (q < 1 || q > 3 || m < 2 || m > n || !gre || !gim || !deconv || !S) return fail(AK_ERR_INVALID, "bad type1 args");
     cudaStream_t st = (cudaStream_t)stream;
     cufftHandle h;
-    AK_TRY(cached_plan(q, n, CUFFT_D2Z, st, &h));
+    bool tmp_plan = false;
+    AK_TRY(cached_plan(q, n, CUFFT_D2Z, st, &h, &tmp_plan));
     const int64_t hs = ipow_rt(n, q - 1) * (n / 2 + 1);
     double2* Y = nullptr;
-    AK_CUDA(cudaMallocAsync(&Y, sizeof(double2) * hs * 2, st));
+    if (cudaMallocAsync(&Y, sizeof(double2) * hs * 2, st) != cudaSuccess) {
+        cudaGetLastError();
+        release_plan(h, tmp_plan, st);
+        return fail(AK_ERR_ALLOC, "type-1 workspace allocation failed");
+    }
     int rc = AK_OK;
     {
         std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -1470,6 +1489,7 @@ extern "C" int ak_type1_band(int32_t q, int32_t n, int32_t m, const double* gre,
         rc = launched();
     }
     cudaFreeAsync(Y, st);
+    release_plan(h, tmp_plan, st);
     return rc;
 }
 
@@ -1510,10 +1530,15 @@ extern "C" int ak_type2_grid(int32_t q, int32_t n, int32_t m, const double* c, c
     if (q < 1 || q > 3 || m < 2 || m > n || !c || !deconv || !gre || !gim) return fail(AK_ERR_INVALID, "bad type2 args");
     cudaStream_t st = (cudaStream_t)stream;
     cufftHandle h;
-    AK_TRY(cached_plan(q, n, CUFFT_Z2Z, st, &h));
+    bool tmp_plan = false;
+    AK_TRY(cached_plan(q, n, CUFFT_Z2Z, st, &h, &tmp_plan));
     const int64_t tot = ipow_rt(n, q);
     double2* G = nullptr;
-    AK_CUDA(cudaMallocAsync(&G, sizeof(double2) * tot, st));
+    if (cudaMallocAsync(&G, sizeof(double2) * tot, st) != cudaSuccess) {
+        cudaGetLastError();
+        release_plan(h, tmp_plan, st);
+        return fail(AK_ERR_ALLOC, "type-2 workspace allocation failed");
+    }
     int rc = cudaMemsetAsync(G, 0, sizeof(double2) * tot, st) == cudaSuccess ? AK_OK
                                                                                : fail(AK_ERR_CUDA, "memset failed");
     if (rc == AK_OK) {
@@ -1533,5 +1558,6 @@ extern "C" int ak_type2_grid(int32_t q, int32_t n, int32_t m, const double* c, c
         rc = launched();
     }
     cudaFreeAsync(G, st);
+    release_plan(h, tmp_plan, st);
     return rc;
 }
