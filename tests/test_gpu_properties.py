@@ -80,6 +80,26 @@ def test_device_tensors_stay_on_device(c4_plan, cuda):
     assert rel(out.cpu().numpy(), fast_matvec(plan, wl.V[0])) <= 1e-14
 
 
+def test_pinned_host_input(c4_plan, cuda):
+    """A page-locked caller buffer takes the non-blocking upload; reusing and
+    overwriting it between calls must not leak into earlier results."""
+    from paper_2404_17344_b200.fastsum import fast_matvec, fast_matvecs
+
+    wl, plan = c4_plan
+    buf = cuda.empty(wl.data.n_rows, dtype=cuda.float64, pin_memory=True).numpy()
+    buf[:] = wl.V[0]
+    first = fast_matvec(plan, buf)
+    buf[:] = -wl.V[0]
+    second = fast_matvec(plan, buf)
+    ref = fast_matvec(plan, np.array(wl.V[0]))
+    assert rel(first, ref) <= 1e-14
+    assert rel(second, -ref) <= 1e-14
+    B = cuda.empty((2, wl.data.n_rows), dtype=cuda.float64, pin_memory=True).numpy()
+    B[0], B[1] = wl.V[0], 2.0 * wl.V[0]
+    res = fast_matvecs(plan, B)["K"]
+    assert rel(res[1], 2.0 * ref) <= 1e-13
+
+
 def _oracle_check(X, windows, v, family="gauss", ell=0.3, d_max=3, preset="default", sf=1.0, tol=1e-8):
     from oracle import restate as R
     from paper_2404_17344_b200.fastsum import PRESETS, build_plan, fast_matvec
