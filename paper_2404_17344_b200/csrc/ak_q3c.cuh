@@ -15,6 +15,13 @@
 #pragma once
 #include "ak_q3m.cuh"
 
+#ifndef AK_FASTPATH
+#define AK_FASTPATH 1
+#endif
+#ifndef AK_SPREAD3C_VREG
+#define AK_SPREAD3C_VREG 1
+#endif
+
 namespace ak {
 
 // 222 registers (no spills) -> 9 warps per SM; __launch_bounds__(32, 8) let ptxas use
@@ -100,6 +107,34 @@ __device__ __forceinline__ void spread3c_unit(Spread3cSmem<B>& sm, int unit, con
         if (bi + 2 < nbatch && lane < min(B, it.count - off - 2 * B))
             cp_async8(&cib[(bi + 2) % 3][lane], CIit + off + 2 * B + lane);
         cp_async_commit();
+#if AK_SPREAD3C_VREG
+        __syncwarp();
+        // v folded into the per-point products in the FMA loop (3 DMUL per point and
+        // lane) instead of a per-batch staging pass over the w0 rows
+        double a0[P0], a1[P1], a2[P2], b0[P0], b1[P1], b2[P2], av, bv;
+        auto load = [&](double (&w0)[P0], double (&w1)[P1], double (&w2)[P2], const double* row) {
+#pragma unroll
+            for (int a = 0; a < P0; ++a) w0[a] = row[AO + g0 * P0 + a];
+#pragma unroll
+            for (int b = 0; b < P1; ++b) w1[b] = row[T + g1 * P1 + b];
+#pragma unroll
+            for (int c = 0; c < P2; ++c) w2[c] = row[2 * T + g2 * P2 + c];
+        };
+        load(a0, a1, a2, &wbuf[s][0][0]);
+        av = vb[s][0];
+        int j = 0;
+        for (; j + 1 < nb; j += 2) {
+            load(b0, b1, b2, &wbuf[s][j + 1][0]);
+            bv = vb[s][j + 1];
+            spread_fma_v(acc, a0, a1, a2, av);
+            const int jn = j + 2 < nb ? j + 2 : j + 1;
+            load(a0, a1, a2, &wbuf[s][jn][0]);
+            av = vb[s][jn];
+            spread_fma_v(acc, b0, b1, b2, bv);
+        }
+        if (j < nb) spread_fma_v(acc, a0, a1, a2, av);
+        __syncwarp();
+#else
         {
             constexpr int PER = (B * T + 31) / 32;
             double x[PER], y[PER];
@@ -138,10 +173,26 @@ __device__ __forceinline__ void spread3c_unit(Spread3cSmem<B>& sm, int unit, con
             spread_fma(acc, b0, b1, b2);
         }
         if (j < nb) spread_fma(acc, a0, a1, a2);
+#endif
     }
 
     const int c0 = it.sc & 1023, c1 = (it.sc >> 10) & 1023, c2 = (it.sc >> 20) & 1023;
     double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
+#if AK_FASTPATH
+    const int o0 = c0 - (T / 2 - 1), o1 = c1 - (T / 2 - 1), o2 = c2 - (T / 2 - 1);
+    if (o0 >= 0 && o0 + T <= n && o1 >= 0 && o1 + T <= n && o2 >= 0 && o2 + T <= n) {
+        // footprint inside the grid (no periodic wrap): one base pointer, constant strides
+        const int64_t nn = (int64_t)n * n;
+        double* __restrict__ base = g + (int64_t)(o0 + AO + g0 * P0) * nn + (int64_t)(o1 + g1 * P1) * n + o2 + g2 * P2;
+#pragma unroll
+        for (int a = 0; a < P0; ++a)
+#pragma unroll
+            for (int b = 0; b < P1; ++b)
+#pragma unroll
+                for (int c = 0; c < P2; ++c) red_add(base + a * nn + b * n + c, acc[a][b][c]);
+        return;
+    }
+#endif
     {
         // flush the register tile straight to the grid (a shared-memory staged, row-
         // coalesced flush measured 3% slower on B200)
@@ -224,6 +275,24 @@ __device__ __forceinline__ void interp3c_unit(Interp3cSmem<B>& sm, int unit, con
         const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
         const int nn = lane >> 2, kk = lane & 3;
         const int qq = nn >> 1, e = nn & 1;
+#if AK_FASTPATH
+        const int o0 = c0 - (T / 2 - 1), o1 = c1 - (T / 2 - 1), o2 = c2 - (T / 2 - 1);
+        if (o0 >= 0 && o0 + T <= n && o1 >= 0 && o1 + T <= n && o2 >= 0 && o2 + T <= n) {
+            // footprint inside the grid: lane base + per-tile (a, b) plane/row offsets
+            const int64_t n2 = (int64_t)n * n;
+            const double* __restrict__ base = g + (int64_t)(o0 + AO) * n2 + (int64_t)(o1 + 3 * qq) * n + o2 + kk;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                // pair i = 2t + e: a = i / 3, b = i % 3 (selected per lane parity e)
+                const int i0 = 2 * t, i1 = 2 * t + 1;
+                const int64_t off0 = (i0 / 3) * n2 + (i0 % 3) * n, off1 = (i1 / 3) * n2 + (i1 % 3) * n;
+                const double* row = base + (e ? off1 : off0);
+#pragma unroll
+                for (int ks = 0; ks < 3; ++ks) gf[t][ks] = __ldg(row + 4 * ks);
+            }
+        } else
+#endif
+        {
         int z[3];
 #pragma unroll
         for (int ks = 0; ks < 3; ++ks) z[ks] = wrap(c2 - (T / 2 - 1) + 4 * ks + kk, n);
@@ -234,6 +303,7 @@ __device__ __forceinline__ void interp3c_unit(Interp3cSmem<B>& sm, int unit, con
             const int64_t rowb = ((int64_t)wrap(c0 - (T / 2 - 1) + a, n) * n + wrap(c1 - (T / 2 - 1) + b, n)) * n;
 #pragma unroll
             for (int ks = 0; ks < 3; ++ks) gf[t][ks] = __ldg(g + rowb + z[ks]);
+        }
         }
     }
     const double sc = scale[it.window];

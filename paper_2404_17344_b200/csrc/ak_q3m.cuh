@@ -18,6 +18,10 @@
 #pragma once
 #include "ak_q3w.cuh"
 
+#ifndef AK_INTERP_SPLIT
+#define AK_INTERP_SPLIT 0
+#endif
+
 namespace ak {
 
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
@@ -70,6 +74,27 @@ __device__ __forceinline__ double interp_group_mma(const double (&gf)[3 * A / 2]
     // lane (pj, q) holds U[pj][(a, b)] for a = AO + i/3, b = 3q + i%3, i = 2t + e:
     // out = sum_b w1[b] (sum_a w0[a] U[a][b]) -- 3 chains of A FMAs, then 3 more
     double s[3];
+#if AK_INTERP_SPLIT
+    // two interleaved chains of A/2 per b (shorter dependency chains), summed at the end
+    double s2[3];
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) {
+        s[bb] = w[AO] * C[bb >> 1][bb & 1];
+        s2[bb] = w[AO + 1] * C[(3 + bb) >> 1][(3 + bb) & 1];
+    }
+#pragma unroll
+    for (int a = 2; a < A; a += 2) {
+        const double w0a = w[AO + a], w0b = w[AO + a + 1];
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb) {
+            const int i = 3 * a + bb, i2 = 3 * (a + 1) + bb;
+            s[bb] = fma(w0a, C[i >> 1][i & 1], s[bb]);
+            s2[bb] = fma(w0b, C[i2 >> 1][i2 & 1], s2[bb]);
+        }
+    }
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) s[bb] += s2[bb];
+#else
 #pragma unroll
     for (int bb = 0; bb < 3; ++bb) s[bb] = w[AO] * C[bb >> 1][bb & 1];
 #pragma unroll
@@ -81,6 +106,7 @@ __device__ __forceinline__ double interp_group_mma(const double (&gf)[3 * A / 2]
             s[bb] = fma(w0a, C[i >> 1][i & 1], s[bb]);
         }
     }
+#endif
     const double* w1 = w + 12 + 3 * q;
     const double v = fma(w1[2], s[2], fma(w1[1], s[1], w1[0] * s[0]));
     return valid ? v : 0.0;
