@@ -1,0 +1,305 @@
+// Band-pruned, multiplier-fused transform stage for 3-D windows, on the FP64 tensor
+// cores.
+//
+// The reference (nufft.py:362-365, 379-383, fastsum.py:159) takes the full n^3 FFT of
+// each grid, keeps the band of m modes per axis, multiplies by the kernel's
+// coefficients and the window deconvolution (one real multiplier H per band entry; the
+// (-1)^k signs cancel), zero-pads and takes the full inverse FFT.  Only the band (m of
+// n frequencies per axis, m/2 along the real axis) is ever used, so these kernels
+// compute exactly the band, as DFT-matrix products on the FP64 tensor cores
+// (mma.sync m8n8k4, operands in shared memory):
+//   fwd12 : per plane x0 of a grid:  real P[x1][x2] -> B[x0][k1][k2]
+//           S1  A[x1][(k2,re|im)] = P . T1                (M n,  N m,    K n)
+//           S2  [Bre; Bim] = [[Wr, -Wi], [Wi, Wr]] . [Are; Aim]   (M 2m, N m/2, K 2n)
+//   fwd0  : per (k1, grid) slab:     B[.][k1][.] -> S[k0][k1][k2], the compact band
+//           spectrum (multi-GPU exchange buffer, layout of k_band_pack)  (M 2m, N m/2, K 2n)
+//   inv0  : per (k1, grid) slab:     H * S -> C[x0][k1][k2]   (multiplier fused; M 2n, N m/2, K 2m)
+//   inv12 : per plane x0:            C[x0] -> D[x1][k2] (M 2n, N m/2, K 2m)
+//           -> real g[x1][x2] = sum_k2 c_k2 Re(D e^{+i w k2 x2}) = [Dre | Dim] . T3  (M n, N n, K m)
+// Frequencies: band index b in [0, m) is k = b (b < m/2) or b - m; w = 2 pi / n.
+// Along the real axis k2 runs over [0, m/2) with c_0 = 1, c_k2 = 2 otherwise, which is
+// cuFFT's Z2D on the Hermitian-consistent band (H even, forward input real).
+// Every stage is a 131K-MAC GEMM per plane/slab at n = 64, m = 32 (512 DMMA).
+#pragma once
+#include "ak_common.cuh"
+
+namespace ak {
+
+constexpr int FFT3_THREADS = 256;
+
+// row strides (doubles) that keep the m8n8k4 fragment loads conflict-free:
+// A operands (8 rows x 4 k) want ld = 4 (mod 16), B operands (4 k x 8 cols) ld = 8 (mod 16)
+__host__ __device__ constexpr int fft3_ldA(int cols) { return cols + ((4 - cols) % 16 + 16) % 16; }
+__host__ __device__ constexpr int fft3_ldB(int cols) { return cols + ((8 - cols) % 16 + 16) % 16; }
+
+__device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// C[M][N] = sum_k A(r, k) B(k, c) over the CTA's warps; each warp takes blocks of
+// TM x TN 8x8 output tiles.  a(r, k) / b(k, c) fetch operand elements (shared memory),
+// st(r, c, v) consumes each result.  M % (8 TM) == N % (8 TN) == K % 4 == 0.
+template <int TM, int TN, class FA, class FB, class FS>
+__device__ __forceinline__ void cta_gemm(int M, int N, int K, FA a, FB b, FS st)
+{
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int mt = M / (8 * TM), nt = N / (8 * TN);
+    const int lr = lane >> 2, lk = lane & 3;
+    for (int blk = warp; blk < mt * nt; blk += nw) {
+        const int r0 = (blk / nt) * 8 * TM, c0 = (blk % nt) * 8 * TN;
+        double acc[TM][TN][2];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        // fragments of KC k-steps are fetched together (one load latency per KC steps)
+        constexpr int KC = 4;
+        int k = 0;
+        for (; k + 4 * KC <= K; k += 4 * KC) {
+            double af[KC][TM], bf[KC][TN];
+#pragma unroll
+            for (int s = 0; s < KC; ++s) {
+#pragma unroll
+                for (int i = 0; i < TM; ++i) af[s][i] = a(r0 + 8 * i + lr, k + 4 * s + lk);
+#pragma unroll
+                for (int j = 0; j < TN; ++j) bf[s][j] = b(k + 4 * s + lk, c0 + 8 * j + lr);
+            }
+#pragma unroll
+            for (int s = 0; s < KC; ++s)
+#pragma unroll
+                for (int i = 0; i < TM; ++i)
+#pragma unroll
+                    for (int j = 0; j < TN; ++j) dmma_884(acc[i][j][0], acc[i][j][1], af[s][i], bf[s][j]);
+        }
+        for (; k < K; k += 4) {
+            double af[TM], bf[TN];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) af[i] = a(r0 + 8 * i + lr, k + lk);
+#pragma unroll
+            for (int j = 0; j < TN; ++j) bf[j] = b(k + lk, c0 + 8 * j + lr);
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) dmma_884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) {
+                st(r0 + 8 * i + lr, c0 + 8 * j + 2 * lk, acc[i][j][0]);
+                st(r0 + 8 * i + lr, c0 + 8 * j + 2 * lk + 1, acc[i][j][1]);
+            }
+    }
+}
+
+// 2 x 2 tiles per warp when the shape allows it and still feeds every warp, else smaller
+template <class FA, class FB, class FS>
+__device__ __forceinline__ void cta_gemm_auto(int M, int N, int K, FA a, FB b, FS st)
+{
+    const int nw = blockDim.x >> 5;
+    if (M % 16 == 0 && N % 16 == 0 && (M / 16) * (N / 16) >= nw) cta_gemm<2, 2>(M, N, K, a, b, st);
+    else if (N % 16 == 0 && (M / 8) * (N / 16) >= nw) cta_gemm<1, 2>(M, N, K, a, b, st);
+    else if (M % 16 == 0 && (M / 16) * (N / 8) >= nw) cta_gemm<2, 1>(M, N, K, a, b, st);
+    else cta_gemm<1, 1>(M, N, K, a, b, st);
+}
+
+// Twiddle tables (one device buffer per operator, built on the host):
+//   T1 [n][m]   T1[x][2k] = cos(w k x), T1[x][2k+1] = -sin(w k x)        (k < m/2)
+//   FR, FI [m][n]  e^{-i w f(b) x} = FR + i FI                            (forward band rows)
+//   IR, II [n][m]  e^{+i w f(b) x} = IR + i II                            (inverse band columns)
+//   T3 [m][n]   T3[k2][x] = c cos(w k2 x), T3[m/2 + k2][x] = -c sin(w k2 x)
+struct Fft3Tables {
+    const double *T1, *FR, *FI, *IR, *II, *T3;
+};
+
+// complex GEMM operand [[R, -I], [I, R]] (rows: output re | im, k: input re | im) from
+// split R / I twiddle matrices of `rows` x `cols` (row-major, global memory: the tables
+// are shared by every CTA and stay L1/L2-resident)
+struct CplxA {
+    const double* __restrict__ R;
+    const double* __restrict__ I;
+    int rows, cols;
+    __device__ __forceinline__ double operator()(int r, int k) const {
+        const int ro = r >= rows, ki = k >= cols;
+        const int rr = r - ro * rows, kk = k - ki * cols;
+        const double v = __ldg(((ro == ki) ? R : I) + rr * cols + kk);
+        return (ki && !ro) ? -v : v;
+    }
+};
+
+// plane copy global -> shared with 16-byte loads (cols even, ld even)
+__device__ __forceinline__ void fft3_copy2(double* dst, int ld, const double* __restrict__ src, int rows, int cols) {
+    const int c2 = cols / 2;
+    const double2* __restrict__ s2 = reinterpret_cast<const double2*>(src);
+    for (int e = threadIdx.x; e < rows * c2; e += blockDim.x) {
+        const int r = e / c2, c = e - r * c2;
+        *reinterpret_cast<double2*>(dst + r * ld + 2 * c) = __ldg(s2 + e);
+    }
+}
+
+// fbuf (per grid, per plane x0): split complex [2][m][mh] doubles
+// fwd12: grids [nb][n][n][n] real -> fbuf [nb][n(x0)][2][m(b1)][mh]
+template <int n, int m>
+__global__ void __launch_bounds__(FFT3_THREADS, 3)
+k_fft3_fwd12(const double* __restrict__ grids, double* __restrict__ fbuf, Fft3Tables tb)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int mh = m / 2, x0 = blockIdx.x;
+    const int64_t b = blockIdx.y;
+    const int ldP = fft3_ldA(n), ldX = fft3_ldB(mh);
+    double* P = sm;                       // [n][ldP]     (S1 A)
+    double* X = P + n * ldP;              // [2n][ldX]    (S1 out, S2 B)
+    fft3_copy2(P, ldP, grids + (b * n + x0) * n * n, n, n);
+    __syncthreads();
+    const double* __restrict__ T1 = tb.T1;
+    cta_gemm_auto(
+        n, m, n, [&](int r, int k) { return P[r * ldP + k]; }, [&](int k, int c) { return __ldg(T1 + k * m + c); },
+        [&](int r, int c, double v) { X[((c & 1) * n + r) * ldX + (c >> 1)] = v; });
+    __syncthreads();
+    double* __restrict__ dst = fbuf + (b * n + x0) * 2 * m * mh;
+    cta_gemm_auto(
+        2 * m, mh, 2 * n, CplxA{tb.FR, tb.FI, m, n}, [&](int k, int c) { return X[k * ldX + c]; },
+        [&](int r, int c, double v) { dst[r * mh + c] = v; });
+}
+
+// fwd0: fbuf [nb][n(x0)][2][m(b1)][mh] -> band [nb][m(b0)][m(b1)][mh] complex
+template <int n, int m>
+__global__ void __launch_bounds__(FFT3_THREADS, 3)
+k_fft3_fwd0(const double* __restrict__ fbuf, double* __restrict__ band, Fft3Tables tb)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int mh = m / 2, b1 = blockIdx.x;
+    const int64_t b = blockIdx.y;
+    const int ldX = fft3_ldB(mh);
+    double* X = sm;                       // [2n (re x0 | im x0)][ldX]
+    const int h2 = mh / 2;
+    for (int e = threadIdx.x; e < 2 * n * h2; e += blockDim.x) {
+        const int row = e / h2, c = e - row * h2;     // row = ri * n + x0
+        const int ri = row / n, x0 = row - ri * n;
+        *reinterpret_cast<double2*>(X + row * ldX + 2 * c) =
+            __ldg(reinterpret_cast<const double2*>(fbuf + (((b * n + x0) * 2 + ri) * m + b1) * mh) + c);
+    }
+    __syncthreads();
+    double* __restrict__ dst = band + b * 2 * (int64_t)m * m * mh;
+    cta_gemm_auto(
+        2 * m, mh, 2 * n, CplxA{tb.FR, tb.FI, m, n}, [&](int k, int c) { return X[k * ldX + c]; },
+        [&](int r, int c, double v) {
+            const int ro = r >= m, b0 = r - ro * m;
+            dst[2 * (((int64_t)b0 * m + b1) * mh + c) + ro] = v;
+        });
+}
+
+// inv0: H * band -> fbuf [nb][n(x0)][2][m(b1)][mh]; the multiplier of grid b is
+// H[hsel][(b0 m + b1) mh + k2] with hsel as in k_band_multiply
+template <int n, int m>
+__global__ void __launch_bounds__(FFT3_THREADS, 3)
+k_fft3_inv0(const double* __restrict__ band, double* __restrict__ fbuf, Fft3Tables tb, int R,
+            const int* __restrict__ gwin, const double* const* __restrict__ H, int hbase, int P, int per_rhs)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int mh = m / 2, b1 = blockIdx.x;
+    const int64_t b = blockIdx.y;
+    const int ldY = fft3_ldB(mh);
+    double* Y = sm;                       // [2m (re b0 | im b0)][ldY]
+    const int w = gwin[b / R];
+    const double* __restrict__ h = H[per_rhs ? (int)(b % R) * P + w : hbase + w];
+    const double2* __restrict__ src = reinterpret_cast<const double2*>(band + b * 2 * (int64_t)m * m * mh);
+    for (int e = threadIdx.x; e < m * mh; e += blockDim.x) {
+        const int b0 = e / mh, k2 = e - b0 * mh;
+        const int64_t ci = ((int64_t)b0 * m + b1) * mh + k2;
+        const double hv = __ldg(h + ci);
+        const double2 v = __ldg(src + ci);
+        Y[b0 * ldY + k2] = hv * v.x;
+        Y[(m + b0) * ldY + k2] = hv * v.y;
+    }
+    __syncthreads();
+    cta_gemm_auto(
+        2 * n, mh, 2 * m, CplxA{tb.IR, tb.II, n, m}, [&](int k, int c) { return Y[k * ldY + c]; },
+        [&](int r, int c, double v) {
+            const int ro = r >= n, x0 = r - ro * n;
+            fbuf[(((b * n + x0) * 2 + ro) * m + b1) * mh + c] = v;
+        });
+}
+
+// inv12: fbuf [nb][n(x0)][2][m][mh] -> grids [nb][n][n][n] real (one block per (x0, grid))
+template <int n, int m>
+__global__ void __launch_bounds__(FFT3_THREADS, 3)
+k_fft3_inv12(const double* __restrict__ fbuf, double* __restrict__ out, Fft3Tables tb)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int mh = m / 2, x0 = blockIdx.x;
+    const int64_t b = blockIdx.y;
+    const int ldC = fft3_ldB(mh), ldD = fft3_ldA(mh);
+    double* C = sm;                       // [2m][ldC]  (I1 B)
+    double* D = C + 2 * m * ldC;          // [2n][ldD]  (I1 out, I2 A)
+    fft3_copy2(C, ldC, fbuf + (b * n + x0) * 2 * m * mh, 2 * m, mh);
+    __syncthreads();
+    cta_gemm_auto(
+        2 * n, mh, 2 * m, CplxA{tb.IR, tb.II, n, m}, [&](int k, int c) { return C[k * ldC + c]; },
+        [&](int r, int c, double v) { D[r * ldD + c] = v; });
+    __syncthreads();
+    double* __restrict__ dst = out + (b * n + x0) * n * n;
+    const double* __restrict__ T3 = tb.T3;
+    cta_gemm_auto(
+        n, n, m,
+        [&](int r, int k) {
+            const int ri = k >= mh;
+            return D[(ri * n + r) * ldD + k - ri * mh];
+        },
+        [&](int k, int c) { return __ldg(T3 + k * n + c); }, [&](int r, int c, double v) { dst[r * n + c] = v; });
+}
+
+// dynamic shared memory (bytes) of each kernel
+inline size_t fft3_smem_fwd12(int n, int m) {
+    return sizeof(double) * ((size_t)n * fft3_ldA(n) + (size_t)2 * n * fft3_ldB(m / 2));
+}
+inline size_t fft3_smem_fwd0(int n, int m) { return sizeof(double) * (size_t)2 * n * fft3_ldB(m / 2); }
+inline size_t fft3_smem_inv0(int n, int m) { return sizeof(double) * (size_t)2 * m * fft3_ldB(m / 2); }
+inline size_t fft3_smem_inv12(int n, int m) {
+    return sizeof(double) * ((size_t)2 * m * fft3_ldB(m / 2) + (size_t)2 * n * fft3_ldA(m / 2));
+}
+inline size_t fft3_smem_max(int n, int m) {
+    return std::max(std::max(fft3_smem_fwd12(n, m), fft3_smem_fwd0(n, m)),
+                    std::max(fft3_smem_inv0(n, m), fft3_smem_inv12(n, m)));
+}
+
+// Host: the twiddle tables for (n, m) in one buffer, order T1, FR, FI, IR, II, T3.
+inline std::vector<double> fft3_host_tables(int n, int m) {
+    const int mh = m / 2;
+    std::vector<long double> c(n), s(n);
+    for (int j = 0; j < n; ++j) {
+        const long double a = 2.0L * 3.14159265358979323846264338327950288L * j / n;
+        c[j] = cosl(a);
+        s[j] = sinl(a);
+    }
+    auto f = [&](int bi) { return bi < mh ? bi : bi - m + n; };
+    std::vector<double> t((size_t)6 * n * m);
+    double* T1 = t.data();
+    double* FR = T1 + (size_t)n * m;
+    double* FI = FR + (size_t)n * m;
+    double* IR = FI + (size_t)n * m;
+    double* II = IR + (size_t)n * m;
+    double* T3 = II + (size_t)n * m;
+    for (int x = 0; x < n; ++x)
+        for (int k = 0; k < mh; ++k) {
+            const int j = (int)((int64_t)k * x % n);
+            T1[x * m + 2 * k] = (double)c[j];
+            T1[x * m + 2 * k + 1] = (double)-s[j];
+            const double w = k == 0 ? 1.0 : 2.0;
+            T3[k * n + x] = w * (double)c[j];
+            T3[(mh + k) * n + x] = -w * (double)s[j];
+        }
+    for (int bi = 0; bi < m; ++bi)
+        for (int x = 0; x < n; ++x) {
+            const int j = (int)((int64_t)f(bi) * x % n);
+            FR[bi * n + x] = (double)c[j];
+            FI[bi * n + x] = (double)-s[j];
+            IR[x * m + bi] = (double)c[j];
+            II[x * m + bi] = (double)s[j];
+        }
+    return t;
+}
+
+}  // namespace ak

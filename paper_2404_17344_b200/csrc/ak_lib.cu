@@ -24,6 +24,7 @@
 #include "ak_q3m.cuh"
 #include "ak_q3c.cuh"
 #include "ak_q2c.cuh"
+#include "ak_fft3.cuh"
 
 using namespace ak;
 
@@ -1178,6 +1179,34 @@ __global__ void k_band_pack(double2* __restrict__ spec, double2* __restrict__ ba
     }
 }
 
+// The fused 3-D transform stage is compiled for the default and rough presets at the
+// default oversampling (n, m) = (64, 32), (32, 16); other shapes and AK_FFT3=cufft use
+// the full cuFFT transforms.
+template <int n, int m>
+static void fft3_attrs() {
+    cudaFuncSetAttribute(ak::k_fft3_fwd12<n, m>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)ak::fft3_smem_fwd12(n, m));
+    cudaFuncSetAttribute(ak::k_fft3_fwd0<n, m>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)ak::fft3_smem_fwd0(n, m));
+    cudaFuncSetAttribute(ak::k_fft3_inv0<n, m>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)ak::fft3_smem_inv0(n, m));
+    cudaFuncSetAttribute(ak::k_fft3_inv12<n, m>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)ak::fft3_smem_inv12(n, m));
+}
+
+static bool fft3_fused_ok(int n, int m) {
+    const char* e = getenv("AK_FFT3");   // read per operator (tests switch it)
+    if (e && !strcmp(e, "cufft")) return false;
+    if (n == 64 && m == 32) fft3_attrs<64, 32>();
+    else if (n == 32 && m == 16) fft3_attrs<32, 16>();
+    else return false;
+    return true;
+}
+
+struct ak_op;
+static int fft3_forward(ak_op* op, cudaStream_t st);
+static int fft3_inverse(ak_op* op, const double* const* H, int hbase, int per_rhs, cudaStream_t st);
+
 struct ak_op {
     const ak_geom* gs = nullptr;
     const ak_geom* gi = nullptr;
@@ -1196,18 +1225,66 @@ struct ak_op {
     int nwin[4] = {0, 0, 0, 0};
     cufftHandle fwd[4] = {0, 0, 0, 0}, inv[4] = {0, 0, 0, 0};
     bool has[4] = {false, false, false, false};
+    bool planned[4] = {false, false, false, false};   // cuFFT plans made for this q
+    bool fused3 = false;          // q = 3: band-pruned fused transforms (ak_fft3.cuh) instead of cuFFT
+    double* fbuf = nullptr;       // fused3: per-plane partial transforms [R nwin3][n][2][m][m/2]
+    double* ftab = nullptr;       // fused3: twiddle tables (ak::Fft3Tables)
     int* gwin_d[4] = {nullptr, nullptr, nullptr, nullptr};
 };
+
+static ak::Fft3Tables fft3_tables(const ak_op* op) {
+    const size_t nm = (size_t)op->gs->n * op->m;
+    const double* t = op->ftab;
+    return ak::Fft3Tables{t, t + nm, t + 2 * nm, t + 3 * nm, t + 4 * nm, t + 5 * nm};
+}
+
+// fused q = 3 transforms: grids -> compact band spectra (op->band, q = 3 section)
+template <int n, int m>
+static int fft3_forward_t(ak_op* op, cudaStream_t st) {
+    const unsigned nb = (unsigned)(op->R * op->nwin[3]);
+    const ak::Fft3Tables tb = fft3_tables(op);
+    ak::k_fft3_fwd12<n, m><<<dim3(n, nb), ak::FFT3_THREADS, ak::fft3_smem_fwd12(n, m), st>>>(
+        op->grids + op->grid_off[3], op->fbuf, tb);
+    AK_TRY(launched());
+    ak::k_fft3_fwd0<n, m><<<dim3(m, nb), ak::FFT3_THREADS, ak::fft3_smem_fwd0(n, m), st>>>(
+        op->fbuf, reinterpret_cast<double*>(op->band + op->band_off[3]), tb);
+    return launched();
+}
+
+// fused q = 3: H (set hbase / per RHS) x band spectra -> op->gbuf grids
+template <int n, int m>
+static int fft3_inverse_t(ak_op* op, const double* const* H, int hbase, int per_rhs, cudaStream_t st) {
+    const unsigned nb = (unsigned)(op->R * op->nwin[3]);
+    const ak::Fft3Tables tb = fft3_tables(op);
+    ak::k_fft3_inv0<n, m><<<dim3(m, nb), ak::FFT3_THREADS, ak::fft3_smem_inv0(n, m), st>>>(
+        reinterpret_cast<const double*>(op->band + op->band_off[3]), op->fbuf, tb, op->R, op->gwin_d[3], H, hbase,
+        op->gs->P, per_rhs);
+    AK_TRY(launched());
+    ak::k_fft3_inv12<n, m><<<dim3(n, nb), ak::FFT3_THREADS, ak::fft3_smem_inv12(n, m), st>>>(
+        op->fbuf, op->gbuf + op->grid_off[3], tb);
+    return launched();
+}
+
+static int fft3_forward(ak_op* op, cudaStream_t st) {
+    return op->gs->n == 64 ? fft3_forward_t<64, 32>(op, st) : fft3_forward_t<32, 16>(op, st);
+}
+
+static int fft3_inverse(ak_op* op, const double* const* H, int hbase, int per_rhs, cudaStream_t st) {
+    return op->gs->n == 64 ? fft3_inverse_t<64, 32>(op, H, hbase, per_rhs, st)
+                           : fft3_inverse_t<32, 16>(op, H, hbase, per_rhs, st);
+}
 
 extern "C" int ak_op_destroy(ak_op* op) {
     if (!op) return AK_OK;
     for (int q = 1; q <= 3; ++q) {
-        if (op->has[q]) {
+        if (op->planned[q]) {
             cufftDestroy(op->fwd[q]);
             cufftDestroy(op->inv[q]);
         }
         cudaFree(op->gwin_d[q]);
     }
+    cudaFree(op->fbuf);
+    cudaFree(op->ftab);
     cudaFree(op->grids);
     cudaFree(op->gbuf);
     cudaFree(op->spec);
@@ -1231,17 +1308,27 @@ static int op_build(ak_op* op, cudaStream_t st) {
         op->spec_off[q] = soff;
         if (ws.empty()) continue;
         op->grid_off[q] = (int64_t)op->R * g->canon_off[ws[0]];
-        soff += op->hs[q] * op->R * (int64_t)ws.size();
         AK_CUDA(cudaMalloc(&op->gwin_d[q], sizeof(int) * ws.size()));
         AK_CUDA(cudaMemcpyAsync(op->gwin_d[q], ws.data(), sizeof(int) * ws.size(), cudaMemcpyHostToDevice, st));
-        int dims[3] = {n, n, n};
+        op->has[q] = true;
         const int batch = op->R * (int)ws.size();
+        if (q == 3 && fft3_fused_ok(n, op->m)) {
+            op->fused3 = true;
+            AK_CUDA(cudaMalloc(&op->fbuf, sizeof(double) * (size_t)batch * n * op->m * op->m));
+            const std::vector<double> tabs = ak::fft3_host_tables(n, op->m);
+            AK_CUDA(cudaMalloc(&op->ftab, sizeof(double) * tabs.size()));
+            AK_CUDA(cudaMemcpyAsync(op->ftab, tabs.data(), sizeof(double) * tabs.size(), cudaMemcpyHostToDevice, st));
+            AK_CUDA(cudaStreamSynchronize(st));
+            continue;
+        }
+        soff += op->hs[q] * batch;
+        int dims[3] = {n, n, n};
         AK_CUFFT(cufftPlanMany(&op->fwd[q], q, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_D2Z, batch));
         if (cufftPlanMany(&op->inv[q], q, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2D, batch) != CUFFT_SUCCESS) {
             cufftDestroy(op->fwd[q]);
             return fail(AK_ERR_CUFFT, "cufftPlanMany Z2D failed");
         }
-        op->has[q] = true;
+        op->planned[q] = true;
     }
     int64_t boff = 0;
     for (int q = 3; q >= 1; --q) {
@@ -1319,7 +1406,9 @@ extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double
     if (flags & AK_APPLY_SPREAD_ONLY) return AK_OK;
     if (flags & AK_APPLY_SPECTRUM_ONLY) {
         for (int q = 3; q >= 1; --q)
-            if (op->has[q]) {
+            if (q == 3 && op->fused3) {
+                AK_TRY(fft3_forward(op, st));
+            } else if (op->has[q]) {
                 AK_CUFFT(cufftSetStream(op->fwd[q], st));
                 AK_CUFFT(cufftExecD2Z(op->fwd[q], op->grids + op->grid_off[q],
                                       (cufftDoubleComplex*)(op->spec + op->spec_off[q])));
@@ -1344,7 +1433,10 @@ extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double
     }
     if (gi->N == 0) return AK_OK;
     for (int q = 3; q >= 1; --q)
-        if (op->has[q]) {
+        if (q == 3 && op->fused3) {
+            // the band spectrum is the fused stage's intermediate: from-spectrum starts at the inverse
+            if (!(flags & AK_APPLY_FROM_SPECTRUM)) AK_TRY(fft3_forward(op, st));
+        } else if (op->has[q]) {
             if (flags & AK_APPLY_FROM_SPECTRUM) {
                 const int64_t total = op->bs[q] * R * op->nwin[q];
                 k_band_pack<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(
@@ -1360,6 +1452,10 @@ extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double
     for (int c = 0; c < op->C; ++c) {
         for (int q = 3; q >= 1; --q) {
             if (!op->has[q]) continue;
+            if (q == 3 && op->fused3) {
+                AK_TRY(fft3_inverse(op, H, c * P, (flags & AK_APPLY_H_PER_RHS) ? 1 : 0, st));
+                continue;
+            }
             const int64_t total = op->hs[q] * R * op->nwin[q];
             const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
             k_band_multiply<<<blocks, 256, 0, st>>>(op->spec + op->spec_off[q], op->spec2 + op->spec_off[q], q, gs->n,

@@ -199,6 +199,36 @@ def test_kernel_variants_match_reference(cuda, monkeypatch, variant):
             assert rel(res["dK_dell"], g["dK_dell_default"]) <= TOL, (variant, name)
 
 
+def test_fused_band_transforms_match_cufft(cuda, monkeypatch):
+    """The band-pruned, multiplier-fused 3-D transform stage (ak_fft3.cuh) against the
+    full cuFFT transforms + band multiply (AK_FFT3=cufft) and the reference goldens:
+    default and rough presets, K and dK/dl, 8 RHS."""
+    from paper_2404_17344_b200.fastsum import fast_matvecs
+
+    for name in ("c3", "c4"):
+        g = golden(name)
+        dell = "dK_dell_default" in g
+        outs = {}
+        for mode in ("fused", "cufft"):
+            if mode == "cufft":
+                monkeypatch.setenv("AK_FFT3", "cufft")
+            else:
+                monkeypatch.delenv("AK_FFT3", raising=False)
+            outs[mode] = fast_matvecs(_plan(g), g["V"], dell=dell)
+            assert rel(outs[mode]["K"], g["K_default"]) <= TOL, (mode, name)
+        assert rel(outs["fused"]["K"], outs["cufft"]["K"]) <= 1e-13, name
+        if dell:
+            assert rel(outs["fused"]["dK_dell"], outs["cufft"]["dK_dell"]) <= 1e-13, name
+    g = golden("c4")
+    for mode in ("fused", "cufft"):
+        if mode == "cufft":
+            monkeypatch.setenv("AK_FFT3", "cufft")
+        else:
+            monkeypatch.delenv("AK_FFT3", raising=False)
+        outs[mode] = fast_matvecs(_plan(g, preset="rough"), g["V"])["K"]
+    assert rel(outs["fused"], outs["cufft"]) <= 1e-13
+
+
 @pytest.mark.parametrize("sc2", ["1", "8"])
 def test_q2_item_kernels_match_reference(cuda, monkeypatch, sc2):
     """2-D windows through the single-cell tensor-core kernels (AK_SUPERCELL2=1) and the
