@@ -23,6 +23,10 @@
 #pragma once
 #include "ak_common.cuh"
 
+#ifndef AK_FFT3_KC
+#define AK_FFT3_KC 4
+#endif
+
 namespace ak {
 
 constexpr int FFT3_THREADS = 256;
@@ -55,7 +59,7 @@ __device__ __forceinline__ void cta_gemm(int M, int N, int K, FA a, FB b, FS st)
 #pragma unroll
             for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
         // fragments of KC k-steps are fetched together (one load latency per KC steps)
-        constexpr int KC = 4;
+        constexpr int KC = AK_FFT3_KC;
         int k = 0;
         for (; k + 4 * KC <= K; k += 4 * KC) {
             double af[KC][TM], bf[KC][TN];
