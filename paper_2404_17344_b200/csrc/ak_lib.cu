@@ -1312,7 +1312,7 @@ static int op_build(ak_op* op, cudaStream_t st) {
         AK_CUDA(cudaMemcpyAsync(op->gwin_d[q], ws.data(), sizeof(int) * ws.size(), cudaMemcpyHostToDevice, st));
         op->has[q] = true;
         const int batch = op->R * (int)ws.size();
-        if (q == 3 && fft3_fused_ok(n, op->m)) {
+        if (q == 3 && batch <= 65535 && fft3_fused_ok(n, op->m)) {   // grids on gridDim.y
             op->fused3 = true;
             AK_CUDA(cudaMalloc(&op->fbuf, sizeof(double) * (size_t)batch * n * op->m * op->m));
             const std::vector<double> tabs = ak::fft3_host_tables(n, op->m);
