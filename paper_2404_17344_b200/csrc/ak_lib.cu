@@ -24,6 +24,7 @@
 #include "ak_q3m.cuh"
 #include "ak_q3c.cuh"
 #include "ak_q2c.cuh"
+#include "ak_q3r.cuh"
 #include "ak_fft3.cuh"
 
 using namespace ak;
@@ -840,10 +841,22 @@ static void launch_spread3w_b(const ak_geom* g, int64_t i0, int64_t ni, const do
     }
 }
 
+// AK_SPREAD3R=0 keeps even RHS counts on the DFMA tile (k_spread3c)
+static bool spread3r_enabled() {
+    const char* e = getenv("AK_SPREAD3R");
+    return !(e && !strcmp(e, "0"));
+}
+
 template <int T>
 static void launch_spread3_t(const ak_geom* g, int64_t i0, int64_t ni, const double* V, int R, int64_t ldv,
                              double* grids, cudaStream_t st)
 {
+    if (T == 12 && g->cached && g->sedge[3] == 1 && !g->trim3 && R % 2 == 0 && spread3r_enabled()) {
+        // pairs of RHS on the FP64 tensor cores (ak_q3r.cuh)
+        k_spread3r<32><<<(unsigned)(ni * (R / 2)), 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv,
+                                                                grids, g->canon_off_d, R, g->n);
+        return;
+    }
     if (T == 12 && g->cached && g->sedge[3] == 1) {
         const unsigned grid = (unsigned)(ni * R);  // item-major, RHS fastest
         if (g->batch3 == 32 && g->trim3)

@@ -164,6 +164,33 @@ def test_dense_2d_windows_tensor_core_items(cuda, monkeypatch):
     assert rel(auto, lane) <= 1e-13
 
 
+@pytest.mark.parametrize("R", [2, 4, 6])
+def test_rhs_pair_tensor_core_spread(cuda, monkeypatch, R):
+    """Even RHS counts on densely occupied 3-D windows take the RHS-pair tensor-core
+    spread (k_spread3r): each column equals the one-RHS product (DFMA tile), the
+    AK_SPREAD3R=0 batch, and the oracle; footprints on the periodic boundary included."""
+    from oracle import restate as R_
+    from paper_2404_17344_b200.fastsum import build_plan, fast_matvec, fast_matvecs
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    rng = np.random.default_rng(20 + R)
+    N = 30_000
+    X = np.concatenate([rng.uniform(-0.012, 0.012, size=(N // 2, 6)),
+                        rng.uniform(-0.5, -0.49, size=(N - N // 2, 6))])   # centre and wrapping cells
+    V = rng.normal(size=(R, N))
+    ws = WindowSet(((1, 2, 3), (4, 5, 6)), d_max=3)
+    plan = build_plan(KernelSpec("gauss", 0.3), ws, "default", _ds(X, 3))
+    res = fast_matvecs(plan, V, dell=True)
+    for r in range(R):
+        assert rel(res["K"][r], fast_matvec(plan, V[r])) <= 1e-13
+    monkeypatch.setenv("AK_SPREAD3R", "0")
+    ref = fast_matvecs(plan, V, dell=True)
+    assert rel(res["K"], ref["K"]) <= 1e-13 and rel(res["dK_dell"], ref["dK_dell"]) <= 1e-13
+    orc = R_.FastSum("gauss", 0.3, 1.0, [(0, 1, 2), (3, 4, 5)], X).matvec(V[R - 1])
+    assert rel(res["K"][R - 1], orc) <= 1e-8
+
+
 @pytest.mark.parametrize("preset", ["rough", "fine", 48])
 def test_other_grid_sizes(cuda, preset):
     rng = np.random.default_rng(4)
