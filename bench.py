@@ -21,13 +21,16 @@ n = 64, cutoff 6, Kaiser-Bessel).  A step is one full K v over all windows.
 * ``cpu_baseline``: the CPU oracle port (oracle/, serial C loops + numpy FFT,
   the reference's algorithm and cost structure) timed on three windows at full N.
 
-Multi-GPU (torchrun): --shard hybrid (default) splits the ranks into G window
-groups x Q row blocks (G from distributed.hybrid_layout: 2 x 4 on 8 GPUs for
-config 4); each rank spreads its rows into its windows' grids, the band
-spectra are all-reduced within the window group, each rank interpolates its
-rows, and the row partials are all-reduced across window groups.  --shard
-point (G = 1) / window (Q = 1) are the two pure decompositions.  Timing is the
-max over ranks; the roofline is rank 0's local kernels.
+Multi-GPU (torchrun): --shard cell (default) splits the ranks into G window
+groups x Q cell slabs (G from distributed.hybrid_layout: 2 x 4 on 8 GPUs for
+config 4); each rank spreads the rows of its slab of whole grid cells of each
+owned window (one row-masked plan), the band spectra are all-reduced within
+the window group, each rank interpolates its slab rows, and one all-reduce of
+the length-N partials assembles K v.  --shard hybrid uses row blocks instead
+of cell slabs (same collectives; thinner cells per rank: per-rank device time
+0.871 vs 0.808 ms at 4 ranks, equal at 2 and 8, tools/rank_emulate.py);
+--shard point (G = 1) / window (Q = 1) are the two pure decompositions.
+Timing is the max over ranks; the roofline is rank 0's local kernels.
 """
 
 from __future__ import annotations
@@ -66,8 +69,9 @@ def parse():
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo: functional check of the multi-rank path with several ranks on one device "
                          "(host-side collectives; its timings are not bench values)")
-    ap.add_argument("--shard", choices=["hybrid", "point", "window"], default="hybrid",
-                    help="multi-GPU decomposition (N > 1): rows (default) or windows")
+    ap.add_argument("--shard", choices=["cell", "hybrid", "point", "window"], default="cell",
+                    help="multi-GPU decomposition (N > 1): window groups x cell slabs (default), x row blocks, "
+                         "rows only, windows only")
     return ap.parse_args()
 
 
@@ -348,6 +352,9 @@ def extra_workloads(torch, steps=5, warmup=2):
 
 
 def _parallelism(shard, dplan, world):
+    if shard == "cell":
+        return (f"cell slabs x{world}: {dplan.G} window groups x {dplan.Q} cell slabs; NCCL all-reduce of band "
+                f"spectra within a window group, of the length-N partials over all ranks")
     if shard == "hybrid":
         return (f"hybrid x{world}: {dplan.G} window groups x {dplan.Q} row blocks; NCCL all-reduce of band "
                 f"spectra within a window group, of row partials across groups")
@@ -384,9 +391,11 @@ def run_ours(args):
 
     t0 = time.perf_counter()
     if world > 1:
-        from paper_2404_17344_b200.distributed import HybridShardedPlan, PointShardedPlan, WindowShardedPlan
+        from paper_2404_17344_b200.distributed import (CellShardedPlan, HybridShardedPlan, PointShardedPlan,
+                                                           WindowShardedPlan)
 
-        cls = {"hybrid": HybridShardedPlan, "point": PointShardedPlan, "window": WindowShardedPlan}[args.shard]
+        cls = {"cell": CellShardedPlan, "hybrid": HybridShardedPlan, "point": PointShardedPlan,
+               "window": WindowShardedPlan}[args.shard]
         dplan = cls(wl.spec, wl.window_set, "default", wl.data)
         plan = dplan.plan
     else:
@@ -417,10 +426,10 @@ def run_ours(args):
     def step_deriv():
         if world > 1:
             fams = ("gauss", "der_gauss")
-            if args.shard != "window":
-                outs = dplan.matvecs_local(v_dev[dplan.lo:dplan.hi].reshape(1, -1), fams)
-            else:
+            if args.shard in ("cell", "window"):
                 outs = dplan.matvecs(v_dev.reshape(1, -1), fams)
+            else:
+                outs = dplan.matvecs_local(v_dev[dplan.lo:dplan.hi].reshape(1, -1), fams)
             return outs
         return fast_matvecs(plan, v_dev, dell=True, dsigma=True)
 

@@ -91,6 +91,20 @@ int64_t ak_launch_count(void);
 int ak_geom_create(int32_t n, int32_t P, const int32_t* q, const int32_t* cols,
                    const double* X, int64_t N, int64_t ld,
                    const ak_window_fn* wf, void* stream, ak_geom** out);
+
+/*
+ * ak_geom_create_masked -- ak_geom_create with a row subset per window (no
+ * reference counterpart: the multi-GPU cell-slab layout, distributed.py
+ * CellShardedPlan).  Window w spreads from / interpolates to only the rows r with
+ * masks[w*N + r] != 0; the other rows contribute nothing and receive nothing
+ * (outputs stay row-indexed over all N rows).
+ *   masks     device uint8[P*N]
+ *   rows_in   host int64[P]: number of nonzero mask entries per window
+ */
+int ak_geom_create_masked(int32_t n, int32_t P, const int32_t* q, const int32_t* cols,
+                          const double* X, int64_t N, int64_t ld,
+                          const uint8_t* masks, const int64_t* rows_in,
+                          const ak_window_fn* wf, void* stream, ak_geom** out);
 int     ak_geom_destroy(ak_geom* g);
 int64_t ak_geom_num_points(const ak_geom* g);
 int32_t ak_geom_num_windows(const ak_geom* g);

@@ -39,7 +39,7 @@ AK_NCOEF = 7
 #: symbols the header declares; tests check the library exports every one
 EXPORTED = (
     "ak_last_error", "ak_version", "ak_launch_count",
-    "ak_geom_create", "ak_geom_destroy", "ak_geom_num_points", "ak_geom_num_windows",
+    "ak_geom_create", "ak_geom_create_masked", "ak_geom_destroy", "ak_geom_num_points", "ak_geom_num_windows",
     "ak_geom_num_items", "ak_geom_grid_elems", "ak_geom_canon_offset", "ak_geom_canon_total",
     "ak_spread", "ak_interp", "ak_op_create", "ak_op_destroy", "ak_op_apply", "ak_op_grids", "ak_op_band",
     "ak_type1_band", "ak_type2_grid", "ak_dense_apply", "ak_probe_fp64", "ak_probe_dmma",
@@ -71,6 +71,9 @@ def _declare(lib: ctypes.CDLL) -> None:
         "ak_launch_count": (_i64, []),
         "ak_geom_create": (_c_int, [_i32, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32), _dp, _i64, _i64,
                                     ctypes.POINTER(WindowFn), _vp, ctypes.POINTER(_vp)]),
+        "ak_geom_create_masked": (_c_int, [_i32, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32), _dp, _i64, _i64,
+                                           _dp, ctypes.POINTER(_i64), ctypes.POINTER(WindowFn), _vp,
+                                           ctypes.POINTER(_vp)]),
         "ak_geom_destroy": (_c_int, [_vp]),
         "ak_geom_num_points": (_i64, [_vp]),
         "ak_geom_num_windows": (_i32, [_vp]),

@@ -89,6 +89,7 @@ struct ak_geom {
     int64_t* canon_off_d = nullptr;
     ak_window_fn wf{};
     Point* pts = nullptr;               // [P][N]
+    std::vector<int64_t> rows_in;       // per window: rows it uses (N, or the mask count; sorted first)
     WorkItem* items = nullptr;
     int64_t nitems = 0;
     int64_t item_begin[4] = {0, 0, 0, 0}, item_end[4] = {0, 0, 0, 0};
@@ -199,13 +200,18 @@ static int chunk_for(int q, int64_t point_windows) {
     return (int)std::max<int64_t>(64, std::min<int64_t>(hi, point_windows / (2 * (int64_t)slots)));
 }
 
+// mask (optional, the window's N-row slice): rows with mask 0 get the key `sentinel`,
+// which sorts after every cell key, and stay out of the histogram (no work item
+// covers them: a row-subset window for cell-slab sharding).
 __global__ void k_keys(const double* __restrict__ X, int64_t ld, int q, int c0, int c1, int c2, int n, int S,
                        int nsc, int64_t N, uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
-                       int* __restrict__ counts, int* __restrict__ bad)
+                       int* __restrict__ counts, int* __restrict__ bad, const uint8_t* __restrict__ mask = nullptr,
+                       uint32_t sentinel = 0)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
     const int col[3] = {c0, c1, c2};
+    const bool in = !mask || mask[i];
     int sc = 0, sub = 0;
     for (int a = 0; a < q; ++a) {
         double x = X[i * ld + col[a]];
@@ -221,8 +227,9 @@ __global__ void k_keys(const double* __restrict__ X, int64_t ld, int q, int c0, 
     }
     int sq = 1;
     for (int a = 0; a < q; ++a) sq *= S;
-    keys[i] = (uint32_t)sc * (uint32_t)sq + (uint32_t)sub;
+    keys[i] = in ? (uint32_t)sc * (uint32_t)sq + (uint32_t)sub : sentinel;
     vals[i] = (int32_t)i;
+    if (!in) return;
     // warp-aggregated histogram update (clustered data puts many lanes in one supercell)
     const unsigned active = __activemask();
     const unsigned peers = __match_any_sync(active, sc);
@@ -285,11 +292,12 @@ __global__ void k_items(const int* __restrict__ counts, const int* __restrict__ 
 
 // Run boundaries of the sorted keys: a key's run is [kstart, kend) (0/0 when absent).
 __global__ void k_key_bounds(const uint32_t* __restrict__ keys, int64_t N, int* __restrict__ kstart,
-                             int* __restrict__ kend)
+                             int* __restrict__ kend, int64_t nkeys)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
     const uint32_t k = keys[i];
+    if ((int64_t)k >= nkeys) return;   // masked-out rows (sentinel key)
     if (i == 0 || keys[i - 1] != k) kstart[k] = (int)i;
     if (i == N - 1 || keys[i + 1] != k) kend[k] = (int)(i + 1);
 }
@@ -342,7 +350,7 @@ extern "C" int ak_geom_destroy(ak_geom* g) {
 
 // Mean points per occupied cell of window w (bins at S = 1); -1 when the probe fails.
 static double mean_occupancy(const double* X, int64_t ld, const int32_t* cols, int w, int q, int n, int64_t N,
-                             cudaStream_t st)
+                             cudaStream_t st, const uint8_t* mask = nullptr, int64_t n_in = -1)
 {
     const int tot = (int)ipow_rt(n, q);
     int *cnt = nullptr, *aux = nullptr;
@@ -354,13 +362,13 @@ static double mean_occupancy(const double* X, int64_t ld, const int32_t* cols, i
         cudaMemsetAsync(cnt, 0, sizeof(int) * tot, st);
         cudaMemsetAsync(aux, 0, sizeof(int) * 2, st);
         k_keys<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(X, ld, q, cols[3 * w], cols[3 * w + 1], cols[3 * w + 2],
-                                                             n, 1, n, N, kk, vv, cnt, aux);
+                                                             n, 1, n, N, kk, vv, cnt, aux, mask, 0u);
         k_count_nonzero<<<(tot + 255) / 256, 256, 0, st>>>(cnt, tot, aux + 1);
         g_launches.fetch_add(2);
         int h[2] = {0, 0};
         if (cudaMemcpyAsync(h, aux, sizeof(h), cudaMemcpyDeviceToHost, st) == cudaSuccess &&
             cudaStreamSynchronize(st) == cudaSuccess && h[1] > 0)
-            mean = (double)N / h[1];
+            mean = (double)(n_in >= 0 ? n_in : N) / h[1];
     }
     cudaGetLastError();
     cudaFree(cnt);
@@ -385,7 +393,12 @@ struct Scratch {
     }
 };
 
-static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t ld, cudaStream_t st) {
+// masks: optional device uint8 [P][N] (row r belongs to window w iff masks[w N + r]);
+// n_in: host per-window row counts of the masks (occupancy probes)
+static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t ld, cudaStream_t st,
+                      const uint8_t* masks = nullptr, const int64_t* n_in = nullptr) {
+    auto wmask = [&](int w) { return masks ? masks + (int64_t)w * g->N : nullptr; };
+    auto win_rows = [&](int w) { return n_in ? n_in[w] : (int64_t)-1; };
     const int n = g->n, P = g->P;
     const int64_t N = g->N;
     // canonical order: q descending, stable
@@ -441,7 +454,8 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
         s3 = si3 = 2;
         // (the probe and the split item lists keep one int per cell: only for grids up to 256^3)
         if (cached && !g->windows_of_q[3].empty() && n <= 256) {
-            const double occ = mean_occupancy(X, ld, cols, g->windows_of_q[3][0], 3, n, N, st);
+            const int w0 = g->windows_of_q[3][0];
+            const double occ = mean_occupancy(X, ld, cols, w0, 3, n, N, st, wmask(w0), win_rows(w0));
             if (occ >= dense_cell_threshold()) s3 = 1;
             if (occ >= dense_cell_threshold_interp()) si3 = 1;
         }
@@ -454,13 +468,18 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
     if (s2 == 0) {
         s2 = 8;
         if (cached && !g->windows_of_q[2].empty() && n <= 4096 &&
-            mean_occupancy(X, ld, cols, g->windows_of_q[2][0], 2, n, N, st) >= dense_cell_threshold2())
+            mean_occupancy(X, ld, cols, g->windows_of_q[2][0], 2, n, N, st, wmask(g->windows_of_q[2][0]),
+                           win_rows(g->windows_of_q[2][0])) >= dense_cell_threshold2())
             s2 = 1;
     }
     g->sedge[2] = s2;
     g->sedge[3] = s3;
     g->sedge_i3 = si3;
-    for (int q = 1; q <= 3; ++q) g->chunk[q] = chunk_for(q, N * (int64_t)g->windows_of_q[q].size());
+    for (int q = 1; q <= 3; ++q) {
+        int64_t pw = 0;   // point-windows of this length (masked rows excluded)
+        for (int w : g->windows_of_q[q]) pw += n_in ? n_in[w] : N;
+        g->chunk[q] = chunk_for(q, pw);
+    }
     int64_t tcap = 1;     // per-window item capacity of the staging buffer
     int64_t keyspace = 1; // 3-D sort-key space (cells in supercell order) when split
     for (int w = 0; w < P; ++w) {
@@ -539,12 +558,16 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
             const int tot = (int)ipow_rt(nsc, q);
             int bits = 1;
             while ((int64_t)1 << bits < (int64_t)tot * ipow_rt(S, q)) ++bits;
+            // masked rows: sentinel key 2^bits sorts after every cell (one more key bit)
+            const uint32_t sentinel = (uint32_t)1 << bits;
+            if (masks) ++bits;
             const int c0 = cols[3 * w], c1 = cols[3 * w + 1], c2 = cols[3 * w + 2];
             if (N == 0) continue;
             cudaMemsetAsync(counts, 0, sizeof(int) * tot, st);
             const int tb = 256;
             const int nblk = (int)((N + tb - 1) / tb);
-            k_keys<<<nblk, tb, 0, st>>>(X, ld, q, c0, c1, c2, n, S, nsc, N, keys, vals, counts, dflags);
+            k_keys<<<nblk, tb, 0, st>>>(X, ld, q, c0, c1, c2, n, S, nsc, N, keys, vals, counts, dflags, wmask(w),
+                                        sentinel);
             if ((rc = launched()) != AK_OK) break;
             size_t tb2 = temp_bytes;
             if (cub::DeviceRadixSort::SortPairs(temp, tb2, keys, keys2, vals, vals2, (int)N, 0, bits, st) != cudaSuccess) {
@@ -569,7 +592,7 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
                 const int64_t nk = (int64_t)tot * S * S * S;
                 cudaMemsetAsync(kstart, 0, sizeof(int) * nk, st);
                 cudaMemsetAsync(kend, 0, sizeof(int) * nk, st);
-                k_key_bounds<<<nblk, tb, 0, st>>>(keys2, N, kstart, kend);
+                k_key_bounds<<<nblk, tb, 0, st>>>(keys2, N, kstart, kend, nk);
                 if ((rc = launched()) != AK_OK) break;
                 k_items_cells<<<(unsigned)((nk + 255) / 256), 256, 0, st>>>(kstart, kend, nk, S, nsc, g->chunk[3],
                                                                             (int64_t)w * N, w, dflags + 1, titems);
@@ -651,8 +674,29 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
     return rc;
 }
 
+static int geom_create(int32_t n, int32_t P, const int32_t* q, const int32_t* cols, const double* X, int64_t N,
+                       int64_t ld, const uint8_t* masks, const int64_t* n_in, const ak_window_fn* wf, void* stream,
+                       ak_geom** out);
+
 extern "C" int ak_geom_create(int32_t n, int32_t P, const int32_t* q, const int32_t* cols, const double* X,
                               int64_t N, int64_t ld, const ak_window_fn* wf, void* stream, ak_geom** out)
+{
+    return geom_create(n, P, q, cols, X, N, ld, nullptr, nullptr, wf, stream, out);
+}
+
+extern "C" int ak_geom_create_masked(int32_t n, int32_t P, const int32_t* q, const int32_t* cols, const double* X,
+                                     int64_t N, int64_t ld, const uint8_t* masks, const int64_t* rows_in,
+                                     const ak_window_fn* wf, void* stream, ak_geom** out)
+{
+    if (!masks || !rows_in) return fail(AK_ERR_INVALID, "null argument");
+    for (int w = 0; w < P; ++w)
+        if (rows_in[w] < 0 || rows_in[w] > N) return fail(AK_ERR_INVALID, "bad per-window row count");
+    return geom_create(n, P, q, cols, X, N, ld, masks, rows_in, wf, stream, out);
+}
+
+static int geom_create(int32_t n, int32_t P, const int32_t* q, const int32_t* cols, const double* X, int64_t N,
+                       int64_t ld, const uint8_t* masks, const int64_t* n_in, const ak_window_fn* wf, void* stream,
+                       ak_geom** out)
 {
     if (!out || !q || !cols || !wf) return fail(AK_ERR_INVALID, "null argument");
     *out = nullptr;
@@ -672,13 +716,15 @@ extern "C" int ak_geom_create(int32_t n, int32_t P, const int32_t* q, const int3
     g->P = P;
     g->N = N;
     g->q.assign(q, q + P);
+    g->rows_in.assign(P, N);
+    if (n_in) g->rows_in.assign(n_in, n_in + P);
     g->wf = *wf;
     if (wf->taps == 12) {
         bool zero = true;
         for (int k = 0; k < AK_NCOEF; ++k) zero = zero && wf->ce[0][k] == 0.0 && wf->co[0][k] == 0.0;
         g->trim3 = zero;  // taps 0 and 11 vanish: the single-cell q = 3 kernels skip them on axis 0
     }
-    int rc = geom_build(g, cols, X, ld, (cudaStream_t)stream);
+    int rc = geom_build(g, cols, X, ld, (cudaStream_t)stream, masks, n_in);
     if (rc != AK_OK) {
         std::string keep = g_err;
         ak_geom_destroy(g);
@@ -915,6 +961,7 @@ static int spread_group(const ak_geom* g, int q, const double* V, int R, int64_t
     if (g->windows_of_q[q].empty() || g->N == 0) return AK_OK;
     const int T = g->wf.taps;
     bool done = false;
+    if (!force_generic() && ni == 0) return AK_OK;   // only row-masked windows have no items
     if (!force_generic() && ni > 0) {
         done = true;
         if (q == 3 && (T == 12 || T == 8 || T == 4)) launch_spread3(g, i0, ni, V, R, ldv, grids, st);
@@ -933,8 +980,9 @@ static int spread_group(const ak_geom* g, int q, const double* V, int R, int64_t
         if (done) return launched();
     }
     for (int w : g->windows_of_q[q]) {
-        dim3 grid((unsigned)((g->N + 127) / 128), (unsigned)R);
-        k_spread_generic<<<grid, 128, 0, st>>>(g->pts, (int64_t)w * g->N, g->N, q, V, ldv,
+        if (g->rows_in[w] == 0) continue;
+        dim3 grid((unsigned)((g->rows_in[w] + 127) / 128), (unsigned)R);
+        k_spread_generic<<<grid, 128, 0, st>>>(g->pts, (int64_t)w * g->N, g->rows_in[w], q, V, ldv,
                                                grids + (int64_t)R * g->canon_off[w], g->n, g->wf);
         AK_TRY(launched());
     }
@@ -1064,6 +1112,7 @@ static int interp_group(const ak_geom* g, int q, const double* grids, int R, con
     const int T = g->wf.taps;
     const int64_t ws = sum_windows ? 0 : wstride;
     bool done = false;
+    if (!force_generic() && ni == 0) return AK_OK;   // only row-masked windows have no items
     if (!force_generic() && ni > 0) {
         done = true;
         if (q == 3 && (T == 12 || T == 8 || T == 4))
@@ -1081,8 +1130,10 @@ static int interp_group(const ak_geom* g, int q, const double* grids, int R, con
         if (done) return launched();
     }
     for (int w : g->windows_of_q[q]) {
-        dim3 grid((unsigned)((g->N + 127) / 128), (unsigned)R);
-        k_interp_generic<<<grid, 128, 0, st>>>(g->pts, (int64_t)w * g->N, g->N, q, grids + (int64_t)R * g->canon_off[w],
+        if (g->rows_in[w] == 0) continue;
+        dim3 grid((unsigned)((g->rows_in[w] + 127) / 128), (unsigned)R);
+        k_interp_generic<<<grid, 128, 0, st>>>(g->pts, (int64_t)w * g->N, g->rows_in[w], q,
+                                               grids + (int64_t)R * g->canon_off[w],
                                                g->n, g->wf, scale, w, out + (int64_t)w * ws, ldo, atomic_out);
         AK_TRY(launched());
     }

@@ -279,3 +279,115 @@ class HybridShardedPlan:
         bufs = [torch.empty(m, dtype=torch.float64, device="cuda") for _ in sizes]
         dist.all_gather(bufs, pad, group=self.band_group)
         return torch.cat([b[:s] for b, s in zip(bufs, sizes)])
+
+
+def cell_partition(coords, n: int, parts: int) -> list:
+    """Split the rows of one window into `parts` sets of whole grid cells.
+
+    coords: (N, q) prescaled window coordinates in [-1/2, 1/2).  A row's cell is
+    floor((x + 1/2) n) per axis (the cell whose footprint it spreads into,
+    nufft.py:183-186); cells are ordered by linear index (slabs along the first
+    axis) and cut into `parts` contiguous runs with balanced row counts.
+    Returns `parts` ascending int64 row-index arrays (some may be empty when
+    there are fewer occupied cells than parts).
+    """
+    import numpy as np
+
+    coords = np.asarray(coords, dtype=np.float64)
+    if coords.ndim == 1:
+        coords = coords[:, None]
+    t = np.clip(np.floor((coords + 0.5) * n).astype(np.int64), 0, n - 1)
+    lin = np.zeros(coords.shape[0], dtype=np.int64)
+    for a in range(coords.shape[1]):
+        lin = lin * n + t[:, a]
+    order = np.argsort(lin, kind="stable")
+    cells, starts, counts = np.unique(lin[order], return_index=True, return_counts=True)
+    cum = np.cumsum(counts)
+    total = int(cum[-1]) if len(cum) else 0
+    # cell run p ends at the first cell whose cumulative count reaches (p + 1) / parts
+    bounds = [0]
+    for p in range(1, parts):
+        bounds.append(int(np.searchsorted(cum, total * p / parts, side="left")) + 1 if total else 0)
+    bounds.append(len(cells))
+    bounds = np.maximum.accumulate(np.minimum(np.array(bounds), len(cells)))
+    edges = np.append(starts, coords.shape[0])   # row offset of each cell run in `order`
+    return [np.sort(order[edges[bounds[p]]:edges[bounds[p + 1]]]).astype(np.int64) for p in range(parts)]
+
+
+class CellShardedPlan:
+    """Window groups x cell slabs: the hybrid layout with each window's rows split
+    by grid cell instead of by row block.
+
+    world = G x Q ranks as in HybridShardedPlan.  Within a window group every
+    owned window's occupied cells are cut into Q slabs of equal row count
+    (cell_partition), so each rank spreads and interpolates whole cells at the
+    data's full density (the single-cell kernels keep their efficiency, where a
+    row block of N/Q rows thins every cell Q-fold).  The rank holds ONE plan over
+    its owned windows with a per-window row mask (build_plan(row_masks=...),
+    ak_geom_create_masked): one spread / transform / interpolation launch for all
+    of them, outputs indexed by the global rows.  The band spectra are
+    all-reduced among the Q ranks of the group; one all-reduce over all ranks of
+    the length-N partial products assembles K v on every rank.
+    """
+
+    def __init__(self, spec, window_set: WindowSet, preset, data: Dataset, window_groups: int | None = None,
+                 group=None, **kw):
+        import numpy as np
+
+        from .fastsum import build_plan, resolve_m
+        from .nufft import NufftPlan
+
+        dist = _dist()
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        G = window_groups or hybrid_layout(window_set.lengths, world)
+        if G < 1 or world % G or G > len(window_set):
+            raise ValueError("window_groups must divide the world size and not exceed the number of windows")
+        Q = world // G
+        self.world, self.rank, self.G, self.Q, self.group = world, rank, G, Q, group
+        self.gi, self.pj = rank // Q, rank % Q
+        base = dist.get_process_group_ranks(group) if group is not None else list(range(world))
+        self.band_group = None
+        for g in range(G):
+            members = [base[g * Q + j] for j in range(Q)]
+            pg = dist.new_group(members) if Q > 1 else None
+            if g == self.gi:
+                self.band_group = pg
+        self.owned = window_partition(window_set.lengths, G)[self.gi]
+        self.n_rows = data.n_rows
+        self.spec = spec
+        m = resolve_m(preset)
+        wins = tuple(window_set.windows[w] for w in self.owned)
+        masks = np.zeros((len(wins), data.n_rows), dtype=bool)
+        for k, win in enumerate(wins):
+            n = NufftPlan(dims=len(win), m=m, cutoff=kw.get("cutoff", 6),
+                          oversampling=kw.get("oversampling", 2.0)).n
+            masks[k, cell_partition(data.features[:, list(window_set.columns(win))], n, Q)[self.pj]] = True
+        self.rows_per_window = masks.sum(axis=1)
+        self.plan = build_plan(spec, WindowSet(wins, d_max=window_set.d_max), preset, data, row_masks=masks, **kw)
+
+    def matvecs(self, V, families=None):
+        """(R, N) replicated RHS -> list of (R, N) replicated products (one per family)."""
+        import torch
+
+        from . import _native
+
+        dist = _dist()
+        fams = tuple(families or (self.spec.family,))
+        R = V.shape[0]
+        outs = [torch.empty((R, self.n_rows), dtype=torch.float64, device="cuda") for _ in fams]
+        op = self.plan._operator(fams, R)
+        if self.Q > 1:
+            op.spectrum_only(V)
+            dist.all_reduce(op.band(), group=self.band_group)
+            op.apply(None, outs, [True] * len(outs), flags=_native.AK_APPLY_FROM_SPECTRUM)
+        else:
+            op.apply(V, outs, [True] * len(outs))
+        if self.world > 1:
+            for o in outs:
+                dist.all_reduce(o, group=self.group)
+        return outs
+
+    def matvec(self, v):
+        """Full-length v (replicated) -> K v (replicated)."""
+        return self.matvecs(v.reshape(1, -1))[0][0]

@@ -352,11 +352,15 @@ def _eta_warning(ell: float, m: int) -> None:
 
 
 def build_plan(spec: KernelSpec, window_set: WindowSet, preset, data: Dataset, cutoff: int = 6,
-               oversampling: float = 2.0, window: str = "kaiser_bessel", features_device=None) -> FastsumPlan:
+               oversampling: float = 2.0, window: str = "kaiser_bessel", features_device=None,
+               row_masks=None) -> FastsumPlan:
     """Coefficient tables (host, tiny) + bin-sorted device geometry (fastsum.py:105-133).
 
     ``features_device`` optionally passes ``data.features`` already resident
-    on the GPU (a torch CUDA tensor) to skip the upload.
+    on the GPU (a torch CUDA tensor) to skip the upload.  ``row_masks``
+    (windows x rows, bool; extension) restricts each window to a row subset:
+    the product is then sum_w K_w restricted to window w's rows (the cell-slab
+    multi-GPU layout, distributed.CellShardedPlan).
     """
     _check_prescaled(data, window_set)
     m = resolve_m(preset)
@@ -367,7 +371,8 @@ def build_plan(spec: KernelSpec, window_set: WindowSet, preset, data: Dataset, c
     tables = {q: kernel_coefficients(spec.family, spec.ell, q, m) for q in lengths}
     any_plan = nufft_plans[lengths[0]]
     geom = DeviceGeometry(any_plan.n, window_set.lengths, [window_set.columns(w) for w in window_set],
-                          data.features if features_device is None else features_device, any_plan.window_fn())
+                          data.features if features_device is None else features_device, any_plan.window_fn(),
+                          row_masks=row_masks)
     return FastsumPlan(spec=spec, window_set=window_set, m=m, data=data, nufft_plans=nufft_plans,
                        tables=tables, geometries=geom)
 
@@ -511,7 +516,8 @@ def build_mixed_plan(specs, window_set: WindowSet, preset, data: Dataset, cutoff
                    for q in lengths}
     any_plan = nufft_plans[lengths[0]]
     geom = DeviceGeometry(any_plan.n, window_set.lengths, [window_set.columns(w) for w in window_set],
-                          data.features if features_device is None else features_device, any_plan.window_fn())
+                          data.features if features_device is None else features_device, any_plan.window_fn(),
+                          row_masks=row_masks)
     return MixedKernelPlan(specs=specs, window_set=window_set, m=m, data=data, nufft_plans=nufft_plans,
                            geometries=geom)
 

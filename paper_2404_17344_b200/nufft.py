@@ -250,7 +250,9 @@ class DeviceGeometry:
     """Bin-sorted nodes of P windows on the device (replaces the per-window
     ``SpreadGeometry`` tuple, nufft.py:160-191).  Immutable; owns device memory."""
 
-    def __init__(self, n: int, qs, cols, features, window_fn):
+    def __init__(self, n: int, qs, cols, features, window_fn, row_masks=None):
+        """row_masks: optional (P, N) bool array -- window w uses only the rows with
+        row_masks[w] set (ak_geom_create_masked; the multi-GPU cell-slab layout)."""
         torch = _torch()
         lib = _native.lib()
         feats = features
@@ -274,10 +276,21 @@ class DeviceGeometry:
         self.qs = tuple(int(q) for q in qs)
         self.cols = tuple(tuple(int(c) for c in cs) for cs in cols)
         self.n_points = int(feats.shape[0])
-        rc = lib.ak_geom_create(self.n, P, qarr, carr, ctypes.c_void_p(feats.data_ptr()), self.n_points,
-                                int(feats.shape[1]), ctypes.byref(window_fn), _stream_ptr(torch),
-                                ctypes.byref(self._handle))
-        _native.check(rc, "ak_geom_create")
+        if row_masks is None:
+            rc = lib.ak_geom_create(self.n, P, qarr, carr, ctypes.c_void_p(feats.data_ptr()), self.n_points,
+                                    int(feats.shape[1]), ctypes.byref(window_fn), _stream_ptr(torch),
+                                    ctypes.byref(self._handle))
+            _native.check(rc, "ak_geom_create")
+        else:
+            m = np.ascontiguousarray(np.asarray(row_masks, dtype=bool))
+            if m.shape != (P, self.n_points):
+                raise ValueError("row_masks must have shape (windows, rows)")
+            md = torch.as_tensor(m.view(np.uint8), device="cuda")
+            rows_in = (ctypes.c_int64 * P)(*[int(c) for c in m.sum(axis=1)])
+            rc = lib.ak_geom_create_masked(self.n, P, qarr, carr, ctypes.c_void_p(feats.data_ptr()), self.n_points,
+                                           int(feats.shape[1]), ctypes.c_void_p(md.data_ptr()), rows_in,
+                                           ctypes.byref(window_fn), _stream_ptr(torch), ctypes.byref(self._handle))
+            _native.check(rc, "ak_geom_create_masked")
         self.n_windows = P
         self.n_items = int(lib.ak_geom_num_items(self._handle))
         self.canon_total = int(lib.ak_geom_canon_total(self._handle))

@@ -4,7 +4,7 @@ kernels never wait on each other).  Checks the real sharded code paths --
 SPECTRUM_ONLY spread + band all-reduce + FROM_SPECTRUM interpolation (point
 sharding) and the LPT window split + all-reduce (window sharding) -- against the
 single-process product; with 4 ranks also the 2 x 2 hybrid (window groups x
-point groups)."""
+point groups); and the cell-slab layout (CellShardedPlan) for every group count."""
 
 import os
 import socket
@@ -31,7 +31,8 @@ def _worker(rank, world, port, X, V, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2404_17344_b200.dataset import PRESCALED, Dataset
-        from paper_2404_17344_b200.distributed import HybridShardedPlan, PointShardedPlan, WindowShardedPlan
+        from paper_2404_17344_b200.distributed import (CellShardedPlan, HybridShardedPlan, PointShardedPlan,
+                                                       WindowShardedPlan)
         from paper_2404_17344_b200.fastsum import build_plan, fast_matvecs
         from paper_2404_17344_b200.kernels import KernelSpec
         from paper_2404_17344_b200.windows import WindowSet
@@ -64,6 +65,13 @@ def _worker(rank, world, port, X, V, q):
             for name, o in zip(("K", "dK_dell"), local):
                 r = ref[name][:, hp.lo:hp.hi]
                 errs[f"hybrid{G}_local_{name}"] = np.linalg.norm(o.cpu().numpy() - r) / np.linalg.norm(r)
+        for G in sorted({1, 2, world}):
+            cp = CellShardedPlan(spec, ws, "default", ds, window_groups=G)
+            outs = cp.matvecs(Vd, ("gauss", "der_gauss"))
+            for name, o in zip(("K", "dK_dell"), outs):
+                errs[f"cell{G}_{name}"] = np.linalg.norm(o.cpu().numpy() - ref[name]) / np.linalg.norm(ref[name])
+            k1 = cp.matvec(Vd[1]).cpu().numpy()
+            errs[f"cell{G}_matvec"] = np.linalg.norm(k1 - ref["K"][1]) / np.linalg.norm(ref["K"][1])
         q.put((rank, errs))
     finally:
         dist.destroy_process_group()

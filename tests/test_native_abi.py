@@ -84,6 +84,12 @@ def test_argument_validation_without_a_device():
     ctypes.memmove(ctypes.byref(odd), ctypes.byref(wf_bad), ctypes.sizeof(odd))
     odd.taps = 11
     code(lib.ak_geom_create(64, 1, q, cols, X, 10, 3, ctypes.byref(odd), None, ctypes.byref(out)), "taps")
+    rows_in = (ctypes.c_int64 * 1)(10)
+    code(lib.ak_geom_create_masked(64, 1, q, cols, X, 10, 3, None, rows_in, ctypes.byref(wf), None,
+                                   ctypes.byref(out)), "null")
+    bad_rows = (ctypes.c_int64 * 1)(11)
+    code(lib.ak_geom_create_masked(64, 1, q, cols, X, 10, 3, X, bad_rows, ctypes.byref(wf), None,
+                                   ctypes.byref(out)), "row count")
     assert out.value is None
     code(lib.ak_spread(None, None, 1, 0, None, None), "spread")
     code(lib.ak_interp(None, None, 1, None, None, 0, 1, 0, None), "interp")
