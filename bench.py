@@ -28,7 +28,7 @@ owned window (one row-masked plan), the band spectra are all-reduced within
 the window group, each rank interpolates its slab rows, and one all-reduce of
 the length-N partials assembles K v.  --shard hybrid uses row blocks instead
 of cell slabs (same collectives; thinner cells per rank: per-rank device time
-0.871 vs 0.808 ms at 4 ranks, equal at 2 and 8, tools/rank_emulate.py);
+0.871 vs 0.812 ms at 4 ranks, 0.495 vs 0.488 at 8, equal at 2, tools/rank_emulate.py);
 --shard point (G = 1) / window (Q = 1) are the two pure decompositions.
 Timing is the max over ranks; the roofline is rank 0's local kernels.
 """

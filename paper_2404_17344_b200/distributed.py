@@ -31,6 +31,9 @@ from .dataset import Dataset
 from .windows import WindowSet
 
 WINDOW_TAPS = 12
+#: per-cell cost of a work item (prologue + register-tile flush) in row equivalents,
+#: for balancing cell slabs (tools/rank_emulate.py)
+CELL_OVERHEAD_ROWS = 64.0
 
 
 def window_cost(q: int, taps: int = WINDOW_TAPS) -> int:
@@ -281,13 +284,15 @@ class HybridShardedPlan:
         return torch.cat([b[:s] for b, s in zip(bufs, sizes)])
 
 
-def cell_partition(coords, n: int, parts: int) -> list:
+def cell_partition(coords, n: int, parts: int, cell_overhead: float = 0.0) -> list:
     """Split the rows of one window into `parts` sets of whole grid cells.
 
     coords: (N, q) prescaled window coordinates in [-1/2, 1/2).  A row's cell is
     floor((x + 1/2) n) per axis (the cell whose footprint it spreads into,
     nufft.py:183-186); cells are ordered by linear index (slabs along the first
-    axis) and cut into `parts` contiguous runs with balanced row counts.
+    axis) and cut into `parts` contiguous runs of balanced cost, a cell costing
+    its row count plus `cell_overhead` (per-cell work item prologue and flush,
+    in row equivalents).
     Returns `parts` ascending int64 row-index arrays (some may be empty when
     there are fewer occupied cells than parts).
     """
@@ -302,7 +307,7 @@ def cell_partition(coords, n: int, parts: int) -> list:
         lin = lin * n + t[:, a]
     order = np.argsort(lin, kind="stable")
     cells, starts, counts = np.unique(lin[order], return_index=True, return_counts=True)
-    cum = np.cumsum(counts)
+    cum = np.cumsum(counts + cell_overhead)
     total = int(cum[-1]) if len(cum) else 0
     # cell run p ends at the first cell whose cumulative count reaches (p + 1) / parts
     bounds = [0]
@@ -362,7 +367,8 @@ class CellShardedPlan:
         for k, win in enumerate(wins):
             n = NufftPlan(dims=len(win), m=m, cutoff=kw.get("cutoff", 6),
                           oversampling=kw.get("oversampling", 2.0)).n
-            masks[k, cell_partition(data.features[:, list(window_set.columns(win))], n, Q)[self.pj]] = True
+            masks[k, cell_partition(data.features[:, list(window_set.columns(win))], n, Q,
+                                    CELL_OVERHEAD_ROWS)[self.pj]] = True
         self.rows_per_window = masks.sum(axis=1)
         self.plan = build_plan(spec, WindowSet(wins, d_max=window_set.d_max), preset, data, row_masks=masks, **kw)
 

@@ -27,6 +27,7 @@ from paper_2404_17344_b200.windows import WindowSet  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--worlds", type=int, nargs="+", default=[2, 4, 8])
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--overheads", type=float, nargs="+", default=[0.0, 64.0, 256.0])
 args = ap.parse_args()
 
 wl = configs.config4()
@@ -64,14 +65,14 @@ def hybrid_rank(world, rank):
     return timed(step)
 
 
-def cell_rank(world, rank):
-    G = hybrid_layout(ws.lengths, world)
+def cell_rank(world, rank, G=None):
+    G = G or hybrid_layout(ws.lengths, world)
     Q = world // G
     owned = window_partition(ws.lengths, G)[rank // Q]
     wins = tuple(ws.windows[w] for w in owned)
     masks = np.zeros((len(wins), data.n_rows), dtype=bool)
     for k, win in enumerate(wins):
-        masks[k, cell_partition(data.features[:, list(ws.columns(win))], 64, Q)[rank % Q]] = True
+        masks[k, cell_partition(data.features[:, list(ws.columns(win))], 64, Q, OVH)[rank % Q]] = True
     plan = build_plan(spec, WindowSet(wins, d_max=ws.d_max), "default", data, row_masks=masks)
     op = plan._operator((spec.family,), 1)
     out = [torch.empty((1, data.n_rows), dtype=torch.float64, device="cuda")]
@@ -89,8 +90,10 @@ t1 = timed(lambda: op1.apply(V, o1, [True]))
 res = {"single_gpu_ms": t1}
 for world in args.worlds:
     h = [hybrid_rank(world, r) for r in range(world)]
-    c = [cell_rank(world, r) for r in range(world)]
-    res[str(world)] = {"hybrid_max_ms": max(h), "cell_max_ms": max(c), "ideal_ms": t1 / world,
-                       "hybrid_ranks": [round(x, 4) for x in h], "cell_ranks": [round(x, 4) for x in c]}
+    res[str(world)] = {"hybrid_max_ms": max(h), "ideal_ms": t1 / world, "hybrid_ranks": [round(x, 4) for x in h]}
+    for OVH in args.overheads:
+        c = [cell_rank(world, r) for r in range(world)]
+        res[str(world)][f"cell_ovh{OVH:g}_max_ms"] = max(c)
+        res[str(world)][f"cell_ovh{OVH:g}_ranks"] = [round(x, 4) for x in c]
     torch.cuda.empty_cache()
 print(json.dumps(res))
