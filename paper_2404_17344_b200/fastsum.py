@@ -13,9 +13,12 @@ PRESETS, AccuracyWarning) and runs the product as one stream-ordered GPU
 pipeline per call (libaddkern_b200, ak_op_apply):
 
     bin-sorted real spread of every (window, RHS)            [CUDA, FP64]
-    -> batched cuFFT D2Z per window length
-    -> band multiply by H = Re(c_hat) / psi_hat^2 per coefficient set   [CUDA]
-    -> batched cuFFT Z2D
+    -> band of the forward transform                          [3-D: band-pruned DFT GEMMs
+                                                               on the FP64 tensor cores;
+                                                               1-/2-D: batched cuFFT D2Z]
+    -> multiply by H = Re(c_hat) / psi_hat^2 per coefficient set (fused into the
+       3-D inverse; a band-multiply kernel otherwise)
+    -> inverse transform of the band                          [3-D fused / cuFFT Z2D]
     -> interpolation, scaled and summed over windows          [CUDA, FP64]
 
 For real v the reference's complex pipeline has an imaginary part that is
