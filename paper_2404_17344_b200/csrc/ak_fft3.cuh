@@ -114,23 +114,17 @@ __device__ __forceinline__ void cta_gemm_auto(int M, int N, int K, FA a, FB b, F
 //   FR, FI [m][n]  e^{-i w f(b) x} = FR + i FI                            (forward band rows)
 //   IR, II [n][m]  e^{+i w f(b) x} = IR + i II                            (inverse band columns)
 //   T3 [m][n]   T3[k2][x] = c cos(w k2 x), T3[m/2 + k2][x] = -c sin(w k2 x)
+//   FW [2m][2n]  = [[FR, -FI], [FI, FR]]  (complex forward band DFT as one real matrix)
+//   IW [2n][2m]  = [[IR, -II], [II, IR]]  (complex inverse)
 struct Fft3Tables {
-    const double *T1, *FR, *FI, *IR, *II, *T3;
+    const double *T1, *FR, *FI, *IR, *II, *T3, *FW, *IW;
 };
 
-// complex GEMM operand [[R, -I], [I, R]] (rows: output re | im, k: input re | im) from
-// split R / I twiddle matrices of `rows` x `cols` (row-major, global memory: the tables
-// are shared by every CTA and stay L1/L2-resident)
-struct CplxA {
-    const double* __restrict__ R;
-    const double* __restrict__ I;
-    int rows, cols;
-    __device__ __forceinline__ double operator()(int r, int k) const {
-        const int ro = r >= rows, ki = k >= cols;
-        const int rr = r - ro * rows, kk = k - ki * cols;
-        const double v = __ldg(((ro == ki) ? R : I) + rr * cols + kk);
-        return (ki && !ro) ? -v : v;
-    }
+// real GEMM operand from a row-major global table (L1/L2-resident, shared by all CTAs)
+struct TabA {
+    const double* __restrict__ t;
+    int ld;
+    __device__ __forceinline__ double operator()(int r, int k) const { return __ldg(t + r * ld + k); }
 };
 
 // plane copy global -> shared with 16-byte loads (cols even, ld even)
@@ -164,7 +158,7 @@ k_fft3_fwd12(const double* __restrict__ grids, double* __restrict__ fbuf, Fft3Ta
     __syncthreads();
     double* __restrict__ dst = fbuf + (b * n + x0) * 2 * m * mh;
     cta_gemm_auto(
-        2 * m, mh, 2 * n, CplxA{tb.FR, tb.FI, m, n}, [&](int k, int c) { return X[k * ldX + c]; },
+        2 * m, mh, 2 * n, TabA{tb.FW, 2 * n}, [&](int k, int c) { return X[k * ldX + c]; },
         [&](int r, int c, double v) { dst[r * mh + c] = v; });
 }
 
@@ -188,7 +182,7 @@ k_fft3_fwd0(const double* __restrict__ fbuf, double* __restrict__ band, Fft3Tabl
     __syncthreads();
     double* __restrict__ dst = band + b * 2 * (int64_t)m * m * mh;
     cta_gemm_auto(
-        2 * m, mh, 2 * n, CplxA{tb.FR, tb.FI, m, n}, [&](int k, int c) { return X[k * ldX + c]; },
+        2 * m, mh, 2 * n, TabA{tb.FW, 2 * n}, [&](int k, int c) { return X[k * ldX + c]; },
         [&](int r, int c, double v) {
             const int ro = r >= m, b0 = r - ro * m;
             dst[2 * (((int64_t)b0 * m + b1) * mh + c) + ro] = v;
@@ -220,7 +214,7 @@ k_fft3_inv0(const double* __restrict__ band, double* __restrict__ fbuf, Fft3Tabl
     }
     __syncthreads();
     cta_gemm_auto(
-        2 * n, mh, 2 * m, CplxA{tb.IR, tb.II, n, m}, [&](int k, int c) { return Y[k * ldY + c]; },
+        2 * n, mh, 2 * m, TabA{tb.IW, 2 * m}, [&](int k, int c) { return Y[k * ldY + c]; },
         [&](int r, int c, double v) {
             const int ro = r >= n, x0 = r - ro * n;
             fbuf[(((b * n + x0) * 2 + ro) * m + b1) * mh + c] = v;
@@ -241,7 +235,7 @@ k_fft3_inv12(const double* __restrict__ fbuf, double* __restrict__ out, Fft3Tabl
     fft3_copy2(C, ldC, fbuf + (b * n + x0) * 2 * m * mh, 2 * m, mh);
     __syncthreads();
     cta_gemm_auto(
-        2 * n, mh, 2 * m, CplxA{tb.IR, tb.II, n, m}, [&](int k, int c) { return C[k * ldC + c]; },
+        2 * n, mh, 2 * m, TabA{tb.IW, 2 * m}, [&](int k, int c) { return C[k * ldC + c]; },
         [&](int r, int c, double v) { D[r * ldD + c] = v; });
     __syncthreads();
     double* __restrict__ dst = out + (b * n + x0) * n * n;
@@ -269,7 +263,7 @@ inline size_t fft3_smem_max(int n, int m) {
                     std::max(fft3_smem_inv0(n, m), fft3_smem_inv12(n, m)));
 }
 
-// Host: the twiddle tables for (n, m) in one buffer, order T1, FR, FI, IR, II, T3.
+// Host: the twiddle tables for (n, m) in one buffer, order T1, FR, FI, IR, II, T3, FW, IW.
 inline std::vector<double> fft3_host_tables(int n, int m) {
     const int mh = m / 2;
     std::vector<long double> c(n), s(n);
@@ -279,7 +273,7 @@ inline std::vector<double> fft3_host_tables(int n, int m) {
         s[j] = sinl(a);
     }
     auto f = [&](int bi) { return bi < mh ? bi : bi - m + n; };
-    std::vector<double> t((size_t)6 * n * m);
+    std::vector<double> t((size_t)14 * n * m);
     double* T1 = t.data();
     double* FR = T1 + (size_t)n * m;
     double* FI = FR + (size_t)n * m;
@@ -302,6 +296,20 @@ inline std::vector<double> fft3_host_tables(int n, int m) {
             FI[bi * n + x] = (double)-s[j];
             IR[x * m + bi] = (double)c[j];
             II[x * m + bi] = (double)s[j];
+        }
+    double* FW = T3 + (size_t)n * m;          // [2m][2n]
+    double* IW = FW + (size_t)4 * n * m;      // [2n][2m]
+    for (int r = 0; r < 2 * m; ++r)
+        for (int k = 0; k < 2 * n; ++k) {
+            const int ro = r >= m, ki = k >= n, rr = r - ro * m, kk = k - ki * n;
+            const double v = (ro == ki) ? FR[rr * n + kk] : FI[rr * n + kk];
+            FW[r * 2 * n + k] = (ki && !ro) ? -v : v;
+        }
+    for (int r = 0; r < 2 * n; ++r)
+        for (int k = 0; k < 2 * m; ++k) {
+            const int ro = r >= n, ki = k >= m, rr = r - ro * n, kk = k - ki * m;
+            const double v = (ro == ki) ? IR[rr * m + kk] : II[rr * m + kk];
+            IW[r * 2 * m + k] = (ki && !ro) ? -v : v;
         }
     return t;
 }

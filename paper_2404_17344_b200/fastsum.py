@@ -501,7 +501,7 @@ class MixedKernelPlan:
 
 def build_mixed_plan(specs, window_set: WindowSet, preset, data: Dataset, cutoff: int = 6,
                      oversampling: float = 2.0, window: str = "kaiser_bessel",
-                     features_device=None) -> MixedKernelPlan:
+                     features_device=None, row_masks=None) -> MixedKernelPlan:
     specs = tuple(specs)
     if len(specs) != len(window_set):
         raise ValueError("need one KernelSpec per window")

@@ -213,3 +213,28 @@ def test_empty_dataset_rejected_like_the_reference():
 
     with pytest.raises(EmptyDatasetError):
         D.Dataset(np.zeros((0, 5)), np.zeros(0), tuple(f"x{i}" for i in range(5)), scaling_state=D.PRESCALED, d_max=3)
+
+
+def test_plan_builders_reach_the_device_layer():
+    """Every plan builder's host side runs up to the device allocation (a CPU-only
+    host stops there): catches argument plumbing errors without a GPU."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("covered by the GPU tests")
+    from paper_2404_17344_b200 import distributed as DI
+
+    ds = D.Dataset(np.random.default_rng(0).uniform(-0.1, 0.1, size=(50, 3)), np.zeros(50), ("a", "b", "c"),
+                   scaling_state=D.PRESCALED, d_max=2)
+    ws = W.WindowSet(((1, 2), (3,)), d_max=2)
+    spec = K.KernelSpec("gauss", 0.5)
+    masks = np.ones((2, 50), dtype=bool)
+    calls = [lambda: FS.build_plan(spec, ws, "default", ds),
+             lambda: FS.build_plan(spec, ws, "default", ds, row_masks=masks),
+             lambda: FS.build_mixed_plan([spec, K.KernelSpec("matern12", 0.3)], ws, "default", ds),
+             lambda: FS.build_mixed_plan([spec, spec], ws, "default", ds, row_masks=masks)]
+    for call in calls:
+        with pytest.raises(Exception) as err:
+            call()
+        assert not isinstance(err.value, (NameError, TypeError, AttributeError)), err.value
+    assert callable(DI.CellShardedPlan) and callable(DI.cell_partition)
