@@ -29,7 +29,16 @@
 
 namespace ak {
 
-constexpr int FFT3_THREADS = 256;
+#ifndef AK_FFT3_ALIAS
+#define AK_FFT3_ALIAS 1
+#endif
+#ifndef AK_FFT3_THREADS
+#define AK_FFT3_THREADS 128
+#endif
+#ifndef AK_FFT3_MINB
+#define AK_FFT3_MINB 6
+#endif
+constexpr int FFT3_THREADS = AK_FFT3_THREADS;
 
 // row strides (doubles) that keep the m8n8k4 fragment loads conflict-free:
 // A operands (8 rows x 4 k) want ld = 4 (mod 16), B operands (4 k x 8 cols) ld = 8 (mod 16)
@@ -98,6 +107,53 @@ __device__ __forceinline__ void cta_gemm(int M, int N, int K, FA a, FB b, FS st)
     }
 }
 
+// As cta_gemm<2, 2>, but every warp keeps its (at most NB) result blocks in registers
+// and the CTA synchronises before any store: the output may overwrite the operands.
+template <int NB, class FA, class FB, class FS>
+__device__ __forceinline__ void cta_gemm_hold(int M, int N, int K, FA a, FB b, FS st)
+{
+    constexpr int TM = 2, TN = 2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int mt = M / (8 * TM), nt = N / (8 * TN);
+    const int lr = lane >> 2, lk = lane & 3;
+    double acc[NB][TM][TN][2];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+        const int blk = warp + q * nw;
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) acc[q][i][j][0] = acc[q][i][j][1] = 0.0;
+        if (blk >= mt * nt) continue;
+        const int r0 = (blk / nt) * 8 * TM, c0 = (blk % nt) * 8 * TN;
+        for (int k = 0; k < K; k += 4) {
+            double af[TM], bf[TN];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) af[i] = a(r0 + 8 * i + lr, k + lk);
+#pragma unroll
+            for (int j = 0; j < TN; ++j) bf[j] = b(k + lk, c0 + 8 * j + lr);
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) dmma_884(acc[q][i][j][0], acc[q][i][j][1], af[i], bf[j]);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+        const int blk = warp + q * nw;
+        if (blk >= mt * nt) continue;
+        const int r0 = (blk / nt) * 8 * TM, c0 = (blk % nt) * 8 * TN;
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) {
+                st(r0 + 8 * i + lr, c0 + 8 * j + 2 * lk, acc[q][i][j][0]);
+                st(r0 + 8 * i + lr, c0 + 8 * j + 2 * lk + 1, acc[q][i][j][1]);
+            }
+    }
+}
+
 // 2 x 2 tiles per warp when the shape allows it and still feeds every warp, else smaller
 template <class FA, class FB, class FS>
 __device__ __forceinline__ void cta_gemm_auto(int M, int N, int K, FA a, FB b, FS st)
@@ -140,7 +196,7 @@ __device__ __forceinline__ void fft3_copy2(double* dst, int ld, const double* __
 // fbuf (per grid, per plane x0): split complex [2][m][mh] doubles
 // fwd12: grids [nb][n][n][n] real -> fbuf [nb][n(x0)][2][m(b1)][mh]
 template <int n, int m>
-__global__ void __launch_bounds__(FFT3_THREADS, 3)
+__global__ void __launch_bounds__(FFT3_THREADS, AK_FFT3_MINB)
 k_fft3_fwd12(const double* __restrict__ grids, double* __restrict__ fbuf, Fft3Tables tb)
 {
     extern __shared__ __align__(16) double sm[];
@@ -148,13 +204,26 @@ k_fft3_fwd12(const double* __restrict__ grids, double* __restrict__ fbuf, Fft3Ta
     const int64_t b = blockIdx.y;
     const int ldP = fft3_ldA(n), ldX = fft3_ldB(mh);
     double* P = sm;                       // [n][ldP]     (S1 A)
-    double* X = P + n * ldP;              // [2n][ldX]    (S1 out, S2 B)
+#if AK_FFT3_ALIAS
+    double* X = sm;                       // [2n][ldX]    (S1 out over P, S2 B)
+#else
+    double* X = P + n * ldP;
+#endif
     fft3_copy2(P, ldP, grids + (b * n + x0) * n * n, n, n);
     __syncthreads();
     const double* __restrict__ T1 = tb.T1;
+#if AK_FFT3_ALIAS
+    constexpr int NW = FFT3_THREADS / 32, NBLK = (n / 16) * (m / 16);
+    constexpr int NB = (NBLK + NW - 1) / NW;   // S1 blocks per warp (2 x 2 tiles each)
+    static_assert(n % 16 == 0 && m % 16 == 0, "S1 tiling");
+    cta_gemm_hold<NB>(
+        n, m, n, [&](int r, int k) { return P[r * ldP + k]; }, [&](int k, int c) { return __ldg(T1 + k * m + c); },
+        [&](int r, int c, double v) { X[((c & 1) * n + r) * ldX + (c >> 1)] = v; });
+#else
     cta_gemm_auto(
         n, m, n, [&](int r, int k) { return P[r * ldP + k]; }, [&](int k, int c) { return __ldg(T1 + k * m + c); },
         [&](int r, int c, double v) { X[((c & 1) * n + r) * ldX + (c >> 1)] = v; });
+#endif
     __syncthreads();
     double* __restrict__ dst = fbuf + (b * n + x0) * 2 * m * mh;
     cta_gemm_auto(
@@ -164,7 +233,7 @@ k_fft3_fwd12(const double* __restrict__ grids, double* __restrict__ fbuf, Fft3Ta
 
 // fwd0: fbuf [nb][n(x0)][2][m(b1)][mh] -> band [nb][m(b0)][m(b1)][mh] complex
 template <int n, int m>
-__global__ void __launch_bounds__(FFT3_THREADS, 3)
+__global__ void __launch_bounds__(FFT3_THREADS, AK_FFT3_MINB)
 k_fft3_fwd0(const double* __restrict__ fbuf, double* __restrict__ band, Fft3Tables tb)
 {
     extern __shared__ __align__(16) double sm[];
@@ -192,7 +261,7 @@ k_fft3_fwd0(const double* __restrict__ fbuf, double* __restrict__ band, Fft3Tabl
 // inv0: H * band -> fbuf [nb][n(x0)][2][m(b1)][mh]; the multiplier of grid b is
 // H[hsel][(b0 m + b1) mh + k2] with hsel as in k_band_multiply
 template <int n, int m>
-__global__ void __launch_bounds__(FFT3_THREADS, 3)
+__global__ void __launch_bounds__(FFT3_THREADS, AK_FFT3_MINB)
 k_fft3_inv0(const double* __restrict__ band, double* __restrict__ fbuf, Fft3Tables tb, int R,
             const int* __restrict__ gwin, const double* const* __restrict__ H, int hbase, int P, int per_rhs)
 {
@@ -223,7 +292,7 @@ k_fft3_inv0(const double* __restrict__ band, double* __restrict__ fbuf, Fft3Tabl
 
 // inv12: fbuf [nb][n(x0)][2][m][mh] -> grids [nb][n][n][n] real (one block per (x0, grid))
 template <int n, int m>
-__global__ void __launch_bounds__(FFT3_THREADS, 3)
+__global__ void __launch_bounds__(FFT3_THREADS, AK_FFT3_MINB)
 k_fft3_inv12(const double* __restrict__ fbuf, double* __restrict__ out, Fft3Tables tb)
 {
     extern __shared__ __align__(16) double sm[];
@@ -251,7 +320,11 @@ k_fft3_inv12(const double* __restrict__ fbuf, double* __restrict__ out, Fft3Tabl
 
 // dynamic shared memory (bytes) of each kernel
 inline size_t fft3_smem_fwd12(int n, int m) {
+#if AK_FFT3_ALIAS
+    return sizeof(double) * std::max((size_t)n * fft3_ldA(n), (size_t)2 * n * fft3_ldB(m / 2));
+#else
     return sizeof(double) * ((size_t)n * fft3_ldA(n) + (size_t)2 * n * fft3_ldB(m / 2));
+#endif
 }
 inline size_t fft3_smem_fwd0(int n, int m) { return sizeof(double) * (size_t)2 * n * fft3_ldB(m / 2); }
 inline size_t fft3_smem_inv0(int n, int m) { return sizeof(double) * (size_t)2 * m * fft3_ldB(m / 2); }
