@@ -207,7 +207,6 @@ def kernel_roofline(torch, plan, wl, peaks, reps=10):
     lib = _native.lib()
     geom = plan.geometries
     N = plan.n_rows  # this rank's rows (all of them on one GPU)
-    P3 = sum(1 for w in plan.window_set if len(w) == 3)
     T = plan.nufft_plans[3].taps
     V = torch.as_tensor(np.ascontiguousarray(wl.V[:1, :N]), device="cuda").contiguous()
     grids = torch.zeros(geom.canon_total, dtype=torch.float64, device="cuda")
@@ -226,11 +225,14 @@ def kernel_roofline(torch, plan, wl, peaks, reps=10):
         interp()
     t_spread = cuda_time(torch, spread, reps)
     t_interp = cuda_time(torch, interp, reps)
-    flops = 2.0 * T ** 3 * N * P3  # algorithmic: one FMA per tap per point per window
+    # algorithmic: one FMA per tap per point per window (a cell-slab rank's windows hold
+    # only their slab's rows)
+    pw3 = sum(r for w, r in zip(plan.window_set, geom.rows_per_window) if len(w) == 3)
+    flops = 2.0 * T ** 3 * pw3
     fp64 = peaks["fp64_tflops"]
     name, t = ("spread_q3", t_spread) if t_spread >= t_interp else ("interp_q3", t_interp)
     achieved = flops / (t * 1e-3) / 1e12
-    alg_bytes = N * P3 * (24 + 8)  # coordinates + value (spread) / output (interp), compulsory
+    alg_bytes = pw3 * (24 + 8)  # coordinates + value (spread) / output (interp), compulsory
     prof = profiled_traffic(name)
     return {
         "bound": "fp64", "kernel": name, "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",

@@ -276,6 +276,7 @@ class DeviceGeometry:
         self.qs = tuple(int(q) for q in qs)
         self.cols = tuple(tuple(int(c) for c in cs) for cs in cols)
         self.n_points = int(feats.shape[0])
+        self.rows_per_window = (self.n_points,) * P
         if row_masks is None:
             rc = lib.ak_geom_create(self.n, P, qarr, carr, ctypes.c_void_p(feats.data_ptr()), self.n_points,
                                     int(feats.shape[1]), ctypes.byref(window_fn), _stream_ptr(torch),
@@ -286,7 +287,8 @@ class DeviceGeometry:
             if m.shape != (P, self.n_points):
                 raise ValueError("row_masks must have shape (windows, rows)")
             md = torch.as_tensor(m.view(np.uint8), device="cuda")
-            rows_in = (ctypes.c_int64 * P)(*[int(c) for c in m.sum(axis=1)])
+            self.rows_per_window = tuple(int(c) for c in m.sum(axis=1))
+            rows_in = (ctypes.c_int64 * P)(*self.rows_per_window)
             rc = lib.ak_geom_create_masked(self.n, P, qarr, carr, ctypes.c_void_p(feats.data_ptr()), self.n_points,
                                            int(feats.shape[1]), ctypes.c_void_p(md.data_ptr()), rows_in,
                                            ctypes.byref(window_fn), _stream_ptr(torch), ctypes.byref(self._handle))
