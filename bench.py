@@ -235,7 +235,10 @@ def kernel_roofline(torch, plan, wl, peaks, reps=10):
     alg_bytes = pw3 * (24 + 8)  # coordinates + value (spread) / output (interp), compulsory
     prof = profiled_traffic(name)
     return {
-        "bound": "fp64", "kernel": name, "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
+        "bound": "fp64", "bound_note": "FP64 datapath (DFMA spread / FP64-DMMA interp share it): one FMA per tap, "
+                                      "12.9 FLOP per compulsory byte vs a ridge of ~5.6 -- neither HBM- nor "
+                                      "low-precision-tensor-bound; HBM figures below",
+        "kernel": name, "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
         "frac": achieved / fp64, "traffic": prof["bytes"] if prof else None,
         "traffic_source": (f"ncu --set full, {prof['source']} ({prof['kernel'][:40]}); includes the cached "
                            "window-weight stream (288 B/point), see DESIGN.md") if prof else None,
