@@ -165,15 +165,14 @@ __device__ __forceinline__ void cta_gemm_auto(int M, int N, int K, FA a, FB b, F
     else cta_gemm<1, 1>(M, N, K, a, b, st);
 }
 
-// Twiddle tables (one device buffer per operator, built on the host):
-//   T1 [n][m]   T1[x][2k] = cos(w k x), T1[x][2k+1] = -sin(w k x)        (k < m/2)
-//   FR, FI [m][n]  e^{-i w f(b) x} = FR + i FI                            (forward band rows)
-//   IR, II [n][m]  e^{+i w f(b) x} = IR + i II                            (inverse band columns)
-//   T3 [m][n]   T3[k2][x] = c cos(w k2 x), T3[m/2 + k2][x] = -c sin(w k2 x)
-//   FW [2m][2n]  = [[FR, -FI], [FI, FR]]  (complex forward band DFT as one real matrix)
-//   IW [2n][2m]  = [[IR, -II], [II, IR]]  (complex inverse)
+// Twiddle tables (one device buffer per operator, built on the host), w = 2 pi / n,
+// f(b) the frequency of band index b:
+//   T1 [n][m]    T1[x][2k] = cos(w k x), T1[x][2k+1] = -sin(w k x)       (k < m/2)
+//   T3 [m][n]    T3[k2][x] = c cos(w k2 x), T3[m/2 + k2][x] = -c sin(w k2 x)
+//   FW [2m][2n]  [[FR, -FI], [FI, FR]] with FR + i FI = e^{-i w f(b) x}   (forward band DFT)
+//   IW [2n][2m]  [[IR, -II], [II, IR]] with IR + i II = e^{+i w f(b) x}   (inverse)
 struct Fft3Tables {
-    const double *T1, *FR, *FI, *IR, *II, *T3, *FW, *IW;
+    const double *T1, *T3, *FW, *IW;
 };
 
 // real GEMM operand from a row-major global table (L1/L2-resident, shared by all CTAs)
@@ -336,7 +335,7 @@ inline size_t fft3_smem_max(int n, int m) {
                     std::max(fft3_smem_inv0(n, m), fft3_smem_inv12(n, m)));
 }
 
-// Host: the twiddle tables for (n, m) in one buffer, order T1, FR, FI, IR, II, T3, FW, IW.
+// Host: the twiddle tables for (n, m) in one buffer, order T1, T3, FW, IW (10 n m doubles).
 inline std::vector<double> fft3_host_tables(int n, int m) {
     const int mh = m / 2;
     std::vector<long double> c(n), s(n);
@@ -346,13 +345,11 @@ inline std::vector<double> fft3_host_tables(int n, int m) {
         s[j] = sinl(a);
     }
     auto f = [&](int bi) { return bi < mh ? bi : bi - m + n; };
-    std::vector<double> t((size_t)14 * n * m);
+    std::vector<double> t((size_t)10 * n * m);
     double* T1 = t.data();
-    double* FR = T1 + (size_t)n * m;
-    double* FI = FR + (size_t)n * m;
-    double* IR = FI + (size_t)n * m;
-    double* II = IR + (size_t)n * m;
-    double* T3 = II + (size_t)n * m;
+    double* T3 = T1 + (size_t)n * m;
+    double* FW = T3 + (size_t)n * m;          // [2m][2n]
+    double* IW = FW + (size_t)4 * n * m;      // [2n][2m]
     for (int x = 0; x < n; ++x)
         for (int k = 0; k < mh; ++k) {
             const int j = (int)((int64_t)k * x % n);
@@ -365,24 +362,16 @@ inline std::vector<double> fft3_host_tables(int n, int m) {
     for (int bi = 0; bi < m; ++bi)
         for (int x = 0; x < n; ++x) {
             const int j = (int)((int64_t)f(bi) * x % n);
-            FR[bi * n + x] = (double)c[j];
-            FI[bi * n + x] = (double)-s[j];
-            IR[x * m + bi] = (double)c[j];
-            II[x * m + bi] = (double)s[j];
-        }
-    double* FW = T3 + (size_t)n * m;          // [2m][2n]
-    double* IW = FW + (size_t)4 * n * m;      // [2n][2m]
-    for (int r = 0; r < 2 * m; ++r)
-        for (int k = 0; k < 2 * n; ++k) {
-            const int ro = r >= m, ki = k >= n, rr = r - ro * m, kk = k - ki * n;
-            const double v = (ro == ki) ? FR[rr * n + kk] : FI[rr * n + kk];
-            FW[r * 2 * n + k] = (ki && !ro) ? -v : v;
-        }
-    for (int r = 0; r < 2 * n; ++r)
-        for (int k = 0; k < 2 * m; ++k) {
-            const int ro = r >= n, ki = k >= m, rr = r - ro * n, kk = k - ki * m;
-            const double v = (ro == ki) ? IR[rr * m + kk] : II[rr * m + kk];
-            IW[r * 2 * m + k] = (ki && !ro) ? -v : v;
+            const double cr = (double)c[j], sn = (double)s[j];
+            // forward e^{-i..} = cr - i sn: FR = cr, FI = -sn; inverse e^{+i..}: IR = cr, II = sn
+            FW[bi * 2 * n + x] = cr;                 // [re out][re in] =  FR
+            FW[bi * 2 * n + n + x] = sn;             // [re out][im in] = -FI
+            FW[(m + bi) * 2 * n + x] = -sn;          // [im out][re in] =  FI
+            FW[(m + bi) * 2 * n + n + x] = cr;       // [im out][im in] =  FR
+            IW[x * 2 * m + bi] = cr;                 // [re out][re in] =  IR
+            IW[x * 2 * m + m + bi] = -sn;            // [re out][im in] = -II
+            IW[(n + x) * 2 * m + bi] = sn;           // [im out][re in] =  II
+            IW[(n + x) * 2 * m + m + bi] = cr;       // [im out][im in] =  IR
         }
     return t;
 }

@@ -1299,7 +1299,7 @@ struct ak_op {
 static ak::Fft3Tables fft3_tables(const ak_op* op) {
     const size_t nm = (size_t)op->gs->n * op->m;
     const double* t = op->ftab;
-    return ak::Fft3Tables{t, t + nm, t + 2 * nm, t + 3 * nm, t + 4 * nm, t + 5 * nm, t + 6 * nm, t + 10 * nm};
+    return ak::Fft3Tables{t, t + nm, t + 2 * nm, t + 6 * nm};
 }
 
 // fused q = 3 transforms: grids -> compact band spectra (op->band, q = 3 section)
