@@ -20,7 +20,10 @@ decompositions:
   vector).  Balanced for any window mix.  ``exchange="grid"`` all-reduces the
   grids instead (before the FFT).
 
-Both reproduce the single-GPU product up to the order of floating-point sums.
+HybridShardedPlan combines them (window groups x row blocks); CellShardedPlan
+(the bench default) uses window groups x slabs of whole grid cells, so every
+rank keeps the data's full per-cell density.  All reproduce the single-GPU
+product up to the order of floating-point sums.
 """
 
 from __future__ import annotations
