@@ -105,6 +105,45 @@ int ak_geom_create_masked(int32_t n, int32_t P, const int32_t* q, const int32_t*
                           const double* X, int64_t N, int64_t ld,
                           const uint8_t* masks, const int64_t* rows_in,
                           const ak_window_fn* wf, void* stream, ak_geom** out);
+/*
+ * Plan-time kernel selection.  The library never reads the process environment:
+ * every choice below is made at ak_geom_create from the data (cell occupancy,
+ * memory) and can be pinned explicitly with ak_geom_create_ex (tests force each
+ * code path this way; the defaults are the measured-best heuristics).
+ */
+typedef struct ak_tuning {
+    int32_t weight_tables;      /* 1: plan-time tap-weight tables when taps == 12 (default; falls
+                                    back to per-pass window polynomials when they do not fit);
+                                    0: always per-pass polynomials                                   */
+    int32_t cell_items3;        /* 3-D work items: 0 auto (occupancy thresholds below), 1 single
+                                    cells, 2 supercells of 2^3 cells                                  */
+    double  dense_cells3;       /* auto: single-cell 3-D spread items from this many points per
+                                    occupied cell (default 300)                                      */
+    double  dense_cells3_interp;/* auto: single-cell 3-D interpolation items from this many (64)     */
+    int32_t cell_items2;        /* 2-D work items: 0 auto, 1 single cells (tensor-core kernels),
+                                    8 supercells of 8^2 cells (lane kernels)                         */
+    double  dense_cells2;       /* auto: single-cell 2-D items from this many points per cell (2)    */
+    int32_t chunk3;             /* maximum points per 3-D work item: 0 auto, else 64..65536          */
+    int32_t rhs_pair_spread;    /* 1: even RHS counts of dense 3-D windows spread in RHS pairs on
+                                    the FP64 tensor cores (default); 0: one RHS per CTA (DFMA)       */
+    int32_t fused_fft3;         /* 1: band-pruned fused 3-D transforms for (n, m) = (64, 32) /
+                                    (32, 16) (default); 0: cuFFT + band multiply                     */
+    int32_t generic_kernels;    /* 1: one-thread-per-point kernels for every window (cross-check)    */
+} ak_tuning;
+
+/* Fill *t with the defaults ak_geom_create uses. */
+void ak_tuning_default(ak_tuning* t);
+
+/* ak_geom_create_masked with explicit tuning (masks / rows_in may be NULL: all rows). */
+int ak_geom_create_ex(int32_t n, int32_t P, const int32_t* q, const int32_t* cols,
+                      const double* X, int64_t N, int64_t ld,
+                      const uint8_t* masks, const int64_t* rows_in,
+                      const ak_window_fn* wf, const ak_tuning* tuning, void* stream, ak_geom** out);
+
+/* The plan's kernel choices, for diagnostics: a short text such as
+ * "q3: spread cells, interp cells, weights table; q2: cells; q1: supercells 16". */
+const char* ak_geom_describe(const ak_geom* g);
+
 int     ak_geom_destroy(ak_geom* g);
 int64_t ak_geom_num_points(const ak_geom* g);
 int32_t ak_geom_num_windows(const ak_geom* g);
@@ -174,8 +213,14 @@ int ak_op_grids(ak_op* op, double** grids, int64_t* count);
  * point-sharded products with AK_APPLY_SPECTRUM_ONLY / AK_APPLY_FROM_SPECTRUM. */
 int ak_op_band(ak_op* op, double** band, int64_t* count);
 
+#define AK_APPLY_RHS_MINOR    64 /* V and the outputs are row-major with the RHS index fastest:
+                                    V[i*ldv + r], summed out[i*ldo + r], per-window
+                                    out[(w*N + i)*ldo + r] (ldv, ldo >= R).  A point's R values
+                                    share one cache line: the layout the kernels gather / scatter
+                                    in full sectors (the default RHS-major layout is V[r*ldv + i]) */
+
 /*
- *   V          device double[R][ldv]
+ *   V          device double[R][ldv]  (AK_APPLY_RHS_MINOR: double[N][ldv])
  *   H          DEVICE array [C*P] of device pointers to compact band multipliers
  *              (set c, window w at index c*P + w)
  *   scale      device double[C*P] per (set, window) operator scale (fastsum.py:136-138)
@@ -219,6 +264,17 @@ int ak_dense_apply(int32_t family, double ell, double scale, int32_t P, const in
                    const int32_t* cols, const double* Xa, int64_t Na, int64_t lda,
                    const double* Xb, int64_t Nb, int64_t ldb, const double* v,
                    double* out, double* matrix, void* stream);
+
+/*
+ * Per-kernel device timing (diagnostics; off by default, no cost when off).
+ * While enabled, every kernel the library launches is bracketed by a pair of
+ * CUDA events on its stream; ak_prof_report synchronises the device and returns
+ * one line per kernel name: "name<TAB>launches<TAB>total_ms" (the buffer holds
+ * at most `cap` bytes; the return value is the length needed).
+ */
+int ak_prof_enable(int32_t on);
+int ak_prof_reset(void);
+int64_t ak_prof_report(char* buf, int64_t cap);
 
 /* FP64 FMA throughput probe (roofline denominator; MEASURED_PEAKS.json has no FP64 entry).
  * Runs `iters` dependent-chain-free DFMA loops on all SMs; returns achieved TFLOP/s. */

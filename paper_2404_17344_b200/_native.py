@@ -31,6 +31,7 @@ AK_APPLY_FROM_GRIDS = 4
 AK_APPLY_H_PER_RHS = 8
 AK_APPLY_SPECTRUM_ONLY = 16
 AK_APPLY_FROM_SPECTRUM = 32
+AK_APPLY_RHS_MINOR = 64
 
 AK_MAX_TAPS = 16
 AK_MAX_PAIRS = 8
@@ -43,6 +44,8 @@ EXPORTED = (
     "ak_geom_num_items", "ak_geom_grid_elems", "ak_geom_canon_offset", "ak_geom_canon_total",
     "ak_spread", "ak_interp", "ak_op_create", "ak_op_destroy", "ak_op_apply", "ak_op_grids", "ak_op_band",
     "ak_type1_band", "ak_type2_grid", "ak_dense_apply", "ak_probe_fp64", "ak_probe_dmma",
+    "ak_tuning_default", "ak_geom_create_ex", "ak_geom_describe", "ak_prof_enable", "ak_prof_reset",
+    "ak_prof_report",
 )
 
 FAMILY_CODE = {"gauss": 0, "der_gauss": 1, "matern12": 2, "der_matern12": 3}
@@ -55,6 +58,35 @@ class WindowFn(ctypes.Structure):
         ("ce", (ctypes.c_double * AK_NCOEF) * AK_MAX_PAIRS),
         ("co", (ctypes.c_double * AK_NCOEF) * AK_MAX_PAIRS),
     ]
+
+
+class Tuning(ctypes.Structure):
+    """ak_tuning (include/addkern_b200.h): plan-time kernel selection."""
+
+    _fields_ = [
+        ("weight_tables", ctypes.c_int32),
+        ("cell_items3", ctypes.c_int32),
+        ("dense_cells3", ctypes.c_double),
+        ("dense_cells3_interp", ctypes.c_double),
+        ("cell_items2", ctypes.c_int32),
+        ("dense_cells2", ctypes.c_double),
+        ("chunk3", ctypes.c_int32),
+        ("rhs_pair_spread", ctypes.c_int32),
+        ("fused_fft3", ctypes.c_int32),
+        ("generic_kernels", ctypes.c_int32),
+    ]
+
+
+def tuning(**overrides) -> Tuning:
+    """The library's default tuning with the given fields replaced (unknown names raise)."""
+    t = Tuning()
+    lib().ak_tuning_default(ctypes.byref(t))
+    names = {f[0] for f in Tuning._fields_}
+    for k, v in overrides.items():
+        if k not in names:
+            raise ValueError(f"unknown tuning field {k!r}")
+        setattr(t, k, v)
+    return t
 
 
 _c_int = ctypes.c_int
@@ -74,6 +106,14 @@ def _declare(lib: ctypes.CDLL) -> None:
         "ak_geom_create_masked": (_c_int, [_i32, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32), _dp, _i64, _i64,
                                            _dp, ctypes.POINTER(_i64), ctypes.POINTER(WindowFn), _vp,
                                            ctypes.POINTER(_vp)]),
+        "ak_geom_create_ex": (_c_int, [_i32, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32), _dp, _i64, _i64,
+                                       _dp, ctypes.POINTER(_i64), ctypes.POINTER(WindowFn), ctypes.POINTER(Tuning),
+                                       _vp, ctypes.POINTER(_vp)]),
+        "ak_tuning_default": (None, [ctypes.POINTER(Tuning)]),
+        "ak_geom_describe": (ctypes.c_char_p, [_vp]),
+        "ak_prof_enable": (_c_int, [_i32]),
+        "ak_prof_reset": (_c_int, []),
+        "ak_prof_report": (_i64, [ctypes.c_char_p, _i64]),
         "ak_geom_destroy": (_c_int, [_vp]),
         "ak_geom_num_points": (_i64, [_vp]),
         "ak_geom_num_windows": (_i32, [_vp]),
@@ -145,3 +185,33 @@ def check(rc: int, what: str = "") -> None:
 
 def launch_count() -> int:
     return int(lib().ak_launch_count())
+
+
+class KernelTimer:
+    """Per-kernel device time of everything the library launches inside the block
+    (ak_prof_*: CUDA events around each launch on its stream).  Diagnostics only:
+    the events add a little overhead, so timed benchmark regions run without it.
+
+        with KernelTimer() as kt:
+            fast_matvecs(plan, V)
+        kt.report  ->  {"k_spread3c": (launches, total_ms), ...}
+    """
+
+    def __enter__(self):
+        L = lib()
+        L.ak_prof_reset()
+        L.ak_prof_enable(1)
+        self.report = {}
+        return self
+
+    def __exit__(self, *exc):
+        L = lib()
+        L.ak_prof_enable(0)
+        need = int(L.ak_prof_report(None, 0))
+        buf = ctypes.create_string_buffer(max(need, 1))
+        L.ak_prof_report(buf, need)
+        L.ak_prof_reset()
+        for line in buf.value.decode().splitlines():
+            name, cnt, ms = line.split("\t")
+            self.report[name] = (int(cnt), float(ms))
+        return False

@@ -32,6 +32,15 @@ template <> struct SuperCell<2> { static constexpr int S = 8; };
 template <> struct SuperCell<1> { static constexpr int S = 16; };
 
 
+// Element (r, i) of an RHS-indexed array (right-hand sides V or outputs) lives at
+// base + r * rs + i * is: RHS-major (rs = ld, is = 1) or RHS-minor (rs = 1, is = ld),
+// AK_APPLY_RHS_MINOR.  With RHS-minor data the R CTAs of a work item (the RHS index
+// runs fastest in every launch) gather / scatter the R values of a point from one
+// cache line instead of R separate sectors.
+struct Strides {
+    int64_t rs, is;
+};
+
 __device__ __forceinline__ int cell_axis(int32_t packed, int a) { return (packed >> (10 * a)) & 1023; }
 
 // Window weights of one axis: w[a] for the T taps of a point with polynomial

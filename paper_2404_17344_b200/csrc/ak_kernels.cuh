@@ -42,7 +42,7 @@ template <int Q> __host__ __device__ constexpr int ipow(int b) { return Q == 1 ?
 template <int Q, int T>
 __global__ void __launch_bounds__(32)
 k_spread_tile(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
-              const double* __restrict__ V, int64_t ldv,
+              const double* __restrict__ V, Strides vs,
               double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs,
               int n, const ak_window_fn wf)
 {
@@ -62,8 +62,9 @@ k_spread_tile(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
     __shared__ __align__(16) double wst[32][WROW];
     __shared__ int cst[32];
 
-    const WorkItem it = items[blockIdx.x];
-    const int r = blockIdx.y;
+    // the RHS index runs fastest: the nrhs CTAs of one item share its point records in L2
+    const WorkItem it = items[blockIdx.x / nrhs];
+    const int r = blockIdx.x % nrhs;
     const int lane = threadIdx.x;
     const int slot = lane / L;
     const int rl = lane % L;
@@ -83,7 +84,7 @@ k_spread_tile(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
             for (int c = 0; c < P2; ++c) acc[a][b][c] = 0.0;
 
     int cur = -1;
-    const double* __restrict__ Vr = V + (int64_t)r * ldv;
+    const double* __restrict__ Vr = V + (int64_t)r * vs.rs;
     const int end = it.start + it.count;
 
     auto flush = [&](int cell) {
@@ -127,7 +128,7 @@ k_spread_tile(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
         __syncwarp();
         if (lane < nb) {
             const Point p = pts[base + lane];
-            const double val = Vr[p.idx];
+            const double val = Vr[(int64_t)p.idx * vs.is];
             double w[T];
             window_weights<T>(wf, p.s[0], w);
 #pragma unroll
@@ -246,22 +247,22 @@ __global__ void __launch_bounds__(32)
 k_interp_lane(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
               const double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs,
               int n, const ak_window_fn wf, const double* __restrict__ scale,
-              double* __restrict__ out, int64_t ldo, int atomic_out, int64_t wstride)
+              double* __restrict__ out, Strides os, int atomic_out, int64_t wstride)
 {
     constexpr int S = SuperCell<Q>::S;
     constexpr int R = S + T - 1;
     constexpr int TILE = ipow<Q>(R);
     __shared__ double tile[TILE];
 
-    const WorkItem it = items[blockIdx.x];
-    const int r = blockIdx.y;
+    const WorkItem it = items[blockIdx.x / nrhs];
+    const int r = blockIdx.x % nrhs;
     const int lane = threadIdx.x;
     const int sc0 = it.sc & 1023, sc1 = (it.sc >> 10) & 1023;
     const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * ipow<Q>(n);
     load_region<Q, T>(tile, g, n, sc0, sc1, 0, lane);
     __syncwarp();
     const double sc = scale[it.window];
-    double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * ldo;
+    double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * os.rs;
     const int end = it.start + it.count;
     for (int j = it.start + lane; j < end; j += 32) {
         const Point p = pts[j];
@@ -284,7 +285,7 @@ k_interp_lane(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
                 acc = fma(w0[a], s, acc);
             }
         }
-        store_out(o + p.idx, atomic_out, sc * acc);
+        store_out(o + (int64_t)p.idx * os.is, atomic_out, sc * acc);
     }
 }
 
@@ -293,12 +294,12 @@ k_interp_lane(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
 // atomics / loads.  Used for non-default cutoffs; correctness reference for
 // the tiled kernels in the GPU tests.  Launched per window w (points p0..p0+np).
 __global__ void k_spread_generic(const Point* __restrict__ pts, int64_t p0, int64_t np, int q,
-                                 const double* __restrict__ V, int64_t ldv,
+                                 const double* __restrict__ V, Strides vs,
                                  double* __restrict__ g_w /* window w, rhs 0 */, int n,
                                  const ak_window_fn wf);
 __global__ void k_interp_generic(const Point* __restrict__ pts, int64_t p0, int64_t np, int q,
                                  const double* __restrict__ g_w, int n, const ak_window_fn wf,
                                  const double* __restrict__ scale, int w,
-                                 double* __restrict__ out_w /* rhs 0 */, int64_t ldo, int sum_windows);
+                                 double* __restrict__ out_w /* rhs 0 */, Strides os, int sum_windows);
 
 }  // namespace ak

@@ -71,6 +71,99 @@ static int launched() {
     return AK_OK;
 }
 
+// ---------------------------------------------------------------------------
+// per-kernel device timing (ak_prof_*): off by default; when on, each launch site
+// brackets its kernel with two CUDA events on the launching stream.
+
+static std::atomic<bool> g_prof_on{false};
+static std::mutex g_prof_mu;
+struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+};
+static std::vector<ProfRec> g_prof;
+
+struct ProfScope {
+    cudaStream_t st;
+    cudaEvent_t a = nullptr;
+    explicit ProfScope(cudaStream_t s) : st(s) {
+        if (g_prof_on.load(std::memory_order_relaxed) && cudaEventCreate(&a) == cudaSuccess) cudaEventRecord(a, st);
+    }
+    ProfScope(const ProfScope&) = delete;
+    ProfScope& operator=(const ProfScope&) = delete;
+    // after the launch: error check + launch count, then the closing event
+    int done(const char* name, bool counted = false) {
+        const int rc = counted ? AK_OK : launched();
+        close(name);
+        return rc;
+    }
+    void close(const char* name) {
+        if (!a) return;
+        cudaEvent_t b = nullptr;
+        if (cudaEventCreate(&b) == cudaSuccess && cudaEventRecord(b, st) == cudaSuccess) {
+            std::lock_guard<std::mutex> lk(g_prof_mu);
+            g_prof.push_back(ProfRec{name, a, b});
+            a = nullptr;
+        } else if (b) {
+            cudaEventDestroy(b);
+        }
+    }
+    ~ProfScope() {
+        if (a) cudaEventDestroy(a);
+    }
+};
+
+static void prof_clear_locked() {
+    for (auto& r : g_prof) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_prof.clear();
+}
+
+extern "C" int ak_prof_enable(int32_t on) {
+    g_prof_on.store(on != 0);
+    return AK_OK;
+}
+
+extern "C" int ak_prof_reset(void) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (!g_prof.empty()) cudaDeviceSynchronize();
+    prof_clear_locked();
+    return AK_OK;
+}
+
+extern "C" int64_t ak_prof_report(char* buf, int64_t cap) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (!g_prof.empty() && cudaDeviceSynchronize() != cudaSuccess) return fail(AK_ERR_CUDA, "device synchronize failed");
+    std::vector<std::string> names;
+    std::map<std::string, std::pair<int64_t, double>> agg;
+    for (auto& r : g_prof) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) continue;
+        auto it = agg.find(r.name);
+        if (it == agg.end()) {
+            names.push_back(r.name);
+            agg[r.name] = {1, (double)ms};
+        } else {
+            it->second.first += 1;
+            it->second.second += ms;
+        }
+    }
+    std::string out;
+    for (auto& nm : names) {
+        char line[256];
+        snprintf(line, sizeof line, "%s\t%lld\t%.6f\n", nm.c_str(), (long long)agg[nm].first, agg[nm].second);
+        out += line;
+    }
+    if (buf && cap > 0) {
+        const int64_t k = std::min<int64_t>(cap - 1, (int64_t)out.size());
+        memcpy(buf, out.data(), (size_t)k);
+        buf[k] = 0;
+    }
+    return (int64_t)out.size() + 1;
+}
+
 static inline int64_t ipow_rt(int64_t b, int q) {
     int64_t r = 1;
     for (int i = 0; i < q; ++i) r *= b;
@@ -101,12 +194,8 @@ struct ak_geom {
     int64_t iitem_begin3 = 0, iitem_end3 = 0;  // 3-D interpolation items (== spread items unless split)
     // cached 3-D window weights (plan-time table, see ak_q3w.cuh)
     bool cached = false;
-    int batch3 = 16;                    // spread batch (q = 3)
-    int batch3i = 16;                   // interpolation batch (q = 3)
-    int iwarps = 1;                     // warps per CTA of the cached q=3 interp
-    int swarps = 1;                     // warps per CTA of the cached q=3 spread
-    bool vreg = false;                  // RHS value folded in registers (vs a scaling pass)
-    bool imma = true;                   // q=3 interp on FP64 tensor cores (mma.sync m8n8k4; AK_IMMA=0: DFMA)
+    ak_tuning tune{};                   // plan-time kernel selection (ak_geom_create_ex)
+    std::string desc;                   // ak_geom_describe
     double* W3 = nullptr;               // [P3][N][3T]
     CellIdx* CI3 = nullptr;             // [P3][N]
     bool cached2 = false;               // 2-D weight table present (ak_q2c.cuh kernels)
@@ -115,58 +204,18 @@ struct ak_geom {
     int64_t* wshift_d = nullptr;        // per window: (w - rank_q(w)) * N, rank among windows of its q
 };
 
-// AK_WEIGHTS=horner disables the plan-time weight table (weights evaluated per pass).
-static bool weights_cached_default() {
-    const char* e = getenv("AK_WEIGHTS");
-    return !(e && strcmp(e, "horner") == 0);
-}
-// Work items sorted by size, largest first (AK_SORT_ITEMS=0 keeps creation order).
-static bool items_sorted_default() {
-    const char* e = getenv("AK_SORT_ITEMS");
-    return !(e && e[0] == '0');
-}
-
-// Points per staged batch of the cached-weight kernels (AK_BATCH3: 16 or 32; default
-// 32 for single-cell items, whose shared memory is only the weight buffer, else 16).
-static int batch3_default(int sedge3) {
-    const char* e = getenv("AK_BATCH3");
-    if (e && (atoi(e) == 16 || atoi(e) == 32)) return atoi(e);
-    return sedge3 == 1 ? 32 : 16;
-}
-
-// Supercell edge for 3-D windows: 2, 3 or 4 cells (AK_SUPERCELL3 overrides the default 3;
-// measured on B200, config 4: 2 and 3 tie, 4 is ~7% slower).
-// Returns 0 when unset: the plan then chooses 1 (single-cell items) for densely
-// occupied cells and 2 otherwise.
-static int supercell3_default() {
-    const char* e = getenv("AK_SUPERCELL3");
-    const int v = e ? atoi(e) : 0;
-    return (v >= 1 && v <= 4) ? v : 0;
-}
-
-// Mean points per occupied cell above which the 3-D spread / interpolation use
-// single-cell work items (measured on B200 with config-4 data at 125k..2M points).
-static double dense_cell_threshold() {
-    const char* e = getenv("AK_DENSE_CELLS");
-    return e ? atof(e) : 300.0;
-}
-static double dense_cell_threshold_interp() {
-    const char* e = getenv("AK_DENSE_CELLS_INTERP");
-    return e ? atof(e) : 64.0;
-}
-
-// Supercell edge for 2-D windows: AK_SUPERCELL2=1 forces single-cell items (tensor-core
-// kernels, ak_q2c.cuh), 8 the lane-per-point kernels; unset: chosen by occupancy
-// (mean points per occupied cell >= AK_DENSE_CELLS2, default 2; config 2 at ~5 per cell
-// is 2.6x faster with single-cell items).
-static int supercell2_default() {
-    const char* e = getenv("AK_SUPERCELL2");
-    const int v = e ? atoi(e) : 0;
-    return (v == 1 || v == 8) ? v : 0;
-}
-static double dense_cell_threshold2() {
-    const char* e = getenv("AK_DENSE_CELLS2");
-    return e ? atof(e) : 2.0;
+extern "C" void ak_tuning_default(ak_tuning* t) {
+    if (!t) return;
+    t->weight_tables = 1;
+    t->cell_items3 = 0;
+    t->dense_cells3 = 300.0;       // measured on B200, config-4 data at 125k..2M points
+    t->dense_cells3_interp = 64.0;
+    t->cell_items2 = 0;
+    t->dense_cells2 = 2.0;         // config 2 at ~5 points per cell: 2.6x faster with single-cell items
+    t->chunk3 = 0;
+    t->rhs_pair_spread = 1;
+    t->fused_fft3 = 1;
+    t->generic_kernels = 0;
 }
 
 __global__ void k_count_nonzero(const int* __restrict__ counts, int total, int* __restrict__ nz) {
@@ -181,14 +230,10 @@ __global__ void k_count_nonzero(const int* __restrict__ counts, int total, int* 
 // resident CTA slot (SMs x 8), within [64, 2048] (q = 3) / [64, 1024] (q = 2);
 // 2048 for q = 1.  Measured on clustered config-4 data at 30k nodes: the fixed 2048
 // cap left a few 800-point supercell items as the tail (spread 0.140 -> 0.097 ms,
-// interp 0.157 -> 0.082 ms with the adaptive cap).  AK_CHUNK3 overrides q = 3.
-static int chunk_for(int q, int64_t point_windows) {
+// interp 0.157 -> 0.082 ms with the adaptive cap).  ak_tuning::chunk3 pins q = 3.
+static int chunk_for(int q, int64_t point_windows, const ak_tuning& t) {
     if (q == 1) return 2048;
-    if (q == 3) {
-        const char* e = getenv("AK_CHUNK3");
-        const int v = e ? atoi(e) : 0;
-        if (v >= 64 && v <= 65536) return v;
-    }
+    if (q == 3 && t.chunk3 >= 64 && t.chunk3 <= 65536) return t.chunk3;
     static int slots = 0;
     if (!slots) {
         int dev = 0, sms = 0;
@@ -417,7 +462,7 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
 
     AK_CUDA(cudaMalloc(&g->pts, sizeof(Point) * (size_t)std::max<int64_t>(1, N * P)));
     int max_nsc_total = 1;
-    bool cached = g->wf.taps == 12 && N > 0 && weights_cached_default();
+    bool cached = g->wf.taps == 12 && N > 0 && g->tune.weight_tables;
     if (cached) {
         // plan-time weight tables (filled once the points are sorted, below)
         const int64_t P3 = (int64_t)g->windows_of_q[3].size(), P2 = (int64_t)g->windows_of_q[2].size();
@@ -447,7 +492,7 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
     // interpolation from ~64 points per occupied cell, for the spread only from ~300
     // (below that its per-cell register flush costs more than the supercell tile;
     // config-4 data: 210 points per cell at 500k nodes, 427 at 1M).
-    int s3 = supercell3_default();
+    int s3 = (g->tune.cell_items3 == 1 || g->tune.cell_items3 == 2) ? g->tune.cell_items3 : 0;
     if (s3 == 1 && !cached) s3 = 2;  // single-cell kernels exist for the cached-weight path only
     int si3 = s3;
     if (s3 == 0) {
@@ -456,20 +501,20 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
         if (cached && !g->windows_of_q[3].empty() && n <= 256) {
             const int w0 = g->windows_of_q[3][0];
             const double occ = mean_occupancy(X, ld, cols, w0, 3, n, N, st, wmask(w0), win_rows(w0));
-            if (occ >= dense_cell_threshold()) s3 = 1;
-            if (occ >= dense_cell_threshold_interp()) si3 = 1;
+            if (occ >= g->tune.dense_cells3) s3 = 1;
+            if (occ >= g->tune.dense_cells3_interp) si3 = 1;
         }
     }
     if (s3 == 1) si3 = 1;
     if (n > 256) si3 = s3;  // no split item lists for huge grids (see above)
     const bool split3 = (si3 == 1 && s3 != 1);
-    int s2 = supercell2_default();
+    int s2 = (g->tune.cell_items2 == 1 || g->tune.cell_items2 == 8) ? g->tune.cell_items2 : 0;
     if (s2 == 1 && !cached) s2 = 8;
     if (s2 == 0) {
         s2 = 8;
         if (cached && !g->windows_of_q[2].empty() && n <= 4096 &&
             mean_occupancy(X, ld, cols, g->windows_of_q[2][0], 2, n, N, st, wmask(g->windows_of_q[2][0]),
-                           win_rows(g->windows_of_q[2][0])) >= dense_cell_threshold2())
+                           win_rows(g->windows_of_q[2][0])) >= g->tune.dense_cells2)
             s2 = 1;
     }
     g->sedge[2] = s2;
@@ -478,7 +523,7 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
     for (int q = 1; q <= 3; ++q) {
         int64_t pw = 0;   // point-windows of this length (masked rows excluded)
         for (int w : g->windows_of_q[q]) pw += n_in ? n_in[w] : N;
-        g->chunk[q] = chunk_for(q, pw);
+        g->chunk[q] = chunk_for(q, pw, g->tune);
     }
     int64_t tcap = 1;     // per-window item capacity of the staging buffer
     int64_t keyspace = 1; // 3-D sort-key space (cells in supercell order) when split
@@ -541,7 +586,7 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
     };
     // Largest items first (blocks are dispatched in index order: LPT-like tail).
     auto append_sorted = [&](std::vector<WorkItem>& v, int64_t& begin, int64_t& end) {
-        if (v.size() > 1 && items_sorted_default())
+        if (v.size() > 1)
             std::stable_sort(v.begin(), v.end(), [](const WorkItem& a, const WorkItem& b) {
                 if (a.count != b.count) return a.count > b.count;
                 return a.start < b.start;
@@ -659,44 +704,56 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
                 rc = fail(AK_ERR_CUDA, "weight table setup failed");
             }
         }
-        g->batch3 = batch3_default(g->sedge[3]);
-        g->batch3i = batch3_default(g->sedge_i3);
-        const char* iw = getenv("AK_IWARPS");
-        g->iwarps = (iw && atoi(iw) == 2) ? 2 : 1;
-        const char* sw = getenv("AK_SWARPS");
-        g->swarps = (sw && atoi(sw) == 2) ? 2 : 1;
-        const char* im = getenv("AK_IMMA");
-        g->imma = !(im && im[0] == '0');
-        const char* vr = getenv("AK_VREG");
-        g->vreg = vr && vr[0] == '1';
     }
     cudaStreamSynchronize(st);
     return rc;
 }
 
 static int geom_create(int32_t n, int32_t P, const int32_t* q, const int32_t* cols, const double* X, int64_t N,
-                       int64_t ld, const uint8_t* masks, const int64_t* n_in, const ak_window_fn* wf, void* stream,
-                       ak_geom** out);
+                       int64_t ld, const uint8_t* masks, const int64_t* n_in, const ak_window_fn* wf,
+                       const ak_tuning* tuning, void* stream, ak_geom** out);
 
 extern "C" int ak_geom_create(int32_t n, int32_t P, const int32_t* q, const int32_t* cols, const double* X,
                               int64_t N, int64_t ld, const ak_window_fn* wf, void* stream, ak_geom** out)
 {
-    return geom_create(n, P, q, cols, X, N, ld, nullptr, nullptr, wf, stream, out);
+    return geom_create(n, P, q, cols, X, N, ld, nullptr, nullptr, wf, nullptr, stream, out);
+}
+
+static int check_masks(int32_t P, int64_t N, const uint8_t* masks, const int64_t* rows_in) {
+    if (!masks || !rows_in) return fail(AK_ERR_INVALID, "null argument");
+    for (int w = 0; w < P; ++w)
+        if (rows_in[w] < 0 || rows_in[w] > N) return fail(AK_ERR_INVALID, "bad per-window row count");
+    return AK_OK;
 }
 
 extern "C" int ak_geom_create_masked(int32_t n, int32_t P, const int32_t* q, const int32_t* cols, const double* X,
                                      int64_t N, int64_t ld, const uint8_t* masks, const int64_t* rows_in,
                                      const ak_window_fn* wf, void* stream, ak_geom** out)
 {
-    if (!masks || !rows_in) return fail(AK_ERR_INVALID, "null argument");
-    for (int w = 0; w < P; ++w)
-        if (rows_in[w] < 0 || rows_in[w] > N) return fail(AK_ERR_INVALID, "bad per-window row count");
-    return geom_create(n, P, q, cols, X, N, ld, masks, rows_in, wf, stream, out);
+    AK_TRY(check_masks(P, N, masks, rows_in));
+    return geom_create(n, P, q, cols, X, N, ld, masks, rows_in, wf, nullptr, stream, out);
+}
+
+extern "C" int ak_geom_create_ex(int32_t n, int32_t P, const int32_t* q, const int32_t* cols, const double* X,
+                                 int64_t N, int64_t ld, const uint8_t* masks, const int64_t* rows_in,
+                                 const ak_window_fn* wf, const ak_tuning* tuning, void* stream, ak_geom** out)
+{
+    if ((masks == nullptr) != (rows_in == nullptr)) return fail(AK_ERR_INVALID, "masks and rows_in go together");
+    if (masks) AK_TRY(check_masks(P, N, masks, rows_in));
+    if (tuning) {
+        const ak_tuning& t = *tuning;
+        if ((t.cell_items3 != 0 && t.cell_items3 != 1 && t.cell_items3 != 2) ||
+            (t.cell_items2 != 0 && t.cell_items2 != 1 && t.cell_items2 != 8) ||
+            (t.chunk3 != 0 && (t.chunk3 < 64 || t.chunk3 > 65536)) || !(t.dense_cells3 >= 0.0) ||
+            !(t.dense_cells3_interp >= 0.0) || !(t.dense_cells2 >= 0.0))
+            return fail(AK_ERR_INVALID, "bad tuning value");
+    }
+    return geom_create(n, P, q, cols, X, N, ld, masks, rows_in, wf, tuning, stream, out);
 }
 
 static int geom_create(int32_t n, int32_t P, const int32_t* q, const int32_t* cols, const double* X, int64_t N,
-                       int64_t ld, const uint8_t* masks, const int64_t* n_in, const ak_window_fn* wf, void* stream,
-                       ak_geom** out)
+                       int64_t ld, const uint8_t* masks, const int64_t* n_in, const ak_window_fn* wf,
+                       const ak_tuning* tuning, void* stream, ak_geom** out)
 {
     if (!out || !q || !cols || !wf) return fail(AK_ERR_INVALID, "null argument");
     *out = nullptr;
@@ -719,6 +776,8 @@ static int geom_create(int32_t n, int32_t P, const int32_t* q, const int32_t* co
     g->rows_in.assign(P, N);
     if (n_in) g->rows_in.assign(n_in, n_in + P);
     g->wf = *wf;
+    if (tuning) g->tune = *tuning;
+    else ak_tuning_default(&g->tune);
     if (wf->taps == 12) {
         bool zero = true;
         for (int k = 0; k < AK_NCOEF; ++k) zero = zero && wf->ce[0][k] == 0.0 && wf->co[0][k] == 0.0;
@@ -731,9 +790,21 @@ static int geom_create(int32_t n, int32_t P, const int32_t* q, const int32_t* co
         g_err = keep;
         return rc;
     }
+    {
+        char buf[256];
+        const bool has3 = !g->windows_of_q[3].empty(), has2 = !g->windows_of_q[2].empty();
+        snprintf(buf, sizeof buf, "q3: spread %s, interp %s, %s; q2: %s%s; taps %d%s",
+                 !has3 ? "-" : (g->sedge[3] == 1 ? "cells" : "supercells 2"),
+                 !has3 ? "-" : (g->sedge_i3 == 1 ? "cells" : "supercells 2"),
+                 g->cached ? "weight table" : "polynomials", !has2 ? "-" : (g->sedge[2] == 1 ? "cells" : "supercells 8"),
+                 has2 && g->cached2 ? " (weight table)" : "", g->wf.taps, g->tune.generic_kernels ? "; generic" : "");
+        g->desc = buf;
+    }
     *out = g;
     return AK_OK;
 }
+
+extern "C" const char* ak_geom_describe(const ak_geom* g) { return g ? g->desc.c_str() : ""; }
 
 extern "C" int64_t ak_geom_num_points(const ak_geom* g) { return g ? g->N : -1; }
 extern "C" int32_t ak_geom_num_windows(const ak_geom* g) { return g ? g->P : -1; }
@@ -753,14 +824,14 @@ extern "C" int64_t ak_geom_canon_total(const ak_geom* g) { return g ? g->canon_t
 
 namespace ak {
 __global__ void k_spread_generic(const Point* __restrict__ pts, int64_t p0, int64_t np, int q,
-                                 const double* __restrict__ V, int64_t ldv, double* __restrict__ g_w, int n,
+                                 const double* __restrict__ V, Strides vs, double* __restrict__ g_w, int n,
                                  const ak_window_fn wf)
 {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= np) return;
     const int r = blockIdx.y;
     const Point p = pts[p0 + j];
-    const double v = V[(int64_t)r * ldv + p.idx];
+    const double v = V[(int64_t)r * vs.rs + (int64_t)p.idx * vs.is];
     double* g = g_w + (int64_t)r * (q == 3 ? (int64_t)n * n * n : (q == 2 ? (int64_t)n * n : n));
     const int T = wf.taps;
     double w[3][AK_MAX_TAPS];
@@ -792,7 +863,7 @@ __global__ void k_spread_generic(const Point* __restrict__ pts, int64_t p0, int6
 
 __global__ void k_interp_generic(const Point* __restrict__ pts, int64_t p0, int64_t np, int q,
                                  const double* __restrict__ g_w, int n, const ak_window_fn wf,
-                                 const double* __restrict__ scale, int w, double* __restrict__ out_w, int64_t ldo,
+                                 const double* __restrict__ scale, int w, double* __restrict__ out_w, Strides os,
                                  int sum_windows)
 {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -830,7 +901,7 @@ __global__ void k_interp_generic(const Point* __restrict__ pts, int64_t p0, int6
             acc = fma(wt[0][a], sa, acc);
         }
     }
-    double* o = out_w + (int64_t)r * ldo + p.idx;
+    double* o = out_w + (int64_t)r * os.rs + (int64_t)p.idx * os.is;
     const double v = scale[w] * acc;
     if (sum_windows) red_add(o, v);
     else *o = v;
@@ -838,272 +909,131 @@ __global__ void k_interp_generic(const Point* __restrict__ pts, int64_t p0, int6
 }  // namespace ak
 
 // ---------------------------------------------------------------------------
-// spread / interp dispatch
-
-// AK_FORCE_GENERIC=1 routes every spread/interp through the one-thread-per-point
-// kernels (test hook: cross-checks the tiled kernels).  Read per call.
-static bool force_generic() {
-    const char* e = getenv("AK_FORCE_GENERIC");
-    return e && e[0] == '1';
-}
+// spread / interp dispatch.  Every choice is fixed at plan time (ak_geom::sedge,
+// cached tables, ak_geom::tune); each launcher returns the kernel's name for the
+// per-kernel timing (ak_prof_*).  Grids of every tiled launch are 1-D with the RHS
+// index fastest: unit = item * R + r.
 
 template <int Q, int T>
-static void launch_spread_tile(const ak_geom* g, int64_t i0, int64_t ni, const double* V, int R, int64_t ldv,
-                               double* grids, cudaStream_t st)
+static const char* launch_spread_tile(const ak_geom* g, int64_t i0, int64_t ni, const double* V, Strides vs, int R,
+                                      double* grids, cudaStream_t st)
 {
-    dim3 grid((unsigned)ni, (unsigned)R);
-    k_spread_tile<Q, T><<<grid, 32, 0, st>>>(g->pts, g->items + i0, V, ldv, grids, g->canon_off_d, R, g->n, g->wf);
-}
-
-template <int T, int S>
-static void launch_spread3_ts(const ak_geom* g, int64_t i0, int64_t ni, const double* V, int R, int64_t ldv,
-                              double* grids, cudaStream_t st)
-{
-    dim3 grid((unsigned)ni, (unsigned)R);
-    k_spread3<T, S><<<grid, 32, 0, st>>>(g->pts, g->items + i0, V, ldv, grids, g->canon_off_d, R, g->n, g->wf);
-}
-
-template <int S, int B>
-static void launch_spread3w_sb(const ak_geom* g, int64_t i0, int64_t ni, const double* V, int R, int64_t ldv,
-                               double* grids, cudaStream_t st)
-{
-    dim3 grid((unsigned)ni, (unsigned)R);
-    if (g->vreg)
-        k_spread3w<12, S, B, true><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
-                                                        g->canon_off_d, R, g->n);
-    else
-        k_spread3w<12, S, B, false><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
-                                                         g->canon_off_d, R, g->n);
-}
-
-template <int B>
-static void launch_spread3w_b(const ak_geom* g, int64_t i0, int64_t ni, const double* V, int R, int64_t ldv,
-                              double* grids, cudaStream_t st)
-{
-    switch (g->sedge[3]) {
-        case 2: launch_spread3w_sb<2, B>(g, i0, ni, V, R, ldv, grids, st); break;
-        case 3: launch_spread3w_sb<3, B>(g, i0, ni, V, R, ldv, grids, st); break;
-        default: launch_spread3w_sb<4, B>(g, i0, ni, V, R, ldv, grids, st); break;
-    }
-}
-
-// AK_SPREAD3R=0 keeps even RHS counts on the DFMA tile (k_spread3c)
-static bool spread3r_enabled() {
-    const char* e = getenv("AK_SPREAD3R");
-    return !(e && !strcmp(e, "0"));
+    k_spread_tile<Q, T><<<(unsigned)(ni * R), 32, 0, st>>>(g->pts, g->items + i0, V, vs, grids, g->canon_off_d, R,
+                                                           g->n, g->wf);
+    return Q == 2 ? "k_spread_tile<2>" : "k_spread_tile<1>";
 }
 
 template <int T>
-static void launch_spread3_t(const ak_geom* g, int64_t i0, int64_t ni, const double* V, int R, int64_t ldv,
-                             double* grids, cudaStream_t st)
+static const char* launch_spread3_t(const ak_geom* g, int64_t i0, int64_t ni, const double* V, Strides vs, int R,
+                                    double* grids, cudaStream_t st)
 {
-    if (T == 12 && g->cached && g->sedge[3] == 1 && !g->trim3 && R % 2 == 0 && spread3r_enabled()) {
-        // pairs of RHS on the FP64 tensor cores (ak_q3r.cuh)
-        k_spread3r<32><<<(unsigned)(ni * (R / 2)), 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv,
-                                                                grids, g->canon_off_d, R, g->n);
-        return;
-    }
-    if (T == 12 && g->cached && g->sedge[3] == 1) {
-        const unsigned grid = (unsigned)(ni * R);  // item-major, RHS fastest
-        if (g->batch3 == 32 && g->trim3)
-            k_spread3c<32, 10><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
-                                                    g->canon_off_d, R, g->n);
-        else if (g->batch3 == 32)
-            k_spread3c<32><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
-                                                g->canon_off_d, R, g->n);
-        else
-            k_spread3c<16><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
-                                                g->canon_off_d, R, g->n);
-        return;
-    }
-    if (T == 12 && g->cached && g->swarps == 2) {
-        dim3 grid((unsigned)ni, (unsigned)R);
-        switch (g->sedge[3]) {
-            case 2:
-                k_spread3w2<12, 2><<<grid, 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
-                                                        g->canon_off_d, R, g->n);
-                break;
-            case 3:
-                k_spread3w2<12, 3><<<grid, 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
-                                                        g->canon_off_d, R, g->n);
-                break;
-            default:
-                k_spread3w2<12, 4><<<grid, 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, ldv, grids,
-                                                        g->canon_off_d, R, g->n);
-                break;
+    const unsigned units = (unsigned)(ni * R);
+    if constexpr (T == 12) {
+        if (g->cached && g->sedge[3] == 1) {
+            if (!g->trim3 && R % 2 == 0 && g->tune.rhs_pair_spread) {
+                // pairs of RHS on the FP64 tensor cores (ak_q3r.cuh)
+                k_spread3r<32><<<(unsigned)(ni * (R / 2)), 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V,
+                                                                        vs, grids, g->canon_off_d, R, g->n);
+                return "k_spread3r";
+            }
+            if (g->trim3) {
+                k_spread3c<32, 10><<<units, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, vs, grids,
+                                                         g->canon_off_d, R, g->n);
+                return "k_spread3c<10>";
+            }
+            k_spread3c<32><<<units, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, vs, grids,
+                                                 g->canon_off_d, R, g->n);
+            return "k_spread3c";
         }
-        return;
+        if (g->cached) {
+            k_spread3w<12, 2, 16><<<units, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, vs, grids,
+                                                        g->canon_off_d, R, g->n);
+            return "k_spread3w";
+        }
     }
-    if (T == 12 && g->cached) {
-        if (g->batch3 == 16) launch_spread3w_b<16>(g, i0, ni, V, R, ldv, grids, st);
-        else launch_spread3w_b<32>(g, i0, ni, V, R, ldv, grids, st);
-        return;
-    }
-    switch (g->sedge[3]) {
-        case 2: launch_spread3_ts<T, 2>(g, i0, ni, V, R, ldv, grids, st); break;
-        case 3: launch_spread3_ts<T, 3>(g, i0, ni, V, R, ldv, grids, st); break;
-        default: launch_spread3_ts<T, 4>(g, i0, ni, V, R, ldv, grids, st); break;
-    }
+    k_spread3<T, 2><<<units, 32, 0, st>>>(g->pts, g->items + i0, V, vs, grids, g->canon_off_d, R, g->n, g->wf);
+    return "k_spread3";
 }
 
-static void launch_spread3(const ak_geom* g, int64_t i0, int64_t ni, const double* V, int R, int64_t ldv,
-                           double* grids, cudaStream_t st)
-{
-    switch (g->wf.taps) {
-        case 12: launch_spread3_t<12>(g, i0, ni, V, R, ldv, grids, st); break;
-        case 8: launch_spread3_t<8>(g, i0, ni, V, R, ldv, grids, st); break;
-        default: launch_spread3_t<4>(g, i0, ni, V, R, ldv, grids, st); break;
-    }
-}
-
-static int spread_group(const ak_geom* g, int q, const double* V, int R, int64_t ldv, double* grids, cudaStream_t st) {
+static int spread_group(const ak_geom* g, int q, const double* V, Strides vs, int R, double* grids, cudaStream_t st) {
     const int64_t i0 = g->item_begin[q], ni = g->item_end[q] - g->item_begin[q];
     if (g->windows_of_q[q].empty() || g->N == 0) return AK_OK;
     const int T = g->wf.taps;
-    bool done = false;
-    if (!force_generic() && ni == 0) return AK_OK;   // only row-masked windows have no items
-    if (!force_generic() && ni > 0) {
-        done = true;
-        if (q == 3 && (T == 12 || T == 8 || T == 4)) launch_spread3(g, i0, ni, V, R, ldv, grids, st);
-        else if (q == 2 && T == 12 && g->cached2 && g->sedge[2] == 1)
-            k_spread2c<32><<<(unsigned)(ni * R), 32, 0, st>>>(g->CI2, g->W2, g->wshift_d, g->items + i0, V,
-                                                                           ldv, grids, g->canon_off_d, R, g->n);
-        else if (q == 2 && T == 12) launch_spread_tile<2, 12>(g, i0, ni, V, R, ldv, grids, st);
-        else if (q == 2 && T == 8) launch_spread_tile<2, 8>(g, i0, ni, V, R, ldv, grids, st);
-        else if (q == 2 && T == 16) launch_spread_tile<2, 16>(g, i0, ni, V, R, ldv, grids, st);
-        else if (q == 2 && T == 4) launch_spread_tile<2, 4>(g, i0, ni, V, R, ldv, grids, st);
-        else if (q == 1 && T == 12) launch_spread_tile<1, 12>(g, i0, ni, V, R, ldv, grids, st);
-        else if (q == 1 && T == 8) launch_spread_tile<1, 8>(g, i0, ni, V, R, ldv, grids, st);
-        else if (q == 1 && T == 16) launch_spread_tile<1, 16>(g, i0, ni, V, R, ldv, grids, st);
-        else if (q == 1 && T == 4) launch_spread_tile<1, 4>(g, i0, ni, V, R, ldv, grids, st);
-        else done = false;
-        if (done) return launched();
+    const bool generic = g->tune.generic_kernels != 0;
+    if (!generic && ni == 0) return AK_OK;   // only row-masked windows have no items
+    if (!generic) {
+        ProfScope ps(st);
+        const char* name = nullptr;
+        if (q == 3 && T == 12) name = launch_spread3_t<12>(g, i0, ni, V, vs, R, grids, st);
+        else if (q == 3 && T == 8) name = launch_spread3_t<8>(g, i0, ni, V, vs, R, grids, st);
+        else if (q == 3 && T == 4) name = launch_spread3_t<4>(g, i0, ni, V, vs, R, grids, st);
+        else if (q == 2 && T == 12 && g->cached2 && g->sedge[2] == 1) {
+            k_spread2c<32><<<(unsigned)(ni * R), 32, 0, st>>>(g->CI2, g->W2, g->wshift_d, g->items + i0, V, vs, grids,
+                                                              g->canon_off_d, R, g->n);
+            name = "k_spread2c";
+        }
+        else if (q == 2 && T == 12) name = launch_spread_tile<2, 12>(g, i0, ni, V, vs, R, grids, st);
+        else if (q == 2 && T == 8) name = launch_spread_tile<2, 8>(g, i0, ni, V, vs, R, grids, st);
+        else if (q == 2 && T == 16) name = launch_spread_tile<2, 16>(g, i0, ni, V, vs, R, grids, st);
+        else if (q == 2 && T == 4) name = launch_spread_tile<2, 4>(g, i0, ni, V, vs, R, grids, st);
+        else if (q == 1 && T == 12) name = launch_spread_tile<1, 12>(g, i0, ni, V, vs, R, grids, st);
+        else if (q == 1 && T == 8) name = launch_spread_tile<1, 8>(g, i0, ni, V, vs, R, grids, st);
+        else if (q == 1 && T == 16) name = launch_spread_tile<1, 16>(g, i0, ni, V, vs, R, grids, st);
+        else if (q == 1 && T == 4) name = launch_spread_tile<1, 4>(g, i0, ni, V, vs, R, grids, st);
+        if (name) return ps.done(name);
     }
     for (int w : g->windows_of_q[q]) {
         if (g->rows_in[w] == 0) continue;
+        ProfScope ps(st);
         dim3 grid((unsigned)((g->rows_in[w] + 127) / 128), (unsigned)R);
-        k_spread_generic<<<grid, 128, 0, st>>>(g->pts, (int64_t)w * g->N, g->rows_in[w], q, V, ldv,
+        k_spread_generic<<<grid, 128, 0, st>>>(g->pts, (int64_t)w * g->N, g->rows_in[w], q, V, vs,
                                                grids + (int64_t)R * g->canon_off[w], g->n, g->wf);
-        AK_TRY(launched());
+        AK_TRY(ps.done("k_spread_generic"));
     }
     return AK_OK;
 }
 
-template <int T, int S>
-static void launch_interp3_ts(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R,
-                              const double* scale, double* out, int64_t ldo, int atomic_out, int64_t wstride,
-                              cudaStream_t st)
-{
-    dim3 grid((unsigned)ni, (unsigned)R);
-    k_interp3<T, S><<<grid, 32, 0, st>>>(g->pts, g->items + i0, grids, g->canon_off_d, R, g->n, g->wf, scale, out,
-                                         ldo, atomic_out, wstride);
-}
-
-template <int S, int B>
-static void launch_interp3w_sb(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R,
-                               const double* scale, double* out, int64_t ldo, int atomic_out, int64_t wstride,
-                               cudaStream_t st)
-{
-    dim3 grid((unsigned)ni, (unsigned)R);
-    if (g->imma) {
-        // B fragments read from the shared region tile inside the DMMA loop (default;
-        // AK_IMMA_SMEM=0: 54 fragment registers per lane loaded per cell run)
-        const char* sb = getenv("AK_IMMA_SMEM");
-        if (!(sb && sb[0] == '0') && g->iwarps == 1) {
-            k_interp3m<S, B, 1, true><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids,
-                                                           g->canon_off_d, R, g->n, scale, out, ldo, atomic_out,
-                                                           wstride);
-            return;
-        }
-        if (g->iwarps == 2 && B == 16)
-            k_interp3m<S, 16, 2><<<grid, 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids,
-                                                      g->canon_off_d, R, g->n, scale, out, ldo, atomic_out, wstride);
-        else
-            k_interp3m<S, B, 1><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids,
-                                                     g->canon_off_d, R, g->n, scale, out, ldo, atomic_out, wstride);
-        return;
-    }
-    if constexpr (B == 16) {
-        if (g->iwarps == 2) {
-            k_interp3w<12, S, B, 2><<<grid, 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids,
-                                                         g->canon_off_d, R, g->n, scale, out, ldo, atomic_out,
-                                                         wstride);
-            return;
-        }
-    }
-    if (false)
-        k_interp3w<12, S, B, 1><<<grid, 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids,
-                                                     g->canon_off_d, R, g->n, scale, out, ldo, atomic_out, wstride);
-    else
-        k_interp3w<12, S, B, 1><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids,
-                                                     g->canon_off_d, R, g->n, scale, out, ldo, atomic_out, wstride);
-}
-
-template <int B>
-static void launch_interp3w_b(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R,
-                              const double* scale, double* out, int64_t ldo, int atomic_out, int64_t wstride,
-                              cudaStream_t st)
-{
-    switch (g->sedge[3]) {
-        case 2: launch_interp3w_sb<2, B>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
-        case 3: launch_interp3w_sb<3, B>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
-        default: launch_interp3w_sb<4, B>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
-    }
-}
-
 template <int T>
-static void launch_interp3_t(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R,
-                             const double* scale, double* out, int64_t ldo, int atomic_out, int64_t wstride,
-                             cudaStream_t st)
+static const char* launch_interp3_t(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R,
+                                    const double* scale, double* out, Strides os, int atomic_out, int64_t wstride,
+                                    cudaStream_t st)
 {
-    if (T == 12 && g->cached && g->sedge_i3 == 1) {
-        const unsigned grid = (unsigned)(ni * R);  // item-major, RHS fastest
-        if (g->batch3i == 32 && g->trim3)
-            k_interp3c<32, 10><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids,
-                                                    g->canon_off_d, R, g->n, scale, out, ldo, atomic_out, wstride);
-        else if (g->batch3i == 32)
-            k_interp3c<32><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids, g->canon_off_d, R,
-                                                g->n, scale, out, ldo, atomic_out, wstride);
-        else
-            k_interp3c<16><<<grid, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids, g->canon_off_d, R,
-                                                g->n, scale, out, ldo, atomic_out, wstride);
-        return;
+    const unsigned units = (unsigned)(ni * R);
+    if constexpr (T == 12) {
+        if (g->cached && g->sedge_i3 == 1) {
+            if (g->trim3) {
+                k_interp3c<32, 10><<<units, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids,
+                                                         g->canon_off_d, R, g->n, scale, out, os, atomic_out, wstride);
+                return "k_interp3c<10>";
+            }
+            k_interp3c<32><<<units, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids, g->canon_off_d, R,
+                                                 g->n, scale, out, os, atomic_out, wstride);
+            return "k_interp3c";
+        }
+        if (g->cached) {
+            k_interp3m<2, 16><<<units, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids, g->canon_off_d,
+                                                    R, g->n, scale, out, os, atomic_out, wstride);
+            return "k_interp3m";
+        }
     }
-    if (T == 12 && g->cached) {
-        if (g->batch3 == 16) launch_interp3w_b<16>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st);
-        else launch_interp3w_b<32>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st);
-        return;
-    }
-    switch (g->sedge[3]) {
-        case 2: launch_interp3_ts<T, 2>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
-        case 3: launch_interp3_ts<T, 3>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
-        default: launch_interp3_ts<T, 4>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
-    }
-}
-
-static void launch_interp3(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R, const double* scale,
-                           double* out, int64_t ldo, int atomic_out, int64_t wstride, cudaStream_t st)
-{
-    switch (g->wf.taps) {
-        case 12: launch_interp3_t<12>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
-        case 8: launch_interp3_t<8>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
-        default: launch_interp3_t<4>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, wstride, st); break;
-    }
+    k_interp3<T, 2><<<units, 32, 0, st>>>(g->pts, g->items + i0, grids, g->canon_off_d, R, g->n, g->wf, scale, out, os,
+                                          atomic_out, wstride);
+    return "k_interp3";
 }
 
 template <int Q, int T>
-static void launch_interp_lane(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R,
-                               const double* scale, double* out, int64_t ldo, int atomic_out, int64_t wstride,
-                               cudaStream_t st)
+static const char* launch_interp_lane(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R,
+                                      const double* scale, double* out, Strides os, int atomic_out, int64_t wstride,
+                                      cudaStream_t st)
 {
-    dim3 grid((unsigned)ni, (unsigned)R);
-    k_interp_lane<Q, T><<<grid, 32, 0, st>>>(g->pts, g->items + i0, grids, g->canon_off_d, R, g->n, g->wf, scale,
-                                             out, ldo, atomic_out, wstride);
+    k_interp_lane<Q, T><<<(unsigned)(ni * R), 32, 0, st>>>(g->pts, g->items + i0, grids, g->canon_off_d, R, g->n, g->wf,
+                                                           scale, out, os, atomic_out, wstride);
+    return Q == 2 ? "k_interp_lane<2>" : "k_interp_lane<1>";
 }
 
 // out(w) = out + (sum_windows ? 0 : w * wstride); atomic_out: RED instead of store
 static int interp_group(const ak_geom* g, int q, const double* grids, int R, const double* scale, double* out,
-                        int64_t ldo, int sum_windows, int atomic_out, int64_t wstride, cudaStream_t st)
+                        Strides os, int sum_windows, int atomic_out, int64_t wstride, cudaStream_t st)
 {
     // 3-D windows may interpolate over their own (single-cell) item list
     const int64_t i0 = q == 3 ? g->iitem_begin3 : g->item_begin[q];
@@ -1111,31 +1041,34 @@ static int interp_group(const ak_geom* g, int q, const double* grids, int R, con
     if (g->windows_of_q[q].empty() || g->N == 0) return AK_OK;
     const int T = g->wf.taps;
     const int64_t ws = sum_windows ? 0 : wstride;
-    bool done = false;
-    if (!force_generic() && ni == 0) return AK_OK;   // only row-masked windows have no items
-    if (!force_generic() && ni > 0) {
-        done = true;
-        if (q == 3 && (T == 12 || T == 8 || T == 4))
-            launch_interp3(g, i0, ni, grids, R, scale, out, ldo, atomic_out, ws, st);
-        else if (q == 2 && T == 12 && g->cached2 && g->sedge[2] == 1)
-            k_interp2c<32><<<(unsigned)(ni * R), 32, 0, st>>>(g->CI2, g->W2, g->wshift_d, g->items + i0,
-                                                                           grids, g->canon_off_d, R, g->n, scale, out,
-                                                                           ldo, atomic_out, ws);
+    const bool generic = g->tune.generic_kernels != 0;
+    if (!generic && ni == 0) return AK_OK;   // only row-masked windows have no items
+    if (!generic) {
+        ProfScope ps(st);
+        const char* name = nullptr;
+        if (q == 3 && T == 12) name = launch_interp3_t<12>(g, i0, ni, grids, R, scale, out, os, atomic_out, ws, st);
+        else if (q == 3 && T == 8) name = launch_interp3_t<8>(g, i0, ni, grids, R, scale, out, os, atomic_out, ws, st);
+        else if (q == 3 && T == 4) name = launch_interp3_t<4>(g, i0, ni, grids, R, scale, out, os, atomic_out, ws, st);
+        else if (q == 2 && T == 12 && g->cached2 && g->sedge[2] == 1) {
+            k_interp2c<32><<<(unsigned)(ni * R), 32, 0, st>>>(g->CI2, g->W2, g->wshift_d, g->items + i0, grids,
+                                                              g->canon_off_d, R, g->n, scale, out, os, atomic_out, ws);
+            name = "k_interp2c";
+        }
 #define AK_LANE(QQ, TT) \
-        else if (q == QQ && T == TT) launch_interp_lane<QQ, TT>(g, i0, ni, grids, R, scale, out, ldo, atomic_out, ws, st);
+        else if (q == QQ && T == TT) name = launch_interp_lane<QQ, TT>(g, i0, ni, grids, R, scale, out, os, atomic_out, ws, st);
         AK_LANE(2, 4) AK_LANE(2, 6) AK_LANE(2, 8) AK_LANE(2, 10) AK_LANE(2, 12) AK_LANE(2, 14) AK_LANE(2, 16)
         AK_LANE(1, 4) AK_LANE(1, 6) AK_LANE(1, 8) AK_LANE(1, 10) AK_LANE(1, 12) AK_LANE(1, 14) AK_LANE(1, 16)
 #undef AK_LANE
-        else done = false;
-        if (done) return launched();
+        if (name) return ps.done(name);
     }
     for (int w : g->windows_of_q[q]) {
         if (g->rows_in[w] == 0) continue;
+        ProfScope ps(st);
         dim3 grid((unsigned)((g->rows_in[w] + 127) / 128), (unsigned)R);
         k_interp_generic<<<grid, 128, 0, st>>>(g->pts, (int64_t)w * g->N, g->rows_in[w], q,
                                                grids + (int64_t)R * g->canon_off[w],
-                                               g->n, g->wf, scale, w, out + (int64_t)w * ws, ldo, atomic_out);
-        AK_TRY(launched());
+                                               g->n, g->wf, scale, w, out + (int64_t)w * ws, os, atomic_out);
+        AK_TRY(ps.done("k_interp_generic"));
     }
     return AK_OK;
 }
@@ -1148,21 +1081,23 @@ static int check_rhs(const ak_geom* g, int R) {
 }
 
 extern "C" int ak_spread(const ak_geom* g, const double* V, int32_t R, int64_t ldv, double* grids, void* stream) {
-    if (!g || R < 1 || (g->N > 0 && (!V || !grids))) return fail(AK_ERR_INVALID, "bad spread arguments");
+    if (!g || R < 1 || (g->N > 0 && (!V || !grids)) || ldv < g->N) return fail(AK_ERR_INVALID, "bad spread arguments");
     AK_TRY(check_rhs(g, R));
     cudaStream_t st = (cudaStream_t)stream;
-    for (int q = 3; q >= 1; --q) AK_TRY(spread_group(g, q, V, R, ldv, grids, st));
+    for (int q = 3; q >= 1; --q) AK_TRY(spread_group(g, q, V, Strides{ldv, 1}, R, grids, st));
     return AK_OK;
 }
 
 extern "C" int ak_interp(const ak_geom* g, const double* grids, int32_t R, const double* scale, double* out,
                          int64_t ldo, int32_t sum_windows, int64_t wstride, void* stream)
 {
-    if (!g || R < 1 || !scale || (g->N > 0 && (!grids || !out))) return fail(AK_ERR_INVALID, "bad interp arguments");
+    if (!g || R < 1 || !scale || (g->N > 0 && (!grids || !out)) || ldo < g->N)
+        return fail(AK_ERR_INVALID, "bad interp arguments");
     AK_TRY(check_rhs(g, R));
     cudaStream_t st = (cudaStream_t)stream;
     for (int q = 3; q >= 1; --q)
-        AK_TRY(interp_group(g, q, grids, R, scale, out, ldo, sum_windows, sum_windows ? 1 : 0, wstride, st));
+        AK_TRY(interp_group(g, q, grids, R, scale, out, Strides{ldo, 1}, sum_windows, sum_windows ? 1 : 0, wstride,
+                            st));
     return AK_OK;
 }
 
@@ -1244,8 +1179,8 @@ __global__ void k_band_pack(double2* __restrict__ spec, double2* __restrict__ ba
 }
 
 // The fused 3-D transform stage is compiled for the default and rough presets at the
-// default oversampling (n, m) = (64, 32), (32, 16); other shapes and AK_FFT3=cufft use
-// the full cuFFT transforms.
+// default oversampling (n, m) = (64, 32), (32, 16); other shapes (and a geometry with
+// ak_tuning::fused_fft3 = 0) use the full cuFFT transforms.
 template <int n, int m>
 static void fft3_attrs() {
     cudaFuncSetAttribute(ak::k_fft3_fwd12<n, m>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1258,9 +1193,8 @@ static void fft3_attrs() {
                          (int)ak::fft3_smem_inv12(n, m));
 }
 
-static bool fft3_fused_ok(int n, int m) {
-    const char* e = getenv("AK_FFT3");   // read per operator (tests switch it)
-    if (e && !strcmp(e, "cufft")) return false;
+static bool fft3_fused_ok(const ak_geom* g, int n, int m) {
+    if (!g->tune.fused_fft3) return false;
     if (n == 64 && m == 32) fft3_attrs<64, 32>();
     else if (n == 32 && m == 16) fft3_attrs<32, 16>();
     else return false;
@@ -1307,12 +1241,16 @@ template <int n, int m>
 static int fft3_forward_t(ak_op* op, cudaStream_t st) {
     const unsigned nb = (unsigned)(op->R * op->nwin[3]);
     const ak::Fft3Tables tb = fft3_tables(op);
-    ak::k_fft3_fwd12<n, m><<<dim3(n, nb), ak::FFT3_THREADS, ak::fft3_smem_fwd12(n, m), st>>>(
-        op->grids + op->grid_off[3], op->fbuf, tb);
-    AK_TRY(launched());
+    {
+        ProfScope ps(st);
+        ak::k_fft3_fwd12<n, m><<<dim3(n, nb), ak::FFT3_THREADS, ak::fft3_smem_fwd12(n, m), st>>>(
+            op->grids + op->grid_off[3], op->fbuf, tb);
+        AK_TRY(ps.done("k_fft3_fwd12"));
+    }
+    ProfScope ps(st);
     ak::k_fft3_fwd0<n, m><<<dim3(m, nb), ak::FFT3_THREADS, ak::fft3_smem_fwd0(n, m), st>>>(
         op->fbuf, reinterpret_cast<double*>(op->band + op->band_off[3]), tb);
-    return launched();
+    return ps.done("k_fft3_fwd0");
 }
 
 // fused q = 3: H (set hbase / per RHS) x band spectra -> op->gbuf grids
@@ -1320,13 +1258,17 @@ template <int n, int m>
 static int fft3_inverse_t(ak_op* op, const double* const* H, int hbase, int per_rhs, cudaStream_t st) {
     const unsigned nb = (unsigned)(op->R * op->nwin[3]);
     const ak::Fft3Tables tb = fft3_tables(op);
-    ak::k_fft3_inv0<n, m><<<dim3(m, nb), ak::FFT3_THREADS, ak::fft3_smem_inv0(n, m), st>>>(
-        reinterpret_cast<const double*>(op->band + op->band_off[3]), op->fbuf, tb, op->R, op->gwin_d[3], H, hbase,
-        op->gs->P, per_rhs);
-    AK_TRY(launched());
+    {
+        ProfScope ps(st);
+        ak::k_fft3_inv0<n, m><<<dim3(m, nb), ak::FFT3_THREADS, ak::fft3_smem_inv0(n, m), st>>>(
+            reinterpret_cast<const double*>(op->band + op->band_off[3]), op->fbuf, tb, op->R, op->gwin_d[3], H, hbase,
+            op->gs->P, per_rhs);
+        AK_TRY(ps.done("k_fft3_inv0"));
+    }
+    ProfScope ps(st);
     ak::k_fft3_inv12<n, m><<<dim3(n, nb), ak::FFT3_THREADS, ak::fft3_smem_inv12(n, m), st>>>(
         op->fbuf, op->gbuf + op->grid_off[3], tb);
-    return launched();
+    return ps.done("k_fft3_inv12");
 }
 
 static int fft3_forward(ak_op* op, cudaStream_t st) {
@@ -1376,7 +1318,7 @@ static int op_build(ak_op* op, cudaStream_t st) {
         AK_CUDA(cudaMemcpyAsync(op->gwin_d[q], ws.data(), sizeof(int) * ws.size(), cudaMemcpyHostToDevice, st));
         op->has[q] = true;
         const int batch = op->R * (int)ws.size();
-        if (q == 3 && batch <= 65535 && fft3_fused_ok(n, op->m)) {   // grids on gridDim.y
+        if (q == 3 && batch <= 65535 && fft3_fused_ok(g, n, op->m)) {   // grids on gridDim.y
             op->fused3 = true;
             AK_CUDA(cudaMalloc(&op->fbuf, sizeof(double) * (size_t)batch * n * op->m * op->m));
             const std::vector<double> tabs = ak::fft3_host_tables(n, op->m);
@@ -1451,6 +1393,24 @@ extern "C" int ak_op_band(ak_op* op, double** band, int64_t* count) {
     return AK_OK;
 }
 
+// cuFFT transform of one window-length group, timed as one "kernel" when profiling
+static int cufft_d2z(ak_op* op, int q, cudaStream_t st) {
+    ProfScope ps(st);
+    AK_CUFFT(cufftSetStream(op->fwd[q], st));
+    AK_CUFFT(cufftExecD2Z(op->fwd[q], op->grids + op->grid_off[q], (cufftDoubleComplex*)(op->spec + op->spec_off[q])));
+    g_launches.fetch_add(1);
+    ps.close(q == 3 ? "cufft_d2z<3>" : (q == 2 ? "cufft_d2z<2>" : "cufft_d2z<1>"));
+    return AK_OK;
+}
+
+static int band_pack(ak_op* op, int q, int dir, cudaStream_t st) {
+    ProfScope ps(st);
+    const int64_t total = op->bs[q] * op->R * op->nwin[q];
+    k_band_pack<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(
+        op->spec + op->spec_off[q], op->band + op->band_off[q], q, op->gs->n, op->m, op->hs[q], op->bs[q], total, dir);
+    return ps.done("k_band_pack");
+}
+
 extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double* const* H, const double* scale,
                            double* const* outs, int64_t ldo, const int32_t* sum_windows, int32_t flags,
                            void* stream)
@@ -1461,11 +1421,13 @@ extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double
     const ak_geom* gi = op->gi;
     const int R = op->R, P = gs->P;
     const int accumulate = flags & AK_APPLY_ACCUMULATE;
+    const bool minor = (flags & AK_APPLY_RHS_MINOR) != 0;
     if (!(flags & (AK_APPLY_FROM_GRIDS | AK_APPLY_FROM_SPECTRUM))) {
-        if (ldv < gs->N || (gs->N > 0 && !V)) return fail(AK_ERR_INVALID, "bad right-hand sides");
+        if ((minor ? ldv < R : ldv < gs->N) || (gs->N > 0 && !V)) return fail(AK_ERR_INVALID, "bad right-hand sides");
+        const Strides vs = minor ? Strides{1, ldv} : Strides{ldv, 1};
         AK_CUDA(cudaMemsetAsync(op->grids, 0, sizeof(double) * gs->canon_total * R, st));
         if (gs->N > 0)
-            for (int q = 3; q >= 1; --q) AK_TRY(spread_group(gs, q, V, R, ldv, op->grids, st));
+            for (int q = 3; q >= 1; --q) AK_TRY(spread_group(gs, q, V, vs, R, op->grids, st));
     }
     if (flags & AK_APPLY_SPREAD_ONLY) return AK_OK;
     if (flags & AK_APPLY_SPECTRUM_ONLY) {
@@ -1473,26 +1435,23 @@ extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double
             if (q == 3 && op->fused3) {
                 AK_TRY(fft3_forward(op, st));
             } else if (op->has[q]) {
-                AK_CUFFT(cufftSetStream(op->fwd[q], st));
-                AK_CUFFT(cufftExecD2Z(op->fwd[q], op->grids + op->grid_off[q],
-                                      (cufftDoubleComplex*)(op->spec + op->spec_off[q])));
-                g_launches.fetch_add(1);
-                const int64_t total = op->bs[q] * R * op->nwin[q];
-                k_band_pack<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(
-                    op->spec + op->spec_off[q], op->band + op->band_off[q], q, gs->n, op->m, op->hs[q], op->bs[q],
-                    total, 0);
-                AK_TRY(launched());
+                AK_TRY(cufft_d2z(op, q, st));
+                AK_TRY(band_pack(op, q, 0, st));
             }
         return AK_OK;
     }
     if (!H || !scale || !outs || !sum_windows) return fail(AK_ERR_INVALID, "null argument");
-    if (ldo < gi->N) return fail(AK_ERR_INVALID, "leading dimension too small");
+    if (minor ? ldo < R : ldo < gi->N) return fail(AK_ERR_INVALID, "leading dimension too small");
     if ((flags & AK_APPLY_H_PER_RHS) && op->C != 1) return fail(AK_ERR_INVALID, "per-RHS multipliers need C == 1");
+    // RHS-major: summed out[r*ldo + i], per window out[(w*R + r)*ldo + i];
+    // RHS-minor: summed out[i*ldo + r], per window out[(w*N + i)*ldo + r]
+    const Strides os = minor ? Strides{1, ldo} : Strides{ldo, 1};
+    const int64_t wstride = minor ? gi->N * ldo : (int64_t)R * ldo;
     for (int c = 0; c < op->C; ++c) {
         if (!outs[c]) return fail(AK_ERR_INVALID, "null output");
         if (!accumulate) {
-            const int64_t rows = sum_windows[c] ? R : (int64_t)R * P;
-            AK_CUDA(cudaMemsetAsync(outs[c], 0, sizeof(double) * rows * ldo, st));
+            const int64_t one = minor ? gi->N * ldo : (int64_t)R * ldo;
+            AK_CUDA(cudaMemsetAsync(outs[c], 0, sizeof(double) * one * (sum_windows[c] ? 1 : P), st));
         }
     }
     if (gi->N == 0) return AK_OK;
@@ -1501,17 +1460,8 @@ extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double
             // the band spectrum is the fused stage's intermediate: from-spectrum starts at the inverse
             if (!(flags & AK_APPLY_FROM_SPECTRUM)) AK_TRY(fft3_forward(op, st));
         } else if (op->has[q]) {
-            if (flags & AK_APPLY_FROM_SPECTRUM) {
-                const int64_t total = op->bs[q] * R * op->nwin[q];
-                k_band_pack<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(
-                    op->spec + op->spec_off[q], op->band + op->band_off[q], q, gs->n, op->m, op->hs[q], op->bs[q],
-                    total, 1);
-                AK_TRY(launched());
-                continue;
-            }
-            AK_CUFFT(cufftSetStream(op->fwd[q], st));
-            AK_CUFFT(cufftExecD2Z(op->fwd[q], op->grids + op->grid_off[q], (cufftDoubleComplex*)(op->spec + op->spec_off[q])));
-            g_launches.fetch_add(1);
+            if (flags & AK_APPLY_FROM_SPECTRUM) AK_TRY(band_pack(op, q, 1, st));
+            else AK_TRY(cufft_d2z(op, q, st));
         }
     for (int c = 0; c < op->C; ++c) {
         for (int q = 3; q >= 1; --q) {
@@ -1522,18 +1472,24 @@ extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double
             }
             const int64_t total = op->hs[q] * R * op->nwin[q];
             const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-            k_band_multiply<<<blocks, 256, 0, st>>>(op->spec + op->spec_off[q], op->spec2 + op->spec_off[q], q, gs->n,
-                                                    op->m, R, op->hs[q], total, op->gwin_d[q], H, c * P, P,
-                                                    (flags & AK_APPLY_H_PER_RHS) ? 1 : 0);
-            AK_TRY(launched());
+            {
+                ProfScope ps(st);
+                k_band_multiply<<<blocks, 256, 0, st>>>(op->spec + op->spec_off[q], op->spec2 + op->spec_off[q], q,
+                                                        gs->n, op->m, R, op->hs[q], total, op->gwin_d[q], H, c * P, P,
+                                                        (flags & AK_APPLY_H_PER_RHS) ? 1 : 0);
+                AK_TRY(ps.done("k_band_multiply"));
+            }
+            ProfScope ps(st);
             AK_CUFFT(cufftSetStream(op->inv[q], st));
-            AK_CUFFT(cufftExecZ2D(op->inv[q], (cufftDoubleComplex*)(op->spec2 + op->spec_off[q]), op->gbuf + op->grid_off[q]));
+            AK_CUFFT(cufftExecZ2D(op->inv[q], (cufftDoubleComplex*)(op->spec2 + op->spec_off[q]),
+                                  op->gbuf + op->grid_off[q]));
             g_launches.fetch_add(1);
+            ps.close(q == 3 ? "cufft_z2d<3>" : (q == 2 ? "cufft_z2d<2>" : "cufft_z2d<1>"));
         }
         const int atomic_out = (sum_windows[c] || accumulate) ? 1 : 0;
         for (int q = 3; q >= 1; --q)
-            AK_TRY(interp_group(gi, q, op->gbuf, R, scale + (int64_t)c * P, outs[c], ldo, sum_windows[c], atomic_out,
-                                (int64_t)R * ldo, st));
+            AK_TRY(interp_group(gi, q, op->gbuf, R, scale + (int64_t)c * P, outs[c], os, sum_windows[c], atomic_out,
+                                wstride, st));
     }
     return AK_OK;
 }

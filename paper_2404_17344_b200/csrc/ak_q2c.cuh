@@ -22,7 +22,7 @@ namespace ak {
 template <int B>
 __global__ void __launch_bounds__(32, 16)
 k_spread2c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
-           const WorkItem* __restrict__ items, const double* __restrict__ V, int64_t ldv,
+           const WorkItem* __restrict__ items, const double* __restrict__ V, Strides vs,
            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
 {
     constexpr int T = 12;
@@ -38,7 +38,7 @@ k_spread2c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     const WorkItem it = items[blockIdx.x / nrhs];
     const int r = blockIdx.x % nrhs;
     const int lane = threadIdx.x;
-    const double* __restrict__ Vr = V + (int64_t)r * ldv;
+    const double* __restrict__ Vr = V + (int64_t)r * vs.rs;
     const int nbatch = (it.count + B - 1) / B;
     const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
     const CellIdx* __restrict__ CIit = ci + (it.start - wshift[it.window]);
@@ -55,7 +55,7 @@ k_spread2c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     cp_async_commit();
     cp_async_wait_all();
     __syncwarp();
-    if (lane < min(B, it.count)) cp_async8(&vb[0][lane], Vr + cib[0][lane].idx);
+    if (lane < min(B, it.count)) cp_async8(&vb[0][lane], Vr + (int64_t)cib[0][lane].idx * vs.is);
     cp_async_commit();
 
     const int rn = lane >> 2, kq = lane & 3;
@@ -78,7 +78,7 @@ k_spread2c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
                 fence_proxy_async();
                 tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + B) * RW, (unsigned)(nb1 * RW * 8), &bar[s ^ 1]);
             }
-            if (lane < nb1) cp_async8(&vb[s ^ 1][lane], Vr + cib[(bi + 1) % 3][lane].idx);
+            if (lane < nb1) cp_async8(&vb[s ^ 1][lane], Vr + (int64_t)cib[(bi + 1) % 3][lane].idx * vs.is);
         }
         if (bi + 2 < nbatch && lane < min(B, it.count - off - 2 * B))
             cp_async8(&cib[(bi + 2) % 3][lane], CIit + off + 2 * B + lane);
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(32, 16)
 k_interp2c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ grids,
            const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,
-           double* __restrict__ out, int64_t ldo, int atomic_out, int64_t wstride)
+           double* __restrict__ out, Strides os, int atomic_out, int64_t wstride)
 {
     constexpr int T = 12;
     constexpr int RW = 2 * T;
@@ -171,7 +171,7 @@ k_interp2c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         }
     }
     const double sc = scale[it.window];
-    double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * ldo;
+    double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * os.rs;
     const int pj = lane >> 2, q = lane & 3;
 
     for (int bi = 0; bi < nbatch; ++bi) {
@@ -209,7 +209,7 @@ k_interp2c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
             v += __shfl_xor_sync(0xffffffffu, v, 1);
             v += __shfl_xor_sync(0xffffffffu, v, 2);
             if (q == 0 && valid) {
-                double* dst = o + cib[s][k0 + pj].idx;
+                double* dst = o + (int64_t)cib[s][k0 + pj].idx * os.is;
                 if (atomic_out) red_add(dst, sc * v);
                 else *dst = sc * v;
             }

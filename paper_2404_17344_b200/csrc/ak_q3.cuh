@@ -86,7 +86,7 @@ __device__ __forceinline__ void spread_fma(double (&acc)[P0][P1][P2], const doub
 template <int T, int S>
 __global__ void __launch_bounds__(32, 8)
 k_spread3(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
-          const double* __restrict__ V, int64_t ldv,
+          const double* __restrict__ V, Strides vs,
           double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs,
           int n, const ak_window_fn wf)
 {
@@ -99,12 +99,12 @@ k_spread3(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
     __shared__ __align__(16) double wst[32][WS];
     __shared__ int cst[32];
 
-    const WorkItem it = items[blockIdx.x];
-    const int r = blockIdx.y;
+    const WorkItem it = items[blockIdx.x / nrhs];   // RHS index fastest
+    const int r = blockIdx.x % nrhs;
     const int lane = threadIdx.x;
     const int g0 = lane >> 4, g1 = (lane >> 2) & 3, g2 = lane & 3;
     const int sc0 = it.sc & 1023, sc1 = (it.sc >> 10) & 1023, sc2 = (it.sc >> 20) & 1023;
-    const double* __restrict__ Vr = V + (int64_t)r * ldv;
+    const double* __restrict__ Vr = V + (int64_t)r * vs.rs;
     const int end = it.start + it.count;
 
     for (int i = lane; i < TILE; i += 32) tile[i] = 0.0;
@@ -138,7 +138,7 @@ k_spread3(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
     double vn = 0.0;
     if (lane < min(32, end - it.start)) {
         pn = load_point(pts + it.start + lane);
-        vn = __ldg(Vr + pn.idx);
+        vn = __ldg(Vr + (int64_t)pn.idx * vs.is);
     }
     for (int base = it.start; base < end; base += 32) {
         const int nb = min(32, end - base);
@@ -162,7 +162,7 @@ k_spread3(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
             cst[lane] = (cell_axis(p.cell, 0) - sc0 * S) | ((cell_axis(p.cell, 1) - sc1 * S) << 8) |
                         ((cell_axis(p.cell, 2) - sc2 * S) << 16);
         }
-        if (more) vn = __ldg(Vr + pn.idx);
+        if (more) vn = __ldg(Vr + (int64_t)pn.idx * vs.is);
         __syncwarp();
 
         // bit k set <=> point k starts a new cell run (register-only test in the loop)
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(32, 8)
 k_interp3(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
           const double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs,
           int n, const ak_window_fn wf, const double* __restrict__ scale,
-          double* __restrict__ out, int64_t ldo, int atomic_out, int64_t wstride)
+          double* __restrict__ out, Strides os, int atomic_out, int64_t wstride)
 {
     using LN = Q3Lanes<T>;
     constexpr int P0 = LN::P0, P1 = LN::P1, P2 = LN::P2, WS = LN::WS;
@@ -252,8 +252,8 @@ k_interp3(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
     __shared__ int cst[32];
     __shared__ int ist[32];
 
-    const WorkItem it = items[blockIdx.x];
-    const int r = blockIdx.y;
+    const WorkItem it = items[blockIdx.x / nrhs];   // RHS index fastest
+    const int r = blockIdx.x % nrhs;
     const int lane = threadIdx.x;
     const int g0 = lane >> 4, g1 = (lane >> 2) & 3, g2 = lane & 3;
     const int sc0 = it.sc & 1023, sc1 = (it.sc >> 10) & 1023, sc2 = (it.sc >> 20) & 1023;
@@ -273,7 +273,7 @@ k_interp3(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
         __syncwarp();
     }
     const double sc = scale[it.window];
-    double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * ldo;
+    double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * os.rs;
 
     double tv[P0][P1][P2];
     int cur = -1;
@@ -354,7 +354,7 @@ k_interp3(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
             v += __shfl_xor_sync(0xffffffffu, v, 8);
             v += __shfl_xor_sync(0xffffffffu, v, 16);
             if (lane < 8 && grp + lane < nb) {
-                double* dst = o + ist[grp + lane];
+                double* dst = o + (int64_t)ist[grp + lane] * os.is;
                 if (atomic_out) red_add(dst, sc * v);
                 else *dst = sc * v;
             }

@@ -15,13 +15,6 @@
 #pragma once
 #include "ak_q3m.cuh"
 
-#ifndef AK_FASTPATH
-#define AK_FASTPATH 1
-#endif
-#ifndef AK_SPREAD3C_VREG
-#define AK_SPREAD3C_VREG 1
-#endif
-
 namespace ak {
 
 // 222 registers (no spills) -> 9 warps per SM; __launch_bounds__(32, 8) let ptxas use
@@ -42,7 +35,7 @@ struct alignas(128) Spread3cSmem {
 // skips the zero taps 0 and 11, 5 x 3 x 3 instead of 6 x 3 x 3 accumulators).
 template <int B, int A = 12>
 __device__ __forceinline__ void spread3c_unit(Spread3cSmem<B>& sm, int unit, const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
-           const WorkItem* __restrict__ items, const double* __restrict__ V, int64_t ldv,
+           const WorkItem* __restrict__ items, const double* __restrict__ V, Strides vs,
            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
 {
     constexpr int T = 12;
@@ -61,7 +54,7 @@ __device__ __forceinline__ void spread3c_unit(Spread3cSmem<B>& sm, int unit, con
     const int r = unit % nrhs;
     const int lane = threadIdx.x;
     const int g0 = lane >> 4, g1 = (lane >> 2) & 3, g2 = lane & 3;
-    const double* __restrict__ Vr = V + (int64_t)r * ldv;
+    const double* __restrict__ Vr = V + (int64_t)r * vs.rs;
     const int nbatch = (it.count + B - 1) / B;
     const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
     const CellIdx* __restrict__ CIit = ci + (it.start - wshift[it.window]);
@@ -78,7 +71,7 @@ __device__ __forceinline__ void spread3c_unit(Spread3cSmem<B>& sm, int unit, con
     cp_async_commit();
     cp_async_wait_all();
     __syncwarp();
-    if (lane < min(B, it.count)) cp_async8(&vb[0][lane], Vr + cib[0][lane].idx);
+    if (lane < min(B, it.count)) cp_async8(&vb[0][lane], Vr + (int64_t)cib[0][lane].idx * vs.is);
     cp_async_commit();
 
     double acc[P0][P1][P2];
@@ -102,12 +95,11 @@ __device__ __forceinline__ void spread3c_unit(Spread3cSmem<B>& sm, int unit, con
                 fence_proxy_async();
                 tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + B) * RW, (unsigned)(nb1 * RW * 8), &bar[s ^ 1]);
             }
-            if (lane < nb1) cp_async8(&vb[s ^ 1][lane], Vr + cib[(bi + 1) % 3][lane].idx);
+            if (lane < nb1) cp_async8(&vb[s ^ 1][lane], Vr + (int64_t)cib[(bi + 1) % 3][lane].idx * vs.is);
         }
         if (bi + 2 < nbatch && lane < min(B, it.count - off - 2 * B))
             cp_async8(&cib[(bi + 2) % 3][lane], CIit + off + 2 * B + lane);
         cp_async_commit();
-#if AK_SPREAD3C_VREG
         __syncwarp();
         // v folded into the per-point products in the FMA loop (3 DMUL per point and
         // lane) instead of a per-batch staging pass over the w0 rows
@@ -134,51 +126,10 @@ __device__ __forceinline__ void spread3c_unit(Spread3cSmem<B>& sm, int unit, con
         }
         if (j < nb) spread_fma_v(acc, a0, a1, a2, av);
         __syncwarp();
-#else
-        {
-            constexpr int PER = (B * T + 31) / 32;
-            double x[PER], y[PER];
-#pragma unroll
-            for (int i = 0; i < PER; ++i) {
-                const int e = lane + 32 * i;
-                const int row = e / T;
-                if (row < nb) {
-                    x[i] = wbuf[s][row][e - row * T];
-                    y[i] = vb[s][row];
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < PER; ++i) {
-                const int e = lane + 32 * i;
-                const int row = e / T;
-                if (row < nb) wbuf[s][row][e - row * T] = x[i] * y[i];
-            }
-        }
-        __syncwarp();
-        double a0[P0], a1[P1], a2[P2], b0[P0], b1[P1], b2[P2];
-        auto load = [&](double (&w0)[P0], double (&w1)[P1], double (&w2)[P2], const double* row) {
-#pragma unroll
-            for (int a = 0; a < P0; ++a) w0[a] = row[AO + g0 * P0 + a];
-#pragma unroll
-            for (int b = 0; b < P1; ++b) w1[b] = row[T + g1 * P1 + b];
-#pragma unroll
-            for (int c = 0; c < P2; ++c) w2[c] = row[2 * T + g2 * P2 + c];
-        };
-        load(a0, a1, a2, &wbuf[s][0][0]);
-        int j = 0;
-        for (; j + 1 < nb; j += 2) {
-            load(b0, b1, b2, &wbuf[s][j + 1][0]);
-            spread_fma(acc, a0, a1, a2);
-            load(a0, a1, a2, &wbuf[s][j + 2 < nb ? j + 2 : j + 1][0]);
-            spread_fma(acc, b0, b1, b2);
-        }
-        if (j < nb) spread_fma(acc, a0, a1, a2);
-#endif
     }
 
     const int c0 = it.sc & 1023, c1 = (it.sc >> 10) & 1023, c2 = (it.sc >> 20) & 1023;
     double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
-#if AK_FASTPATH
     const int o0 = c0 - (T / 2 - 1), o1 = c1 - (T / 2 - 1), o2 = c2 - (T / 2 - 1);
     if (o0 >= 0 && o0 + T <= n && o1 >= 0 && o1 + T <= n && o2 >= 0 && o2 + T <= n) {
         // footprint inside the grid (no periodic wrap): one base pointer, constant strides
@@ -192,7 +143,6 @@ __device__ __forceinline__ void spread3c_unit(Spread3cSmem<B>& sm, int unit, con
                 for (int c = 0; c < P2; ++c) red_add(base + a * nn + b * n + c, acc[a][b][c]);
         return;
     }
-#endif
     {
         // flush the register tile straight to the grid (a shared-memory staged, row-
         // coalesced flush measured 3% slower on B200)
@@ -219,11 +169,11 @@ __device__ __forceinline__ void spread3c_unit(Spread3cSmem<B>& sm, int unit, con
 template <int B, int A = 12>
 __global__ void AK_SPREAD3C_BOUNDS
 k_spread3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
-           const WorkItem* __restrict__ items, const double* __restrict__ V, int64_t ldv,
+           const WorkItem* __restrict__ items, const double* __restrict__ V, Strides vs,
            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
 {
     __shared__ Spread3cSmem<B> sm;
-    spread3c_unit<B, A>(sm, blockIdx.x, ci, W, wshift, items, V, ldv, grids, canon_off, nrhs, n);
+    spread3c_unit<B, A>(sm, blockIdx.x, ci, W, wshift, items, V, vs, grids, canon_off, nrhs, n);
 }
 
 template <int B>
@@ -239,7 +189,7 @@ template <int B, int A = 12>
 __device__ __forceinline__ void interp3c_unit(Interp3cSmem<B>& sm, int unit, const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ grids,
            const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,
-           double* __restrict__ out, int64_t ldo, int atomic_out, int64_t wstride)
+           double* __restrict__ out, Strides os, int atomic_out, int64_t wstride)
 {
     constexpr int T = 12;
     constexpr int RW = 3 * T;
@@ -267,7 +217,7 @@ __device__ __forceinline__ void interp3c_unit(Interp3cSmem<B>& sm, int unit, con
     if (lane < min(B, it.count)) cp_async8(&cib[0][lane], CIit + lane);
     cp_async_commit();
 
-    // footprint fragments straight from the grid (same permuted layout as load_fragments)
+    // footprint fragments straight from the grid (the permuted layout of fragment_offsets)
     constexpr int NT = 3 * A / 2, AO = (T - A) / 2;
     double gf[NT][3];
     {
@@ -275,7 +225,6 @@ __device__ __forceinline__ void interp3c_unit(Interp3cSmem<B>& sm, int unit, con
         const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
         const int nn = lane >> 2, kk = lane & 3;
         const int qq = nn >> 1, e = nn & 1;
-#if AK_FASTPATH
         const int o0 = c0 - (T / 2 - 1), o1 = c1 - (T / 2 - 1), o2 = c2 - (T / 2 - 1);
         if (o0 >= 0 && o0 + T <= n && o1 >= 0 && o1 + T <= n && o2 >= 0 && o2 + T <= n) {
             // footprint inside the grid: lane base + per-tile (a, b) plane/row offsets
@@ -291,7 +240,6 @@ __device__ __forceinline__ void interp3c_unit(Interp3cSmem<B>& sm, int unit, con
                 for (int ks = 0; ks < 3; ++ks) gf[t][ks] = __ldg(row + 4 * ks);
             }
         } else
-#endif
         {
         int z[3];
 #pragma unroll
@@ -307,7 +255,7 @@ __device__ __forceinline__ void interp3c_unit(Interp3cSmem<B>& sm, int unit, con
         }
     }
     const double sc = scale[it.window];
-    double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * ldo;
+    double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * os.rs;
 
     for (int bi = 0; bi < nbatch; ++bi) {
         const int s = bi & 1;
@@ -332,7 +280,7 @@ __device__ __forceinline__ void interp3c_unit(Interp3cSmem<B>& sm, int unit, con
             v += __shfl_xor_sync(0xffffffffu, v, 2);
             const int pj = lane >> 2;
             if ((lane & 3) == 0 && pj < cnt) {
-                double* dst = o + cib[s][k0 + pj].idx;
+                double* dst = o + (int64_t)cib[s][k0 + pj].idx * os.is;
                 if (atomic_out) red_add(dst, sc * v);
                 else *dst = sc * v;
             }
@@ -346,10 +294,10 @@ __global__ void __launch_bounds__(32, 8)
 k_interp3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ grids,
            const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,
-           double* __restrict__ out, int64_t ldo, int atomic_out, int64_t wstride)
+           double* __restrict__ out, Strides os, int atomic_out, int64_t wstride)
 {
     __shared__ Interp3cSmem<B> sm;
-    interp3c_unit<B, A>(sm, blockIdx.x, ci, W, wshift, items, grids, canon_off, nrhs, n, scale, out, ldo, atomic_out,
+    interp3c_unit<B, A>(sm, blockIdx.x, ci, W, wshift, items, grids, canon_off, nrhs, n, scale, out, os, atomic_out,
                      wstride);
 }
 

@@ -18,34 +18,12 @@
 #pragma once
 #include "ak_q3w.cuh"
 
-#ifndef AK_INTERP_SPLIT
-#define AK_INTERP_SPLIT 0
-#endif
-
 namespace ak {
 
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
                  : "d"(a), "d"(b));
-}
-
-// Footprint fragments of the cell at local coordinates (l0, l1, l2):
-// gf[t][ks] = G[a][b][c] with c = 4 ks + lane%4 and column n = lane/4 of tile t
-// mapped to pair i = 2t + (n & 1), quad n >> 1: a = i / 3, b = 3 (n >> 1) + i % 3.
-template <int R>
-__device__ __forceinline__ void load_fragments(double (&gf)[18][3], const double* tile, int cell, int lane) {
-    const int l0 = cell & 255, l1 = (cell >> 8) & 255, l2 = (cell >> 16) & 255;
-    const int n = lane >> 2, kk = lane & 3;
-    const int qq = n >> 1, e = n & 1;
-#pragma unroll
-    for (int t = 0; t < 18; ++t) {
-        const int i = 2 * t + e;
-        const int a = i / 3, b = 3 * qq + i % 3;
-        const double* row = tile + ((l0 + a) * R + (l1 + b)) * R + l2 + kk;
-#pragma unroll
-        for (int ks = 0; ks < 3; ++ks) gf[t][ks] = row[4 * ks];
-    }
 }
 
 // One group of up to 8 points (rows k0 .. k0+cnt-1 of the staged batch), all in the
@@ -74,27 +52,6 @@ __device__ __forceinline__ double interp_group_mma(const double (&gf)[3 * A / 2]
     // lane (pj, q) holds U[pj][(a, b)] for a = AO + i/3, b = 3q + i%3, i = 2t + e:
     // out = sum_b w1[b] (sum_a w0[a] U[a][b]) -- 3 chains of A FMAs, then 3 more
     double s[3];
-#if AK_INTERP_SPLIT
-    // two interleaved chains of A/2 per b (shorter dependency chains), summed at the end
-    double s2[3];
-#pragma unroll
-    for (int bb = 0; bb < 3; ++bb) {
-        s[bb] = w[AO] * C[bb >> 1][bb & 1];
-        s2[bb] = w[AO + 1] * C[(3 + bb) >> 1][(3 + bb) & 1];
-    }
-#pragma unroll
-    for (int a = 2; a < A; a += 2) {
-        const double w0a = w[AO + a], w0b = w[AO + a + 1];
-#pragma unroll
-        for (int bb = 0; bb < 3; ++bb) {
-            const int i = 3 * a + bb, i2 = 3 * (a + 1) + bb;
-            s[bb] = fma(w0a, C[i >> 1][i & 1], s[bb]);
-            s2[bb] = fma(w0b, C[i2 >> 1][i2 & 1], s2[bb]);
-        }
-    }
-#pragma unroll
-    for (int bb = 0; bb < 3; ++bb) s[bb] += s2[bb];
-#else
 #pragma unroll
     for (int bb = 0; bb < 3; ++bb) s[bb] = w[AO] * C[bb >> 1][bb & 1];
 #pragma unroll
@@ -106,14 +63,14 @@ __device__ __forceinline__ double interp_group_mma(const double (&gf)[3 * A / 2]
             s[bb] = fma(w0a, C[i >> 1][i & 1], s[bb]);
         }
     }
-#endif
     const double* w1 = w + 12 + 3 * q;
     const double v = fma(w1[2], s[2], fma(w1[1], s[1], w1[0] * s[0]));
     return valid ? v : 0.0;
 }
 
-// Per-lane tile offsets of the 18 permuted B-fragment columns (same mapping as
-// load_fragments): column n = lane/4 of tile t is pair i = 2t + (n & 1) of quad n >> 1.
+// Per-lane tile offsets of the 18 permuted B-fragment columns: column n = lane/4 of
+// tile t is pair i = 2t + (n & 1) of quad n >> 1, i.e. a = i / 3, b = 3 (n >> 1) + i % 3;
+// row kk = lane % 4 of k-step ks is c = 4 ks + kk.
 template <int R>
 __device__ __forceinline__ void fragment_offsets(int (&off)[18], int lane) {
     const int n = lane >> 2, kk = lane & 3;
@@ -161,12 +118,15 @@ __device__ __forceinline__ double interp_group_mma_s(const double* cb, const int
     return valid ? v : 0.0;
 }
 
-template <int S, int B, int NW, bool SMEMB = false>
-__global__ void __launch_bounds__(32 * NW, (SMEMB ? 12 : 8) / NW)
+// Multi-cell (supercell) work items: the item's (S+11)^3 grid region is staged in
+// shared memory once, and every 8-point group of a cell run reads its B fragments
+// from it inside the DMMA loop (no per-cell register copy of the footprint).
+template <int S, int B>
+__global__ void __launch_bounds__(32, 12)
 k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ grids,
            const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,
-           double* __restrict__ out, int64_t ldo, int atomic_out, int64_t wstride)
+           double* __restrict__ out, Strides os, int atomic_out, int64_t wstride)
 {
     constexpr int T = 12;
     constexpr int RW = 3 * T;
@@ -175,20 +135,16 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     static_assert(B % 8 == 0 && B <= 32, "batch: multiple of 8, at most 32");
 
     __shared__ double tile[TILE];
-    __shared__ __align__(128) double wbuf_all[NW][2][B][RW];
-    __shared__ __align__(16) CellIdx cib_all[NW][2][B];
-    __shared__ int cst_all[NW][B];
+    __shared__ __align__(128) double wbuf[2][B][RW];
+    __shared__ __align__(16) CellIdx cib[2][B];
+    __shared__ int cst[B];
     __shared__ int widx[3][R];
-    __shared__ __align__(8) uint64_t bar_all[NW][2];
+    __shared__ __align__(8) uint64_t bar[2];
 
-    const WorkItem it = items[blockIdx.x];
-    const int r = blockIdx.y;
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    double (*wbuf)[B][RW] = wbuf_all[warp];
-    CellIdx (*cib)[B] = cib_all[warp];
-    int* cst = cst_all[warp];
-    uint64_t* bar = bar_all[warp];
+    // the RHS index runs fastest: the nrhs CTAs of one item share its weight rows in L2
+    const WorkItem it = items[blockIdx.x / nrhs];
+    const int r = blockIdx.x % nrhs;
+    const int lane = threadIdx.x;
     const int sc0 = it.sc & 1023, sc1 = (it.sc >> 10) & 1023, sc2 = (it.sc >> 20) & 1023;
     const int nbatch = (it.count + B - 1) / B;
     const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
@@ -200,47 +156,42 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         mbar_fence_init();
     }
     __syncwarp();
-    if (warp < nbatch) {
-        const int cnt = min(B, it.count - warp * B);
-        if (lane == 0) tma_load_1d(&wbuf[0][0][0], Wit + (int64_t)warp * B * RW, (unsigned)(cnt * RW * 8), &bar[0]);
-        if (lane < cnt) cp_async8(&cib[0][lane], CIit + warp * B + lane);
+    {
+        const int cnt = min(B, it.count);
+        if (lane == 0) tma_load_1d(&wbuf[0][0][0], Wit, (unsigned)(cnt * RW * 8), &bar[0]);
+        if (lane < cnt) cp_async8(&cib[0][lane], CIit + lane);
     }
     {
         const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
-        region_axes<R>(widx, sc0 * S - (T / 2 - 1), sc1 * S - (T / 2 - 1), sc2 * S - (T / 2 - 1), n, threadIdx.x,
-                       32 * NW);
-        if (NW > 1) __syncthreads();
-        else __syncwarp();
-        for_region_rows<R>(widx, n, threadIdx.x, 32 * NW, [&](int i, int64_t gi) { cp_async8(&tile[i], g + gi); });
+        region_axes<R>(widx, sc0 * S - (T / 2 - 1), sc1 * S - (T / 2 - 1), sc2 * S - (T / 2 - 1), n, lane, 32);
+        __syncwarp();
+        for_region_rows<R>(widx, n, lane, 32, [&](int i, int64_t gi) { cp_async8(&tile[i], g + gi); });
     }
     cp_async_commit();
     cp_async_wait_all();
-    if (NW > 1) __syncthreads();
-    else __syncwarp();
+    __syncwarp();
     const double sc = scale[it.window];
-    double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * ldo;
+    double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * os.rs;
 
-    double gf[SMEMB ? 1 : 18][3];
     int foff[18];
-    if constexpr (SMEMB) fragment_offsets<R>(foff, lane);
+    fragment_offsets<R>(foff, lane);
     const double* cb = tile;
     int cur = -1;
 
-    for (int bi = warp, u = 0; bi < nbatch; bi += NW, ++u) {
-        const int s = u & 1;
+    for (int bi = 0; bi < nbatch; ++bi) {
+        const int s = bi & 1;
         const int off = bi * B;
         const int nb = min(B, it.count - off);
         cp_async_wait_all();
-        mbar_wait(&bar[s], (u >> 1) & 1);
+        mbar_wait(&bar[s], (bi >> 1) & 1);
         __syncwarp();
-        if (bi + NW < nbatch) {
-            const int nb1 = min(B, it.count - off - NW * B);
+        if (bi + 1 < nbatch) {
+            const int nb1 = min(B, it.count - off - B);
             if (lane == 0) {
                 fence_proxy_async();
-                tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + NW * B) * RW, (unsigned)(nb1 * RW * 8),
-                            &bar[s ^ 1]);
+                tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + B) * RW, (unsigned)(nb1 * RW * 8), &bar[s ^ 1]);
             }
-            if (lane < nb1) cp_async8(&cib[s ^ 1][lane], CIit + off + NW * B + lane);
+            if (lane < nb1) cp_async8(&cib[s ^ 1][lane], CIit + off + B + lane);
         }
         cp_async_commit();
         if (lane < nb) {
@@ -255,23 +206,18 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         for (int k = 0; k < nb;) {
             if ((chg >> k) & 1u) {
                 cur = cst[k];
-                if constexpr (SMEMB)
-                    cb = tile + ((cur & 255) * R + ((cur >> 8) & 255)) * R + ((cur >> 16) & 255);
-                else
-                    load_fragments<R>(reinterpret_cast<double (&)[18][3]>(gf), tile, cur, lane);
+                cb = tile + ((cur & 255) * R + ((cur >> 8) & 255)) * R + ((cur >> 16) & 255);
             }
             const unsigned later = k < 31 ? chg & ~((2u << k) - 1u) : 0u;
             const int kend = later ? min(__ffs(later) - 1, nb) : nb;
             for (int k0 = k; k0 < kend; k0 += 8) {
                 const int cnt = min(8, kend - k0);
-                double v;
-                if constexpr (SMEMB) v = interp_group_mma_s<R, RW>(cb, foff, wbuf[s], k0, cnt, lane);
-                else v = interp_group_mma<RW>(reinterpret_cast<double (&)[18][3]>(gf), wbuf[s], k0, cnt, lane);
+                double v = interp_group_mma_s<R, RW>(cb, foff, wbuf[s], k0, cnt, lane);
                 v += __shfl_xor_sync(0xffffffffu, v, 1);
                 v += __shfl_xor_sync(0xffffffffu, v, 2);
                 const int pj = lane >> 2;
                 if ((lane & 3) == 0 && pj < cnt) {
-                    double* dst = o + cib[s][k0 + pj].idx;
+                    double* dst = o + (int64_t)cib[s][k0 + pj].idx * os.is;
                     if (atomic_out) red_add(dst, sc * v);
                     else *dst = sc * v;
                 }

@@ -28,7 +28,7 @@ struct alignas(128) Spread3rSmem {
 template <int B>
 __global__ void __launch_bounds__(64, 4)
 k_spread3r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
-           const WorkItem* __restrict__ items, const double* __restrict__ V, int64_t ldv,
+           const WorkItem* __restrict__ items, const double* __restrict__ V, Strides vs,
            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
 {
     constexpr int T = 12, RW = 3 * T, NT = 9;   // n-tiles per warp
@@ -44,7 +44,7 @@ k_spread3r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     const int pr = blockIdx.x % npair;          // RHS pair (fastest: pairs of an item share its rows in L2)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int lr = lane >> 2, kk = lane & 3;
-    const double* __restrict__ V0 = V + (int64_t)(2 * pr) * ldv;
+    const double* __restrict__ V0 = V + (int64_t)(2 * pr) * vs.rs;
     const int nbatch = (it.count + B - 1) / B;
     const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
     const CellIdx* __restrict__ CIit = ci + (it.start - wshift[it.window]);
@@ -63,7 +63,7 @@ k_spread3r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     __syncthreads();
     for (int e = tid; e < 2 * min(B, it.count); e += 64) {
         const int r = e / min(B, it.count), j = e - r * min(B, it.count);
-        cp_async8(&vb[0][r][j], V0 + (int64_t)r * ldv + cib[0][j].idx);
+        cp_async8(&vb[0][r][j], V0 + (int64_t)r * vs.rs + (int64_t)cib[0][j].idx * vs.is);
     }
     cp_async_commit();
 
@@ -102,7 +102,7 @@ k_spread3r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
             }
             for (int e = tid; e < 2 * nb1; e += 64) {
                 const int r = e / nb1, j = e - r * nb1;
-                cp_async8(&vb[s ^ 1][r][j], V0 + (int64_t)r * ldv + cib[(bi + 1) % 3][j].idx);
+                cp_async8(&vb[s ^ 1][r][j], V0 + (int64_t)r * vs.rs + (int64_t)cib[(bi + 1) % 3][j].idx * vs.is);
             }
         }
         if (bi + 2 < nbatch && tid < min(B, it.count - off - 2 * B))

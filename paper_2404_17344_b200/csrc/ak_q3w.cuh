@@ -147,10 +147,10 @@ __device__ __forceinline__ void for_region_rows(const int (*widx)[R], int n, int
     }
 }
 
-template <int T, int S, int B, bool VREG = false>
+template <int T, int S, int B>
 __global__ void __launch_bounds__(32, 8)
 k_spread3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
-           const WorkItem* __restrict__ items, const double* __restrict__ V, int64_t ldv,
+           const WorkItem* __restrict__ items, const double* __restrict__ V, Strides vs,
            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
 {
     using LN = Q3Lanes<T>;
@@ -168,12 +168,13 @@ k_spread3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     __shared__ int widx[3][R];
     __shared__ __align__(8) uint64_t bar[2];
 
-    const WorkItem it = items[blockIdx.x];
-    const int r = blockIdx.y;
+    // the RHS index runs fastest: the nrhs CTAs of one item share its weight rows in L2
+    const WorkItem it = items[blockIdx.x / nrhs];
+    const int r = blockIdx.x % nrhs;
     const int lane = threadIdx.x;
     const int g0 = lane >> 4, g1 = (lane >> 2) & 3, g2 = lane & 3;
     const int sc0 = it.sc & 1023, sc1 = (it.sc >> 10) & 1023, sc2 = (it.sc >> 20) & 1023;
-    const double* __restrict__ Vr = V + (int64_t)r * ldv;
+    const double* __restrict__ Vr = V + (int64_t)r * vs.rs;
     const int end = it.start + it.count;
     const int nbatch = (it.count + B - 1) / B;
     const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
@@ -192,7 +193,7 @@ k_spread3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     cp_async_commit();
     cp_async_wait_all();
     __syncwarp();
-    if (lane < min(B, it.count)) cp_async8(&vb[0][lane], Vr + cib[0][lane].idx);
+    if (lane < min(B, it.count)) cp_async8(&vb[0][lane], Vr + (int64_t)cib[0][lane].idx * vs.is);
     cp_async_commit();
 
     double acc[P0][P1][P2];
@@ -232,12 +233,12 @@ k_spread3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
                 fence_proxy_async();
                 tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + B) * RW, (unsigned)(nb1 * RW * 8), &bar[s ^ 1]);
             }
-            if (lane < nb1) cp_async8(&vb[s ^ 1][lane], Vr + cib[(bi + 1) % 3][lane].idx);
+            if (lane < nb1) cp_async8(&vb[s ^ 1][lane], Vr + (int64_t)cib[(bi + 1) % 3][lane].idx * vs.is);
         }
         if (bi + 2 < nbatch && lane < min(B, it.count - off - 2 * B))
             cp_async8(&cib[(bi + 2) % 3][lane], CIit + off + 2 * B + lane);
         cp_async_commit();
-        if (!VREG) {
+        {
             // axis-0 weights times the RHS value, element-parallel over the batch
             constexpr int PER = (B * T + 31) / 32;  // elements of the batch's w0 block per lane
             double x[PER], y[PER];
@@ -274,31 +275,16 @@ k_spread3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
             const unsigned later = k < 31 ? chg & ~((2u << k) - 1u) : 0u;
             const int kend = later ? min(__ffs(later) - 1, nb) : nb;
             double a0[P0], a1[P1], a2[P2], b0[P0], b1[P1], b2[P2];
-            double av = 1.0, bv = 1.0;
             load_w<T>(a0, a1, a2, &wbuf[s][k][0], g0, g1, g2);
-            if (VREG) av = vb[s][k];
             int j = k;
             for (; j + 1 < kend; j += 2) {
                 load_w<T>(b0, b1, b2, &wbuf[s][j + 1][0], g0, g1, g2);
-                if (VREG) {
-                    bv = vb[s][j + 1];
-                    spread_fma_v(acc, a0, a1, a2, av);
-                } else {
-                    spread_fma(acc, a0, a1, a2);
-                }
+                spread_fma(acc, a0, a1, a2);
                 const int jn = j + 2 < kend ? j + 2 : j + 1;
                 load_w<T>(a0, a1, a2, &wbuf[s][jn][0], g0, g1, g2);
-                if (VREG) {
-                    av = vb[s][jn];
-                    spread_fma_v(acc, b0, b1, b2, bv);
-                } else {
-                    spread_fma(acc, b0, b1, b2);
-                }
+                spread_fma(acc, b0, b1, b2);
             }
-            if (j < kend) {
-                if (VREG) spread_fma_v(acc, a0, a1, a2, av);
-                else spread_fma(acc, a0, a1, a2);
-            }
+            if (j < kend) spread_fma(acc, a0, a1, a2);
             k = kend;
         }
     }
@@ -313,333 +299,6 @@ k_spread3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         if (val != 0.0) red_add(g + gi, val);
     });
     (void)end;
-}
-
-// Two warps per CTA on one work item: they share the (S+T-1)^3 tile, the
-// weight double buffer (batches of B = 32 points) and the point records, and
-// split every cell run between them (warp w takes the run's points of parity
-// w), each with its own register tile.  At a cell change both warps flush the
-// same footprint positions, serialised by two named barriers:
-//   bar 1 (64 threads); warp 0 flushes; bar 2; warp 1 flushes
-// (the next event's bar 1 also orders warp 1's flush before warp 0's).
-// More warps per SM (10 vs 7) hide the per-batch latencies of one warp
-// behind the other's FMA stream.
-__device__ __forceinline__ void named_bar(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-template <int T, int S>
-__global__ void __launch_bounds__(64, 5)
-k_spread3w2(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
-            const WorkItem* __restrict__ items, const double* __restrict__ V, int64_t ldv,
-            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
-{
-    using LN = Q3Lanes<T>;
-    constexpr int P0 = LN::P0, P1 = LN::P1, P2 = LN::P2;
-    constexpr int RW = 3 * T;
-    constexpr int R = S + T - 1;
-    constexpr int TILE = R * R * R;
-    constexpr int B = 32;
-
-    __shared__ double tile[TILE];
-    __shared__ __align__(128) double wbuf[2][B][RW];
-    __shared__ __align__(16) CellIdx cib[3][B];
-    __shared__ double vb[2][B];
-    __shared__ __align__(8) uint64_t bar[2];
-
-    const WorkItem it = items[blockIdx.x];
-    const int r = blockIdx.y;
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5;
-    const int lane = tid & 31;
-    const int g0 = lane >> 4, g1 = (lane >> 2) & 3, g2 = lane & 3;
-    const int sc0 = it.sc & 1023, sc1 = (it.sc >> 10) & 1023, sc2 = (it.sc >> 20) & 1023;
-    const double* __restrict__ Vr = V + (int64_t)r * ldv;
-    const int nbatch = (it.count + B - 1) / B;
-    const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
-    const CellIdx* __restrict__ CIit = ci + (it.start - wshift[it.window]);
-
-    for (int i = tid; i < TILE; i += 64) tile[i] = 0.0;
-    if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        mbar_fence_init();
-    }
-    __syncthreads();
-    if (warp == 0) {
-        if (lane == 0) tma_load_1d(&wbuf[0][0][0], Wit, (unsigned)(min(B, it.count) * RW * 8), &bar[0]);
-        if (lane < min(B, it.count)) cp_async8(&cib[0][lane], CIit + lane);
-        if (nbatch > 1 && lane < min(B, it.count - B)) cp_async8(&cib[1][lane], CIit + B + lane);
-        cp_async_commit();
-        cp_async_wait_all();
-        __syncwarp();
-        if (lane < min(B, it.count)) cp_async8(&vb[0][lane], Vr + cib[0][lane].idx);
-        cp_async_commit();
-    }
-
-    double acc[P0][P1][P2];
-#pragma unroll
-    for (int a = 0; a < P0; ++a)
-#pragma unroll
-        for (int b = 0; b < P1; ++b)
-#pragma unroll
-            for (int c = 0; c < P2; ++c) acc[a][b][c] = 0.0;
-    int cur = -1;
-
-    auto flush_own = [&](int cell) {
-        const int l0 = cell & 255, l1 = (cell >> 8) & 255, l2 = (cell >> 16) & 255;
-#pragma unroll
-        for (int a = 0; a < P0; ++a)
-#pragma unroll
-            for (int b = 0; b < P1; ++b)
-#pragma unroll
-                for (int c = 0; c < P2; ++c) {
-                    double* t = &tile[((l0 + g0 * P0 + a) * R + (l1 + g1 * P1 + b)) * R + (l2 + g2 * P2 + c)];
-                    *t += acc[a][b][c];
-                    acc[a][b][c] = 0.0;
-                }
-    };
-    auto flush_both = [&](int cell) {
-        named_bar(1, 64);
-        if (warp == 0) flush_own(cell);
-        named_bar(2, 64);
-        if (warp == 1) flush_own(cell);
-    };
-
-    for (int bi = 0; bi < nbatch; ++bi) {
-        const int s = bi & 1;
-        const int off = bi * B;
-        const int nb = min(B, it.count - off);
-        if (warp == 0) cp_async_wait_all();
-        mbar_wait(&bar[s], (bi >> 1) & 1);
-        __syncthreads();
-        if (warp == 0) {
-            if (bi + 1 < nbatch) {
-                const int nb1 = min(B, it.count - off - B);
-                if (lane == 0) {
-                    fence_proxy_async();
-                    tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + B) * RW, (unsigned)(nb1 * RW * 8),
-                                &bar[s ^ 1]);
-                }
-                if (lane < nb1) cp_async8(&vb[s ^ 1][lane], Vr + cib[(bi + 1) % 3][lane].idx);
-            }
-            if (bi + 2 < nbatch && lane < min(B, it.count - off - 2 * B))
-                cp_async8(&cib[(bi + 2) % 3][lane], CIit + off + 2 * B + lane);
-            cp_async_commit();
-        }
-        // each warp scales the axis-0 weights of the rows (points) it will use: parity == warp
-        {
-            constexpr int PER = (B / 2 * T + 31) / 32;
-            double x[PER], y[PER];
-#pragma unroll
-            for (int i = 0; i < PER; ++i) {
-                const int e = lane + 32 * i;
-                const int row = 2 * (e / T) + warp;
-                if (row < nb) {
-                    x[i] = wbuf[s][row][e % T];
-                    y[i] = vb[s][row];
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < PER; ++i) {
-                const int e = lane + 32 * i;
-                const int row = 2 * (e / T) + warp;
-                if (row < nb) wbuf[s][row][e % T] = x[i] * y[i];
-            }
-        }
-        int mycell = -2;
-        if (lane < nb) {
-            const int c = cib[bi % 3][lane].cell;
-            mycell = (cell_axis(c, 0) - sc0 * S) | ((cell_axis(c, 1) - sc1 * S) << 8) |
-                     ((cell_axis(c, 2) - sc2 * S) << 16);
-        }
-        __syncwarp();
-        const int prev = __shfl_up_sync(0xffffffffu, mycell, 1);
-        const unsigned chg = __ballot_sync(0xffffffffu, lane < nb && (lane == 0 ? mycell != cur : mycell != prev));
-        for (int k = 0; k < nb;) {
-            if ((chg >> k) & 1u) {
-                if (cur >= 0) flush_both(cur);
-                cur = __shfl_sync(0xffffffffu, mycell, k);
-            }
-            const unsigned later = k < 31 ? chg & ~((2u << k) - 1u) : 0u;
-            const int kend = later ? min(__ffs(later) - 1, nb) : nb;
-            int j = k + ((warp - k) & 1);
-            if (j < kend) {
-                double a0[P0], a1[P1], a2[P2], b0[P0], b1[P1], b2[P2];
-                load_w<T>(a0, a1, a2, &wbuf[s][j][0], g0, g1, g2);
-                for (; j + 2 < kend; j += 4) {
-                    load_w<T>(b0, b1, b2, &wbuf[s][j + 2][0], g0, g1, g2);
-                    spread_fma(acc, a0, a1, a2);
-                    load_w<T>(a0, a1, a2, &wbuf[s][j + 4 < kend ? j + 4 : j + 2][0], g0, g1, g2);
-                    spread_fma(acc, b0, b1, b2);
-                }
-                if (j < kend) spread_fma(acc, a0, a1, a2);
-            }
-            k = kend;
-        }
-    }
-    if (cur >= 0) flush_both(cur);
-    __syncthreads();
-
-    double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
-    const int o0 = sc0 * S - (T / 2 - 1);
-    const int o1 = sc1 * S - (T / 2 - 1);
-    const int o2 = sc2 * S - (T / 2 - 1);
-    for (int i = tid; i < TILE; i += 64) {
-        const double val = tile[i];
-        if (val != 0.0) red_add(g + region_index<R>(i, o0, o1, o2, n), val);
-    }
-}
-
-// NW warps per CTA share the read-only region tile; warp w takes the batches
-// w, w+NW, w+2NW, ... of the item, each with its own weight double buffer.
-template <int T, int S, int B, int NW>
-__global__ void __launch_bounds__(32 * NW, 8 / NW)
-k_interp3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
-           const WorkItem* __restrict__ items, const double* __restrict__ grids,
-           const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,
-           double* __restrict__ out, int64_t ldo, int atomic_out, int64_t wstride)
-{
-    using LN = Q3Lanes<T>;
-    constexpr int P0 = LN::P0, P1 = LN::P1, P2 = LN::P2;
-    constexpr int RW = 3 * T;
-    constexpr int R = S + T - 1;
-    constexpr int TILE = R * R * R;
-    static_assert(B % 8 == 0 && B <= 32, "batch: multiple of 8, at most 32");
-
-    __shared__ double tile[TILE];
-    __shared__ __align__(128) double wbuf_all[NW][2][B][RW];
-    __shared__ __align__(16) CellIdx cib_all[NW][2][B];
-    __shared__ int cst_all[NW][B];
-    __shared__ int widx[3][R];
-    __shared__ __align__(8) uint64_t bar_all[NW][2];
-
-    const WorkItem it = items[blockIdx.x];
-    const int r = blockIdx.y;
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    double (*wbuf)[B][RW] = wbuf_all[warp];
-    CellIdx (*cib)[B] = cib_all[warp];
-    int* cst = cst_all[warp];
-    uint64_t* bar = bar_all[warp];
-    const int g0 = lane >> 4, g1 = (lane >> 2) & 3, g2 = lane & 3;
-    const int sc0 = it.sc & 1023, sc1 = (it.sc >> 10) & 1023, sc2 = (it.sc >> 20) & 1023;
-    const int nbatch = (it.count + B - 1) / B;
-    const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
-    const CellIdx* __restrict__ CIit = ci + (it.start - wshift[it.window]);
-
-    if (lane == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        mbar_fence_init();
-    }
-    __syncwarp();
-    if (warp < nbatch) {
-        const int cnt = min(B, it.count - warp * B);
-        if (lane == 0) tma_load_1d(&wbuf[0][0][0], Wit + (int64_t)warp * B * RW, (unsigned)(cnt * RW * 8), &bar[0]);
-        if (lane < cnt) cp_async8(&cib[0][lane], CIit + warp * B + lane);
-    }
-    {
-        // region tile by cp.async (no register round trip: all loads in flight at once)
-        const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
-        region_axes<R>(widx, sc0 * S - (T / 2 - 1), sc1 * S - (T / 2 - 1), sc2 * S - (T / 2 - 1), n, threadIdx.x,
-                       32 * NW);
-        if (NW > 1) __syncthreads();
-        else __syncwarp();
-        for_region_rows<R>(widx, n, threadIdx.x, 32 * NW, [&](int i, int64_t gi) { cp_async8(&tile[i], g + gi); });
-    }
-    cp_async_commit();
-    cp_async_wait_all();
-    if (NW > 1) __syncthreads();
-    const double sc = scale[it.window];
-    double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * ldo;
-
-    double tv[P0][P1][P2];
-    int cur = -1;
-
-    for (int bi = warp, u = 0; bi < nbatch; bi += NW, ++u) {
-        const int s = u & 1;
-        const int off = bi * B;
-        const int nb = min(B, it.count - off);
-        cp_async_wait_all();
-        mbar_wait(&bar[s], (u >> 1) & 1);
-        __syncwarp();
-        if (bi + NW < nbatch) {
-            const int nb1 = min(B, it.count - off - NW * B);
-            if (lane == 0) {
-                fence_proxy_async();
-                tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + NW * B) * RW, (unsigned)(nb1 * RW * 8),
-                            &bar[s ^ 1]);
-            }
-            if (lane < nb1) cp_async8(&cib[s ^ 1][lane], CIit + off + NW * B + lane);
-        }
-        cp_async_commit();
-        if (lane < nb) {
-            const int c = cib[s][lane].cell;
-            cst[lane] = (cell_axis(c, 0) - sc0 * S) | ((cell_axis(c, 1) - sc1 * S) << 8) |
-                        ((cell_axis(c, 2) - sc2 * S) << 16);
-        }
-        __syncwarp();
-        const int mycell = lane < nb ? cst[lane] : -2;
-        const int prev = __shfl_up_sync(0xffffffffu, mycell, 1);
-        const unsigned chg = __ballot_sync(0xffffffffu, lane < nb && (lane == 0 ? mycell != cur : mycell != prev));
-
-        for (int grp = 0; grp < nb; grp += 8) {
-            double part[8];
-            if (grp + 8 <= nb && ((chg >> grp) & 0xffu) == 0u) {
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    part[kk] = footprint_dot<P0, P1, P2>(tv, &wbuf[s][grp + kk][0], g0, g1, g2);
-            } else {
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const int k = grp + kk;
-                    part[kk] = 0.0;
-                    if (k < nb) {
-                        if ((chg >> k) & 1u) {
-                            cur = cst[k];
-                            const int l0 = cur & 255, l1 = (cur >> 8) & 255, l2 = (cur >> 16) & 255;
-#pragma unroll
-                            for (int a = 0; a < P0; ++a)
-#pragma unroll
-                                for (int b = 0; b < P1; ++b)
-#pragma unroll
-                                    for (int c = 0; c < P2; ++c)
-                                        tv[a][b][c] = tile[((l0 + g0 * P0 + a) * R + (l1 + g1 * P1 + b)) * R +
-                                                           (l2 + g2 * P2 + c)];
-                        }
-                        part[kk] = footprint_dot<P0, P1, P2>(tv, &wbuf[s][k][0], g0, g1, g2);
-                    }
-                }
-            }
-            const bool hi4 = lane & 4;
-            double q4[4];
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-                const double send = hi4 ? part[jj] : part[jj + 4];
-                const double keep = hi4 ? part[jj + 4] : part[jj];
-                q4[jj] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-            }
-            const bool hi2 = lane & 2;
-            double q2[2];
-#pragma unroll
-            for (int jj = 0; jj < 2; ++jj) {
-                const double send = hi2 ? q4[jj] : q4[jj + 2];
-                const double keep = hi2 ? q4[jj + 2] : q4[jj];
-                q2[jj] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-            }
-            const bool hi1 = lane & 1;
-            const double send = hi1 ? q2[0] : q2[1];
-            double v = (hi1 ? q2[1] : q2[0]) + __shfl_xor_sync(0xffffffffu, send, 1);
-            v += __shfl_xor_sync(0xffffffffu, v, 8);
-            v += __shfl_xor_sync(0xffffffffu, v, 16);
-            if (lane < 8 && grp + lane < nb) {
-                double* dst = o + cib[s][grp + lane].idx;
-                if (atomic_out) red_add(dst, sc * v);
-                else *dst = sc * v;
-            }
-        }
-    }
 }
 
 }  // namespace ak

@@ -171,8 +171,13 @@ class _Operator:
         rc = lib.ak_op_create(gs.handle, gi.handle, m, R, C, _stream_ptr(torch), ctypes.byref(self._handle))
         _native.check(rc, "ak_op_create")
 
-    def apply(self, V, outs: list, sum_windows: list, accumulate: bool = False, flags: int = 0) -> None:
-        """One product: spread V, transform, interpolate into outs (ak_op_apply)."""
+    def apply(self, V, outs: list, sum_windows: list, accumulate: bool = False, flags: int = 0,
+              rhs_minor: bool = False) -> None:
+        """One product: spread V, transform, interpolate into outs (ak_op_apply).
+
+        RHS-major (default): V (R, N), summed outs (R, N), per-window outs (P, R, N).
+        rhs_minor: V (N, R), summed outs (N, R), per-window outs (P, N, R) -- a
+        point's R values share a cache line (AK_APPLY_RHS_MINOR)."""
         torch = _torch()
         C = self.C
         optrs = (ctypes.c_void_p * C)(*[o.data_ptr() for o in outs])
@@ -181,8 +186,10 @@ class _Operator:
         f = flags | (_native.AK_APPLY_ACCUMULATE if accumulate else 0)
         if self.per_rhs:
             f |= _native.AK_APPLY_H_PER_RHS
+        if rhs_minor:
+            f |= _native.AK_APPLY_RHS_MINOR
         vptr = V.data_ptr() if V is not None else 0
-        ldv = int(V.shape[-1]) if V is not None else self.gs.n_points
+        ldv = int(V.shape[-1]) if V is not None else (self.R if rhs_minor else self.gs.n_points)
         rc = self._lib.ak_op_apply(self._handle, vptr, ldv, self.hptr.data_ptr(), self.scale.data_ptr(), optrs, ldo,
                                    sw, f, _stream_ptr(torch))
         _native.check(rc, "ak_op_apply")
@@ -262,6 +269,15 @@ def _rows_on_device(v, n: int, what: str):
     return t.contiguous(), single, on_device
 
 
+def _rhs_minor(Vd):
+    """(R, N) device RHS -> (N, R) contiguous (RHS-minor: the layout the kernels gather in
+    full sectors).  A caller's tensor that already is the transpose of an (N, R) array is
+    used as is."""
+    if Vd.stride() == (1, Vd.shape[0]):
+        return Vd.t()
+    return Vd.t().contiguous()
+
+
 def _to_caller(t, single: bool, on_device: bool):
     """Device result -> caller: CUDA tensor as is, or a fresh numpy array.
 
@@ -273,6 +289,7 @@ def _to_caller(t, single: bool, on_device: bool):
     if on_device:
         return t
     torch = _torch()
+    t = t.contiguous()   # RHS-minor results: transposed on the device, then one DMA
     host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
     host.copy_(t, non_blocking=True)
     torch.cuda.current_stream().synchronize()
@@ -356,14 +373,15 @@ def _eta_warning(ell: float, m: int) -> None:
 
 def build_plan(spec: KernelSpec, window_set: WindowSet, preset, data: Dataset, cutoff: int = 6,
                oversampling: float = 2.0, window: str = "kaiser_bessel", features_device=None,
-               row_masks=None) -> FastsumPlan:
+               row_masks=None, tuning=None) -> FastsumPlan:
     """Coefficient tables (host, tiny) + bin-sorted device geometry (fastsum.py:105-133).
 
     ``features_device`` optionally passes ``data.features`` already resident
     on the GPU (a torch CUDA tensor) to skip the upload.  ``row_masks``
     (windows x rows, bool; extension) restricts each window to a row subset:
     the product is then sum_w K_w restricted to window w's rows (the cell-slab
-    multi-GPU layout, distributed.CellShardedPlan).
+    multi-GPU layout, distributed.CellShardedPlan).  ``tuning`` (extension) pins
+    kernel choices by ak_tuning field name (tests; nufft.DeviceGeometry).
     """
     _check_prescaled(data, window_set)
     m = resolve_m(preset)
@@ -375,7 +393,7 @@ def build_plan(spec: KernelSpec, window_set: WindowSet, preset, data: Dataset, c
     any_plan = nufft_plans[lengths[0]]
     geom = DeviceGeometry(any_plan.n, window_set.lengths, [window_set.columns(w) for w in window_set],
                           data.features if features_device is None else features_device, any_plan.window_fn(),
-                          row_masks=row_masks)
+                          row_masks=row_masks, tuning=tuning)
     return FastsumPlan(spec=spec, window_set=window_set, m=m, data=data, nufft_plans=nufft_plans,
                        tables=tables, geometries=geom)
 
@@ -411,8 +429,14 @@ def fast_matvecs(plan: FastsumPlan, V, dell: bool = False, dsigma: bool = False)
     torch = _torch()
     R = Vd.shape[0]
     fams = (plan.spec.family,) + ((DERIVATIVE_FAMILY[plan.spec.family],) if dell else ())
-    outs = [torch.empty((R, plan.n_rows), dtype=torch.float64, device="cuda") for _ in fams]
-    plan._operator(fams, R).apply(Vd, outs, [True] * len(fams))
+    if R > 1:
+        # RHS-minor products; device results are (R, N) views of the (N, R) outputs
+        outs = [torch.empty((plan.n_rows, R), dtype=torch.float64, device="cuda") for _ in fams]
+        plan._operator(fams, R).apply(_rhs_minor(Vd), outs, [True] * len(fams), rhs_minor=True)
+        outs = [o.t() for o in outs]
+    else:
+        outs = [torch.empty((R, plan.n_rows), dtype=torch.float64, device="cuda") for _ in fams]
+        plan._operator(fams, R).apply(Vd, outs, [True] * len(fams))
     res = {"K": _to_caller(outs[0], single, on_dev)}
     if dell:
         res["dK_dell"] = _to_caller(outs[1], single, on_dev)
@@ -430,7 +454,7 @@ def prepare_eval_points(plan: FastsumPlan, data: Dataset) -> DeviceGeometry:
     ws = plan.window_set
     any_plan = next(iter(plan.nufft_plans.values()))
     return DeviceGeometry(any_plan.n, ws.lengths, [ws.columns(w) for w in ws], data.features,
-                          any_plan.window_fn())
+                          any_plan.window_fn(), tuning=plan.geometries.tuning)
 
 
 def fast_cross_matvec(plan: FastsumPlan, eval_geoms: DeviceGeometry, v, n_eval: int):
@@ -501,7 +525,7 @@ class MixedKernelPlan:
 
 def build_mixed_plan(specs, window_set: WindowSet, preset, data: Dataset, cutoff: int = 6,
                      oversampling: float = 2.0, window: str = "kaiser_bessel",
-                     features_device=None, row_masks=None) -> MixedKernelPlan:
+                     features_device=None, row_masks=None, tuning=None) -> MixedKernelPlan:
     specs = tuple(specs)
     if len(specs) != len(window_set):
         raise ValueError("need one KernelSpec per window")
@@ -520,7 +544,7 @@ def build_mixed_plan(specs, window_set: WindowSet, preset, data: Dataset, cutoff
     any_plan = nufft_plans[lengths[0]]
     geom = DeviceGeometry(any_plan.n, window_set.lengths, [window_set.columns(w) for w in window_set],
                           data.features if features_device is None else features_device, any_plan.window_fn(),
-                          row_masks=row_masks)
+                          row_masks=row_masks, tuning=tuning)
     return MixedKernelPlan(specs=specs, window_set=window_set, m=m, data=data, nufft_plans=nufft_plans,
                            geometries=geom)
 
@@ -530,14 +554,24 @@ def mixed_matvecs(plan: MixedKernelPlan, V, dell: bool = True, dsigma: bool = Tr
     Vd, single, on_dev = _rows_on_device(V, plan.n_rows, "V must be (N,) or (R, N)")
     torch = _torch()
     R, N, P = Vd.shape[0], plan.n_rows, len(plan.window_set)
-    outs = [torch.empty((R, N), dtype=torch.float64, device="cuda")]
-    if dell:
-        outs.append(torch.empty((P, R, N), dtype=torch.float64, device="cuda"))
-    plan._operator(R, dell).apply(Vd, outs, [True, False][: len(outs)])
+    minor = R > 1
+    if minor:
+        # RHS-minor products: K (N, R), per-window dK/dl_w (P, N, R); returned as
+        # (R, N) / (P, R, N) views on the device
+        outs = [torch.empty((N, R), dtype=torch.float64, device="cuda")]
+        if dell:
+            outs.append(torch.empty((P, N, R), dtype=torch.float64, device="cuda"))
+        plan._operator(R, dell).apply(_rhs_minor(Vd), outs, [True, False][: len(outs)], rhs_minor=True)
+        outs = [outs[0].t()] + ([outs[1].permute(0, 2, 1)] if dell else [])
+    else:
+        outs = [torch.empty((R, N), dtype=torch.float64, device="cuda")]
+        if dell:
+            outs.append(torch.empty((P, R, N), dtype=torch.float64, device="cuda"))
+        plan._operator(R, dell).apply(Vd, outs, [True, False][: len(outs)])
     res = {"K": _to_caller(outs[0], single, on_dev)}
     if dell:
         d = outs[1][:, 0] if single else outs[1]
-        res["dK_dell"] = d if on_dev else d.cpu().numpy()
+        res["dK_dell"] = d if on_dev else d.contiguous().cpu().numpy()
     if dsigma:
         res["dK_dsigma"] = _to_caller(outs[0] * (2.0 / plan.sigma_f), single, on_dev)
     return res

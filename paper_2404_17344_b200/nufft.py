@@ -250,9 +250,11 @@ class DeviceGeometry:
     """Bin-sorted nodes of P windows on the device (replaces the per-window
     ``SpreadGeometry`` tuple, nufft.py:160-191).  Immutable; owns device memory."""
 
-    def __init__(self, n: int, qs, cols, features, window_fn, row_masks=None):
+    def __init__(self, n: int, qs, cols, features, window_fn, row_masks=None, tuning=None):
         """row_masks: optional (P, N) bool array -- window w uses only the rows with
-        row_masks[w] set (ak_geom_create_masked; the multi-GPU cell-slab layout)."""
+        row_masks[w] set (the multi-GPU cell-slab layout).  tuning: optional dict of
+        ak_tuning fields that pin the plan's kernel choices (tests; the defaults are
+        the library's measured heuristics) -- ak_geom_create_ex."""
         torch = _torch()
         lib = _native.lib()
         feats = features
@@ -277,22 +279,22 @@ class DeviceGeometry:
         self.cols = tuple(tuple(int(c) for c in cs) for cs in cols)
         self.n_points = int(feats.shape[0])
         self.rows_per_window = (self.n_points,) * P
-        if row_masks is None:
-            rc = lib.ak_geom_create(self.n, P, qarr, carr, ctypes.c_void_p(feats.data_ptr()), self.n_points,
-                                    int(feats.shape[1]), ctypes.byref(window_fn), _stream_ptr(torch),
-                                    ctypes.byref(self._handle))
-            _native.check(rc, "ak_geom_create")
-        else:
+        md, rows_in = None, None
+        if row_masks is not None:
             m = np.ascontiguousarray(np.asarray(row_masks, dtype=bool))
             if m.shape != (P, self.n_points):
                 raise ValueError("row_masks must have shape (windows, rows)")
             md = torch.as_tensor(m.view(np.uint8), device="cuda")
             self.rows_per_window = tuple(int(c) for c in m.sum(axis=1))
             rows_in = (ctypes.c_int64 * P)(*self.rows_per_window)
-            rc = lib.ak_geom_create_masked(self.n, P, qarr, carr, ctypes.c_void_p(feats.data_ptr()), self.n_points,
-                                           int(feats.shape[1]), ctypes.c_void_p(md.data_ptr()), rows_in,
-                                           ctypes.byref(window_fn), _stream_ptr(torch), ctypes.byref(self._handle))
-            _native.check(rc, "ak_geom_create_masked")
+        tune = _native.tuning(**(tuning or {}))
+        rc = lib.ak_geom_create_ex(self.n, P, qarr, carr, ctypes.c_void_p(feats.data_ptr()), self.n_points,
+                                   int(feats.shape[1]), ctypes.c_void_p(md.data_ptr() if md is not None else 0),
+                                   rows_in, ctypes.byref(window_fn), ctypes.byref(tune), _stream_ptr(torch),
+                                   ctypes.byref(self._handle))
+        _native.check(rc, "ak_geom_create_ex")
+        self.describe = (lib.ak_geom_describe(self._handle) or b"").decode()
+        self.tuning = dict(tuning) if tuning else None
         self.n_windows = P
         self.n_items = int(lib.ak_geom_num_items(self._handle))
         self.canon_total = int(lib.ak_geom_canon_total(self._handle))
@@ -325,12 +327,13 @@ def _points_array(plan: NufftPlan, points) -> np.ndarray:
     return np.ascontiguousarray(pts)
 
 
-def prepare_points(plan: NufftPlan, points) -> DeviceGeometry:
-    """Validate nodes and bin-sort them on the GPU (nufft.py:169-191)."""
+def prepare_points(plan: NufftPlan, points, tuning=None) -> DeviceGeometry:
+    """Validate nodes and bin-sort them on the GPU (nufft.py:169-191).  ``tuning``
+    (extension): ak_tuning fields pinning the kernel choices (DeviceGeometry)."""
     pts = _points_array(plan, points)
     if np.any(pts < -0.5) or np.any(pts >= 0.5):
         raise PointOutOfDomainError("points must lie in [-1/2, 1/2)")
-    return DeviceGeometry(plan.n, (plan.dims,), (tuple(range(plan.dims)),), pts, plan.window_fn())
+    return DeviceGeometry(plan.n, (plan.dims,), (tuple(range(plan.dims)),), pts, plan.window_fn(), tuning=tuning)
 
 
 def _as_geometry(plan: NufftPlan, points) -> DeviceGeometry:

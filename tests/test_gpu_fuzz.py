@@ -52,14 +52,14 @@ def _case(seed):
     knobs = {}
     k = rng.integers(0, 4)
     if k == 1:
-        knobs["AK_SUPERCELL3"] = "1"
+        knobs["cell_items3"] = 1
     elif k == 2:
-        knobs["AK_SUPERCELL3"] = "2"
+        knobs["cell_items3"] = 2
     elif k == 3:
-        knobs["AK_DENSE_CELLS"] = "1e9"
-        knobs["AK_DENSE_CELLS_INTERP"] = "0"
+        knobs["dense_cells3"] = 1e9
+        knobs["dense_cells3_interp"] = 0.0
     if rng.random() < 0.3:
-        knobs["AK_CHUNK3"] = str(int(rng.choice([64, 100, 333])))
+        knobs["chunk3"] = int(rng.choice([64, 100, 333]))
     masks = None
     if rng.random() < 0.25:   # row-masked windows (the cell-slab layout's plans)
         masks = rng.random((len(windows), N)) < rng.uniform(0.2, 1.0, size=(len(windows), 1))
@@ -68,7 +68,7 @@ def _case(seed):
 
 
 @pytest.mark.parametrize("seed", range(N_CASES))
-def test_random_configuration_matches_oracle(cuda, monkeypatch, seed):
+def test_random_configuration_matches_oracle(cuda, seed):
     from oracle import restate as R
     from paper_2404_17344_b200.dataset import PRESCALED, Dataset
     from paper_2404_17344_b200.fastsum import PRESETS, build_plan, fast_matvecs
@@ -76,8 +76,6 @@ def test_random_configuration_matches_oracle(cuda, monkeypatch, seed):
     from paper_2404_17344_b200.windows import WindowSet
 
     c = _case(seed)
-    for k, v in c["knobs"].items():
-        monkeypatch.setenv(k, v)
     ds = Dataset(c["X"], np.zeros(c["N"]), tuple(f"x{i}" for i in range(6)), scaling_state=PRESCALED, d_max=3)
     ws = WindowSet(tuple(tuple(col + 1 for col in w) for w in c["windows"]), d_max=3)
     spec = KernelSpec(c["family"], c["ell"], 0.7)
@@ -85,7 +83,7 @@ def test_random_configuration_matches_oracle(cuda, monkeypatch, seed):
 
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")  # AccuracyWarning for small ell * m is expected here
-        plan = build_plan(spec, ws, c["preset"], ds, row_masks=c["masks"])
+        plan = build_plan(spec, ws, c["preset"], ds, row_masks=c["masks"], tuning=c["knobs"])
     base = DERIVATIVE_PREFACTOR[c["family"]] is None
     res = fast_matvecs(plan, c["V"], dell=base)
     m = PRESETS.get(c["preset"], c["preset"])

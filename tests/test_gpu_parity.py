@@ -145,17 +145,14 @@ def test_cross_matvec_matches_reference(cuda):
     assert rel(out, g["dense"]) < 1e-3
 
 
-def test_generic_kernels_agree_with_tiled(cuda, monkeypatch):
-    """The one-thread-per-point kernels (AK_FORCE_GENERIC=1) and the tiled ones."""
+def test_generic_kernels_agree_with_tiled(cuda):
+    """The one-thread-per-point kernels (tuning generic_kernels=1) and the tiled ones."""
     from paper_2404_17344_b200.fastsum import fast_matvec
 
     for name in ("c2", "c4"):
         g = golden(name)
-        plan = _plan(g)
-        tiled = fast_matvec(plan, g["V"][0])
-        monkeypatch.setenv("AK_FORCE_GENERIC", "1")
-        generic = fast_matvec(plan, g["V"][0])
-        monkeypatch.delenv("AK_FORCE_GENERIC")
+        tiled = fast_matvec(_plan(g), g["V"][0])
+        generic = fast_matvec(_plan(g, tuning={"generic_kernels": 1}), g["V"][0])
         assert rel(tiled, generic) <= 1e-13
 
 
@@ -171,87 +168,75 @@ def test_native_library_is_what_runs(cuda):
 
 
 @pytest.mark.parametrize("variant", [
-    {"AK_IMMA": "0"},                       # DFMA interp (transposed warp reduction)
-    {"AK_IMMA_SMEM": "0", "AK_SUPERCELL3": "2"},  # DMMA interp, fragments in registers per cell run
-    {"AK_WEIGHTS": "horner"},               # weights evaluated per pass (no plan-time table)
-    {"AK_SWARPS": "2"},                     # two-warp spread CTAs with barrier-serialised flushes
-    {"AK_IWARPS": "2"},                     # two-warp interp CTAs sharing the region tile
-    {"AK_SUPERCELL3": "4", "AK_CHUNK3": "256", "AK_SORT_ITEMS": "0"},
-    {"AK_BATCH3": "32", "AK_VREG": "1"},
-    {"AK_SUPERCELL3": "1"},                 # single-cell work items (auto-selected for dense data)
-    {"AK_SUPERCELL3": "1", "AK_BATCH3": "16", "AK_CHUNK3": "100"},
+    {"weight_tables": 0},                       # weights evaluated per pass (no plan-time table)
+    {"cell_items3": 2, "chunk3": 256},          # supercell items, small chunks
+    {"cell_items3": 1},                         # single-cell work items (auto-selected for dense data)
+    {"cell_items3": 1, "chunk3": 100},
+    {"cell_items3": 1, "rhs_pair_spread": 0},   # single-cell DFMA spread for every RHS
     # split items: supercell spread, single-cell interpolation over the same sorted points
-    {"AK_DENSE_CELLS": "1e9", "AK_DENSE_CELLS_INTERP": "0"},
-    {"AK_DENSE_CELLS": "1e9", "AK_DENSE_CELLS_INTERP": "0", "AK_CHUNK3": "100"},
+    {"dense_cells3": 1e9, "dense_cells3_interp": 0},
+    {"dense_cells3": 1e9, "dense_cells3_interp": 0, "chunk3": 100},
+    {"generic_kernels": 1},
 ])
-def test_kernel_variants_match_reference(cuda, monkeypatch, variant):
-    """Every tuned kernel variant (selected at plan time) reproduces the reference."""
+def test_kernel_variants_match_reference(cuda, variant):
+    """Every plan-time kernel choice (ak_tuning) reproduces the reference."""
     from paper_2404_17344_b200.fastsum import fast_matvecs
 
-    for k, v in variant.items():
-        monkeypatch.setenv(k, v)
     for name in ("c3", "c4"):
         g = golden(name)
-        plan = _plan(g)
+        plan = _plan(g, tuning=variant)
         res = fast_matvecs(plan, g["V"], dell="dK_dell_default" in g)
         assert rel(res["K"], g["K_default"]) <= TOL, (variant, name)
         if "dK_dell_default" in g:
             assert rel(res["dK_dell"], g["dK_dell_default"]) <= TOL, (variant, name)
 
 
-def test_fused_band_transforms_match_cufft(cuda, monkeypatch):
+def test_fused_band_transforms_match_cufft(cuda):
     """The band-pruned, multiplier-fused 3-D transform stage (ak_fft3.cuh) against the
-    full cuFFT transforms + band multiply (AK_FFT3=cufft) and the reference goldens:
-    default and rough presets, K and dK/dl, 8 RHS."""
+    full cuFFT transforms + band multiply (tuning fused_fft3=0) and the reference
+    goldens: default and rough presets, K and dK/dl, 8 RHS."""
     from paper_2404_17344_b200.fastsum import fast_matvecs
 
+    cufft = {"fused_fft3": 0}
     for name in ("c3", "c4"):
         g = golden(name)
         dell = "dK_dell_default" in g
         outs = {}
         for mode in ("fused", "cufft"):
-            if mode == "cufft":
-                monkeypatch.setenv("AK_FFT3", "cufft")
-            else:
-                monkeypatch.delenv("AK_FFT3", raising=False)
-            outs[mode] = fast_matvecs(_plan(g), g["V"], dell=dell)
+            outs[mode] = fast_matvecs(_plan(g, tuning=cufft if mode == "cufft" else None), g["V"], dell=dell)
             assert rel(outs[mode]["K"], g["K_default"]) <= TOL, (mode, name)
         assert rel(outs["fused"]["K"], outs["cufft"]["K"]) <= 1e-13, name
         if dell:
             assert rel(outs["fused"]["dK_dell"], outs["cufft"]["dK_dell"]) <= 1e-13, name
     g = golden("c4")
     for mode in ("fused", "cufft"):
-        if mode == "cufft":
-            monkeypatch.setenv("AK_FFT3", "cufft")
-        else:
-            monkeypatch.delenv("AK_FFT3", raising=False)
-        outs[mode] = fast_matvecs(_plan(g, preset="rough"), g["V"])["K"]
+        outs[mode] = fast_matvecs(_plan(g, preset="rough", tuning=cufft if mode == "cufft" else None), g["V"])["K"]
     assert rel(outs["fused"], outs["cufft"]) <= 1e-13
 
 
 @pytest.mark.parametrize("sc2", ["1", "8"])
-def test_q2_item_kernels_match_reference(cuda, monkeypatch, sc2):
-    """2-D windows through the single-cell tensor-core kernels (AK_SUPERCELL2=1) and the
-    lane-per-point kernels (8): configs 2 and 5 and the q = 2 NUFFT goldens."""
+def test_q2_item_kernels_match_reference(cuda, sc2):
+    """2-D windows through the single-cell tensor-core kernels (tuning cell_items2=1) and
+    the lane-per-point kernels (8): configs 2 and 5 and the q = 2 NUFFT goldens."""
     from paper_2404_17344_b200.fastsum import build_mixed_plan, fast_matvecs, mixed_matvecs
     from paper_2404_17344_b200.kernels import KernelSpec
     from paper_2404_17344_b200.nufft import NufftPlan, nufft_type1, nufft_type2, prepare_points
 
-    monkeypatch.setenv("AK_SUPERCELL2", sc2)
+    tun = {"cell_items2": int(sc2)}
     g = golden("c2")
-    res = fast_matvecs(_plan(g), g["V"], dell=True)
+    res = fast_matvecs(_plan(g, tuning=tun), g["V"], dell=True)
     assert rel(res["K"], g["K_default"]) <= TOL
     assert rel(res["dK_dell"], g["dK_dell_default"]) <= TOL
     g = golden("c5")
     specs = [KernelSpec(str(f), float(l), 1.0) for f, l in zip(g["families"], g["ells"])]
-    res = mixed_matvecs(build_mixed_plan(specs, _ws(g), "default", _ds(g["X"], g["d_max"])), g["V"])
+    res = mixed_matvecs(build_mixed_plan(specs, _ws(g), "default", _ds(g["X"], g["d_max"]), tuning=tun), g["V"])
     assert rel(res["K"], g["K_default"]) <= TOL
     for w in range(len(specs)):
         assert rel(res["dK_dell"][w], g["dK_dell_default"][w]) <= TOL
     g = golden("nufft")
     for m in (8, 16):
         plan = NufftPlan(dims=2, m=m)
-        geom = prepare_points(plan, g[f"q2_m{m}_pts"])
+        geom = prepare_points(plan, g[f"q2_m{m}_pts"], tuning=tun)
         assert rel(nufft_type1(plan, geom, g[f"q2_m{m}_w"]), g[f"q2_m{m}_type1"]) <= TOL
         assert rel(nufft_type2(plan, geom, g[f"q2_m{m}_c"]), g[f"q2_m{m}_type2"]) <= TOL
 

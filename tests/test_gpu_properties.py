@@ -43,20 +43,6 @@ def test_c4_full_linearity_symmetry_zero(c4_plan):
     np.testing.assert_allclose(fast_dsigma_matvec(plan, v), 2.0 * Kv, rtol=0, atol=1e-13 * np.max(np.abs(Kv)))
 
 
-def test_c4_full_window_parity_vs_oracle(c4_plan):
-    """One 3-D window of config 4 at the full N = 1,000,000 against the oracle."""
-    from oracle import restate as R
-    from paper_2404_17344_b200.fastsum import build_plan, fast_matvec
-    from paper_2404_17344_b200.windows import WindowSet
-
-    wl, _ = c4_plan
-    v = wl.V[0]
-    one = WindowSet(((1, 2, 3),), d_max=3)
-    plan = build_plan(wl.spec, one, "default", wl.data)
-    ref = R.FastSum("gauss", wl.spec.ell, 1.0, [(0, 1, 2)], wl.data.features).matvec(v)
-    assert rel(fast_matvec(plan, v), ref) <= 1e-8
-
-
 def test_batched_rhs_equal_single(c4_plan):
     from paper_2404_17344_b200.fastsum import fast_matvec, fast_matvecs
 
@@ -100,14 +86,14 @@ def test_pinned_host_input(c4_plan, cuda):
     assert rel(res[1], 2.0 * ref) <= 1e-13
 
 
-def _oracle_check(X, windows, v, family="gauss", ell=0.3, d_max=3, preset="default", sf=1.0, tol=1e-8):
+def _oracle_check(X, windows, v, family="gauss", ell=0.3, d_max=3, preset="default", sf=1.0, tol=1e-8, tuning=None):
     from oracle import restate as R
     from paper_2404_17344_b200.fastsum import PRESETS, build_plan, fast_matvec
     from paper_2404_17344_b200.kernels import KernelSpec
     from paper_2404_17344_b200.windows import WindowSet
 
     ws = WindowSet(tuple(tuple(c + 1 for c in w) for w in windows), d_max=d_max)
-    plan = build_plan(KernelSpec(family, ell, sf), ws, preset, _ds(X, d_max))
+    plan = build_plan(KernelSpec(family, ell, sf), ws, preset, _ds(X, d_max), tuning=tuning)
     out = fast_matvec(plan, v)
     ref = R.FastSum(family, ell, sf, windows, X, m=PRESETS.get(preset, preset)).matvec(v)
     assert rel(out, ref) <= tol
@@ -121,28 +107,24 @@ def test_single_point(cuda):
 
 
 @pytest.mark.parametrize("items", ["auto", "single_cell"])
-def test_points_on_the_box_boundary_and_wraparound(cuda, monkeypatch, items):
+def test_points_on_the_box_boundary_and_wraparound(cuda, items):
     """Nodes at -1/2, just below +1/2 and on cell boundaries: footprints wrap."""
-    if items == "single_cell":
-        monkeypatch.setenv("AK_SUPERCELL2", "1")
-        monkeypatch.setenv("AK_SUPERCELL3", "1")
+    tun = {"cell_items2": 1, "cell_items3": 1} if items == "single_cell" else None
     rng = np.random.default_rng(1)
     X = rng.uniform(-0.5, 0.5, size=(600, 6))
     X[:50] = -0.5
     X[50:100] = np.nextafter(0.5, 0.0)
     X[100:150] = np.floor(X[100:150] * 64) / 64  # exact cell boundaries (t integer)
-    _oracle_check(X, [(0, 1, 2), (3, 4), (5,)], rng.normal(size=600), ell=0.2)
+    _oracle_check(X, [(0, 1, 2), (3, 4), (5,)], rng.normal(size=600), ell=0.2, tuning=tun)
 
 
 @pytest.mark.parametrize("items", ["auto", "single_cell"])
-def test_all_points_in_one_cell(cuda, monkeypatch, items):
+def test_all_points_in_one_cell(cuda, items):
     """One heavy cell: exercises work-item chunking (several chunks per supercell)."""
-    if items == "single_cell":
-        monkeypatch.setenv("AK_SUPERCELL2", "1")
-        monkeypatch.setenv("AK_SUPERCELL3", "1")
+    tun = {"cell_items2": 1, "cell_items3": 1} if items == "single_cell" else None
     rng = np.random.default_rng(2)
     X = 0.001 + 1e-5 * rng.random(size=(5000, 3))
-    _oracle_check(X, [(0, 1, 2), (0, 1), (2,)], rng.normal(size=5000))
+    _oracle_check(X, [(0, 1, 2), (0, 1), (2,)], rng.normal(size=5000), tuning=tun)
 
 
 def test_clustered_data_many_chunks(cuda):
@@ -152,23 +134,22 @@ def test_clustered_data_many_chunks(cuda):
     _oracle_check(X, [(0, 1, 2)], rng.normal(size=X.shape[0]), ell=0.5)
 
 
-def test_dense_2d_windows_tensor_core_items(cuda, monkeypatch):
+def test_dense_2d_windows_tensor_core_items(cuda):
     """300k nodes in 2-D windows (mean occupancy ~70 per cell: single-cell tensor-core items
     chosen automatically) against the oracle and against the lane-per-point kernels."""
     rng = np.random.default_rng(7)
     X = rng.uniform(-0.5, 0.5, size=(300_000, 4))
     v = rng.normal(size=300_000)
     auto, _ = _oracle_check(X, [(0, 1), (2, 3), (1, 2)], v, family="matern12", ell=0.3)
-    monkeypatch.setenv("AK_SUPERCELL2", "8")
-    lane, _ = _oracle_check(X, [(0, 1), (2, 3), (1, 2)], v, family="matern12", ell=0.3)
+    lane, _ = _oracle_check(X, [(0, 1), (2, 3), (1, 2)], v, family="matern12", ell=0.3, tuning={"cell_items2": 8})
     assert rel(auto, lane) <= 1e-13
 
 
 @pytest.mark.parametrize("R", [2, 4, 6])
-def test_rhs_pair_tensor_core_spread(cuda, monkeypatch, R):
+def test_rhs_pair_tensor_core_spread(cuda, R):
     """Even RHS counts on densely occupied 3-D windows take the RHS-pair tensor-core
     spread (k_spread3r): each column equals the one-RHS product (DFMA tile), the
-    AK_SPREAD3R=0 batch, and the oracle; footprints on the periodic boundary included."""
+    rhs_pair_spread=0 batch, and the oracle; footprints on the periodic boundary included."""
     from oracle import restate as R_
     from paper_2404_17344_b200.fastsum import build_plan, fast_matvec, fast_matvecs
     from paper_2404_17344_b200.kernels import KernelSpec
@@ -184,15 +165,15 @@ def test_rhs_pair_tensor_core_spread(cuda, monkeypatch, R):
     res = fast_matvecs(plan, V, dell=True)
     for r in range(R):
         assert rel(res["K"][r], fast_matvec(plan, V[r])) <= 1e-13
-    monkeypatch.setenv("AK_SPREAD3R", "0")
-    ref = fast_matvecs(plan, V, dell=True)
+    ref = fast_matvecs(build_plan(KernelSpec("gauss", 0.3), ws, "default", _ds(X, 3), tuning={"rhs_pair_spread": 0}),
+                       V, dell=True)
     assert rel(res["K"], ref["K"]) <= 1e-13 and rel(res["dK_dell"], ref["dK_dell"]) <= 1e-13
     orc = R_.FastSum("gauss", 0.3, 1.0, [(0, 1, 2), (3, 4, 5)], X).matvec(V[R - 1])
     assert rel(res["K"][R - 1], orc) <= 1e-8
 
 
 @pytest.mark.parametrize("kernels", ["tuned", "generic"])
-def test_row_masked_windows(cuda, monkeypatch, kernels):
+def test_row_masked_windows(cuda, kernels):
     """build_plan(row_masks=...) (ak_geom_create_masked): each window uses only its
     rows -- equal to plans built on the row subsets, zeros elsewhere; all-true masks
     equal the unmasked plan."""
@@ -202,8 +183,7 @@ def test_row_masked_windows(cuda, monkeypatch, kernels):
     from paper_2404_17344_b200.kernels import KernelSpec
     from paper_2404_17344_b200.windows import WindowSet
 
-    if kernels == "generic":
-        monkeypatch.setenv("AK_FORCE_GENERIC", "1")
+    tun = {"generic_kernels": 1} if kernels == "generic" else None
     rng = np.random.default_rng(31)
     N = 40_000
     X = rng.uniform(-0.14, 0.14, size=(N, 7))
@@ -211,20 +191,22 @@ def test_row_masked_windows(cuda, monkeypatch, kernels):
     ds = _ds(X, 3)
     ws = WindowSet(((1, 2, 3), (4, 5), (6,), (2, 4, 7)), d_max=3)
     spec = KernelSpec("gauss", 0.4)
-    full = fast_matvecs(build_plan(spec, ws, "default", ds), V, dell=True)
-    ones = fast_matvecs(build_plan(spec, ws, "default", ds, row_masks=np.ones((4, N), bool)), V, dell=True)
+    full = fast_matvecs(build_plan(spec, ws, "default", ds, tuning=tun), V, dell=True)
+    ones = fast_matvecs(build_plan(spec, ws, "default", ds, row_masks=np.ones((4, N), bool), tuning=tun), V,
+                        dell=True)
     assert rel(ones["K"], full["K"]) <= 1e-13 and rel(ones["dK_dell"], full["dK_dell"]) <= 1e-13
     masks = rng.random((4, N)) < np.array([0.3, 0.5, 0.7, 0.0])[:, None]
     masks[3, :5] = True                          # a nearly empty window
     masks[2] = False                             # an empty one
-    got = fast_matvecs(build_plan(spec, ws, "default", ds, row_masks=masks), V, dell=True)
+    got = fast_matvecs(build_plan(spec, ws, "default", ds, row_masks=masks, tuning=tun), V, dell=True)
     want = {k: np.zeros_like(got[k]) for k in ("K", "dK_dell")}
     for w, win in enumerate(ws.windows):
         rows = np.flatnonzero(masks[w])
         if not len(rows):
             continue
         sub = replace(ds, features=X[rows], targets=ds.targets[rows])
-        part = fast_matvecs(build_plan(spec, WindowSet((win,), d_max=3), "default", sub), V[:, rows], dell=True)
+        part = fast_matvecs(build_plan(spec, WindowSet((win,), d_max=3), "default", sub, tuning=tun), V[:, rows],
+                            dell=True)
         for k in want:
             want[k][:, rows] += part[k]
     assert rel(got["K"], want["K"]) <= 1e-13 and rel(got["dK_dell"], want["dK_dell"]) <= 1e-13
@@ -457,23 +439,6 @@ def test_concurrent_streams_share_a_plan(cuda):
     assert not errors, errors
     for k in range(2):
         assert rel(outs[k].cpu().numpy(), refs[k].cpu().numpy()) <= 1e-13
-
-
-@pytest.mark.parametrize("name", ["C2", "C3"])
-def test_full_size_config_vs_oracle(cuda, name):
-    """Configs 2 and 3 at their full BASELINE sizes (20k and 100k nodes) against the oracle:
-    K and dK/dl for the first RHS, every window."""
-    from oracle import restate as R
-    from paper_2404_17344_b200 import configs
-    from paper_2404_17344_b200.fastsum import build_plan, fast_matvecs
-
-    wl = configs.CONFIGS[name]()
-    plan = build_plan(wl.spec, wl.window_set, "default", wl.data)
-    res = fast_matvecs(plan, wl.V, dell=True)
-    cols = [wl.window_set.columns(w) for w in wl.window_set]
-    for fam, key in ((wl.spec.family, "K"), ("der_" + wl.spec.family, "dK_dell")):
-        ref = R.FastSum(fam, wl.spec.ell, wl.spec.sigma_f, cols, wl.data.features).matvec(wl.V[0], threads=8)
-        assert rel(res[key][0], ref) <= 1e-8, (name, key)
 
 
 def test_c5_full_size_properties(cuda):

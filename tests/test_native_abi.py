@@ -98,3 +98,46 @@ def test_argument_validation_without_a_device():
     code(lib.ak_type1_band(4, 64, 32, None, None, None, None, None), "type1")
     code(lib.ak_type2_grid(3, 64, 128, None, None, None, None, None), "type2")
     code(lib.ak_dense_apply(9, 1.0, 1.0, 1, q, cols, None, 0, 3, None, 0, 3, None, None, None, None), "dense")
+
+
+def test_tuning_defaults_and_validation():
+    """ak_tuning: the defaults the library uses (the measured heuristics)
+    and rejection of out-of-range values by ak_geom_create_ex before any device work.
+    The library reads no environment variables (the kernel choice is a plan property)."""
+    import ctypes
+
+    import pytest
+
+    from paper_2404_17344_b200.nufft import NufftPlan
+
+    t = _native.tuning()
+    assert (t.weight_tables, t.cell_items3, t.cell_items2, t.chunk3, t.rhs_pair_spread, t.fused_fft3,
+            t.generic_kernels) == (1, 0, 0, 0, 1, 1, 0)
+    assert (t.dense_cells3, t.dense_cells3_interp, t.dense_cells2) == (300.0, 64.0, 2.0)
+    with pytest.raises(ValueError):
+        _native.tuning(no_such_knob=1)
+    lib = _native.lib()
+    wf = NufftPlan(dims=3, m=32).window_fn()
+    out = ctypes.c_void_p()
+    q = (ctypes.c_int32 * 1)(3)
+    cols = (ctypes.c_int32 * 3)(0, 1, 2)
+    X = ctypes.c_void_p(1)
+    for bad in ({"cell_items3": 3}, {"cell_items2": 2}, {"chunk3": 10}, {"dense_cells3": -1.0}):
+        rc = lib.ak_geom_create_ex(64, 1, q, cols, X, 10, 3, None, None, ctypes.byref(wf),
+                                   ctypes.byref(_native.tuning(**bad)), None, ctypes.byref(out))
+        assert rc == _native.AK_ERR_INVALID and b"tuning" in lib.ak_last_error(), bad
+    rows_in = (ctypes.c_int64 * 1)(10)
+    rc = lib.ak_geom_create_ex(64, 1, q, cols, X, 10, 3, None, rows_in, ctypes.byref(wf), None, None,
+                               ctypes.byref(out))
+    assert rc == _native.AK_ERR_INVALID
+    # no environment reads in the library's own sources (the CUDA runtime linked into it
+    # reads CUDA_* variables itself)
+    for src in (ROOT / "paper_2404_17344_b200" / "csrc").iterdir():
+        assert "getenv" not in src.read_text(), src.name
+
+
+def test_profiler_report_empty_without_launches():
+    lib = _native.lib()
+    assert lib.ak_prof_enable(0) == 0
+    assert lib.ak_prof_reset() == 0
+    assert lib.ak_prof_report(None, 0) == 1   # empty report: just the terminator

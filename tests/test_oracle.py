@@ -184,3 +184,69 @@ def test_oracle_nufft_dense_boundary_cells():
         geom = R.Geometry(plan, g[f"q{q}_pts"])
         assert rel(R.type1(plan, geom, g[f"q{q}_w"]), g[f"q{q}_type1"]) <= 1e-13
         assert rel(R.type2(plan, geom, g[f"q{q}_c"]), g[f"q{q}_type2"]) <= 1e-13
+
+
+def test_fullsize_oracle_matches_reference_c5_and_c3():
+    """oracle/fullsize.py (row chunks on a thread pool, one window at a time, one
+    spread shared by K and dK/dl) reproduces the reference's own outputs."""
+    from oracle.fullsize import products
+
+    g = golden("c5")
+    wins = windows_of(g)
+    specs = [(str(g["families"][k]), float(g["ells"][k]), 1.0) for k in range(len(wins))]
+    res = products(g["X"], wins, specs, g["V"], dell=True, per_window_dell=True, threads=4, chunks=3)
+    for r in range(len(g["V"])):
+        assert rel(res["K"][r], g["K_default"][r]) <= 1e-13
+        for k in range(len(wins)):
+            assert rel(res["dK_dell"][k, r], g["dK_dell_default"][k, r]) <= 1e-13
+    g = golden("c3")
+    fam, ell, sf = str(g["families"][0]), float(g["ells"][0]), float(g["sigma_f"])
+    wins = windows_of(g)
+    res = products(g["X"], wins, [(fam, ell, sf)] * len(wins), g["V"], dell=True, threads=3, chunks=5)
+    for r in range(len(g["V"])):
+        assert rel(res["K"][r], g["K_default"][r]) <= 1e-13
+        assert rel(res["dK_dell"][r], g["dK_dell_default"][r]) <= 1e-13
+
+
+def test_bounds_match_reference():
+    """oracle/bounds.py (Theorems 3.2/3.3) reproduces the reference's analytic_bound
+    (bounds.py:103-130) on a grid covering every branch, including eta < 1 refusals,
+    and dominates the reference's measured worst case."""
+    from oracle import bounds as B
+
+    g = golden("bounds")
+    for fam in ("gauss", "der_gauss"):
+        for q in (1, 3):
+            tab = g[f"{fam}_q{q}"]
+            for i, ell in enumerate(g["ells"]):
+                for j, m in enumerate(g["ms"]):
+                    if np.isnan(tab[i, j]):
+                        with pytest.raises(B.EtaTooSmall):
+                            B.analytic_bound(fam, q, float(ell), int(m))
+                    else:
+                        got = B.analytic_bound(fam, q, float(ell), int(m))
+                        assert abs(got - tab[i, j]) <= 1e-14 * abs(tab[i, j]), (fam, q, ell, m)
+    cells = (("gauss", 1, 0.1, 16), ("gauss", 3, 0.3, 16), ("der_gauss", 1, 0.2, 16), ("der_gauss", 3, 0.5, 8))
+    for (fam, q, ell, m), meas in zip(cells, g["measured"]):
+        assert meas <= B.analytic_bound(fam, q, ell, m)
+    with pytest.raises(ValueError):
+        B.analytic_bound("matern12", 3, 1.0, 32)
+    with pytest.raises(ValueError):
+        B.analytic_bound("gauss", 2, 1.0, 32)
+
+
+def test_oracle_c1_within_paper_bound():
+    """The reference algorithm (oracle) on BASELINE config 1 at full size stays within the
+    per-entry analytic bound of the exact dense product."""
+    from oracle.bounds import per_entry_bound
+
+    from paper_2404_17344_b200 import configs
+
+    wl = configs.config1()
+    cols = [wl.window_set.columns(w) for w in wl.window_set]
+    v = wl.V[0]
+    for fam in ("gauss", "der_gauss"):
+        fast = R.FastSum(fam, wl.spec.ell, 1.0, cols, wl.data.features).matvec(v)
+        dense = R.dense_matvec(fam, wl.spec.ell, 1.0, cols, wl.data.features, v)
+        bound = per_entry_bound(fam, wl.window_set.lengths, wl.spec.ell, 32, 1.0, v)
+        assert np.max(np.abs(fast - dense)) <= bound

@@ -1,6 +1,6 @@
-"""Device time of one step of configs 2, 3 and 5 (current env knobs), CUDA events.
+"""Device time of one step of configs 2, 3 and 5, CUDA events.
 
-    AK_SUPERCELL2=8 python tools/cfg_time.py
+    python tools/cfg_time.py [cell_items2=8,...]   (ak_tuning overrides)
 """
 import json
 import os
@@ -22,14 +22,18 @@ def timed(fn, reps):
     return bench.cuda_time(torch, fn, reps)
 
 
-out = {"env": {k: v for k, v in os.environ.items() if k.startswith("AK_")}}
+tun = {}
+for kv in filter(None, (sys.argv[1] if len(sys.argv) > 1 else "").split(",")):
+    k, v = kv.split("=")
+    tun[k] = float(v) if "." in v or "e" in v else int(v)
+out = {"tuning": tun}
 for name in ("C2", "C3"):
     wl = configs.CONFIGS[name]()
-    plan = build_plan(wl.spec, wl.window_set, "default", wl.data)
+    plan = build_plan(wl.spec, wl.window_set, "default", wl.data, tuning=tun)
     V = torch.as_tensor(wl.V, device="cuda")
     out[name] = timed(lambda: fast_matvecs(plan, V, dell=True), 10)
 wl = configs.config5()
-plan = build_mixed_plan(wl.specs, wl.window_set, "default", wl.data)
+plan = build_mixed_plan(wl.specs, wl.window_set, "default", wl.data, tuning=tun)
 V = torch.as_tensor(wl.V, device="cuda")
 out["C5"] = timed(lambda: mixed_matvecs(plan, V), 3)
 print(json.dumps(out))

@@ -1,6 +1,6 @@
 """RHS pairs vs cell density: config-4 data at N rows, R = 2 / 8 RHS, K V device time
 with the plan's automatic supercell choice and with single-cell items forced
-(AK_SUPERCELL3=1, which the RHS-pair tensor-core spread needs).
+(tuning cell_items3=1, which the RHS-pair tensor-core spread needs).
 
     python tools/rhs_pair_density.py
 """
@@ -20,7 +20,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "--one":
 
     n, R = int(sys.argv[2]), int(sys.argv[3])
     wl = configs.config4(n)
-    plan = build_plan(wl.spec, wl.window_set, "default", wl.data)
+    tun = {"cell_items3": 1} if len(sys.argv) > 4 and sys.argv[4] == "single_cell" else None
+    plan = build_plan(wl.spec, wl.window_set, "default", wl.data, tuning=tun)
     import numpy as np
 
     V = torch.as_tensor(np.random.default_rng(0).normal(size=(R, n)), device="cuda")
@@ -40,9 +41,9 @@ res = []
 for n in (125_000, 250_000, 500_000):
     for R in (2, 8):
         row = {"N": n, "R": R}
-        for tag, env in (("auto", {}), ("single_cell", {"AK_SUPERCELL3": "1"})):
-            out = subprocess.run([sys.executable, __file__, "--one", str(n), str(R)], capture_output=True, text=True,
-                                 env={**os.environ, **env})
+        for tag in ("auto", "single_cell"):
+            out = subprocess.run([sys.executable, __file__, "--one", str(n), str(R), tag], capture_output=True,
+                                 text=True)
             row[tag] = json.loads(out.stdout.strip().splitlines()[-1])["ms"]
         res.append(row)
         print(json.dumps(row), flush=True)
