@@ -415,6 +415,8 @@ def cpu_baseline(wl, gpu_window0):
 
 
 def _kernel_q(name: str) -> int:
+    if not name.startswith("k_"):
+        return 0       # cuFFT transforms (library)
     if name.startswith(("k_spread3", "k_interp3")):
         return 3
     if name.startswith(("k_spread2", "k_interp2")) or "<2>" in name:

@@ -25,6 +25,8 @@
 #include "ak_q3c.cuh"
 #include "ak_q2c.cuh"
 #include "ak_q3r.cuh"
+#include "ak_q1r.cuh"
+#include "ak_q2r.cuh"
 #include "ak_fft3.cuh"
 
 using namespace ak;
@@ -923,6 +925,70 @@ static const char* launch_spread_tile(const ak_geom* g, int64_t i0, int64_t ni, 
     return Q == 2 ? "k_spread_tile<2>" : "k_spread_tile<1>";
 }
 
+// q = 1, RHS-minor data, R >= 8: RHS across the lanes (ak_q1r.cuh), RC RHS per warp
+static int q1r_chunk(int R) { return R <= 8 ? 8 : (R <= 16 ? 16 : 32); }
+
+static const char* launch_spread1r(const ak_geom* g, int64_t i0, int64_t ni, const double* V, Strides vs, int R,
+                                   double* grids, cudaStream_t st)
+{
+    const int rc = q1r_chunk(R);
+    const dim3 grid((unsigned)(ni * Q1_SPLIT), (unsigned)((R + rc - 1) / rc));
+    if (rc == 8) k_spread1r<12, 8><<<grid, 32, 0, st>>>(g->pts, g->items + i0, V, vs, grids, g->canon_off_d, R, g->n, g->wf);
+    else if (rc == 16) k_spread1r<12, 16><<<grid, 32, 0, st>>>(g->pts, g->items + i0, V, vs, grids, g->canon_off_d, R, g->n, g->wf);
+    else k_spread1r<12, 32><<<grid, 32, 0, st>>>(g->pts, g->items + i0, V, vs, grids, g->canon_off_d, R, g->n, g->wf);
+    return "k_spread1r";
+}
+
+static const char* launch_interp1r(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R,
+                                   const double* scale, double* out, Strides os, int atomic_out, int64_t wstride,
+                                   cudaStream_t st)
+{
+    const int rc = q1r_chunk(R);
+    const dim3 grid((unsigned)(ni * Q1_SPLIT), (unsigned)((R + rc - 1) / rc));
+    if (rc == 8)
+        k_interp1r<12, 8><<<grid, 32, 0, st>>>(g->pts, g->items + i0, grids, g->canon_off_d, R, g->n, g->wf, scale,
+                                               out, os, atomic_out, wstride);
+    else if (rc == 16)
+        k_interp1r<12, 16><<<grid, 32, 0, st>>>(g->pts, g->items + i0, grids, g->canon_off_d, R, g->n, g->wf, scale,
+                                                out, os, atomic_out, wstride);
+    else
+        k_interp1r<12, 32><<<grid, 32, 0, st>>>(g->pts, g->items + i0, grids, g->canon_off_d, R, g->n, g->wf, scale,
+                                                out, os, atomic_out, wstride);
+    return "k_interp1r";
+}
+
+// q = 2 single-cell items, RHS-minor data, R >= 8: 8 RHS per warp, NW warps per item
+static int q2r_warps(int R) { return R <= 8 ? 1 : (R <= 16 ? 2 : 4); }
+
+static const char* launch_spread2r(const ak_geom* g, int64_t i0, int64_t ni, const double* V, Strides vs, int R,
+                                   double* grids, cudaStream_t st)
+{
+    const int nw = q2r_warps(R);
+    const dim3 grid((unsigned)ni, (unsigned)((R + 8 * nw - 1) / (8 * nw)));
+#define AK_S2R(NW) k_spread2r<32, NW><<<grid, 32 * NW, 0, st>>>(g->CI2, g->W2, g->wshift_d, g->items + i0, V, vs, \
+                                                               grids, g->canon_off_d, R, g->n)
+    if (nw == 1) AK_S2R(1);
+    else if (nw == 2) AK_S2R(2);
+    else AK_S2R(4);
+#undef AK_S2R
+    return "k_spread2r";
+}
+
+static const char* launch_interp2r(const ak_geom* g, int64_t i0, int64_t ni, const double* grids, int R,
+                                   const double* scale, double* out, Strides os, int atomic_out, int64_t wstride,
+                                   cudaStream_t st)
+{
+    const int nw = q2r_warps(R);
+    const dim3 grid((unsigned)ni, (unsigned)((R + 8 * nw - 1) / (8 * nw)));
+#define AK_I2R(NW) k_interp2r<32, NW><<<grid, 32 * NW, 0, st>>>(g->CI2, g->W2, g->wshift_d, g->items + i0, grids, \
+                                                                g->canon_off_d, R, g->n, scale, out, os, atomic_out, wstride)
+    if (nw == 1) AK_I2R(1);
+    else if (nw == 2) AK_I2R(2);
+    else AK_I2R(4);
+#undef AK_I2R
+    return "k_interp2r";
+}
+
 template <int T>
 static const char* launch_spread3_t(const ak_geom* g, int64_t i0, int64_t ni, const double* V, Strides vs, int R,
                                     double* grids, cudaStream_t st)
@@ -967,6 +1033,8 @@ static int spread_group(const ak_geom* g, int q, const double* V, Strides vs, in
         if (q == 3 && T == 12) name = launch_spread3_t<12>(g, i0, ni, V, vs, R, grids, st);
         else if (q == 3 && T == 8) name = launch_spread3_t<8>(g, i0, ni, V, vs, R, grids, st);
         else if (q == 3 && T == 4) name = launch_spread3_t<4>(g, i0, ni, V, vs, R, grids, st);
+        else if (q == 2 && T == 12 && g->cached2 && g->sedge[2] == 1 && vs.rs == 1 && R >= 8)
+            name = launch_spread2r(g, i0, ni, V, vs, R, grids, st);
         else if (q == 2 && T == 12 && g->cached2 && g->sedge[2] == 1) {
             k_spread2c<32><<<(unsigned)(ni * R), 32, 0, st>>>(g->CI2, g->W2, g->wshift_d, g->items + i0, V, vs, grids,
                                                               g->canon_off_d, R, g->n);
@@ -976,6 +1044,7 @@ static int spread_group(const ak_geom* g, int q, const double* V, Strides vs, in
         else if (q == 2 && T == 8) name = launch_spread_tile<2, 8>(g, i0, ni, V, vs, R, grids, st);
         else if (q == 2 && T == 16) name = launch_spread_tile<2, 16>(g, i0, ni, V, vs, R, grids, st);
         else if (q == 2 && T == 4) name = launch_spread_tile<2, 4>(g, i0, ni, V, vs, R, grids, st);
+        else if (q == 1 && T == 12 && vs.rs == 1 && R >= 8) name = launch_spread1r(g, i0, ni, V, vs, R, grids, st);
         else if (q == 1 && T == 12) name = launch_spread_tile<1, 12>(g, i0, ni, V, vs, R, grids, st);
         else if (q == 1 && T == 8) name = launch_spread_tile<1, 8>(g, i0, ni, V, vs, R, grids, st);
         else if (q == 1 && T == 16) name = launch_spread_tile<1, 16>(g, i0, ni, V, vs, R, grids, st);
@@ -1049,11 +1118,15 @@ static int interp_group(const ak_geom* g, int q, const double* grids, int R, con
         if (q == 3 && T == 12) name = launch_interp3_t<12>(g, i0, ni, grids, R, scale, out, os, atomic_out, ws, st);
         else if (q == 3 && T == 8) name = launch_interp3_t<8>(g, i0, ni, grids, R, scale, out, os, atomic_out, ws, st);
         else if (q == 3 && T == 4) name = launch_interp3_t<4>(g, i0, ni, grids, R, scale, out, os, atomic_out, ws, st);
+        else if (q == 2 && T == 12 && g->cached2 && g->sedge[2] == 1 && os.rs == 1 && R >= 8)
+            name = launch_interp2r(g, i0, ni, grids, R, scale, out, os, atomic_out, ws, st);
         else if (q == 2 && T == 12 && g->cached2 && g->sedge[2] == 1) {
             k_interp2c<32><<<(unsigned)(ni * R), 32, 0, st>>>(g->CI2, g->W2, g->wshift_d, g->items + i0, grids,
                                                               g->canon_off_d, R, g->n, scale, out, os, atomic_out, ws);
             name = "k_interp2c";
         }
+        else if (q == 1 && T == 12 && os.rs == 1 && R >= 8)
+            name = launch_interp1r(g, i0, ni, grids, R, scale, out, os, atomic_out, ws, st);
 #define AK_LANE(QQ, TT) \
         else if (q == QQ && T == TT) name = launch_interp_lane<QQ, TT>(g, i0, ni, grids, R, scale, out, os, atomic_out, ws, st);
         AK_LANE(2, 4) AK_LANE(2, 6) AK_LANE(2, 8) AK_LANE(2, 10) AK_LANE(2, 12) AK_LANE(2, 14) AK_LANE(2, 16)

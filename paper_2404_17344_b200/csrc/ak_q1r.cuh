@@ -1,0 +1,202 @@
+// q = 1 spread / interpolation with the RHS index across the lanes (RHS-minor data).
+//
+// A 1-D window has 12 taps per point: per point and RHS the gridding work is 12
+// FMAs, so with R right-hand sides the kernels are bound by moving the R values
+// of each point (one cache line at R = 16 in the RHS-minor layout), not by FP64.
+// One warp = a quarter of a work item (a chunk of <= 2048 bin-sorted points of a
+// 16-cell supercell) x one chunk of RC right-hand sides:
+//   lanes = SP point streams x RC RHS lanes (SP = 32 / RC);
+//   per batch of 32 points each lane evaluates the 12 window weights of one
+//   point (the weights serve all RC RHS) and the warp gathers / scatters the
+//   points' RHS values as whole lines (lane = RHS within a point: coalesced);
+//   interp: a stream keeps its current cell's 12 grid values per RHS lane in
+//           registers and contracts them with each point's weights;
+//   spread: a stream accumulates a cell run in registers (12 per lane), flushes
+//           into its own shared region tile on a cell change; the streams' tiles
+//           are summed and added to the grid with one RED per region value.
+// Replaces the lane-per-point kernels (ak_kernels.cuh) for R >= 8 RHS-minor
+// products: those recompute the weights per RHS and touch one 8-byte value per
+// point per CTA.
+#pragma once
+#include "ak_common.cuh"
+
+namespace ak {
+
+template <int RC>
+struct Q1Lanes {
+    static constexpr int SP = 32 / RC;   // point streams per warp
+};
+
+// Launch-time split of a work item into Q1_SPLIT contiguous point ranges (one warp
+// each): a q = 1 item holds up to 2048 points of one 16-cell supercell, and a warp
+// per item leaves too few warps in flight to cover the gather latency.
+constexpr int Q1_SPLIT = 4;
+
+__device__ __forceinline__ void q1_range(const WorkItem& it, int part, int& beg, int& end) {
+    beg = it.start + (int)((int64_t)it.count * part / Q1_SPLIT);
+    end = it.start + (int)((int64_t)it.count * (part + 1) / Q1_SPLIT);
+}
+
+// weights, local cell offset and row of the batch's points (one point per lane,
+// already in registers: the next batch's records are loaded before this one is used)
+template <int T>
+__device__ __forceinline__ void q1_stage(const Point& p, bool valid, int sc0, int lane, const ak_window_fn& wf,
+                                         double (*wst)[T], int* lst, int* ist)
+{
+    if (valid) {
+        double w[T];
+        window_weights<T>(wf, p.s[0], w);
+#pragma unroll
+        for (int a = 0; a < T; ++a) wst[lane][a] = w[a];
+        lst[lane] = cell_axis(p.cell, 0) - sc0 * 16;
+        ist[lane] = p.idx;
+    }
+}
+
+template <int T, int RC>
+__global__ void __launch_bounds__(32, 24)
+k_interp1r(const Point* __restrict__ pts, const WorkItem* __restrict__ items, const double* __restrict__ grids,
+           const int64_t* __restrict__ canon_off, int nrhs, int n, const ak_window_fn wf,
+           const double* __restrict__ scale, double* __restrict__ out, Strides os, int atomic_out, int64_t wstride)
+{
+    constexpr int S = 16, REG = S + T - 1, SP = Q1Lanes<RC>::SP;
+    __shared__ double tile[REG][RC];
+    __shared__ __align__(16) double wst[32][T];
+    __shared__ int lst[32], ist[32];
+
+    const WorkItem it = items[blockIdx.x / Q1_SPLIT];
+    int beg, end;
+    q1_range(it, blockIdx.x % Q1_SPLIT, beg, end);
+    const int r0 = blockIdx.y * RC;
+    const int lane = threadIdx.x, rl = lane % RC, sp = lane / RC;
+    const int nr = min(RC, nrhs - r0);
+    const int sc0 = it.sc & 1023;
+    const int o0 = sc0 * S - (T / 2 - 1);
+    Point pn;
+    if (lane < end - beg) pn = pts[beg + lane];
+    {
+        const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r0 * n;
+        for (int e = lane; e < REG * RC; e += 32) {
+            const int i = e / RC, rr = e - i * RC;
+            tile[i][rr] = rr < nr ? __ldg(g + (int64_t)rr * n + wrap(o0 + i, n)) : 0.0;
+        }
+    }
+    const double sc = scale[it.window];
+    double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)(r0 + rl) * os.rs;
+    int cur = -1;
+    double tv[T];
+    for (int base = beg; base < end; base += 32) {
+        const int nb = min(32, end - base);
+        const Point p = pn;
+        if (lane < end - base - 32) pn = pts[base + 32 + lane];
+        __syncwarp();
+        q1_stage<T>(p, lane < nb, sc0, lane, wf, wst, lst, ist);
+        __syncwarp();
+        // stream sp, lane rl: point j, RHS r0 + rl -- the RC lanes of a stream write one
+        // point's RC values (a whole line at RC = 16 in the RHS-minor layout)
+        for (int j = sp; j < nb; j += SP) {
+            const int l = lst[j];
+            if (l != cur) {
+                cur = l;
+#pragma unroll
+                for (int a = 0; a < T; ++a) tv[a] = tile[l + a][rl];
+            }
+            double acc = 0.0;
+#pragma unroll
+            for (int a = 0; a < T; ++a) acc = fma(wst[j][a], tv[a], acc);
+            if (rl < nr) {
+                double* dst = o + (int64_t)ist[j] * os.is;
+                if (atomic_out) red_add(dst, sc * acc);
+                else *dst = sc * acc;
+            }
+        }
+    }
+}
+
+template <int T, int RC>
+__global__ void __launch_bounds__(32, 16)
+k_spread1r(const Point* __restrict__ pts, const WorkItem* __restrict__ items, const double* __restrict__ V,
+           Strides vs, double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n,
+           const ak_window_fn wf)
+{
+    constexpr int S = 16, REG = S + T - 1, SP = Q1Lanes<RC>::SP, PPS = 32 / SP;   // points per stream per batch
+    __shared__ double tile[SP][REG][RC];
+    __shared__ __align__(16) double wst[32][T];
+    __shared__ double vst[32][RC];
+    __shared__ int lst[32];
+
+    const WorkItem it = items[blockIdx.x / Q1_SPLIT];
+    int beg, end;
+    q1_range(it, blockIdx.x % Q1_SPLIT, beg, end);
+    const int r0 = blockIdx.y * RC;
+    const int lane = threadIdx.x, rl = lane % RC, sp = lane / RC;
+    const int nr = min(RC, nrhs - r0);
+    const int sc0 = it.sc & 1023;
+    Point pn;
+    if (lane < end - beg) pn = pts[beg + lane];
+    for (int e = lane; e < SP * REG * RC; e += 32) (&tile[0][0][0])[e] = 0.0;
+    const double* __restrict__ Vr = V + (int64_t)(r0 + rl) * vs.rs;
+
+    int cur = -1;
+    double acc[T];
+#pragma unroll
+    for (int a = 0; a < T; ++a) acc[a] = 0.0;
+    for (int base = beg; base < end; base += 32) {
+        const int nb = min(32, end - base);
+        const Point p = pn;
+        if (lane < end - base - 32) pn = pts[base + 32 + lane];
+        // the stream's RHS values of the batch (point j = sp + SP k, RHS r0 + rl): all
+        // loads issued before the weights are evaluated; a stream's RC lanes read one
+        // line per point
+        double vv[PPS];
+#pragma unroll
+        for (int k = 0; k < PPS; ++k) {
+            const int j = sp + SP * k;
+            const int idx = __shfl_sync(0xffffffffu, p.idx, j);
+            vv[k] = (j < nb && rl < nr) ? __ldg(Vr + (int64_t)idx * vs.is) : 0.0;
+        }
+        __syncwarp();
+        if (lane < nb) {
+            double w[T];
+            window_weights<T>(wf, p.s[0], w);
+#pragma unroll
+            for (int a = 0; a < T; ++a) wst[lane][a] = w[a];
+            lst[lane] = cell_axis(p.cell, 0) - sc0 * 16;
+        }
+#pragma unroll
+        for (int k = 0; k < PPS; ++k) vst[sp + SP * k][rl] = vv[k];
+        __syncwarp();
+        for (int j = sp; j < nb; j += SP) {
+            const int l = lst[j];
+            if (l != cur) {
+                if (cur >= 0) {
+#pragma unroll
+                    for (int a = 0; a < T; ++a) {
+                        tile[sp][cur + a][rl] += acc[a];
+                        acc[a] = 0.0;
+                    }
+                }
+                cur = l;
+            }
+            const double v = vst[j][rl];
+#pragma unroll
+            for (int a = 0; a < T; ++a) acc[a] = fma(wst[j][a], v, acc[a]);
+        }
+    }
+    if (cur >= 0) {
+#pragma unroll
+        for (int a = 0; a < T; ++a) tile[sp][cur + a][rl] += acc[a];
+    }
+    __syncwarp();
+    const int o0 = sc0 * S - (T / 2 - 1);
+    double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r0 * n;
+    for (int e = lane; e < REG * RC; e += 32) {
+        const int i = e / RC, rr = e - i * RC;
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < SP; ++k) s += tile[k][i][rr];
+        if (rr < nr && s != 0.0) red_add(g + (int64_t)rr * n + wrap(o0 + i, n), s);
+    }
+}
+
+}  // namespace ak

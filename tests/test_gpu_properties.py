@@ -503,3 +503,74 @@ def test_plans_release_device_memory(cuda):
     torch.cuda.empty_cache()
     free1 = torch.cuda.mem_get_info()[0]
     assert free0 - free1 < 64 * 2**20, (free0 - free1) / 2**20
+
+
+@pytest.mark.parametrize("R", [8, 11, 16, 33])
+def test_q1_rhs_lane_kernels(cuda, R):
+    """R >= 8 RHS on 1-D windows run with the RHS across the lanes (k_spread1r /
+    k_interp1r, RHS-minor data): every column equals the one-RHS product (lane-per-point
+    kernels) and the oracle; per-window outputs (mixed plans) and the wrap-around
+    boundary included; R = 33 spans two RHS chunks."""
+    from oracle import restate as R_
+    from paper_2404_17344_b200 import _native
+    from paper_2404_17344_b200.fastsum import build_mixed_plan, build_plan, fast_matvec, fast_matvecs, mixed_matvecs
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    rng = np.random.default_rng(40 + R)
+    N = 60_000
+    X = np.concatenate([rng.normal(scale=0.05, size=(N - 3000, 3)), rng.uniform(-0.5, -0.48, size=(3000, 3))])
+    X = np.clip(X, -0.5, 0.49)
+    V = rng.normal(size=(R, N))
+    ws = WindowSet(((1,), (2,), (3,)), d_max=3)
+    plan = build_plan(KernelSpec("matern12", 0.2), ws, "default", _ds(X, 3))
+    with _native.KernelTimer() as kt:
+        res = fast_matvecs(plan, V, dell=True)
+    assert "k_spread1r" in kt.report and "k_interp1r" in kt.report, kt.report
+    for r in (0, R // 2, R - 1):
+        assert rel(res["K"][r], fast_matvec(plan, V[r])) <= 1e-13
+    orc = R_.FastSum("matern12", 0.2, 1.0, [(0,), (1,), (2,)], X).matvec(V[R - 1])
+    assert rel(res["K"][R - 1], orc) <= 1e-8
+    mplan = build_mixed_plan([KernelSpec("matern12", 0.2), KernelSpec("gauss", 0.3), KernelSpec("matern12", 0.5)],
+                             ws, "default", _ds(X, 3))
+    mix = mixed_matvecs(mplan, V)
+    for w, (fam, ell) in enumerate((("matern12", 0.2), ("gauss", 0.3), ("matern12", 0.5))):
+        one = build_plan(KernelSpec(fam, ell), WindowSet((ws.windows[w],), d_max=3), "default", _ds(X, 3))
+        col = fast_matvecs(one, V[R - 1], dell=True)["dK_dell"]
+        assert rel(mix["dK_dell"][w][R - 1], col) <= 1e-13
+
+
+@pytest.mark.parametrize("R", [8, 12, 16, 40])
+def test_q2_rhs_batched_kernels(cuda, R):
+    """R >= 8 RHS on densely occupied 2-D windows run one CTA per cell item for 8 RHS per
+    warp (k_spread2r / k_interp2r, RHS-minor data): every column equals the one-RHS
+    product (k_spread2c / k_interp2c) and the oracle; per-window outputs and wrapping
+    footprints included; R = 12 and 40 leave partial warps / CTAs."""
+    from oracle import restate as R_
+    from paper_2404_17344_b200 import _native
+    from paper_2404_17344_b200.fastsum import build_mixed_plan, build_plan, fast_matvec, fast_matvecs, mixed_matvecs
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    rng = np.random.default_rng(60 + R)
+    N = 50_000
+    X = np.concatenate([rng.uniform(-0.1, 0.1, size=(N - 4000, 4)), rng.uniform(0.47, 0.5, size=(4000, 4))])
+    X = np.minimum(X, np.nextafter(0.5, 0.0))
+    V = rng.normal(size=(R, N))
+    ws = WindowSet(((1, 2), (3, 4)), d_max=2)
+    plan = build_plan(KernelSpec("gauss", 0.25), ws, "default", _ds(X, 2))
+    with _native.KernelTimer() as kt:
+        res = fast_matvecs(plan, V, dell=True)
+    assert "k_spread2r" in kt.report and "k_interp2r" in kt.report, kt.report
+    for r in (0, R // 2, R - 1):
+        assert rel(res["K"][r], fast_matvec(plan, V[r])) <= 1e-13
+    orc = R_.FastSum("gauss", 0.25, 1.0, [(0, 1), (2, 3)], X).matvec(V[R - 1])
+    assert rel(res["K"][R - 1], orc) <= 1e-8
+    dorc = R_.FastSum("der_gauss", 0.25, 1.0, [(0, 1), (2, 3)], X).matvec(V[0])
+    assert rel(res["dK_dell"][0], dorc) <= 1e-8
+    mplan = build_mixed_plan([KernelSpec("matern12", 0.2), KernelSpec("gauss", 0.3)], ws, "default", _ds(X, 2))
+    mix = mixed_matvecs(mplan, V)
+    for w, (fam, ell) in enumerate((("matern12", 0.2), ("gauss", 0.3))):
+        one = build_plan(KernelSpec(fam, ell), WindowSet((ws.windows[w],), d_max=2), "default", _ds(X, 2))
+        col = fast_matvecs(one, V[R - 1], dell=True)["dK_dell"]
+        assert rel(mix["dK_dell"][w][R - 1], col) <= 1e-13
