@@ -26,10 +26,16 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _stale() -> bool:
-    if not LIB.exists():
+#: checked variant (-DAK_CHECKED: device invariant traps, guard bands + NaN poisoning of
+#: the library's buffers, verified after every entry point) -- test infrastructure,
+#: loaded only by tests/test_gpu_checked.py through AK_LIB_PATH
+CHECKED_LIB = PKG / "libaddkern_b200_checked.so"
+
+
+def _stale(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
+    t = lib.stat().st_mtime
     deps = [CSRC / s for s in SOURCES] + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "addkern_b200.h", Path(__file__)]
     return any(d.stat().st_mtime > t for d in deps)
 
@@ -59,6 +65,13 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None, d
         raise RuntimeError(f"nvcc failed ({res.returncode})")
     os.replace(str(target) + ".tmp", target)
     return target
+
+
+def build_checked(force: bool = False) -> Path:
+    """The checked variant (see CHECKED_LIB)."""
+    if not force and not _stale(CHECKED_LIB):
+        return CHECKED_LIB
+    return build(force=True, out=CHECKED_LIB, defines=("AK_CHECKED",))
 
 
 if __name__ == "__main__":

@@ -77,17 +77,39 @@ __device__ __forceinline__ double window_weight_rt(const ak_window_fn& wf, doubl
     return mirror ? fma(-s, o, e) : fma(s, o, e);
 }
 
+// Checked builds (-DAK_CHECKED, tools/checked_build.py): device-side invariant checks
+// that trap with a message; compiled out of the product library.
+#ifdef AK_CHECKED
+#define AK_DCHECK(cond)                                                                           \
+    do {                                                                                          \
+        if (!(cond)) {                                                                            \
+            printf("AK_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                           \
+            __trap();                                                                             \
+        }                                                                                         \
+    } while (0)
+#else
+#define AK_DCHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 // Periodic grid index.  Every index the kernels form (footprints and supercell
 // regions: S <= 16, T <= 16) lies in [-7, n + 22], so for n >= 32 one conditional
 // add/subtract suffices (a few integer ops instead of a ~20-instruction integer
 // division); n is warp-uniform, the branch does not diverge.
 __device__ __forceinline__ int wrap(int i, int n) {
+    int r;
     if (n >= 32) {
+        AK_DCHECK(i >= -n && i < 2 * n);
         i += i < 0 ? n : 0;
-        return i >= n ? i - n : i;
+        r = i >= n ? i - n : i;
+    } else {
+        i %= n;
+        r = i < 0 ? i + n : i;
     }
-    i %= n;
-    return i < 0 ? i + n : i;
+    AK_DCHECK(r >= 0 && r < n);
+    return r;
 }
 
 // cp.async (LDGSTS): global -> shared without a register round trip.

@@ -146,6 +146,7 @@ k_spread_tile(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
             const int l0 = cell_axis(p.cell, 0) - sc0 * S;
             const int l1 = Q >= 2 ? cell_axis(p.cell, 1) - sc1 * S : 0;
             const int l2 = Q >= 3 ? cell_axis(p.cell, 2) - sc2 * S : 0;
+            AK_DCHECK(l0 >= 0 && l0 < S && l1 >= 0 && l1 < S && l2 >= 0 && l2 < S);
             cst[lane] = l0 | (l1 << 8) | (l2 << 16);
         }
         __syncwarp();
@@ -269,6 +270,7 @@ k_interp_lane(const Point* __restrict__ pts, const WorkItem* __restrict__ items,
         double w0[T], w1[T];
         window_weights<T>(wf, p.s[0], w0);
         const int l0 = cell_axis(p.cell, 0) - sc0 * S;
+        AK_DCHECK(l0 >= 0 && l0 < S);
         double acc = 0.0;
         if (Q == 1) {
 #pragma unroll

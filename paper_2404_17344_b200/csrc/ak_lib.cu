@@ -166,6 +166,71 @@ extern "C" int64_t ak_prof_report(char* buf, int64_t cap) {
     return (int64_t)out.size() + 1;
 }
 
+// ---------------------------------------------------------------------------
+// device allocations of the library's own buffers.  Checked builds (-DAK_CHECKED,
+// tools/checked_build.py) surround each with guard bands that are verified after
+// every entry point, and poison the buffer with NaN bytes so that a read of memory
+// no kernel wrote shows up in the results (a memcheck / initcheck substitute).
+
+#ifdef AK_CHECKED
+static constexpr size_t kGuard = 4096;
+struct GuardRec {
+    char* base;
+    size_t bytes;
+    std::string name;
+};
+static std::mutex g_guard_mu;
+static std::map<void*, GuardRec> g_guards;
+
+static cudaError_t ak_malloc_named(void** p, size_t bytes, const char* name) {
+    char* base = nullptr;
+    cudaError_t e = cudaMalloc(&base, bytes + 2 * kGuard);
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        return e;
+    }
+    cudaMemset(base, 0xA5, kGuard);
+    cudaMemset(base + kGuard + bytes, 0xA5, kGuard);
+    cudaMemset(base + kGuard, 0xFF, bytes);
+    *p = base + kGuard;
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    g_guards[*p] = GuardRec{base, bytes, name};
+    return cudaSuccess;
+}
+
+static void ak_free(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    auto it = g_guards.find(p);
+    if (it != g_guards.end()) {
+        cudaFree(it->second.base);
+        g_guards.erase(it);
+    } else {
+        cudaFree(p);
+    }
+}
+
+static int fail(int code, const std::string& msg);
+static int guards_verify(const char* where) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return fail(AK_ERR_CUDA, std::string("device fault in ") + where);
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    std::vector<unsigned char> h(2 * kGuard);
+    for (auto& kv : g_guards) {
+        const GuardRec& r = kv.second;
+        cudaMemcpy(h.data(), r.base, kGuard, cudaMemcpyDeviceToHost);
+        cudaMemcpy(h.data() + kGuard, r.base + kGuard + r.bytes, kGuard, cudaMemcpyDeviceToHost);
+        for (unsigned char c : h)
+            if (c != 0xA5) return fail(AK_ERR_CUDA, "guard band of " + r.name + " overwritten (" + where + ")");
+    }
+    return AK_OK;
+}
+#else
+static inline cudaError_t ak_malloc_named(void** p, size_t bytes, const char*) { return cudaMalloc(p, bytes); }
+static inline void ak_free(void* p) { cudaFree(p); }
+static inline int guards_verify(const char*) { return AK_OK; }
+#endif
+#define AK_MALLOC(ptr, bytes) ak_malloc_named(reinterpret_cast<void**>(ptr), (bytes), #ptr)
+
 static inline int64_t ipow_rt(int64_t b, int q) {
     int64_t r = 1;
     for (int i = 0; i < q; ++i) r *= b;
@@ -383,14 +448,14 @@ extern "C" int64_t ak_launch_count(void) { return g_launches.load(); }
 
 extern "C" int ak_geom_destroy(ak_geom* g) {
     if (!g) return AK_OK;
-    cudaFree(g->pts);
-    cudaFree(g->items);
-    cudaFree(g->canon_off_d);
-    cudaFree(g->W3);
-    cudaFree(g->CI3);
-    cudaFree(g->W2);
-    cudaFree(g->CI2);
-    cudaFree(g->wshift_d);
+    ak_free(g->pts);
+    ak_free(g->items);
+    ak_free(g->canon_off_d);
+    ak_free(g->W3);
+    ak_free(g->CI3);
+    ak_free(g->W2);
+    ak_free(g->CI2);
+    ak_free(g->wshift_d);
     delete g;
     return AK_OK;
 }
@@ -429,12 +494,12 @@ static double mean_occupancy(const double* X, int64_t ld, const int32_t* cols, i
 struct Scratch {
     std::vector<void*> bufs;
     ~Scratch() {
-        for (void* b : bufs) cudaFree(b);
+        for (void* b : bufs) ak_free(b);
     }
     template <typename T>
     cudaError_t alloc(T** p, size_t bytes) {
         *p = nullptr;
-        const cudaError_t e = cudaMalloc(p, bytes);
+        const cudaError_t e = AK_MALLOC(p, bytes);
         if (e == cudaSuccess) bufs.push_back(*p);
         return e;
     }
@@ -459,30 +524,30 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
                 g->windows_of_q[q].push_back(w);
             }
     g->canon_total = off;
-    AK_CUDA(cudaMalloc(&g->canon_off_d, sizeof(int64_t) * P));
+    AK_CUDA(AK_MALLOC(&g->canon_off_d, sizeof(int64_t) * P));
     AK_CUDA(cudaMemcpyAsync(g->canon_off_d, g->canon_off.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice, st));
 
-    AK_CUDA(cudaMalloc(&g->pts, sizeof(Point) * (size_t)std::max<int64_t>(1, N * P)));
+    AK_CUDA(AK_MALLOC(&g->pts, sizeof(Point) * (size_t)std::max<int64_t>(1, N * P)));
     int max_nsc_total = 1;
     bool cached = g->wf.taps == 12 && N > 0 && g->tune.weight_tables;
     if (cached) {
         // plan-time weight tables (filled once the points are sorted, below)
         const int64_t P3 = (int64_t)g->windows_of_q[3].size(), P2 = (int64_t)g->windows_of_q[2].size();
         const int T = g->wf.taps;
-        bool ok = cudaMalloc(&g->wshift_d, sizeof(int64_t) * P) == cudaSuccess;
+        bool ok = AK_MALLOC(&g->wshift_d, sizeof(int64_t) * P) == cudaSuccess;
         if (ok && P3 > 0)
-            ok = cudaMalloc(&g->W3, sizeof(double) * P3 * N * 3 * T) == cudaSuccess &&
-                 cudaMalloc(&g->CI3, sizeof(CellIdx) * P3 * N) == cudaSuccess;
+            ok = AK_MALLOC(&g->W3, sizeof(double) * P3 * N * 3 * T) == cudaSuccess &&
+                 AK_MALLOC(&g->CI3, sizeof(CellIdx) * P3 * N) == cudaSuccess;
         if (ok && P2 > 0)
-            ok = cudaMalloc(&g->W2, sizeof(double) * P2 * N * 2 * T) == cudaSuccess &&
-                 cudaMalloc(&g->CI2, sizeof(CellIdx) * P2 * N) == cudaSuccess;
+            ok = AK_MALLOC(&g->W2, sizeof(double) * P2 * N * 2 * T) == cudaSuccess &&
+                 AK_MALLOC(&g->CI2, sizeof(CellIdx) * P2 * N) == cudaSuccess;
         if (!ok) {
             cudaGetLastError();  // not enough memory for the tables: evaluate weights per pass
-            cudaFree(g->W3);
-            cudaFree(g->CI3);
-            cudaFree(g->W2);
-            cudaFree(g->CI2);
-            cudaFree(g->wshift_d);
+            ak_free(g->W3);
+            ak_free(g->CI3);
+            ak_free(g->W2);
+            ak_free(g->CI2);
+            ak_free(g->wshift_d);
             g->W3 = g->W2 = nullptr;
             g->CI3 = g->CI2 = nullptr;
             g->wshift_d = nullptr;
@@ -668,7 +733,7 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
         }
     }
     if (rc == AK_OK) {
-        if (cudaMalloc(&g->items, sizeof(WorkItem) * std::max<size_t>(1, all.size())) != cudaSuccess) {
+        if (AK_MALLOC(&g->items, sizeof(WorkItem) * std::max<size_t>(1, all.size())) != cudaSuccess) {
             cudaGetLastError();
             rc = fail(AK_ERR_ALLOC, "item allocation failed");
         } else if (!all.empty() &&
@@ -803,7 +868,7 @@ static int geom_create(int32_t n, int32_t P, const int32_t* q, const int32_t* co
         g->desc = buf;
     }
     *out = g;
-    return AK_OK;
+    return guards_verify("ak_geom_create");
 }
 
 extern "C" const char* ak_geom_describe(const ak_geom* g) { return g ? g->desc.c_str() : ""; }
@@ -1158,7 +1223,7 @@ extern "C" int ak_spread(const ak_geom* g, const double* V, int32_t R, int64_t l
     AK_TRY(check_rhs(g, R));
     cudaStream_t st = (cudaStream_t)stream;
     for (int q = 3; q >= 1; --q) AK_TRY(spread_group(g, q, V, Strides{ldv, 1}, R, grids, st));
-    return AK_OK;
+    return guards_verify("ak_spread");
 }
 
 extern "C" int ak_interp(const ak_geom* g, const double* grids, int32_t R, const double* scale, double* out,
@@ -1171,7 +1236,7 @@ extern "C" int ak_interp(const ak_geom* g, const double* grids, int32_t R, const
     for (int q = 3; q >= 1; --q)
         AK_TRY(interp_group(g, q, grids, R, scale, out, Strides{ldo, 1}, sum_windows, sum_windows ? 1 : 0, wstride,
                             st));
-    return AK_OK;
+    return guards_verify("ak_interp");
 }
 
 // ---------------------------------------------------------------------------
@@ -1360,15 +1425,15 @@ extern "C" int ak_op_destroy(ak_op* op) {
             cufftDestroy(op->fwd[q]);
             cufftDestroy(op->inv[q]);
         }
-        cudaFree(op->gwin_d[q]);
+        ak_free(op->gwin_d[q]);
     }
-    cudaFree(op->fbuf);
-    cudaFree(op->ftab);
-    cudaFree(op->grids);
-    cudaFree(op->gbuf);
-    cudaFree(op->spec);
-    cudaFree(op->spec2);
-    cudaFree(op->band);
+    ak_free(op->fbuf);
+    ak_free(op->ftab);
+    ak_free(op->grids);
+    ak_free(op->gbuf);
+    ak_free(op->spec);
+    ak_free(op->spec2);
+    ak_free(op->band);
     delete op;
     return AK_OK;
 }
@@ -1377,8 +1442,8 @@ static int op_build(ak_op* op, cudaStream_t st) {
     const ak_geom* g = op->gs;
     const int n = g->n;
     const int64_t total = g->canon_total * op->R;
-    AK_CUDA(cudaMalloc(&op->grids, sizeof(double) * total));
-    AK_CUDA(cudaMalloc(&op->gbuf, sizeof(double) * total));
+    AK_CUDA(AK_MALLOC(&op->grids, sizeof(double) * total));
+    AK_CUDA(AK_MALLOC(&op->gbuf, sizeof(double) * total));
     int64_t soff = 0;
     for (int q = 3; q >= 1; --q) {
         const auto& ws = g->windows_of_q[q];
@@ -1387,15 +1452,15 @@ static int op_build(ak_op* op, cudaStream_t st) {
         op->spec_off[q] = soff;
         if (ws.empty()) continue;
         op->grid_off[q] = (int64_t)op->R * g->canon_off[ws[0]];
-        AK_CUDA(cudaMalloc(&op->gwin_d[q], sizeof(int) * ws.size()));
+        AK_CUDA(AK_MALLOC(&op->gwin_d[q], sizeof(int) * ws.size()));
         AK_CUDA(cudaMemcpyAsync(op->gwin_d[q], ws.data(), sizeof(int) * ws.size(), cudaMemcpyHostToDevice, st));
         op->has[q] = true;
         const int batch = op->R * (int)ws.size();
         if (q == 3 && batch <= 65535 && fft3_fused_ok(g, n, op->m)) {   // grids on gridDim.y
             op->fused3 = true;
-            AK_CUDA(cudaMalloc(&op->fbuf, sizeof(double) * (size_t)batch * n * op->m * op->m));
+            AK_CUDA(AK_MALLOC(&op->fbuf, sizeof(double) * (size_t)batch * n * op->m * op->m));
             const std::vector<double> tabs = ak::fft3_host_tables(n, op->m);
-            AK_CUDA(cudaMalloc(&op->ftab, sizeof(double) * tabs.size()));
+            AK_CUDA(AK_MALLOC(&op->ftab, sizeof(double) * tabs.size()));
             AK_CUDA(cudaMemcpyAsync(op->ftab, tabs.data(), sizeof(double) * tabs.size(), cudaMemcpyHostToDevice, st));
             AK_CUDA(cudaStreamSynchronize(st));
             continue;
@@ -1416,9 +1481,9 @@ static int op_build(ak_op* op, cudaStream_t st) {
         boff += op->bs[q] * op->R * op->nwin[q];
     }
     op->band_total = boff;
-    AK_CUDA(cudaMalloc(&op->band, sizeof(double2) * std::max<int64_t>(boff, 1)));
-    AK_CUDA(cudaMalloc(&op->spec, sizeof(double2) * std::max<int64_t>(soff, 1)));
-    AK_CUDA(cudaMalloc(&op->spec2, sizeof(double2) * std::max<int64_t>(soff, 1)));
+    AK_CUDA(AK_MALLOC(&op->band, sizeof(double2) * std::max<int64_t>(boff, 1)));
+    AK_CUDA(AK_MALLOC(&op->spec, sizeof(double2) * std::max<int64_t>(soff, 1)));
+    AK_CUDA(AK_MALLOC(&op->spec2, sizeof(double2) * std::max<int64_t>(soff, 1)));
     AK_CUDA(cudaStreamSynchronize(st));
     return AK_OK;
 }
@@ -1484,9 +1549,19 @@ static int band_pack(ak_op* op, int q, int dir, cudaStream_t st) {
     return ps.done("k_band_pack");
 }
 
+static int op_apply(ak_op* op, const double* V, int64_t ldv, const double* const* H, const double* scale,
+                    double* const* outs, int64_t ldo, const int32_t* sum_windows, int32_t flags, void* stream);
+
 extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double* const* H, const double* scale,
                            double* const* outs, int64_t ldo, const int32_t* sum_windows, int32_t flags,
                            void* stream)
+{
+    const int rc = op_apply(op, V, ldv, H, scale, outs, ldo, sum_windows, flags, stream);
+    return rc == AK_OK ? guards_verify("ak_op_apply") : rc;
+}
+
+static int op_apply(ak_op* op, const double* V, int64_t ldv, const double* const* H, const double* scale,
+                    double* const* outs, int64_t ldo, const int32_t* sum_windows, int32_t flags, void* stream)
 {
     if (!op) return fail(AK_ERR_INVALID, "null argument");
     cudaStream_t st = (cudaStream_t)stream;
@@ -1679,7 +1754,7 @@ extern "C" int ak_type1_band(int32_t q, int32_t n, int32_t m, const double* gre,
     }
     cudaFreeAsync(Y, st);
     release_plan(h, tmp_plan, st);
-    return rc;
+    return rc == AK_OK ? guards_verify("ak_type1_band") : rc;
 }
 
 __global__ void k_type2_pad(const double2* __restrict__ c, int q, int n, int m, const double* __restrict__ deconv,
@@ -1748,5 +1823,5 @@ extern "C" int ak_type2_grid(int32_t q, int32_t n, int32_t m, const double* c, c
     }
     cudaFreeAsync(G, st);
     release_plan(h, tmp_plan, st);
-    return rc;
+    return rc == AK_OK ? guards_verify("ak_type2_grid") : rc;
 }

@@ -49,6 +49,7 @@ __device__ __forceinline__ void q1_stage(const Point& p, bool valid, int sc0, in
 #pragma unroll
         for (int a = 0; a < T; ++a) wst[lane][a] = w[a];
         lst[lane] = cell_axis(p.cell, 0) - sc0 * 16;
+        AK_DCHECK(lst[lane] >= 0 && lst[lane] < 16);
         ist[lane] = p.idx;
     }
 }
@@ -162,6 +163,7 @@ k_spread1r(const Point* __restrict__ pts, const WorkItem* __restrict__ items, co
 #pragma unroll
             for (int a = 0; a < T; ++a) wst[lane][a] = w[a];
             lst[lane] = cell_axis(p.cell, 0) - sc0 * 16;
+            AK_DCHECK(lst[lane] >= 0 && lst[lane] < 16);
         }
 #pragma unroll
         for (int k = 0; k < PPS; ++k) vst[sp + SP * k][rl] = vv[k];

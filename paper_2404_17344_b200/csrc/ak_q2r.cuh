@@ -7,11 +7,15 @@
 // double-buffered weight rows (one TMA stream per item), warp w owns RHS
 // r0 + 8w .. r0 + 8w + 7, and the RHS values / results of a batch move between
 // HBM and shared memory as whole lines (a point's RHS are contiguous).
-// The per-RHS math is that of ak_q2c.cuh:
-//   spread : G_r[a][b] += sum_j (v_rj w0_j[a]) w1_j[b]  -- 4 DMMA per 4 points per RHS,
-//            the B operand (w1) shared by the warp's 8 RHS;
-//   interp : U_r[j][a] = sum_b w1_j[b] G_r[a][b]        -- 6 DMMA per 8 points per RHS,
-//            the A operand (w1 of the 8 points) shared; out = sum_a w0_j[a] U_r[j][a].
+// The math runs on RHS pairs (as the 3-D RHS-pair spread, ak_q3r.cuh), so the
+// 12-wide tap axis that ak_q2c.cuh pads to 16 tiles exactly as 2 x 12 = 24:
+//   spread : G_r[a][b] += sum_j (v_rj w0_j[a]) w1_j[b]; rows (r, a) of the pair = 3
+//            m-tiles, columns b = 2 n-tiles (16, padded), K = points: 6 DMMA per 4
+//            points per pair (8 for two single-RHS products), B (w1) shared by the pairs;
+//   interp : U[j][(r, a)] = sum_b w1_j[b] G_r[a][b]; columns (r, a) of the pair = 3
+//            n-tiles (no padding), K = b = 3 k-steps: 9 DMMA per 8 points per pair
+//            (12 single-RHS); the columns are permuted so lane quad q holds
+//            r = q >> 1, a = 6 (q & 1) + 0..5: out = 6 FMA + one quad shuffle.
 #pragma once
 #include "ak_q2c.cuh"
 
@@ -60,34 +64,31 @@ k_interp2r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     if (tid < min(B, it.count)) cp_async8(&cib[0][tid], CIit + tid);
     cp_async_commit();
 
-    // B fragments of the warp's 8 footprints (mapping of k_interp2c)
-    double gf[Q2R_RPW][2][3];
+    // B fragments of the warp's 4 RHS pairs: lane (k = lane % 4, n = lane / 4) of n-tile t
+    // holds G_r[a][b] with r = pair + (n >> 2), a = 6 ((n >> 1) & 1) + 2 t + (n & 1),
+    // b = 4 ks + k (columns permuted: lane quad q of C holds r = q >> 1, a = 6 (q & 1) + 0..5)
+    constexpr int NP = Q2R_RPW / 2;
+    double gf[NP][3][3];
     {
         const int c0 = it.sc & 1023, c1 = (it.sc >> 10) & 1023;
         const int nn = lane >> 2, kk = lane & 3;
+        const int rl = nn >> 2, ah = 6 * ((nn >> 1) & 1), ae = nn & 1;
         int z[3];
 #pragma unroll
         for (int ks = 0; ks < 3; ++ks) z[ks] = wrap(c1 - (T / 2 - 1) + 4 * ks + kk, n);
-        int64_t rowoff[2];
-        bool ok[2];
+        int64_t rowoff[3];
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            const int i = 2 * t + (nn & 1);
-            const int a = 3 * (nn >> 1) + i;
-            ok[t] = i < 3;
-            rowoff[t] = (int64_t)wrap(c0 - (T / 2 - 1) + (ok[t] ? a : 0), n) * n;
-        }
+        for (int t = 0; t < 3; ++t) rowoff[t] = (int64_t)wrap(c0 - (T / 2 - 1) + ah + 2 * t + ae, n) * n;
         const int64_t n2 = (int64_t)n * n;
         const double* __restrict__ g0 = grids + (int64_t)nrhs * canon_off[it.window];
 #pragma unroll
-        for (int rr = 0; rr < Q2R_RPW; ++rr) {
-            const int r = r0 + warp * Q2R_RPW + rr;
+        for (int pr = 0; pr < NP; ++pr) {
+            const int r = r0 + warp * Q2R_RPW + 2 * pr + rl;
             const double* __restrict__ g = g0 + (int64_t)min(r, nrhs - 1) * n2;
 #pragma unroll
-            for (int t = 0; t < 2; ++t)
+            for (int t = 0; t < 3; ++t)
 #pragma unroll
-                for (int ks = 0; ks < 3; ++ks)
-                    gf[rr][t][ks] = (ok[t] && r < nrhs) ? __ldg(g + rowoff[t] + z[ks]) : 0.0;
+                for (int ks = 0; ks < 3; ++ks) gf[pr][t][ks] = r < nrhs ? __ldg(g + rowoff[t] + z[ks]) : 0.0;
         }
     }
     const double sc = scale[it.window];
@@ -117,19 +118,25 @@ k_interp2r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
             double af[3];
 #pragma unroll
             for (int ks = 0; ks < 3; ++ks) af[ks] = valid ? w[T + 4 * ks + q] : 0.0;
-            const double w0a = w[3 * q], w0b = w[3 * q + 1], w0c = w[3 * q + 2];
+            double w0[6];
 #pragma unroll
-            for (int rr = 0; rr < Q2R_RPW; ++rr) {
-                double C[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+            for (int i = 0; i < 6; ++i) w0[i] = w[6 * (q & 1) + i];
 #pragma unroll
-                for (int ks = 0; ks < 3; ++ks) {
-                    dmma_8x8x4(C[0][0], C[0][1], af[ks], gf[rr][0][ks]);
-                    dmma_8x8x4(C[1][0], C[1][1], af[ks], gf[rr][1][ks]);
-                }
-                double v = fma(w0c, C[1][0], fma(w0b, C[0][1], w0a * C[0][0]));
+            for (int pr = 0; pr < NP; ++pr) {
+                double C[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+                for (int ks = 0; ks < 3; ++ks)
+#pragma unroll
+                    for (int t = 0; t < 3; ++t) dmma_8x8x4(C[t][0], C[t][1], af[ks], gf[pr][t][ks]);
+                // lane (pj, q): columns a = 6 (q & 1) + 2 t + e of RHS 2 pr + (q >> 1)
+                double v = w0[0] * C[0][0];
+                v = fma(w0[1], C[0][1], v);
+                v = fma(w0[2], C[1][0], v);
+                v = fma(w0[3], C[1][1], v);
+                v = fma(w0[4], C[2][0], v);
+                v = fma(w0[5], C[2][1], v);
                 v += __shfl_xor_sync(0xffffffffu, v, 1);
-                v += __shfl_xor_sync(0xffffffffu, v, 2);
-                if (q == 0 && valid) ob[s][k0 + pj][warp * Q2R_RPW + rr] = sc * v;
+                if ((q & 1) == 0 && valid) ob[s][k0 + pj][warp * Q2R_RPW + 2 * pr + (q >> 1)] = sc * v;
             }
         }
         __syncthreads();
@@ -192,14 +199,24 @@ k_spread2r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     gather(0, 0, min(B, it.count));
     cp_async_commit();
 
+    // A fragments: row (r, a) = divmod(8 mt + lane / 4, 12) of the pair, k = lane % 4;
+    // B: k = lane % 4, column b = 8 nt + lane / 4 (b >= 12 padding)
+    constexpr int NP = Q2R_RPW / 2;
     const int rn = lane >> 2, kq = lane & 3;
-    double C[Q2R_RPW][2][2][2];
+    int ar[3], aa[3];
 #pragma unroll
-    for (int rr = 0; rr < Q2R_RPW; ++rr)
+    for (int mt = 0; mt < 3; ++mt) {
+        const int row = 8 * mt + rn;
+        ar[mt] = row / T;
+        aa[mt] = row - ar[mt] * T;
+    }
+    double C[NP][3][2][2];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+    for (int pr = 0; pr < NP; ++pr)
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) C[rr][mt][nt][0] = C[rr][mt][nt][1] = 0.0;
+        for (int mt = 0; mt < 3; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) C[pr][mt][nt][0] = C[pr][mt][nt][1] = 0.0;
 
     for (int bi = 0; bi < nbatch; ++bi) {
         const int s = bi & 1;
@@ -223,44 +240,44 @@ k_spread2r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         for (int k0 = 0; k0 < nb; k0 += 4) {
             const int j = k0 + kq;                       // rows past nb hold zero RHS values
             const double* w = wbuf[s][j < nb ? j : 0];
-            const double x0 = w[rn], x1 = rn < 4 ? w[8 + rn] : 0.0;
+            double x[3];
+#pragma unroll
+            for (int mt = 0; mt < 3; ++mt) x[mt] = w[aa[mt]];
             const double b0 = w[T + rn];
             const double b1 = rn < 4 ? w[T + 8 + rn] : 0.0;
             const double* vr = &vb[s][j][warp * Q2R_RPW];
 #pragma unroll
-            for (int rr = 0; rr < Q2R_RPW; ++rr) {
-                const double v = vr[rr];
-                const double a0 = v * x0, a1 = v * x1;
-                dmma_8x8x4(C[rr][0][0][0], C[rr][0][0][1], a0, b0);
-                dmma_8x8x4(C[rr][0][1][0], C[rr][0][1][1], a0, b1);
-                dmma_8x8x4(C[rr][1][0][0], C[rr][1][0][1], a1, b0);
-                dmma_8x8x4(C[rr][1][1][0], C[rr][1][1][1], a1, b1);
+            for (int pr = 0; pr < NP; ++pr) {
+#pragma unroll
+                for (int mt = 0; mt < 3; ++mt) {
+                    const double a = vr[2 * pr + ar[mt]] * x[mt];
+                    dmma_8x8x4(C[pr][mt][0][0], C[pr][mt][0][1], a, b0);
+                    dmma_8x8x4(C[pr][mt][1][0], C[pr][mt][1][1], a, b1);
+                }
             }
         }
     }
 
-    // lane holds G_r[a = rn + 8 mt][b = 2 kq + e + 8 nt] for its warp's 8 RHS
+    // lane holds G_r[a][b] for (r, a) = divmod(8 mt + lane / 4, 12) of each pair,
+    // b = 8 nt + 2 (lane % 4) + e
     const int c0 = it.sc & 1023, c1 = (it.sc >> 10) & 1023;
     const int64_t n2 = (int64_t)n * n;
 #pragma unroll
-    for (int rr = 0; rr < Q2R_RPW; ++rr) {
-        const int r = r0 + warp * Q2R_RPW + rr;
-        if (r >= nrhs) break;
-        double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n2;
+    for (int pr = 0; pr < NP; ++pr)
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-            const int a = rn + 8 * mt;
-            if (a >= T) continue;
-            double* row = g + (int64_t)wrap(c0 - (T / 2 - 1) + a, n) * n;
+        for (int mt = 0; mt < 3; ++mt) {
+            const int r = r0 + warp * Q2R_RPW + 2 * pr + ar[mt];
+            if (r >= nrhs) continue;
+            double* row = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n2 +
+                          (int64_t)wrap(c0 - (T / 2 - 1) + aa[mt], n) * n;
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int b = 2 * kq + e + 8 * nt;
-                    if (b < T) red_add(row + wrap(c1 - (T / 2 - 1) + b, n), C[rr][mt][nt][e]);
+                    if (b < T) red_add(row + wrap(c1 - (T / 2 - 1) + b, n), C[pr][mt][nt][e]);
                 }
         }
-    }
 }
 
 }  // namespace ak

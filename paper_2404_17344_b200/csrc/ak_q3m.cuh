@@ -196,6 +196,9 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         cp_async_commit();
         if (lane < nb) {
             const int c = cib[s][lane].cell;
+            AK_DCHECK(cell_axis(c, 0) - sc0 * S >= 0 && cell_axis(c, 0) - sc0 * S < S &&
+                      cell_axis(c, 1) - sc1 * S >= 0 && cell_axis(c, 1) - sc1 * S < S &&
+                      cell_axis(c, 2) - sc2 * S >= 0 && cell_axis(c, 2) - sc2 * S < S);
             cst[lane] = (cell_axis(c, 0) - sc0 * S) | ((cell_axis(c, 1) - sc1 * S) << 8) |
                         ((cell_axis(c, 2) - sc2 * S) << 16);
         }

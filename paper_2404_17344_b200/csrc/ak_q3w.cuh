@@ -142,6 +142,7 @@ __device__ __forceinline__ void for_region_rows(const int (*widx)[R], int n, int
 #pragma unroll
         for (int t = 0; t < RPL; ++t) {
             const int i1 = sub + RPP * t;
+            AK_DCHECK(i1 >= R || (pl + rowoff[t] >= 0 && pl + rowoff[t] < (int64_t)n * n * n));
             if (i1 < R) f((i0 * R + i1) * R + k, pl + rowoff[t]);
         }
     }
@@ -260,6 +261,9 @@ k_spread3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         }
         if (lane < nb) {
             const int c = cib[bi % 3][lane].cell;
+            AK_DCHECK(cell_axis(c, 0) - sc0 * S >= 0 && cell_axis(c, 0) - sc0 * S < S &&
+                      cell_axis(c, 1) - sc1 * S >= 0 && cell_axis(c, 1) - sc1 * S < S &&
+                      cell_axis(c, 2) - sc2 * S >= 0 && cell_axis(c, 2) - sc2 * S < S);
             cst[lane] = (cell_axis(c, 0) - sc0 * S) | ((cell_axis(c, 1) - sc1 * S) << 8) |
                         ((cell_axis(c, 2) - sc2 * S) << 16);
         }

@@ -77,6 +77,71 @@ def _dist():
     return dist
 
 
+_GROUPS: dict = {}
+_GROUPS_WORLD = [None]   # the default group the cache belongs to (re-initialised: cache dropped)
+
+
+def _new_group(members):
+    """dist.new_group, cached per member list: plans rebuilt under one process group
+    (a grid search, repeated hyperparameters) reuse the communicators instead of
+    creating new ones every time.  Like new_group itself, every rank must call it for
+    every group, in the same order."""
+    dist = _dist()
+    if _GROUPS_WORLD[0] is not dist.group.WORLD:
+        _GROUPS.clear()
+        _GROUPS_WORLD[0] = dist.group.WORLD
+    key = tuple(members)
+    pg = _GROUPS.get(key)
+    if pg is None:
+        pg = dist.new_group(list(members))
+        _GROUPS[key] = pg
+    return pg
+
+
+class _StageClock:
+    """Optional per-stage device timing of a sharded product (CUDA events on the
+    current stream, collectives included): `profile(fn, steps)` returns the mean ms
+    per step of each stage."""
+
+    def __init__(self):
+        self.on = False
+        self.events = []
+
+    def mark(self, name):
+        if not self.on:
+            return
+        import torch
+
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.events.append((name, ev))
+
+    def profile(self, fn, steps: int) -> dict:
+        import torch
+
+        self.on, self.events = True, []
+        torch.cuda.synchronize()
+        for _ in range(steps):
+            self.mark("start")
+            fn()
+            self.mark("end")
+        torch.cuda.synchronize()
+        self.on = False
+        out = {}
+        for (_, a), (name, b) in zip(self.events[:-1], self.events[1:]):
+            if name == "start":
+                continue
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b) / steps
+        self.events = []
+        return out
+
+
+def _default_builder():
+    from .fastsum import build_plan
+
+    return build_plan
+
+
 def _subset_rows(data: Dataset, lo: int, hi: int) -> Dataset:
     from dataclasses import replace
 
@@ -86,33 +151,38 @@ def _subset_rows(data: Dataset, lo: int, hi: int) -> Dataset:
 class WindowShardedPlan:
     """K v over all windows with the windows split across ranks."""
 
-    def __init__(self, spec, window_set: WindowSet, preset, data: Dataset, group=None, **kw):
-        from .fastsum import build_plan
-
+    def __init__(self, spec, window_set: WindowSet, preset, data: Dataset, group=None, plan_builder=None, **kw):
         dist = _dist()
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self.spec = spec
         self.owned = window_partition(window_set.lengths, self.world)[self.rank]
         self.n_rows = data.n_rows
         self.plan = None
-        if self.owned:
+        self.clock = _StageClock()
+        if self.owned:   # ranks beyond the window count own nothing and contribute zeros
             sub = WindowSet(tuple(window_set.windows[w] for w in self.owned), d_max=window_set.d_max)
-            self.plan = build_plan(spec, sub, preset, data, **kw)
+            self.plan = (plan_builder or _default_builder())(spec, sub, preset, data, **kw)
 
     def matvecs(self, V, families=None):
-        """(R, N) CUDA tensor -> list of (R, N) products (one per coefficient set), replicated."""
+        """(R, N) tensor -> list of (R, N) products (one per coefficient set), replicated."""
         import torch
 
         dist = _dist()
-        fams = families or ((self.plan.spec.family,) if self.plan else None)
+        fams = tuple(families or (self.spec.family,))
         R = V.shape[0]
-        outs = [torch.zeros((R, self.n_rows), dtype=torch.float64, device="cuda") for _ in fams]
+        outs = [torch.zeros((R, self.n_rows), dtype=torch.float64, device=V.device) for _ in fams]
         if self.plan is not None:
-            self.plan._operator(tuple(fams), R).apply(V, outs, [True] * len(outs))
+            self.plan._operator(fams, R).apply(V, outs, [True] * len(outs))
+        self.clock.mark("windows")
         for o in outs:
             dist.all_reduce(o, group=self.group)
+        self.clock.mark("allreduce_rows")
         return outs
+
+    def stage_times(self, fn, steps: int = 5) -> dict:
+        return self.clock.profile(fn, steps)
 
     def matvec(self, v):
         return self.matvecs(v.reshape(1, -1))[0][0]
@@ -229,12 +299,12 @@ class HybridShardedPlan:
         self.band_group = self.row_group = None
         for g in range(G):
             members = [base[g * Q + j] for j in range(Q)]
-            pg = dist.new_group(members) if Q > 1 else None
+            pg = _new_group(members) if Q > 1 else None
             if g == self.gi:
                 self.band_group = pg
         for j in range(Q):
             members = [base[g * Q + j] for g in range(G)]
-            pg = dist.new_group(members) if G > 1 else None
+            pg = _new_group(members) if G > 1 else None
             if j == self.pj:
                 self.row_group = pg
         self.owned = window_partition(window_set.lengths, G)[self.gi]
@@ -339,10 +409,10 @@ class CellShardedPlan:
     """
 
     def __init__(self, spec, window_set: WindowSet, preset, data: Dataset, window_groups: int | None = None,
-                 group=None, **kw):
+                 group=None, plan_builder=None, **kw):
         import numpy as np
 
-        from .fastsum import build_plan, resolve_m
+        from .fastsum import resolve_m
         from .nufft import NufftPlan
 
         dist = _dist()
@@ -358,12 +428,13 @@ class CellShardedPlan:
         self.band_group = None
         for g in range(G):
             members = [base[g * Q + j] for j in range(Q)]
-            pg = dist.new_group(members) if Q > 1 else None
+            pg = _new_group(members) if Q > 1 else None
             if g == self.gi:
                 self.band_group = pg
         self.owned = window_partition(window_set.lengths, G)[self.gi]
         self.n_rows = data.n_rows
         self.spec = spec
+        self.clock = _StageClock()
         m = resolve_m(preset)
         wins = tuple(window_set.windows[w] for w in self.owned)
         masks = np.zeros((len(wins), data.n_rows), dtype=bool)
@@ -373,7 +444,8 @@ class CellShardedPlan:
             masks[k, cell_partition(data.features[:, list(window_set.columns(win))], n, Q,
                                     CELL_OVERHEAD_ROWS)[self.pj]] = True
         self.rows_per_window = masks.sum(axis=1)
-        self.plan = build_plan(spec, WindowSet(wins, d_max=window_set.d_max), preset, data, row_masks=masks, **kw)
+        self.plan = (plan_builder or _default_builder())(spec, WindowSet(wins, d_max=window_set.d_max), preset, data,
+                                                         row_masks=masks, **kw)
 
     def matvecs(self, V, families=None):
         """(R, N) replicated RHS -> list of (R, N) replicated products (one per family)."""
@@ -384,18 +456,26 @@ class CellShardedPlan:
         dist = _dist()
         fams = tuple(families or (self.spec.family,))
         R = V.shape[0]
-        outs = [torch.empty((R, self.n_rows), dtype=torch.float64, device="cuda") for _ in fams]
+        outs = [torch.empty((R, self.n_rows), dtype=torch.float64, device=V.device) for _ in fams]
         op = self.plan._operator(fams, R)
         if self.Q > 1:
             op.spectrum_only(V)
+            self.clock.mark("spread_fwd_transform")
             dist.all_reduce(op.band(), group=self.band_group)
+            self.clock.mark("allreduce_band")
             op.apply(None, outs, [True] * len(outs), flags=_native.AK_APPLY_FROM_SPECTRUM)
+            self.clock.mark("multiply_inverse_interp")
         else:
             op.apply(V, outs, [True] * len(outs))
+            self.clock.mark("windows")
         if self.world > 1:
             for o in outs:
                 dist.all_reduce(o, group=self.group)
+            self.clock.mark("allreduce_rows")
         return outs
+
+    def stage_times(self, fn, steps: int = 5) -> dict:
+        return self.clock.profile(fn, steps)
 
     def matvec(self, v):
         """Full-length v (replicated) -> K v (replicated)."""

@@ -352,7 +352,19 @@ class FastsumPlan:
             sets = [self._family_set(f) for f in families]
             return _Operator(self.geometries, gi, self.m, R, [s[0] for s in sets], [s[1] for s in sets])
 
-        return _cached_operator(self._cache, ("op", families, R, id(gi), _stream_key()), make)
+        if gi is self.geometries:
+            return _cached_operator(self._cache, ("op", families, R, id(gi), _stream_key()), make)
+        # cross products (evaluation geometry): keep only the most recent one -- an operator
+        # pins its evaluation geometry (weights + workspace), so caching every geometry a
+        # caller ever passed would hold their device memory for the plan's lifetime
+        key = ("xop", families, R, id(gi), _stream_key())
+        op = self._cache.get(key)
+        if op is None:
+            for k in [k for k in self._cache if isinstance(k, tuple) and k and k[0] == "xop"]:
+                del self._cache[k]
+            op = make()
+            self._cache[key] = op
+        return op
 
 
 def _check_prescaled(data: Dataset, window_set: WindowSet) -> None:

@@ -28,7 +28,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .dataset import PRESCALED, Dataset, same_scaling
-from .errors import CgBreakdownError, InvalidScalingError, MaxIterationsError, ScalingMismatchError
+from .errors import (CgBreakdownError, InvalidScalingError, MaxIterationsError, NativeLibraryError,
+                     ScalingMismatchError)
 from .kernels import KernelSpec, dense_cross_matvec, dense_matvec
 from .windows import WindowSet
 
@@ -145,8 +146,14 @@ def _cg_solve_graphed(matvec, y, beta, tol, max_iter, callback):
                 stats.copy_(torch.cat([pAp, rs_new]))
                 p.mul_(rs_new / rs).add_(r)
                 rs.copy_(rs_new)
-    except Exception:  # pragma: no cover - capture unsupported for this product
+    except RuntimeError as exc:
+        # CUDA-graph capture refused (e.g. an op the capture cannot record): fall back to
+        # the eager device loop.  Library, allocation and argument errors propagate.
         torch.cuda.current_stream().wait_stream(s)
+        if isinstance(exc, NativeLibraryError) or "out of memory" in str(exc):
+            raise
+        warnings.warn(f"CUDA-graph capture of the CG iteration failed ({exc}); running it eagerly",
+                      RuntimeWarning, stacklevel=3)
         return None
     torch.cuda.current_stream().wait_stream(s)
     for it in range(1, max_iter + 1):
@@ -409,6 +416,18 @@ def cg_solve_batched(apply, Y, betas, tol: float = DEFAULT_CG_TOL, max_iter: int
     return X, iters, msgs
 
 
+def _grid_chunk(plan, R: int) -> int:
+    """Cells per lockstep batch: the batched CG holds, per cell, the per-RHS operator's
+    two grids and spectra (plus power-of-two bucket operators and the prediction
+    operator, about 4 operator copies) and ~8 length-N vectors; use at most half of
+    the free device memory (the reference runs one cell at a time)."""
+    import torch
+
+    free, _ = torch.cuda.mem_get_info()
+    per_cell = 8 * (4 * 3 * plan.geometries.canon_total + 8 * plan.n_rows)
+    return max(1, min(R, int(0.5 * free // max(per_cell, 1))))
+
+
 def grid_search(train: Dataset, test: Dataset, ws: WindowSet, ell_grid, beta_grid, family: str = "gauss",
                 backend: str = FASTSUM, preset="default", sigma_f: float | None = None,
                 tol: float = DEFAULT_CG_TOL, max_iter: int = DEFAULT_CG_MAX_ITER) -> GridSearchResult:
@@ -448,26 +467,44 @@ def grid_search(train: Dataset, test: Dataset, ws: WindowSet, ell_grid, beta_gri
             _eta_warning(s.ell, plan.m)
     for w in caught:
         warnings.warn_explicit(w.message, w.category, w.filename, w.lineno)
+    tp = time.perf_counter()
     R = len(pairs)
-    op = _grid_operator(plan, specs, R)
-    apply_subset = _subset_applier(plan, specs, op)
-
-    def apply(Pm):
-        out = torch.empty_like(Pm)
-        op.apply(Pm.contiguous(), [out], [True])
-        return out
-
-    Y = torch.as_tensor(np.broadcast_to(train.targets, (R, train.n_rows)).copy(), device="cuda")
-    X, iters, msgs = cg_solve_batched(apply, Y, [b for _, b in pairs], tol=tol, max_iter=max_iter,
-                                      apply_subset=apply_subset)
-    torch.cuda.synchronize()
-    t1 = time.perf_counter()
+    chunk = _grid_chunk(plan, R)
     geoms = prepare_eval_points(plan, test)
-    pop = _grid_operator(plan, specs, R, interp_geom=geoms)
-    pred = torch.empty((R, test.n_rows), dtype=torch.float64, device="cuda")
-    pop.apply(X.contiguous(), [pred], [True])
-    pred_h = pred.cpu().numpy()
-    t2 = time.perf_counter()
+    iters = np.zeros(R, dtype=np.int64)
+    msgs = [None] * R
+    pred_h = np.empty((R, test.n_rows))
+    t_fit = t_pred = 0.0
+    for c0 in range(0, R, chunk):
+        # cells in batches sized to the free device memory (each batch: one lockstep CG)
+        sl = slice(c0, min(R, c0 + chunk))
+        cs, ps = specs[sl], pairs[sl]
+        Rc = len(cs)
+        ta = time.perf_counter()
+        op = _grid_operator(plan, cs, Rc)
+        apply_subset = _subset_applier(plan, cs, op)
+
+        def apply(Pm, op=op):
+            out = torch.empty_like(Pm)
+            op.apply(Pm.contiguous(), [out], [True])
+            return out
+
+        Y = torch.as_tensor(np.broadcast_to(train.targets, (Rc, train.n_rows)).copy(), device="cuda")
+        X, it_c, msg_c = cg_solve_batched(apply, Y, [b for _, b in ps], tol=tol, max_iter=max_iter,
+                                          apply_subset=apply_subset)
+        torch.cuda.synchronize()
+        tb = time.perf_counter()
+        del op, apply_subset, apply, Y
+        pop = _grid_operator(plan, cs, Rc, interp_geom=geoms)
+        pred = torch.empty((Rc, test.n_rows), dtype=torch.float64, device="cuda")
+        pop.apply(X.contiguous(), [pred], [True])
+        pred_h[sl] = pred.cpu().numpy()
+        del pop, pred, X
+        t_fit += tb - ta
+        t_pred += time.perf_counter() - tb
+        iters[sl] = it_c
+        msgs[sl] = msg_c
+    t1, t2 = tp + t_fit, tp + t_fit + t_pred   # plan build counted with the fits (t0 .. tp)
     cells = []
     for r, (e, b) in enumerate(pairs):
         if iters[r] < 0:

@@ -1,5 +1,7 @@
-"""Small cases that reach every kernel family of libaddkern_b200 under
-compute-sanitizer (memcheck / racecheck / synccheck):
+"""Small cases that reach every kernel family of libaddkern_b200, each checked
+against the oracle -- run against the checked library variant
+(AK_LIB_PATH=paper_2404_17344_b200/libaddkern_b200_checked.so, tests/test_gpu_checked.py;
+compute-sanitizer is closed on this GPU pool):
 
   * config-1 distribution, N=400, K + dK/dl (multi-cell q=3 items, fused transforms)
   * densely occupied cells, windows (3), (2), (1): single-cell q=3 spread / DMMA
@@ -9,9 +11,7 @@ compute-sanitizer (memcheck / racecheck / synccheck):
   * sparse data with several RHS (supercell items, region tiles)
   * NUFFT type-1 / type-2 for q = 1..3 (cuFFT + extract / pad kernels)
   * dense GPU product (ak_dense_apply)
-
-Each case checks against the oracle so a sanitizer run also proves the
-results.  Usage: compute-sanitizer --tool memcheck python tools/sanitize_cases.py
+  * 16 RHS on a mixed-kernel plan (RHS-minor batched kernels, RHS-pair spread)
 """
 
 from __future__ import annotations
@@ -85,6 +85,21 @@ def main():
     refd = R.FastSum("der_gauss", 0.5, 1.0, [(0, 1, 2), (3, 4, 5)], Xs).matvec(V[2])
     worst = max(worst, rel(out[2], refd))
     print("sparse dK", rel(out[2], refd), flush=True)
+
+    # many RHS (RHS-minor batched kernels: k_spread1r / k_interp1r, k_spread2r / k_interp2r,
+    # RHS-pair k_spread3r), mixed kernels with per-window outputs, boundary-hugging nodes
+    from paper_2404_17344_b200.fastsum import build_mixed_plan, mixed_matvecs
+    Xm = np.concatenate([rng.uniform(-0.02, 0.02, size=(5000, 6)), rng.uniform(-0.5, -0.48, size=(500, 6))])
+    dsm = Dataset(Xm, np.zeros(len(Xm)), tuple(f"x{i}" for i in range(6)), scaling_state=PRESCALED, d_max=3)
+    wsm = WindowSet(((1, 2, 3), (4, 5), (6,)), d_max=3)
+    specs = [KernelSpec("gauss", 0.3), KernelSpec("matern12", 0.4), KernelSpec("matern12", 0.2)]
+    Vm = rng.normal(size=(16, len(Xm)))
+    res = mixed_matvecs(build_mixed_plan(specs, wsm, "default", dsm), Vm)
+    refm = np.zeros(len(Xm))
+    for (fam, ell), w in zip((("gauss", 0.3), ("matern12", 0.4), ("matern12", 0.2)), [(0, 1, 2), (3, 4), (5,)]):
+        refm += R.FastSum(fam, ell, 1.0, [w], Xm).matvec(Vm[15])
+    worst = max(worst, rel(res["K"][15], refm))
+    print("mixed R=16 K", rel(res["K"][15], refm), flush=True)
 
     for q in (1, 2, 3):
         np_ = nufft.NufftPlan(dims=q, m=16)
