@@ -129,6 +129,10 @@ typedef struct ak_tuning {
     int32_t fused_fft3;         /* 1: band-pruned fused 3-D transforms for (n, m) = (64, 32) /
                                     (32, 16) (default); 0: cuFFT + band multiply                     */
     int32_t generic_kernels;    /* 1: one-thread-per-point kernels for every window (cross-check)    */
+    int32_t sparse_warps;       /* warps sharing a supercell item's region tile in the 3-D sparse
+                                    (multi-cell) interpolation: 1 or 2 (default 2; the spread keeps
+                                    one warp per item: two warps flushing cell runs into one tile
+                                    need shared-memory atomics, measured 2.3x slower on config 3)    */
 } ak_tuning;
 
 /* Fill *t with the defaults ak_geom_create uses. */

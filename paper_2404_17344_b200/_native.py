@@ -74,6 +74,7 @@ class Tuning(ctypes.Structure):
         ("rhs_pair_spread", ctypes.c_int32),
         ("fused_fft3", ctypes.c_int32),
         ("generic_kernels", ctypes.c_int32),
+        ("sparse_warps", ctypes.c_int32),
     ]
 
 

@@ -283,6 +283,7 @@ extern "C" void ak_tuning_default(ak_tuning* t) {
     t->rhs_pair_spread = 1;
     t->fused_fft3 = 1;
     t->generic_kernels = 0;
+    t->sparse_warps = 2;
 }
 
 __global__ void k_count_nonzero(const int* __restrict__ counts, int total, int* __restrict__ nz) {
@@ -812,7 +813,8 @@ extern "C" int ak_geom_create_ex(int32_t n, int32_t P, const int32_t* q, const i
         if ((t.cell_items3 != 0 && t.cell_items3 != 1 && t.cell_items3 != 2) ||
             (t.cell_items2 != 0 && t.cell_items2 != 1 && t.cell_items2 != 8) ||
             (t.chunk3 != 0 && (t.chunk3 < 64 || t.chunk3 > 65536)) || !(t.dense_cells3 >= 0.0) ||
-            !(t.dense_cells3_interp >= 0.0) || !(t.dense_cells2 >= 0.0))
+            !(t.dense_cells3_interp >= 0.0) || !(t.dense_cells2 >= 0.0) ||
+            (t.sparse_warps != 1 && t.sparse_warps != 2))
             return fail(AK_ERR_INVALID, "bad tuning value");
     }
     return geom_create(n, P, q, cols, X, N, ld, masks, rows_in, wf, tuning, stream, out);
@@ -1145,8 +1147,12 @@ static const char* launch_interp3_t(const ak_geom* g, int64_t i0, int64_t ni, co
             return "k_interp3c";
         }
         if (g->cached) {
-            k_interp3m<2, 16><<<units, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids, g->canon_off_d,
-                                                    R, g->n, scale, out, os, atomic_out, wstride);
+#define AK_I3M(NW) k_interp3m<2, 16, NW><<<units, 32 * NW, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids, \
+                                                                    g->canon_off_d, R, g->n, scale, out, os,          \
+                                                                    atomic_out, wstride)
+            if (g->tune.sparse_warps == 2) AK_I3M(2);
+            else AK_I3M(1);
+#undef AK_I3M
             return "k_interp3m";
         }
     }

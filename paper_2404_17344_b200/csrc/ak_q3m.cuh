@@ -121,8 +121,12 @@ __device__ __forceinline__ double interp_group_mma_s(const double* cb, const int
 // Multi-cell (supercell) work items: the item's (S+11)^3 grid region is staged in
 // shared memory once, and every 8-point group of a cell run reads its B fragments
 // from it inside the DMMA loop (no per-cell register copy of the footprint).
-template <int S, int B>
-__global__ void __launch_bounds__(32, 12)
+// NW warps share the region tile (read only); warp w takes the item's batches
+// w, w + NW, ... with its own double-buffered weight rows and barriers (the tile is
+// 17.6 KB at S = 2: one warp per CTA leaves shared memory, not registers, as the
+// occupancy limit).
+template <int S, int B, int NW>
+__global__ void __launch_bounds__(32 * NW, 12 / NW)
 k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ grids,
            const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,
@@ -135,16 +139,21 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     static_assert(B % 8 == 0 && B <= 32, "batch: multiple of 8, at most 32");
 
     __shared__ double tile[TILE];
-    __shared__ __align__(128) double wbuf[2][B][RW];
-    __shared__ __align__(16) CellIdx cib[2][B];
-    __shared__ int cst[B];
+    __shared__ __align__(128) double wbuf_all[NW][2][B][RW];
+    __shared__ __align__(16) CellIdx cib_all[NW][2][B];
+    __shared__ int cst_all[NW][B];
     __shared__ int widx[3][R];
-    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ __align__(8) uint64_t bar_all[NW][2];
 
     // the RHS index runs fastest: the nrhs CTAs of one item share its weight rows in L2
     const WorkItem it = items[blockIdx.x / nrhs];
     const int r = blockIdx.x % nrhs;
-    const int lane = threadIdx.x;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    double (*wbuf)[B][RW] = wbuf_all[warp];
+    CellIdx (*cib)[B] = cib_all[warp];
+    int* cst = cst_all[warp];
+    uint64_t* bar = bar_all[warp];
     const int sc0 = it.sc & 1023, sc1 = (it.sc >> 10) & 1023, sc2 = (it.sc >> 20) & 1023;
     const int nbatch = (it.count + B - 1) / B;
     const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
@@ -156,20 +165,23 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         mbar_fence_init();
     }
     __syncwarp();
-    {
-        const int cnt = min(B, it.count);
-        if (lane == 0) tma_load_1d(&wbuf[0][0][0], Wit, (unsigned)(cnt * RW * 8), &bar[0]);
-        if (lane < cnt) cp_async8(&cib[0][lane], CIit + lane);
+    if (warp < nbatch) {
+        const int cnt = min(B, it.count - warp * B);
+        if (lane == 0) tma_load_1d(&wbuf[0][0][0], Wit + (int64_t)warp * B * RW, (unsigned)(cnt * RW * 8), &bar[0]);
+        if (lane < cnt) cp_async8(&cib[0][lane], CIit + warp * B + lane);
     }
     {
         const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
-        region_axes<R>(widx, sc0 * S - (T / 2 - 1), sc1 * S - (T / 2 - 1), sc2 * S - (T / 2 - 1), n, lane, 32);
-        __syncwarp();
-        for_region_rows<R>(widx, n, lane, 32, [&](int i, int64_t gi) { cp_async8(&tile[i], g + gi); });
+        region_axes<R>(widx, sc0 * S - (T / 2 - 1), sc1 * S - (T / 2 - 1), sc2 * S - (T / 2 - 1), n, threadIdx.x,
+                       32 * NW);
+        if (NW > 1) __syncthreads();
+        else __syncwarp();
+        for_region_rows<R>(widx, n, threadIdx.x, 32 * NW, [&](int i, int64_t gi) { cp_async8(&tile[i], g + gi); });
     }
     cp_async_commit();
     cp_async_wait_all();
-    __syncwarp();
+    if (NW > 1) __syncthreads();
+    else __syncwarp();
     const double sc = scale[it.window];
     double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * os.rs;
 
@@ -178,20 +190,21 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     const double* cb = tile;
     int cur = -1;
 
-    for (int bi = 0; bi < nbatch; ++bi) {
-        const int s = bi & 1;
+    for (int bi = warp, u = 0; bi < nbatch; bi += NW, ++u) {
+        const int s = u & 1;
         const int off = bi * B;
         const int nb = min(B, it.count - off);
         cp_async_wait_all();
-        mbar_wait(&bar[s], (bi >> 1) & 1);
+        mbar_wait(&bar[s], (u >> 1) & 1);
         __syncwarp();
-        if (bi + 1 < nbatch) {
-            const int nb1 = min(B, it.count - off - B);
+        if (bi + NW < nbatch) {
+            const int nb1 = min(B, it.count - off - NW * B);
             if (lane == 0) {
                 fence_proxy_async();
-                tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + B) * RW, (unsigned)(nb1 * RW * 8), &bar[s ^ 1]);
+                tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + NW * B) * RW, (unsigned)(nb1 * RW * 8),
+                            &bar[s ^ 1]);
             }
-            if (lane < nb1) cp_async8(&cib[s ^ 1][lane], CIit + off + B + lane);
+            if (lane < nb1) cp_async8(&cib[s ^ 1][lane], CIit + off + NW * B + lane);
         }
         cp_async_commit();
         if (lane < nb) {

@@ -175,6 +175,26 @@ def test_grid_search_batched_matches_reference(cuda):
     assert tuple(res.best_pair) == tuple(g["best"])
 
 
+def test_grid_search_in_memory_sized_batches(cuda, monkeypatch):
+    """Cells split into lockstep batches (as when the device memory would not hold all
+    cells' operators at once) give the same grid as one batch."""
+    from paper_2404_17344_b200 import solver
+    from paper_2404_17344_b200.windows import WindowSet
+
+    g = golden("solver")
+    tr = _ds(g["Xtr"], g["ytr"], 2)
+    te = _ds(g["Xte"], g["yte"], 2)
+    ws = WindowSet(((1, 2), (3, 4), (5, 6)), d_max=2)
+    one = solver.grid_search(tr, te, ws, [0.5, 1.0, 2.0], [0.01, 0.1])
+    monkeypatch.setattr(solver, "_grid_chunk", lambda plan, R: 4)
+    split = solver.grid_search(tr, te, ws, [0.5, 1.0, 2.0], [0.01, 0.1])
+    for a, b in zip(one.cells, split.cells):
+        assert (a.ell, a.beta) == (b.ell, b.beta)
+        assert abs(a.cg_iterations - b.cg_iterations) <= 1
+        assert abs(a.rmse - b.rmse) <= 1e-6 * abs(a.rmse)
+    assert one.best_pair == split.best_pair
+
+
 def test_cg_solve_batched_equals_sequential(cuda):
     import torch
 
