@@ -421,7 +421,7 @@ def _kernel_q(name: str) -> int:
         return 3
     if name.startswith(("k_spread2", "k_interp2")) or "<2>" in name:
         return 2
-    if "<1>" in name:
+    if name.startswith(("k_spread1", "k_interp1")) or "<1>" in name:
         return 1
     return 0
 
@@ -433,7 +433,9 @@ def kernel_rooflines(report: dict, lengths, rows_per_window, R: int, steps: int,
       FLOPs = 2 T^q per point x window x RHS (one FMA per tap)
       bytes = per point x window: 8 q (coordinates) + 8 R (one RHS value read by the
               spread / one output written by the interpolation, per RHS)
-    Bound: FP64 for q = 3 (12.9 FLOP/B >> ridge), HBM for q <= 2."""
+    Bound: whichever roof the kernel's arithmetic intensity hits first (ridge = FP64
+    peak / HBM peak, ~5.6 FLOP/B): FP64 for q = 3 and for q = 2 with many RHS, HBM for
+    q = 1."""
     T = 12
     out = {}
     for name, (cnt, ms) in report.items():
@@ -447,8 +449,11 @@ def kernel_rooflines(report: dict, lengths, rows_per_window, R: int, steps: int,
         ent = {"launches_per_step": cnt / steps, "ms_per_launch": t * 1e3, "q": q,
                "flops_per_launch": flops, "alg_bytes_per_launch": byts,
                "achieved_tflops": flops / t / 1e12, "achieved_gbs": byts / t / 1e9}
-        if q == 3:
-            ent.update(bound="fp64", frac=ent["achieved_tflops"] / peaks["fp64_tflops"])
+        ridge = peaks["fp64_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+        ent["flop_per_byte"] = flops / byts
+        if flops / byts >= ridge:
+            ent.update(bound="fp64", frac=ent["achieved_tflops"] / peaks["fp64_tflops"],
+                       hbm_frac=ent["achieved_gbs"] / peaks["hbm_gbs"])
         else:
             ent.update(bound="hbm", frac=ent["achieved_gbs"] / peaks["hbm_gbs"],
                        fp64_frac=ent["achieved_tflops"] / peaks["fp64_tflops"])
