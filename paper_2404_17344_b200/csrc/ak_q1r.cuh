@@ -11,9 +11,8 @@
 //   points' RHS values as whole lines (lane = RHS within a point: coalesced);
 //   interp: a stream keeps its current cell's 12 grid values per RHS lane in
 //           registers and contracts them with each point's weights;
-//   spread: a stream accumulates a cell run in registers (12 per lane), flushes
-//           into its own shared region tile on a cell change; the streams' tiles
-//           are summed and added to the grid with one RED per region value.
+//   spread: a stream accumulates a cell run in registers (12 per lane) and adds
+//           them to the grid (RED) when the cell changes.
 // Replaces the lane-per-point kernels (ak_kernels.cuh) for R >= 8 RHS-minor
 // products: those recompute the weights per RHS and touch one 8-byte value per
 // point per CTA.
@@ -54,14 +53,21 @@ __device__ __forceinline__ void q1_stage(const Point& p, bool valid, int sc0, in
     }
 }
 
+// In the q = 1 windows of the BASELINE workloads a cell holds thousands of points
+// (config 5: 1M points per window over 64 cells), so a stream changes cell a few
+// times per work item: the kernels keep no shared region tile -- the interpolation
+// loads a new cell's 12 grid values per RHS lane straight from L2, the spread adds
+// its register accumulators to the grid with 12 REDs per lane at a cell change.
+// Batches whose points all lie in the stream's current cell (almost all) take an
+// unrolled path: independent FMA chains across points, no per-point cell test.
+
 template <int T, int RC>
-__global__ void __launch_bounds__(32, 24)
+__global__ void __launch_bounds__(32, 16)
 k_interp1r(const Point* __restrict__ pts, const WorkItem* __restrict__ items, const double* __restrict__ grids,
            const int64_t* __restrict__ canon_off, int nrhs, int n, const ak_window_fn wf,
            const double* __restrict__ scale, double* __restrict__ out, Strides os, int atomic_out, int64_t wstride)
 {
-    constexpr int S = 16, REG = S + T - 1, SP = Q1Lanes<RC>::SP;
-    __shared__ double tile[REG][RC];
+    constexpr int SP = Q1Lanes<RC>::SP, PPS = 32 / SP;   // point streams, points per stream per batch
     __shared__ __align__(16) double wst[32][T];
     __shared__ int lst[32], ist[32];
 
@@ -70,22 +76,22 @@ k_interp1r(const Point* __restrict__ pts, const WorkItem* __restrict__ items, co
     q1_range(it, blockIdx.x % Q1_SPLIT, beg, end);
     const int r0 = blockIdx.y * RC;
     const int lane = threadIdx.x, rl = lane % RC, sp = lane / RC;
-    const int nr = min(RC, nrhs - r0);
+    const bool ract = r0 + rl < nrhs;
     const int sc0 = it.sc & 1023;
-    const int o0 = sc0 * S - (T / 2 - 1);
+    const int o0 = sc0 * 16 - (T / 2 - 1);
     Point pn;
     if (lane < end - beg) pn = pts[beg + lane];
-    {
-        const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r0 * n;
-        for (int e = lane; e < REG * RC; e += 32) {
-            const int i = e / RC, rr = e - i * RC;
-            tile[i][rr] = rr < nr ? __ldg(g + (int64_t)rr * n + wrap(o0 + i, n)) : 0.0;
-        }
-    }
+    const double* __restrict__ g =
+        grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)(ract ? r0 + rl : r0) * n;
     const double sc = scale[it.window];
     double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)(r0 + rl) * os.rs;
     int cur = -1;
     double tv[T];
+#define AK_Q1_LOAD_CELL(L)                                                        \
+    do {                                                                          \
+        cur = (L);                                                                \
+        _Pragma("unroll") for (int a = 0; a < T; ++a) tv[a] = ract ? __ldg(g + wrap(o0 + cur + a, n)) : 0.0; \
+    } while (0)
     for (int base = beg; base < end; base += 32) {
         const int nb = min(32, end - base);
         const Point p = pn;
@@ -93,25 +99,47 @@ k_interp1r(const Point* __restrict__ pts, const WorkItem* __restrict__ items, co
         __syncwarp();
         q1_stage<T>(p, lane < nb, sc0, lane, wf, wst, lst, ist);
         __syncwarp();
-        // stream sp, lane rl: point j, RHS r0 + rl -- the RC lanes of a stream write one
-        // point's RC values (a whole line at RC = 16 in the RHS-minor layout)
+        // every point of the batch in the warp's current cell (both streams)?
+        const bool same = __all_sync(0xffffffffu, lane >= nb || lst[lane] == cur);
+        if (same && nb == 32) {
+            constexpr int H = PPS > 8 ? 8 : PPS;   // points per pass (independent FMA chains)
+#pragma unroll
+            for (int k0 = 0; k0 < PPS; k0 += H) {
+                double acc[H];
+#pragma unroll
+                for (int k = 0; k < H; ++k) acc[k] = 0.0;
+#pragma unroll
+                for (int a = 0; a < T; ++a)
+#pragma unroll
+                    for (int k = 0; k < H; ++k) acc[k] = fma(wst[sp + SP * (k0 + k)][a], tv[a], acc[k]);
+#pragma unroll
+                for (int k = 0; k < H; ++k) {
+                    double* dst = o + (int64_t)ist[sp + SP * (k0 + k)] * os.is;
+                    if (ract) {
+                        if (atomic_out) red_add(dst, sc * acc[k]);
+                        else *dst = sc * acc[k];
+                    }
+                }
+            }
+            continue;
+        }
+#pragma unroll 1
         for (int j = sp; j < nb; j += SP) {
             const int l = lst[j];
-            if (l != cur) {
-                cur = l;
-#pragma unroll
-                for (int a = 0; a < T; ++a) tv[a] = tile[l + a][rl];
-            }
+            if (l != cur) AK_Q1_LOAD_CELL(l);
             double acc = 0.0;
 #pragma unroll
             for (int a = 0; a < T; ++a) acc = fma(wst[j][a], tv[a], acc);
-            if (rl < nr) {
+            if (ract) {
                 double* dst = o + (int64_t)ist[j] * os.is;
                 if (atomic_out) red_add(dst, sc * acc);
                 else *dst = sc * acc;
             }
         }
+        // both streams continue in the cell of the batch's last point
+        if (cur != lst[nb - 1]) AK_Q1_LOAD_CELL(lst[nb - 1]);
     }
+#undef AK_Q1_LOAD_CELL
 }
 
 template <int T, int RC>
@@ -120,8 +148,7 @@ k_spread1r(const Point* __restrict__ pts, const WorkItem* __restrict__ items, co
            Strides vs, double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n,
            const ak_window_fn wf)
 {
-    constexpr int S = 16, REG = S + T - 1, SP = Q1Lanes<RC>::SP, PPS = 32 / SP;   // points per stream per batch
-    __shared__ double tile[SP][REG][RC];
+    constexpr int SP = Q1Lanes<RC>::SP, PPS = 32 / SP;
     __shared__ __align__(16) double wst[32][T];
     __shared__ double vst[32][RC];
     __shared__ int lst[32];
@@ -131,30 +158,38 @@ k_spread1r(const Point* __restrict__ pts, const WorkItem* __restrict__ items, co
     q1_range(it, blockIdx.x % Q1_SPLIT, beg, end);
     const int r0 = blockIdx.y * RC;
     const int lane = threadIdx.x, rl = lane % RC, sp = lane / RC;
-    const int nr = min(RC, nrhs - r0);
+    const bool ract = r0 + rl < nrhs;
     const int sc0 = it.sc & 1023;
+    const int o0 = sc0 * 16 - (T / 2 - 1);
     Point pn;
     if (lane < end - beg) pn = pts[beg + lane];
-    for (int e = lane; e < SP * REG * RC; e += 32) (&tile[0][0][0])[e] = 0.0;
     const double* __restrict__ Vr = V + (int64_t)(r0 + rl) * vs.rs;
+    double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)(r0 + rl) * n;
 
     int cur = -1;
     double acc[T];
 #pragma unroll
     for (int a = 0; a < T; ++a) acc[a] = 0.0;
+    auto flush = [&]() {
+        if (cur >= 0 && ract) {
+#pragma unroll
+            for (int a = 0; a < T; ++a) red_add(g + wrap(o0 + cur + a, n), acc[a]);
+        }
+#pragma unroll
+        for (int a = 0; a < T; ++a) acc[a] = 0.0;
+    };
     for (int base = beg; base < end; base += 32) {
         const int nb = min(32, end - base);
         const Point p = pn;
         if (lane < end - base - 32) pn = pts[base + 32 + lane];
-        // the stream's RHS values of the batch (point j = sp + SP k, RHS r0 + rl): all
-        // loads issued before the weights are evaluated; a stream's RC lanes read one
-        // line per point
+        // the stream's RHS values of the batch (point j = sp + SP k, RHS r0 + rl), issued
+        // before the weights are evaluated; a stream's RC lanes read one line per point
         double vv[PPS];
 #pragma unroll
         for (int k = 0; k < PPS; ++k) {
             const int j = sp + SP * k;
             const int idx = __shfl_sync(0xffffffffu, p.idx, j);
-            vv[k] = (j < nb && rl < nr) ? __ldg(Vr + (int64_t)idx * vs.is) : 0.0;
+            vv[k] = (j < nb && ract) ? __ldg(Vr + (int64_t)idx * vs.is) : 0.0;
         }
         __syncwarp();
         if (lane < nb) {
@@ -165,40 +200,36 @@ k_spread1r(const Point* __restrict__ pts, const WorkItem* __restrict__ items, co
             lst[lane] = cell_axis(p.cell, 0) - sc0 * 16;
             AK_DCHECK(lst[lane] >= 0 && lst[lane] < 16);
         }
+        __syncwarp();
+        const bool same = __all_sync(0xffffffffu, lane >= nb || lst[lane] == cur);
+        if (same) {
+            // rows past nb hold v = 0
+#pragma unroll
+            for (int k = 0; k < PPS; ++k) {
+                const int j = min(sp + SP * k, nb - 1);
+#pragma unroll
+                for (int a = 0; a < T; ++a) acc[a] = fma(wst[j][a], vv[k], acc[a]);
+            }
+            continue;
+        }
+        // a cell boundary inside the batch: point by point
 #pragma unroll
         for (int k = 0; k < PPS; ++k) vst[sp + SP * k][rl] = vv[k];
         __syncwarp();
+#pragma unroll 1
         for (int j = sp; j < nb; j += SP) {
             const int l = lst[j];
             if (l != cur) {
-                if (cur >= 0) {
-#pragma unroll
-                    for (int a = 0; a < T; ++a) {
-                        tile[sp][cur + a][rl] += acc[a];
-                        acc[a] = 0.0;
-                    }
-                }
+                flush();
                 cur = l;
             }
             const double v = vst[j][rl];
 #pragma unroll
             for (int a = 0; a < T; ++a) acc[a] = fma(wst[j][a], v, acc[a]);
         }
+        __syncwarp();
     }
-    if (cur >= 0) {
-#pragma unroll
-        for (int a = 0; a < T; ++a) tile[sp][cur + a][rl] += acc[a];
-    }
-    __syncwarp();
-    const int o0 = sc0 * S - (T / 2 - 1);
-    double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r0 * n;
-    for (int e = lane; e < REG * RC; e += 32) {
-        const int i = e / RC, rr = e - i * RC;
-        double s = 0.0;
-#pragma unroll
-        for (int k = 0; k < SP; ++k) s += tile[k][i][rr];
-        if (rr < nr && s != 0.0) red_add(g + (int64_t)rr * n + wrap(o0 + i, n), s);
-    }
+    flush();
 }
 
 }  // namespace ak
