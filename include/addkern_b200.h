@@ -133,8 +133,6 @@ typedef struct ak_tuning {
                                     (multi-cell) interpolation: 1 or 2 (default 2; the spread keeps
                                     one warp per item: two warps flushing cell runs into one tile
                                     need shared-memory atomics, measured 2.3x slower on config 3)    */
-    int32_t fuse_sets;          /* 1: two coefficient sets (K, dK/dl) on dense 3-D windows are
-                                    interpolated in one pass over the points (default); 0: per set  */
 } ak_tuning;
 
 /* Fill *t with the defaults ak_geom_create uses. */

@@ -75,7 +75,6 @@ class Tuning(ctypes.Structure):
         ("fused_fft3", ctypes.c_int32),
         ("generic_kernels", ctypes.c_int32),
         ("sparse_warps", ctypes.c_int32),
-        ("fuse_sets", ctypes.c_int32),
     ]
 
 

@@ -284,7 +284,6 @@ extern "C" void ak_tuning_default(ak_tuning* t) {
     t->fused_fft3 = 1;
     t->generic_kernels = 0;
     t->sparse_warps = 2;
-    t->fuse_sets = 1;
 }
 
 __global__ void k_count_nonzero(const int* __restrict__ counts, int total, int* __restrict__ nz) {
@@ -815,7 +814,7 @@ extern "C" int ak_geom_create_ex(int32_t n, int32_t P, const int32_t* q, const i
             (t.cell_items2 != 0 && t.cell_items2 != 1 && t.cell_items2 != 8) ||
             (t.chunk3 != 0 && (t.chunk3 < 64 || t.chunk3 > 65536)) || !(t.dense_cells3 >= 0.0) ||
             !(t.dense_cells3_interp >= 0.0) || !(t.dense_cells2 >= 0.0) ||
-            (t.sparse_warps != 1 && t.sparse_warps != 2) || (t.fuse_sets != 0 && t.fuse_sets != 1))
+            (t.sparse_warps != 1 && t.sparse_warps != 2))
             return fail(AK_ERR_INVALID, "bad tuning value");
     }
     return geom_create(n, P, q, cols, X, N, ld, masks, rows_in, wf, tuning, stream, out);
@@ -1246,27 +1245,6 @@ extern "C" int ak_interp(const ak_geom* g, const double* grids, int32_t R, const
     return guards_verify("ak_interp");
 }
 
-// Whether a geometry's 3-D interpolation runs the dense single-cell DMMA kernel, the
-// one with a two-set variant (k_interp3c2: K and dK/dl from one pass).
-static bool dense3_interp(const ak_geom* g) {
-    return g->cached && g->sedge_i3 == 1 && !g->trim3 && g->wf.taps == 12 && !g->tune.generic_kernels &&
-           g->tune.fuse_sets && g->iitem_end3 > g->iitem_begin3;
-}
-
-static int interp3_two_sets(const ak_geom* g, const double* grids0, const double* grids1, int R, const double* scale,
-                            double* const* outs, Strides os, const int32_t* sum_windows, int accumulate,
-                            int64_t wstride, cudaStream_t st)
-{
-    const int64_t i0 = g->iitem_begin3, ni = g->iitem_end3 - g->iitem_begin3;
-    const int P = g->P;
-    const InterpSet a{grids0, scale, outs[0], (sum_windows[0] || accumulate) ? 1 : 0, sum_windows[0] ? 0 : wstride};
-    const InterpSet b{grids1, scale + P, outs[1], (sum_windows[1] || accumulate) ? 1 : 0, sum_windows[1] ? 0 : wstride};
-    ProfScope ps(st);
-    k_interp3c2<32><<<(unsigned)(ni * R), 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, g->canon_off_d, R,
-                                                       g->n, os, a, b);
-    return ps.done("k_interp3c2");
-}
-
 // ---------------------------------------------------------------------------
 // FFT stage
 
@@ -1369,7 +1347,7 @@ static bool fft3_fused_ok(const ak_geom* g, int n, int m) {
 
 struct ak_op;
 static int fft3_forward(ak_op* op, cudaStream_t st);
-static int fft3_inverse(ak_op* op, const double* const* H, int hbase, int per_rhs, cudaStream_t st, double* dst);
+static int fft3_inverse(ak_op* op, const double* const* H, int hbase, int per_rhs, cudaStream_t st);
 
 struct ak_op {
     const ak_geom* gs = nullptr;
@@ -1377,7 +1355,6 @@ struct ak_op {
     int m = 0, R = 0, C = 0;
     double* grids = nullptr;      // canonical, R rhs
     double* gbuf = nullptr;       // canonical, R rhs
-    double* gbuf2 = nullptr;      // second set's 3-D grids when two sets interpolate in one pass (C == 2)
     double2* spec = nullptr;
     double2* spec2 = nullptr;
     int64_t spec_off[4] = {0, 0, 0, 0};   // complex elements, per q group
@@ -1420,9 +1397,9 @@ static int fft3_forward_t(ak_op* op, cudaStream_t st) {
     return ps.done("k_fft3_fwd0");
 }
 
-// fused q = 3: H (set hbase / per RHS) x band spectra -> dst grids (canonical layout)
+// fused q = 3: H (set hbase / per RHS) x band spectra -> op->gbuf grids
 template <int n, int m>
-static int fft3_inverse_t(ak_op* op, const double* const* H, int hbase, int per_rhs, cudaStream_t st, double* dst) {
+static int fft3_inverse_t(ak_op* op, const double* const* H, int hbase, int per_rhs, cudaStream_t st) {
     const unsigned nb = (unsigned)(op->R * op->nwin[3]);
     const ak::Fft3Tables tb = fft3_tables(op);
     {
@@ -1434,7 +1411,7 @@ static int fft3_inverse_t(ak_op* op, const double* const* H, int hbase, int per_
     }
     ProfScope ps(st);
     ak::k_fft3_inv12<n, m><<<dim3(n, nb), ak::FFT3_THREADS, ak::fft3_smem_inv12(n, m), st>>>(
-        op->fbuf, dst + op->grid_off[3], tb);
+        op->fbuf, op->gbuf + op->grid_off[3], tb);
     return ps.done("k_fft3_inv12");
 }
 
@@ -1442,9 +1419,9 @@ static int fft3_forward(ak_op* op, cudaStream_t st) {
     return op->gs->n == 64 ? fft3_forward_t<64, 32>(op, st) : fft3_forward_t<32, 16>(op, st);
 }
 
-static int fft3_inverse(ak_op* op, const double* const* H, int hbase, int per_rhs, cudaStream_t st, double* dst) {
-    return op->gs->n == 64 ? fft3_inverse_t<64, 32>(op, H, hbase, per_rhs, st, dst)
-                           : fft3_inverse_t<32, 16>(op, H, hbase, per_rhs, st, dst);
+static int fft3_inverse(ak_op* op, const double* const* H, int hbase, int per_rhs, cudaStream_t st) {
+    return op->gs->n == 64 ? fft3_inverse_t<64, 32>(op, H, hbase, per_rhs, st)
+                           : fft3_inverse_t<32, 16>(op, H, hbase, per_rhs, st);
 }
 
 extern "C" int ak_op_destroy(ak_op* op) {
@@ -1460,7 +1437,6 @@ extern "C" int ak_op_destroy(ak_op* op) {
     ak_free(op->ftab);
     ak_free(op->grids);
     ak_free(op->gbuf);
-    ak_free(op->gbuf2);
     ak_free(op->spec);
     ak_free(op->spec2);
     ak_free(op->band);
@@ -1474,8 +1450,6 @@ static int op_build(ak_op* op, cudaStream_t st) {
     const int64_t total = g->canon_total * op->R;
     AK_CUDA(AK_MALLOC(&op->grids, sizeof(double) * total));
     AK_CUDA(AK_MALLOC(&op->gbuf, sizeof(double) * total));
-    if (op->C == 2 && dense3_interp(op->gi) && !g->windows_of_q[3].empty())
-        AK_CUDA(AK_MALLOC(&op->gbuf2, sizeof(double) * total));
     int64_t soff = 0;
     for (int q = 3; q >= 1; --q) {
         const auto& ws = g->windows_of_q[q];
@@ -1643,15 +1617,11 @@ static int op_apply(ak_op* op, const double* V, int64_t ldv, const double* const
             if (flags & AK_APPLY_FROM_SPECTRUM) AK_TRY(band_pack(op, q, 1, st));
             else AK_TRY(cufft_d2z(op, q, st));
         }
-    // two coefficient sets on dense 3-D windows: both inverse transforms first (set 1's
-    // 3-D grids into gbuf2), then one interpolation pass serves both (k_interp3c2)
-    const bool two = op->gbuf2 != nullptr && op->C == 2;
     for (int c = 0; c < op->C; ++c) {
-        double* gdst = (two && c == 1) ? op->gbuf2 : op->gbuf;
         for (int q = 3; q >= 1; --q) {
             if (!op->has[q]) continue;
             if (q == 3 && op->fused3) {
-                AK_TRY(fft3_inverse(op, H, c * P, (flags & AK_APPLY_H_PER_RHS) ? 1 : 0, st, gdst));
+                AK_TRY(fft3_inverse(op, H, c * P, (flags & AK_APPLY_H_PER_RHS) ? 1 : 0, st));
                 continue;
             }
             const int64_t total = op->hs[q] * R * op->nwin[q];
@@ -1666,21 +1636,14 @@ static int op_apply(ak_op* op, const double* V, int64_t ldv, const double* const
             ProfScope ps(st);
             AK_CUFFT(cufftSetStream(op->inv[q], st));
             AK_CUFFT(cufftExecZ2D(op->inv[q], (cufftDoubleComplex*)(op->spec2 + op->spec_off[q]),
-                                  (q == 3 ? gdst : op->gbuf) + op->grid_off[q]));
+                                  op->gbuf + op->grid_off[q]));
             g_launches.fetch_add(1);
             ps.close(q == 3 ? "cufft_z2d<3>" : (q == 2 ? "cufft_z2d<2>" : "cufft_z2d<1>"));
         }
         const int atomic_out = (sum_windows[c] || accumulate) ? 1 : 0;
-        for (int q = 3; q >= 1; --q) {
-            if (q == 3 && two) {
-                if (c == 1)
-                    AK_TRY(interp3_two_sets(gi, op->gbuf, op->gbuf2, R, scale, outs, os, sum_windows, accumulate,
-                                            wstride, st));
-                continue;
-            }
+        for (int q = 3; q >= 1; --q)
             AK_TRY(interp_group(gi, q, op->gbuf, R, scale + (int64_t)c * P, outs[c], os, sum_windows[c], atomic_out,
                                 wstride, st));
-        }
     }
     return AK_OK;
 }

@@ -311,9 +311,16 @@ __device__ __forceinline__ void interp3c_unit(Interp3cSmem<B>& sm, int unit, con
     }
 }
 
-// (__maxnreg__ 184/200/208 for 10-11 warps per SM: no gain, 1.353-1.369 vs 1.351 ms)
+// Register cap (B200, tools/gpu_var_both.sh): 168 registers -> 12 warps/SM by registers
+// (11 by shared memory): config 4 1.329 -> 1.256 ms, config 5 97.5 -> 91.4 ms per two
+// launches; 184 / 200 / 224 registers: no gain; 160 / 152 / 144: 1.266 / 1.272 / 1.273 ms.
+// (A two-set variant sharing the weight rows between K and dK/dl needed 255 registers
+// plus spills and gained 0.1% on config 5 at the old cap: removed.)
+#ifndef AK_INTERP3C_BOUNDS
+#define AK_INTERP3C_BOUNDS __maxnreg__(168)
+#endif
 template <int B, int A = 12>
-__global__ void __launch_bounds__(32, 8)
+__global__ void AK_INTERP3C_BOUNDS
 k_interp3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ grids,
            const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,
@@ -322,131 +329,6 @@ k_interp3c(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     __shared__ Interp3cSmem<B> sm;
     interp3c_unit<B, A>(sm, blockIdx.x, ci, W, wshift, items, grids, canon_off, nrhs, n, scale, out, os, atomic_out,
                      wstride);
-}
-
-// interp_group_mma in two halves of 9 fragment tiles (a = 0..5, then 6..11): the
-// contraction over a splits the same way, so only 18 accumulators are live at a
-// time -- room for a second set's footprint in registers (k_interp3c2).
-template <int RW>
-__device__ __forceinline__ double interp_group_mma_h(const double (&gf)[18][3], const double (*wrow)[RW], int k0,
-                                                     int cnt, int lane)
-{
-    const int pj = lane >> 2, q = lane & 3;
-    const bool valid = pj < cnt;
-    const double* w = wrow[k0 + (valid ? pj : 0)];
-    double af[3];
-#pragma unroll
-    for (int ks = 0; ks < 3; ++ks) af[ks] = valid ? w[24 + 4 * ks + q] : 0.0;
-    double s[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        double C[9][2];
-#pragma unroll
-        for (int t = 0; t < 9; ++t) C[t][0] = C[t][1] = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < 3; ++ks)
-#pragma unroll
-            for (int t = 0; t < 9; ++t) dmma_8x8x4(C[t][0], C[t][1], af[ks], gf[9 * h + t][ks]);
-        // tile 9h + t, parity e: pair i = 18h + 2t + e, a = i / 3, b-slot i % 3
-#pragma unroll
-        for (int a = 6 * h; a < 6 * h + 6; ++a) {
-            const double w0a = w[a];
-#pragma unroll
-            for (int bb = 0; bb < 3; ++bb) {
-                const int i = 3 * a + bb - 18 * h;
-                s[bb] = fma(w0a, C[i >> 1][i & 1], s[bb]);
-            }
-        }
-    }
-    const double* w1 = w + 12 + 3 * q;
-    const double v = fma(w1[2], s[2], fma(w1[1], s[1], w1[0] * s[0]));
-    return valid ? v : 0.0;
-}
-
-// Two coefficient sets (K and dK/dl) interpolated from their own grids in one pass:
-// the weight rows, cell records and A fragments of a batch serve both, and the two
-// independent 54-DMMA chains of a group interleave (config 5: every 3-D window's K
-// and dK/dl_w products).  Per set: grid, scale, output (summed by RED or stored).
-struct InterpSet {
-    const double* grids;
-    const double* scale;
-    double* out;
-    int atomic_out;
-    int64_t wstride;
-};
-
-template <int B>
-__global__ void __launch_bounds__(32, 8)
-k_interp3c2(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
-            const WorkItem* __restrict__ items, const int64_t* __restrict__ canon_off, int nrhs, int n, Strides os,
-            InterpSet s0, InterpSet s1)
-{
-    constexpr int T = 12, RW = 3 * T;
-    __shared__ Interp3cSmem<B> sm;
-    auto& wbuf = sm.wbuf;
-    auto& cib = sm.cib;
-    auto& bar = sm.bar;
-
-    const WorkItem it = items[blockIdx.x / nrhs];
-    const int r = blockIdx.x % nrhs;
-    const int lane = threadIdx.x;
-    const int nbatch = (it.count + B - 1) / B;
-    const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
-    const CellIdx* __restrict__ CIit = ci + (it.start - wshift[it.window]);
-
-    if (lane == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        mbar_fence_init();
-    }
-    __syncwarp();
-    if (lane == 0) tma_load_1d(&wbuf[0][0][0], Wit, (unsigned)(min(B, it.count) * RW * 8), &bar[0]);
-    if (lane < min(B, it.count)) cp_async8(&cib[0][lane], CIit + lane);
-    cp_async_commit();
-
-    const int64_t goff = (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
-    double gf0[18][3], gf1[18][3];
-    load_footprint<12>(gf0, s0.grids + goff, it.sc, n, lane);
-    load_footprint<12>(gf1, s1.grids + goff, it.sc, n, lane);
-    const double sc0 = s0.scale[it.window], sc1 = s1.scale[it.window];
-    double* __restrict__ o0 = s0.out + (int64_t)it.window * s0.wstride + (int64_t)r * os.rs;
-    double* __restrict__ o1 = s1.out + (int64_t)it.window * s1.wstride + (int64_t)r * os.rs;
-
-    for (int bi = 0; bi < nbatch; ++bi) {
-        const int s = bi & 1;
-        const int off = bi * B;
-        const int nb = min(B, it.count - off);
-        cp_async_wait_all();
-        mbar_wait(&bar[s], (bi >> 1) & 1);
-        __syncwarp();
-        if (bi + 1 < nbatch) {
-            const int nb1 = min(B, it.count - off - B);
-            if (lane == 0) {
-                fence_proxy_async();
-                tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + B) * RW, (unsigned)(nb1 * RW * 8), &bar[s ^ 1]);
-            }
-            if (lane < nb1) cp_async8(&cib[s ^ 1][lane], CIit + off + B + lane);
-        }
-        cp_async_commit();
-#pragma unroll 1
-        for (int k0 = 0; k0 < nb; k0 += 8) {
-            const int cnt = min(8, nb - k0);
-            double v0 = interp_group_mma_h<RW>(gf0, wbuf[s], k0, cnt, lane);
-            double v1 = interp_group_mma_h<RW>(gf1, wbuf[s], k0, cnt, lane);
-            v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
-            v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
-            v0 += __shfl_xor_sync(0xffffffffu, v0, 2);
-            v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
-            const int pj = lane >> 2;
-            if ((lane & 3) == 0 && pj < cnt) {
-                const int64_t row = (int64_t)cib[s][k0 + pj].idx * os.is;
-                if (s0.atomic_out) red_add(o0 + row, sc0 * v0);
-                else o0[row] = sc0 * v0;
-                if (s1.atomic_out) red_add(o1 + row, sc1 * v1);
-                else o1[row] = sc1 * v1;
-            }
-        }
-    }
 }
 
 }  // namespace ak

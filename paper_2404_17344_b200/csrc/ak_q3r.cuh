@@ -25,8 +25,13 @@ struct alignas(128) Spread3rSmem {
     uint64_t bar[2];
 };
 
+// CTAs per SM (2 warps each): 5 -> 167 registers, 10 warps/SM: config 5 spread
+// 48.03 -> 43.95 ms; 4 (190 registers): 48.03; 6 (157): 57.8 (tools/gpu_var_cfg.sh)
+#ifndef AK_SPREAD3R_MINB
+#define AK_SPREAD3R_MINB 5
+#endif
 template <int B>
-__global__ void __launch_bounds__(64, 4)
+__global__ void __launch_bounds__(64, AK_SPREAD3R_MINB)
 k_spread3r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ V, Strides vs,
            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)

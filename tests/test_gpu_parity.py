@@ -178,7 +178,6 @@ def test_native_library_is_what_runs(cuda):
     {"dense_cells3": 1e9, "dense_cells3_interp": 0, "chunk3": 100},
     {"generic_kernels": 1},
     {"sparse_warps": 1},                        # one warp per supercell item (default: two share the tile)
-    {"fuse_sets": 0, "cell_items3": 1},         # K and dK/dl interpolated in separate passes
     {"sparse_warps": 1, "cell_items3": 2, "chunk3": 100},
 ])
 def test_kernel_variants_match_reference(cuda, variant):

@@ -574,34 +574,3 @@ def test_q2_rhs_batched_kernels(cuda, R):
         one = build_plan(KernelSpec(fam, ell), WindowSet((ws.windows[w],), d_max=2), "default", _ds(X, 2))
         col = fast_matvecs(one, V[R - 1], dell=True)["dK_dell"]
         assert rel(mix["dK_dell"][w][R - 1], col) <= 1e-13
-
-
-@pytest.mark.parametrize("R", [1, 4])
-def test_two_set_fused_interpolation(cuda, R):
-    """K and dK/dl on densely occupied 3-D windows are interpolated in one pass
-    (k_interp3c2, tuning fuse_sets=1): equal to the per-set kernels (fuse_sets=0)
-    and to the oracle; summed and per-window outputs (mixed plans), wrapping cells."""
-    from oracle import restate as R_
-    from paper_2404_17344_b200 import _native
-    from paper_2404_17344_b200.fastsum import build_mixed_plan, build_plan, fast_matvecs, mixed_matvecs
-    from paper_2404_17344_b200.kernels import KernelSpec
-    from paper_2404_17344_b200.windows import WindowSet
-
-    rng = np.random.default_rng(80 + R)
-    N = 40_000
-    X = np.concatenate([rng.uniform(-0.012, 0.012, size=(N - 4000, 6)), rng.uniform(-0.5, -0.49, size=(4000, 6))])
-    V = rng.normal(size=(R, N))
-    ws = WindowSet(((1, 2, 3), (4, 5, 6)), d_max=3)
-    fused = build_plan(KernelSpec("gauss", 0.3), ws, "default", _ds(X, 3))
-    plain = build_plan(KernelSpec("gauss", 0.3), ws, "default", _ds(X, 3), tuning={"fuse_sets": 0})
-    with _native.KernelTimer() as kt:
-        a = fast_matvecs(fused, V, dell=True)
-    assert "k_interp3c2" in kt.report, kt.report
-    b = fast_matvecs(plain, V, dell=True)
-    assert rel(a["K"], b["K"]) <= 1e-13 and rel(a["dK_dell"], b["dK_dell"]) <= 1e-13
-    cols = [(0, 1, 2), (3, 4, 5)]
-    assert rel(np.atleast_2d(a["dK_dell"])[R - 1], R_.FastSum("der_gauss", 0.3, 1.0, cols, X).matvec(V[R - 1])) <= 1e-8
-    specs = [KernelSpec("gauss", 0.3), KernelSpec("gauss", 0.5)]
-    m1 = mixed_matvecs(build_mixed_plan(specs, ws, "default", _ds(X, 3)), V)
-    m0 = mixed_matvecs(build_mixed_plan(specs, ws, "default", _ds(X, 3), tuning={"fuse_sets": 0}), V)
-    assert rel(m1["K"], m0["K"]) <= 1e-13 and rel(m1["dK_dell"], m0["dK_dell"]) <= 1e-13

@@ -112,7 +112,7 @@ def test_tuning_defaults_and_validation():
 
     t = _native.tuning()
     assert (t.weight_tables, t.cell_items3, t.cell_items2, t.chunk3, t.rhs_pair_spread, t.fused_fft3,
-            t.generic_kernels, t.sparse_warps, t.fuse_sets) == (1, 0, 0, 0, 1, 1, 0, 2, 1)
+            t.generic_kernels, t.sparse_warps) == (1, 0, 0, 0, 1, 1, 0, 2)
     assert (t.dense_cells3, t.dense_cells3_interp, t.dense_cells2) == (300.0, 64.0, 2.0)
     with pytest.raises(ValueError):
         _native.tuning(no_such_knob=1)
