@@ -999,7 +999,7 @@ static const char* launch_spread1r(const ak_geom* g, int64_t i0, int64_t ni, con
                                    double* grids, cudaStream_t st)
 {
     const int rc = q1r_chunk(R);
-    const dim3 grid((unsigned)(ni * Q1_SPLIT), (unsigned)((R + rc - 1) / rc));
+    const dim3 grid((unsigned)(ni * AK_Q1_SPLIT_SPREAD), (unsigned)((R + rc - 1) / rc));
     if (rc == 8) k_spread1r<12, 8><<<grid, 32, 0, st>>>(g->pts, g->items + i0, V, vs, grids, g->canon_off_d, R, g->n, g->wf);
     else if (rc == 16) k_spread1r<12, 16><<<grid, 32, 0, st>>>(g->pts, g->items + i0, V, vs, grids, g->canon_off_d, R, g->n, g->wf);
     else k_spread1r<12, 32><<<grid, 32, 0, st>>>(g->pts, g->items + i0, V, vs, grids, g->canon_off_d, R, g->n, g->wf);
@@ -1011,7 +1011,7 @@ static const char* launch_interp1r(const ak_geom* g, int64_t i0, int64_t ni, con
                                    cudaStream_t st)
 {
     const int rc = q1r_chunk(R);
-    const dim3 grid((unsigned)(ni * Q1_SPLIT), (unsigned)((R + rc - 1) / rc));
+    const dim3 grid((unsigned)(ni * AK_Q1_SPLIT_INTERP), (unsigned)((R + rc - 1) / rc));
     if (rc == 8)
         k_interp1r<12, 8><<<grid, 32, 0, st>>>(g->pts, g->items + i0, grids, g->canon_off_d, R, g->n, g->wf, scale,
                                                out, os, atomic_out, wstride);
@@ -1079,7 +1079,7 @@ static const char* launch_spread3_t(const ak_geom* g, int64_t i0, int64_t ni, co
             return "k_spread3c";
         }
         if (g->cached) {
-            k_spread3w<12, 2, 16><<<units, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, vs, grids,
+            k_spread3w<12, 2, AK_SPARSE_BATCH><<<units, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, vs, grids,
                                                         g->canon_off_d, R, g->n);
             return "k_spread3w";
         }
@@ -1147,7 +1147,7 @@ static const char* launch_interp3_t(const ak_geom* g, int64_t i0, int64_t ni, co
             return "k_interp3c";
         }
         if (g->cached) {
-#define AK_I3M(NW) k_interp3m<2, 16, NW><<<units, 32 * NW, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids, \
+#define AK_I3M(NW) k_interp3m<2, AK_SPARSE_BATCH, NW><<<units, 32 * NW, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids, \
                                                                     g->canon_off_d, R, g->n, scale, out, os,          \
                                                                     atomic_out, wstride)
             if (g->tune.sparse_warps == 2) AK_I3M(2);

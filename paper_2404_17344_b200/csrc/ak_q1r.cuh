@@ -3,7 +3,7 @@
 // A 1-D window has 12 taps per point: per point and RHS the gridding work is 12
 // FMAs, so with R right-hand sides the kernels are bound by moving the R values
 // of each point (one cache line at R = 16 in the RHS-minor layout), not by FP64.
-// One warp = a quarter of a work item (a chunk of <= 2048 bin-sorted points of a
+// One warp = a part of a work item (a chunk of <= 2048 bin-sorted points of a
 // 16-cell supercell) x one chunk of RC right-hand sides:
 //   lanes = SP point streams x RC RHS lanes (SP = 32 / RC);
 //   per batch of 32 points each lane evaluates the 12 window weights of one
@@ -26,14 +26,25 @@ struct Q1Lanes {
     static constexpr int SP = 32 / RC;   // point streams per warp
 };
 
-// Launch-time split of a work item into Q1_SPLIT contiguous point ranges (one warp
-// each): a q = 1 item holds up to 2048 points of one 16-cell supercell, and a warp
-// per item leaves too few warps in flight to cover the gather latency.
-constexpr int Q1_SPLIT = 4;
+// Launch-time split of a work item into contiguous point ranges (one warp each): a
+// q = 1 item holds up to 2048 points of one 16-cell supercell, and a warp per item
+// leaves too few warps in flight to cover the gather latency.  The spread splits less:
+// every part adds its cell-run accumulators to the same few grid values (RED
+// contention).  Config 5 (B200): spread 2 parts 0.377 ms, 4: 0.484, 8: 0.865;
+// interpolation 4 parts 0.392 ms per launch, 2: 0.397, 8: 0.404.
+#ifndef AK_Q1_SPLIT_SPREAD
+#define AK_Q1_SPLIT_SPREAD 2
+#endif
+#ifndef AK_Q1_SPLIT_INTERP
+#define AK_Q1_SPLIT_INTERP 4
+#endif
+#ifndef AK_Q1_MINB
+#define AK_Q1_MINB 16
+#endif
 
-__device__ __forceinline__ void q1_range(const WorkItem& it, int part, int& beg, int& end) {
-    beg = it.start + (int)((int64_t)it.count * part / Q1_SPLIT);
-    end = it.start + (int)((int64_t)it.count * (part + 1) / Q1_SPLIT);
+__device__ __forceinline__ void q1_range(const WorkItem& it, int part, int parts, int& beg, int& end) {
+    beg = it.start + (int)((int64_t)it.count * part / parts);
+    end = it.start + (int)((int64_t)it.count * (part + 1) / parts);
 }
 
 // weights, local cell offset and row of the batch's points (one point per lane,
@@ -62,7 +73,7 @@ __device__ __forceinline__ void q1_stage(const Point& p, bool valid, int sc0, in
 // unrolled path: independent FMA chains across points, no per-point cell test.
 
 template <int T, int RC>
-__global__ void __launch_bounds__(32, 16)
+__global__ void __launch_bounds__(32, AK_Q1_MINB)
 k_interp1r(const Point* __restrict__ pts, const WorkItem* __restrict__ items, const double* __restrict__ grids,
            const int64_t* __restrict__ canon_off, int nrhs, int n, const ak_window_fn wf,
            const double* __restrict__ scale, double* __restrict__ out, Strides os, int atomic_out, int64_t wstride)
@@ -71,9 +82,9 @@ k_interp1r(const Point* __restrict__ pts, const WorkItem* __restrict__ items, co
     __shared__ __align__(16) double wst[32][T];
     __shared__ int lst[32], ist[32];
 
-    const WorkItem it = items[blockIdx.x / Q1_SPLIT];
+    const WorkItem it = items[blockIdx.x / AK_Q1_SPLIT_INTERP];
     int beg, end;
-    q1_range(it, blockIdx.x % Q1_SPLIT, beg, end);
+    q1_range(it, blockIdx.x % AK_Q1_SPLIT_INTERP, AK_Q1_SPLIT_INTERP, beg, end);
     const int r0 = blockIdx.y * RC;
     const int lane = threadIdx.x, rl = lane % RC, sp = lane / RC;
     const bool ract = r0 + rl < nrhs;
@@ -143,7 +154,7 @@ k_interp1r(const Point* __restrict__ pts, const WorkItem* __restrict__ items, co
 }
 
 template <int T, int RC>
-__global__ void __launch_bounds__(32, 16)
+__global__ void __launch_bounds__(32, AK_Q1_MINB)
 k_spread1r(const Point* __restrict__ pts, const WorkItem* __restrict__ items, const double* __restrict__ V,
            Strides vs, double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n,
            const ak_window_fn wf)
@@ -153,9 +164,9 @@ k_spread1r(const Point* __restrict__ pts, const WorkItem* __restrict__ items, co
     __shared__ double vst[32][RC];
     __shared__ int lst[32];
 
-    const WorkItem it = items[blockIdx.x / Q1_SPLIT];
+    const WorkItem it = items[blockIdx.x / AK_Q1_SPLIT_SPREAD];
     int beg, end;
-    q1_range(it, blockIdx.x % Q1_SPLIT, beg, end);
+    q1_range(it, blockIdx.x % AK_Q1_SPLIT_SPREAD, AK_Q1_SPLIT_SPREAD, beg, end);
     const int r0 = blockIdx.y * RC;
     const int lane = threadIdx.x, rl = lane % RC, sp = lane / RC;
     const bool ract = r0 + rl < nrhs;

@@ -23,6 +23,12 @@ namespace ak {
 
 constexpr int Q2R_RPW = 8;   // right-hand sides per warp
 
+// warps per SM the register allocation must allow: 16 (<= 128 registers): config-5
+// interp 1.422 -> 1.347 ms per launch, spread 1.839 -> 1.819 ms; 12 (166 registers) before
+#ifndef AK_Q2R_MINW
+#define AK_Q2R_MINW 16
+#endif
+
 template <int B, int NW>
 struct alignas(128) Q2rSmem {
     double wbuf[2][B][24];
@@ -32,7 +38,7 @@ struct alignas(128) Q2rSmem {
 };
 
 template <int B, int NW>
-__global__ void __launch_bounds__(32 * NW, 12 / NW)
+__global__ void __launch_bounds__(32 * NW, AK_Q2R_MINW / NW)
 k_interp2r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ grids,
            const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,
@@ -153,7 +159,7 @@ k_interp2r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
 }
 
 template <int B, int NW>
-__global__ void __launch_bounds__(32 * NW, 12 / NW)
+__global__ void __launch_bounds__(32 * NW, AK_Q2R_MINW / NW)
 k_spread2r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ V, Strides vs,
            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)

@@ -126,7 +126,10 @@ __device__ __forceinline__ double interp_group_mma_s(const double* cb, const int
 // 17.6 KB at S = 2: one warp per CTA leaves shared memory, not registers, as the
 // occupancy limit).
 template <int S, int B, int NW>
-__global__ void __launch_bounds__(32 * NW, 12 / NW)
+#ifndef AK_INTERP3M_MINW
+#define AK_INTERP3M_MINW 12   // warps per SM the register allocation must allow
+#endif
+__global__ void __launch_bounds__(32 * NW, AK_INTERP3M_MINW / NW)
 k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ grids,
            const int64_t* __restrict__ canon_off, int nrhs, int n, const double* __restrict__ scale,

@@ -148,8 +148,15 @@ __device__ __forceinline__ void for_region_rows(const int (*widx)[R], int n, int
     }
 }
 
+// points per staged weight batch of the sparse (supercell) 3-D kernels
+#ifndef AK_SPARSE_BATCH
+#define AK_SPARSE_BATCH 16
+#endif
+#ifndef AK_SPREAD3W_BOUNDS
+#define AK_SPREAD3W_BOUNDS __launch_bounds__(32, 8)
+#endif
 template <int T, int S, int B>
-__global__ void __launch_bounds__(32, 8)
+__global__ void AK_SPREAD3W_BOUNDS
 k_spread3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ V, Strides vs,
            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
