@@ -89,6 +89,8 @@ def parse():
 def config_dict(args) -> dict:
     """The workload description both arms print (identical dicts: the driver compares them)."""
     par = "single GPU" if args.gpus == 1 else f"{SHARD_NAMES[args.shard]} over {args.gpus} GPUs, NCCL"
+    if args.gpus > 1 and getattr(args, "dist_backend", "nccl") == "gloo":
+        par = f"{SHARD_NAMES[args.shard]} over {args.gpus} ranks on one device, gloo (functional check, not a bench value)"
     return {"workload": WORKLOAD, "N": args.n, "windows": 10, "rhs": 1, "parallelism": par, "l2": L2_NOTE}
 
 

@@ -131,7 +131,8 @@ class _StageClock:
         for (_, a), (name, b) in zip(self.events[:-1], self.events[1:]):
             if name == "start":
                 continue
-            out[name] = out.get(name, 0.0) + a.elapsed_time(b) / steps
+            key = "other" if name == "end" else name   # after the last stage: result assembly
+            out[key] = out.get(key, 0.0) + a.elapsed_time(b) / steps
         self.events = []
         return out
 
