@@ -20,12 +20,9 @@ namespace ak {
 // Register cap of the single-cell spread (config 4, B200, tools/gpu_var.sh): 196 registers
 // under __maxnreg__(208), no spills: 1.523 ms; cap 224 (212 used): 1.541; 192: 1.557;
 // 240 (__launch_bounds__(32, 8)): 1.569.  A single weight set in registers (no
-// double buffering, AK_SPREAD3C_SINGLE) allows 168 registers but loses: 1.594 ms.
+// double buffering) allows 168 registers but loses: 1.594 ms.
 #ifndef AK_SPREAD3C_BOUNDS
 #define AK_SPREAD3C_BOUNDS __maxnreg__(208)
-#endif
-#ifndef AK_SPREAD3C_SINGLE
-#define AK_SPREAD3C_SINGLE 0
 #endif
 template <int B>
 struct alignas(128) Spread3cSmem {
@@ -117,16 +114,6 @@ __device__ __forceinline__ void spread3c_unit(Spread3cSmem<B>& sm, int unit, con
 #pragma unroll
             for (int c = 0; c < P2; ++c) w2[c] = row[2 * T + g2 * P2 + c];
         };
-#if AK_SPREAD3C_SINGLE
-        // one weight set in registers (fewer registers, more resident warps hide the loads)
-        (void)b0; (void)b1; (void)b2; (void)bv;
-#pragma unroll 1
-        for (int j = 0; j < nb; ++j) {
-            load(a0, a1, a2, &wbuf[s][j][0]);
-            av = vb[s][j];
-            spread_fma_v(acc, a0, a1, a2, av);
-        }
-#else
         load(a0, a1, a2, &wbuf[s][0][0]);
         av = vb[s][0];
         int j = 0;
@@ -140,7 +127,6 @@ __device__ __forceinline__ void spread3c_unit(Spread3cSmem<B>& sm, int unit, con
             spread_fma_v(acc, b0, b1, b2, bv);
         }
         if (j < nb) spread_fma_v(acc, a0, a1, a2, av);
-#endif
         __syncwarp();
     }
 
