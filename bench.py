@@ -671,6 +671,9 @@ def run_ours(args):
             result["fp64_probe"] = {"dfma_tflops": fp64, "dmma_tflops": dmma}
             if plan is not None and 3 in plan.nufft_plans:
                 result["roofline"] = kernel_roofline(torch, plan, wl, peaks)
+            if world == 1:
+                # per-kernel device times of a step (every rank would have to join the
+                # collectives of a sharded step: single GPU only)
                 with _native.KernelTimer() as kt:
                     for _ in range(3):
                         step_dev()
