@@ -1563,6 +1563,13 @@ extern "C" int ak_op_apply(ak_op* op, const double* V, int64_t ldv, const double
                            void* stream)
 {
     const int rc = op_apply(op, V, ldv, H, scale, outs, ldo, sum_windows, flags, stream);
+#ifdef AK_CHECKED
+    // (no device synchronisation while the caller captures a CUDA graph: the guard
+    // bands are verified at the next uncaptured entry point)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing((cudaStream_t)stream, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
+        return rc;
+#endif
     return rc == AK_OK ? guards_verify("ak_op_apply") : rc;
 }
 
