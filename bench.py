@@ -403,6 +403,8 @@ def cpu_baseline(wl, gpu_window0):
     plan_s, mv_s, out = ref
     err = float(np.linalg.norm(gpu_window0 - out) / np.linalg.norm(out))
     return ({"value": 1.0 / (P * mv_s), "unit": "matvecs/s", "cores": 1, "kind": "reference",
+             "host_cpu_count": os.cpu_count(), "host_affinity": len(os.sched_getaffinity(0)),
+             "reference_build_plan_s": plan_s,
              "sample": f"the reference's own fastsum.fast_matvec (baseline/_ref, numba, serial) on window 1 of {P} "
                        f"at full N={wl.data.n_rows}: {mv_s:.2f} s per window product (build_plan {plan_s:.2f} s, "
                        f"excluded), scaled x{P}",
