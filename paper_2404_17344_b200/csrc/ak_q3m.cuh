@@ -82,52 +82,75 @@ __device__ __forceinline__ void fragment_offsets(int (&off)[18], int lane) {
     }
 }
 
-// interp_group_mma with the B fragments read from the shared region tile inside the
-// DMMA loop (cell origin `cb`), instead of 54 registers per lane loaded per cell.
-template <int R, int RW>
-__device__ __forceinline__ double interp_group_mma_s(const double* cb, const int (&off)[18],
-                                                     const double (*wrow)[RW], int k0, int cnt, int lane)
+// G consecutive 8-point groups of one cell run (rows k0 + 8 g + pj, cnt[g] valid rows
+// each) against the same footprint: the B fragments are read from the region tile
+// once per run segment instead of once per group.  The 18 column tiles run in three
+// chunks of six (12 pairs = 4 values of a x 3 of b, lane quad q owning b = 3q .. 3q+2
+// as above): per chunk each group's 6 accumulator tiles are contracted over a right
+// away, so a lane holds 18 fragments + 12 accumulators instead of 36 accumulators.
+// Same operations, in the same order, as interp_group_mma (bit-identical results).
+template <int R, int RW, int G>
+__device__ __forceinline__ void interp_groups_mma_s(const double* cb, const int (&off)[18], const double (*wrow)[RW],
+                                                    int k0, const int (&cnt)[G], int lane, double (&v)[G])
 {
     const int pj = lane >> 2, q = lane & 3;
-    const bool valid = pj < cnt;
-    const double* w = wrow[k0 + (valid ? pj : 0)];
-    double af[3];
+    const double* w[G];
+    double af[G][3], s[G][3];
 #pragma unroll
-    for (int ks = 0; ks < 3; ++ks) af[ks] = valid ? w[24 + 4 * ks + q] : 0.0;
-    double C[18][2];
+    for (int g = 0; g < G; ++g) {
+        const bool valid = pj < cnt[g];
+        w[g] = wrow[k0 + 8 * g + (valid ? pj : 0)];
 #pragma unroll
-    for (int t = 0; t < 18; ++t) C[t][0] = C[t][1] = 0.0;
+        for (int ks = 0; ks < 3; ++ks) af[g][ks] = valid ? w[g][24 + 4 * ks + q] : 0.0;
+    }
 #pragma unroll
-    for (int ks = 0; ks < 3; ++ks)
+    for (int ch = 0; ch < 3; ++ch) {
+        double B[6][3];
 #pragma unroll
-        for (int t = 0; t < 18; ++t) dmma_8x8x4(C[t][0], C[t][1], af[ks], cb[off[t] + 4 * ks]);
-    double s[3];
+        for (int tt = 0; tt < 6; ++tt)
 #pragma unroll
-    for (int bb = 0; bb < 3; ++bb) s[bb] = w[0] * C[bb >> 1][bb & 1];
+            for (int ks = 0; ks < 3; ++ks) B[tt][ks] = cb[off[6 * ch + tt] + 4 * ks];
 #pragma unroll
-    for (int a = 1; a < 12; ++a) {
-        const double w0a = w[a];
+        for (int g = 0; g < G; ++g) {
+            double C[6][2];
 #pragma unroll
-        for (int bb = 0; bb < 3; ++bb) {
-            const int i = 3 * a + bb;
-            s[bb] = fma(w0a, C[i >> 1][i & 1], s[bb]);
+            for (int tt = 0; tt < 6; ++tt) C[tt][0] = C[tt][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 3; ++ks)
+#pragma unroll
+                for (int tt = 0; tt < 6; ++tt) dmma_8x8x4(C[tt][0], C[tt][1], af[g][ks], B[tt][ks]);
+            // pair j of the chunk: a = 4 ch + j / 3, b = 3 q + j % 3
+#pragma unroll
+            for (int j = 0; j < 12; ++j) {
+                const double c = C[j >> 1][j & 1];
+                const double w0a = w[g][4 * ch + j / 3];
+                if (ch == 0 && j < 3) s[g][j % 3] = w0a * c;
+                else s[g][j % 3] = fma(w0a, c, s[g][j % 3]);
+            }
         }
     }
-    const double* w1 = w + 12 + 3 * q;
-    const double v = fma(w1[2], s[2], fma(w1[1], s[1], w1[0] * s[0]));
-    return valid ? v : 0.0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const double* w1 = w[g] + 12 + 3 * q;
+        const double r = fma(w1[2], s[g][2], fma(w1[1], s[g][1], w1[0] * s[g][0]));
+        v[g] = pj < cnt[g] ? r : 0.0;
+    }
 }
 
 // Multi-cell (supercell) work items: the item's (S+11)^3 grid region is staged in
-// shared memory once, and every 8-point group of a cell run reads its B fragments
+// shared memory once, and the 8-point groups of a cell run read their B fragments
 // from it inside the DMMA loop (no per-cell register copy of the footprint).
-// NW warps share the region tile (read only); warp w takes the item's batches
-// w, w + NW, ... with its own double-buffered weight rows and barriers (the tile is
-// 17.6 KB at S = 2: one warp per CTA leaves shared memory, not registers, as the
-// occupancy limit).
+// NW (1 or 2) warps share the region tile (read only); each takes a contiguous part
+// of the item (split at a cell boundary) and walks it in batches of at most B points
+// with its own double-buffered weight rows and barriers (the tile is 17.6 KB at
+// S = 2: one warp per CTA leaves shared memory, not registers, as the occupancy
+// limit).  Batches end at their last cell-run start when more points follow, so a
+// run is never cut by a batch boundary except after 16 of its points: a run of L
+// points takes ceil(L / 8) groups.  (Fixed 16-point batches cut ~40% of the runs;
+// at ~12 points per cell the groups were 67% full instead of 78%.)
 template <int S, int B, int NW>
 #ifndef AK_INTERP3M_MINW
-#define AK_INTERP3M_MINW 12   // warps per SM the register allocation must allow
+#define AK_INTERP3M_MINW 10   // warps per SM the register allocation must allow
 #endif
 __global__ void __launch_bounds__(32 * NW, AK_INTERP3M_MINW / NW)
 k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
@@ -139,7 +162,9 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     constexpr int RW = 3 * T;
     constexpr int R = S + T - 1;
     constexpr int TILE = R * R * R;
-    static_assert(B % 8 == 0 && B <= 32, "batch: multiple of 8, at most 32");
+    static_assert(B % 16 == 0 && B <= 32, "batch: multiple of 16, at most 32");
+    static_assert(NW == 1 || NW == 2, "one or two warps per item");
+    constexpr unsigned FULL = 0xffffffffu;
 
     __shared__ double tile[TILE];
     __shared__ __align__(128) double wbuf_all[NW][2][B][RW];
@@ -158,9 +183,20 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     int* cst = cst_all[warp];
     uint64_t* bar = bar_all[warp];
     const int sc0 = it.sc & 1023, sc1 = (it.sc >> 10) & 1023, sc2 = (it.sc >> 20) & 1023;
-    const int nbatch = (it.count + B - 1) / B;
     const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
     const CellIdx* __restrict__ CIit = ci + (it.start - wshift[it.window]);
+
+    // this warp's points [off, wend): two warps split the item at the first cell-run
+    // start at or after its middle (within 32 points; else at the middle)
+    int off = 0, wend = it.count;
+    if (NW == 2) {
+        const int mid = it.count / 2, j = mid + lane;
+        const bool bd = j > 0 && j < it.count && CIit[j].cell != CIit[j - 1].cell;
+        const unsigned m = __ballot_sync(FULL, bd);
+        const int split = m ? mid + __ffs(m) - 1 : mid;
+        off = warp ? split : 0;
+        wend = warp ? it.count : split;
+    }
 
     if (lane == 0) {
         mbar_init(&bar[0], 1);
@@ -168,10 +204,10 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         mbar_fence_init();
     }
     __syncwarp();
-    if (warp < nbatch) {
-        const int cnt = min(B, it.count - warp * B);
-        if (lane == 0) tma_load_1d(&wbuf[0][0][0], Wit + (int64_t)warp * B * RW, (unsigned)(cnt * RW * 8), &bar[0]);
-        if (lane < cnt) cp_async8(&cib[0][lane], CIit + warp * B + lane);
+    if (off < wend) {
+        const int cnt = min(B, wend - off);
+        if (lane == 0) tma_load_1d(&wbuf[0][0][0], Wit + (int64_t)off * RW, (unsigned)(cnt * RW * 8), &bar[0]);
+        if (lane < cnt) cp_async8(&cib[0][lane], CIit + off + lane);
     }
     {
         const double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
@@ -192,24 +228,14 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     fragment_offsets<R>(foff, lane);
     const double* cb = tile;
     int cur = -1;
+    const int pj = lane >> 2;
 
-    for (int bi = warp, u = 0; bi < nbatch; bi += NW, ++u) {
+    for (int u = 0; off < wend; ++u) {
         const int s = u & 1;
-        const int off = bi * B;
-        const int nb = min(B, it.count - off);
+        const int nb = min(B, wend - off);
         cp_async_wait_all();
         mbar_wait(&bar[s], (u >> 1) & 1);
         __syncwarp();
-        if (bi + NW < nbatch) {
-            const int nb1 = min(B, it.count - off - NW * B);
-            if (lane == 0) {
-                fence_proxy_async();
-                tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + NW * B) * RW, (unsigned)(nb1 * RW * 8),
-                            &bar[s ^ 1]);
-            }
-            if (lane < nb1) cp_async8(&cib[s ^ 1][lane], CIit + off + NW * B + lane);
-        }
-        cp_async_commit();
         if (lane < nb) {
             const int c = cib[s][lane].cell;
             AK_DCHECK(cell_axis(c, 0) - sc0 * S >= 0 && cell_axis(c, 0) - sc0 * S < S &&
@@ -220,29 +246,57 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         }
         __syncwarp();
         const int mycell = lane < nb ? cst[lane] : -2;
-        const int prev = __shfl_up_sync(0xffffffffu, mycell, 1);
-        const unsigned chg = __ballot_sync(0xffffffffu, lane < nb && (lane == 0 ? mycell != cur : mycell != prev));
-        for (int k = 0; k < nb;) {
+        const int prev = __shfl_up_sync(FULL, mycell, 1);
+        // run starts inside the batch; the batch's last (possibly unfinished) run moves
+        // to the next batch when more points follow
+        const unsigned inner = __ballot_sync(FULL, lane > 0 && lane < nb && mycell != prev);
+        const int take = (off + nb < wend && inner) ? 31 - __clz(inner) : nb;
+        const int next = off + take;
+        if (next < wend) {
+            const int nb1 = min(B, wend - next);
+            if (lane == 0) {
+                fence_proxy_async();
+                tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)next * RW, (unsigned)(nb1 * RW * 8), &bar[s ^ 1]);
+            }
+            if (lane < nb1) cp_async8(&cib[s ^ 1][lane], CIit + next + lane);
+        }
+        cp_async_commit();
+        const unsigned chg = __ballot_sync(FULL, lane < take && (lane == 0 ? mycell != cur : mycell != prev));
+        for (int k = 0; k < take;) {
             if ((chg >> k) & 1u) {
                 cur = cst[k];
                 cb = tile + ((cur & 255) * R + ((cur >> 8) & 255)) * R + ((cur >> 16) & 255);
             }
             const unsigned later = k < 31 ? chg & ~((2u << k) - 1u) : 0u;
-            const int kend = later ? min(__ffs(later) - 1, nb) : nb;
-            for (int k0 = k; k0 < kend; k0 += 8) {
-                const int cnt = min(8, kend - k0);
-                double v = interp_group_mma_s<R, RW>(cb, foff, wbuf[s], k0, cnt, lane);
-                v += __shfl_xor_sync(0xffffffffu, v, 1);
-                v += __shfl_xor_sync(0xffffffffu, v, 2);
-                const int pj = lane >> 2;
-                if ((lane & 3) == 0 && pj < cnt) {
-                    double* dst = o + (int64_t)cib[s][k0 + pj].idx * os.is;
-                    if (atomic_out) red_add(dst, sc * v);
-                    else *dst = sc * v;
+            const int kend = later ? min(__ffs(later) - 1, take) : take;
+            // two groups per pass while the run has more than 8 points left
+            for (int k0 = k; k0 < kend; k0 += 16) {
+                const int c0 = min(8, kend - k0), c1 = min(8, kend - k0 - 8);
+                auto emit = [&](int g, int cnt, double v) {
+                    v += __shfl_xor_sync(FULL, v, 1);
+                    v += __shfl_xor_sync(FULL, v, 2);
+                    if ((lane & 3) == 0 && pj < cnt) {
+                        double* dst = o + (int64_t)cib[s][k0 + 8 * g + pj].idx * os.is;
+                        if (atomic_out) red_add(dst, sc * v);
+                        else *dst = sc * v;
+                    }
+                };
+                if (c1 > 0) {
+                    const int cnt[2] = {c0, c1};
+                    double v[2];
+                    interp_groups_mma_s<R, RW, 2>(cb, foff, wbuf[s], k0, cnt, lane, v);
+                    emit(0, c0, v[0]);
+                    emit(1, c1, v[1]);
+                } else {
+                    const int cnt[1] = {c0};
+                    double v[1];
+                    interp_groups_mma_s<R, RW, 1>(cb, foff, wbuf[s], k0, cnt, lane, v);
+                    emit(0, c0, v[0]);
                 }
             }
             k = kend;
         }
+        off = next;
     }
 }
 
