@@ -122,8 +122,17 @@ __device__ __forceinline__ void region_axes(int (*widx)[R], int o0, int o1, int 
 // a multi-warp CTA take interleaved planes.  f(tile index, grid index).
 // Measured on sparse data (config 3, ~15 points per cell): the element-wise loop
 // with three constant divisions per element was a quarter of the spread time.
-template <int R, typename F>
-__device__ __forceinline__ void for_region_rows(const int (*widx)[R], int n, int tid, int nthreads, F&& f) {
+// Region tile layouts: element (i0, i1, i2) at i0 * S0 + i1 * S1 + i2 * S2.
+template <int S0, int S1, int S2, int SIZE>
+struct TileLayout {
+    static constexpr int size = SIZE;
+    __host__ __device__ static constexpr int at(int i0, int i1, int i2) { return i0 * S0 + i1 * S1 + i2 * S2; }
+};
+template <int R>
+using DenseTile = TileLayout<R * R, R, 1, R * R * R>;
+
+template <int R, typename F, typename L = DenseTile<R>>
+__device__ __forceinline__ void for_region_rows(const int (*widx)[R], int n, int tid, int nthreads, F&& f, L = L{}) {
     static_assert(R <= 32, "region row must fit a warp");
     constexpr int RPP = 32 / R;                 // rows per warp pass
     constexpr int RPL = (R + RPP - 1) / RPP;    // rows per lane per plane
@@ -143,10 +152,31 @@ __device__ __forceinline__ void for_region_rows(const int (*widx)[R], int n, int
         for (int t = 0; t < RPL; ++t) {
             const int i1 = sub + RPP * t;
             AK_DCHECK(i1 >= R || (pl + rowoff[t] >= 0 && pl + rowoff[t] < (int64_t)n * n * n));
-            if (i1 < R) f((i0 * R + i1) * R + k, pl + rowoff[t]);
+            if (i1 < R) f(L::at(i0, i1, k), pl + rowoff[t]);
         }
     }
 }
+
+// Shared region tile of the sparse spread.  A cell-run flush adds the lane tiles
+// (6 x 3 x 3 per lane: lane (g0, g1, g2) at axis offsets 6 g0, 3 g1, 3 g2) into the
+// region with one 8-byte load + store per element; a half-warp's 16 addresses must
+// fall on 16 different bank pairs.  In the dense 13^3 layout every flush access is
+// 2-way conflicted (3 g1 * 13 + 3 g2 collides mod 16); with axis 2 innermost, axis 0
+// at stride 13 and axis 1 at stride 172 (2236 elements, +2%) all 54 are conflict-free
+// (exhaustive search over axis orders and paddings: tools/bank_search.py).  Config 3
+// (B200): spread 0.862 -> 0.746 ms per launch.
+#ifndef AK_SPREAD3W_PAD
+#define AK_SPREAD3W_PAD 1
+#endif
+template <int R>
+struct Spread3wTile {
+#if AK_SPREAD3W_PAD
+    static_assert(R <= 13, "padded layout holds regions up to 13^3");
+    using L = TileLayout<13, 172, 1, 13 * 172>;
+#else
+    using L = DenseTile<R>;
+#endif
+};
 
 // points per staged weight batch of the sparse (supercell) 3-D kernels
 #ifndef AK_SPARSE_BATCH
@@ -165,7 +195,8 @@ k_spread3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     constexpr int P0 = LN::P0, P1 = LN::P1, P2 = LN::P2;
     constexpr int RW = 3 * T;
     constexpr int R = S + T - 1;
-    constexpr int TILE = R * R * R;
+    using TL = typename Spread3wTile<R>::L;
+    constexpr int TILE = TL::size;
     static_assert(B <= 32, "batch must fit the change mask");
 
     __shared__ double tile[TILE];
@@ -221,7 +252,7 @@ k_spread3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
             for (int b = 0; b < P1; ++b)
 #pragma unroll
                 for (int c = 0; c < P2; ++c) {
-                    double* t = &tile[((l0 + g0 * P0 + a) * R + (l1 + g1 * P1 + b)) * R + (l2 + g2 * P2 + c)];
+                    double* t = &tile[TL::at(l0 + g0 * P0 + a, l1 + g1 * P1 + b, l2 + g2 * P2 + c)];
                     *t += acc[a][b][c];
                     acc[a][b][c] = 0.0;
                 }
@@ -305,10 +336,13 @@ k_spread3w(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     double* __restrict__ g = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
     region_axes<R>(widx, sc0 * S - (T / 2 - 1), sc1 * S - (T / 2 - 1), sc2 * S - (T / 2 - 1), n, lane, 32);
     __syncwarp();
-    for_region_rows<R>(widx, n, lane, 32, [&](int i, int64_t gi) {
-        const double val = tile[i];
-        if (val != 0.0) red_add(g + gi, val);
-    });
+    for_region_rows<R>(
+        widx, n, lane, 32,
+        [&](int i, int64_t gi) {
+            const double val = tile[i];
+            if (val != 0.0) red_add(g + gi, val);
+        },
+        TL{});
     (void)end;
 }
 
