@@ -161,6 +161,11 @@ int64_t ak_geom_grid_elems(const ak_geom* g, int32_t w);
  * ak_geom_canon_total(g) = sum_w n^q[w]  (total doubles for R = 1). */
 int64_t ak_geom_canon_offset(const ak_geom* g, int32_t w);
 int64_t ak_geom_canon_total(const ak_geom* g);
+/* Occupied box of 3-D window w (diagnostics; no reference counterpart): box[2a] = lo,
+ * box[2a+1] = L per axis a -- the cyclic grid-index range [lo, lo + L) mod n that holds
+ * every footprint of the window's points (L a multiple of 16, or n).  The fused 3-D
+ * transforms of ak_op_apply work on this box only.  Other windows: lo = 0, L = n. */
+int ak_geom_box(const ak_geom* g, int32_t w, int32_t* box6);
 
 /*
  * ak_spread -- real-valued spreading of R right-hand sides onto per-window grids

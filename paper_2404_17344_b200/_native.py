@@ -45,7 +45,7 @@ EXPORTED = (
     "ak_spread", "ak_interp", "ak_op_create", "ak_op_destroy", "ak_op_apply", "ak_op_grids", "ak_op_band",
     "ak_type1_band", "ak_type2_grid", "ak_dense_apply", "ak_probe_fp64", "ak_probe_dmma",
     "ak_tuning_default", "ak_geom_create_ex", "ak_geom_describe", "ak_prof_enable", "ak_prof_reset",
-    "ak_prof_report",
+    "ak_prof_report", "ak_geom_box",
 )
 
 FAMILY_CODE = {"gauss": 0, "der_gauss": 1, "matern12": 2, "der_matern12": 3}
@@ -122,6 +122,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "ak_geom_grid_elems": (_i64, [_vp, _i32]),
         "ak_geom_canon_offset": (_i64, [_vp, _i32]),
         "ak_geom_canon_total": (_i64, [_vp]),
+        "ak_geom_box": (_c_int, [_vp, _i32, ctypes.POINTER(_i32)]),
         "ak_spread": (_c_int, [_vp, _dp, _i32, _i64, _dp, _vp]),
         "ak_interp": (_c_int, [_vp, _dp, _i32, _dp, _dp, _i64, _i32, _i64, _vp]),
         "ak_op_create": (_c_int, [_vp, _vp, _i32, _i32, _i32, _vp, ctypes.POINTER(_vp)]),

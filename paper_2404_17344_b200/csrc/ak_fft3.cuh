@@ -19,7 +19,10 @@
 // Frequencies: band index b in [0, m) is k = b (b < m/2) or b - m; w = 2 pi / n.
 // Along the real axis k2 runs over [0, m/2) with c_0 = 1, c_k2 = 2 otherwise, which is
 // cuFFT's Z2D on the Hermitian-consistent band (H even, forward input real).
-// Every stage is a 131K-MAC GEMM per plane/slab at n = 64, m = 32 (512 DMMA).
+// Every stage is a 131K-MAC GEMM per plane/slab at n = 64, m = 32 (512 DMMA) over the
+// whole grid; the kernels work on each window's occupied box (GridBox below), so the
+// x sums / outputs shrink to the box: config 3 transforms 0.264 -> 0.121 ms per step,
+// config 4 2.874 -> 2.844 ms per product (B200).
 #pragma once
 #include "ak_common.cuh"
 
@@ -175,11 +178,38 @@ struct Fft3Tables {
     const double *T1, *T3, *FW, *IW;
 };
 
-// real GEMM operand from a row-major global table (L1/L2-resident, shared by all CTAs)
-struct TabA {
-    const double* __restrict__ t;
-    int ld;
-    __device__ __forceinline__ double operator()(int r, int k) const { return __ldg(t + r * ld + k); }
+// Occupied box of grid b (ak_geom::box of its window; nullptr: the whole grid).  Box
+// index i of axis a is grid index x(a, i) = lo_a + i (mod n); L_a is a multiple of 16.
+// Outside the box a spread grid is zero and an interpolation never reads, so the
+// forward stages contract only over box indices and the inverse stages produce only
+// box outputs: at config-3/4 data (points in a 30^3 corner of the 64^3 grid, L = 32)
+// fwd12 / inv12 do 1/8 and fwd0 / inv0 1/2 of the full-grid work.
+template <int n>
+struct GridBox {
+    int lo[3], L[3];
+    __device__ __forceinline__ GridBox(const int* __restrict__ box, const int* __restrict__ gwin, int64_t b, int R) {
+        if (box) {
+            const int* bx = box + 6 * gwin[b / R];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = __ldg(bx + 2 * a);
+                L[a] = __ldg(bx + 2 * a + 1);
+            }
+        } else {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = 0;
+                L[a] = n;
+            }
+        }
+    }
+    __device__ __forceinline__ int x(int a, int i) const {
+        const int v = lo[a] + i;
+        return v >= n ? v - n : v;
+    }
+    // column of a [..][2n] table / row of a [2n][..] table for split-complex box index
+    // k in [0, 2 L_a): real part at x, imaginary part at n + x
+    __device__ __forceinline__ int x2(int a, int k) const { return k < L[a] ? x(a, k) : n + x(a, k - L[a]); }
 };
 
 // plane copy global -> shared with 16-byte loads (cols even, ld even)
@@ -192,81 +222,113 @@ __device__ __forceinline__ void fft3_copy2(double* dst, int ld, const double* __
     }
 }
 
-// fbuf (per grid, per plane x0): split complex [2][m][mh] doubles
-// fwd12: grids [nb][n][n][n] real -> fbuf [nb][n(x0)][2][m(b1)][mh]
+// box plane copy global -> shared: P[i1][j2] = src[x1(i1)][x2(j2)] (16-byte loads when
+// the axis-2 range is contiguous and even-aligned)
+template <int n>
+__device__ __forceinline__ void fft3_copy_box(double* dst, int ld, const double* __restrict__ src, const GridBox<n>& bx) {
+    const int L1 = bx.L[1], L2 = bx.L[2], lo2 = bx.lo[2];
+    if (lo2 + L2 <= n && (lo2 & 1) == 0) {
+        const int c2 = L2 / 2;
+        for (int e = threadIdx.x; e < L1 * c2; e += blockDim.x) {
+            const int r = e / c2, c = e - r * c2;
+            *reinterpret_cast<double2*>(dst + r * ld + 2 * c) =
+                __ldg(reinterpret_cast<const double2*>(src + bx.x(1, r) * n + lo2) + c);
+        }
+    } else {
+        for (int e = threadIdx.x; e < L1 * L2; e += blockDim.x) {
+            const int r = e / L2, c = e - r * L2;
+            dst[r * ld + c] = __ldg(src + bx.x(1, r) * n + bx.x(2, c));
+        }
+    }
+}
+
+// fbuf (per grid, per box plane i0 of axis 0): split complex [2][m][mh] doubles
+// fwd12: grids [nb][n][n][n] real -> fbuf [nb][L0 (i0)][2][m(b1)][mh]
 template <int n, int m>
 __global__ void __launch_bounds__(FFT3_THREADS, AK_FFT3_MINB)
-k_fft3_fwd12(const double* __restrict__ grids, double* __restrict__ fbuf, Fft3Tables tb)
+k_fft3_fwd12(const double* __restrict__ grids, double* __restrict__ fbuf, Fft3Tables tb,
+             const int* __restrict__ box, const int* __restrict__ gwin, int R)
 {
     extern __shared__ __align__(16) double sm[];
-    const int mh = m / 2, x0 = blockIdx.x;
+    const int mh = m / 2, i0 = blockIdx.x;
     const int64_t b = blockIdx.y;
+    const GridBox<n> bx(box, gwin, b, R);
+    if (i0 >= bx.L[0]) return;
+    const int L1 = bx.L[1], L2 = bx.L[2];
     const int ldP = fft3_ldA(n), ldX = fft3_ldB(mh);
-    double* P = sm;                       // [n][ldP]     (S1 A)
+    double* P = sm;                       // [L1][ldP]     (S1 A)
 #if AK_FFT3_ALIAS
-    double* X = sm;                       // [2n][ldX]    (S1 out over P, S2 B)
+    double* X = sm;                       // [2 L1][ldX]   (S1 out over P, S2 B)
 #else
     double* X = P + n * ldP;
 #endif
-    fft3_copy2(P, ldP, grids + (b * n + x0) * n * n, n, n);
+    fft3_copy_box<n>(P, ldP, grids + (b * n + bx.x(0, i0)) * n * n, bx);
     __syncthreads();
     const double* __restrict__ T1 = tb.T1;
+    auto s1a = [&](int r, int k) { return P[r * ldP + k]; };
+    auto s1b = [&](int k, int c) { return __ldg(T1 + bx.x(2, k) * m + c); };
+    auto s1s = [&](int r, int c, double v) { X[((c & 1) * L1 + r) * ldX + (c >> 1)] = v; };
 #if AK_FFT3_ALIAS
     constexpr int NW = FFT3_THREADS / 32, NBLK = (n / 16) * (m / 16);
     constexpr int NB = (NBLK + NW - 1) / NW;   // S1 blocks per warp (2 x 2 tiles each)
     static_assert(n % 16 == 0 && m % 16 == 0, "S1 tiling");
-    cta_gemm_hold<NB>(
-        n, m, n, [&](int r, int k) { return P[r * ldP + k]; }, [&](int k, int c) { return __ldg(T1 + k * m + c); },
-        [&](int r, int c, double v) { X[((c & 1) * n + r) * ldX + (c >> 1)] = v; });
+    cta_gemm_hold<NB>(L1, m, L2, s1a, s1b, s1s);
 #else
-    cta_gemm_auto(
-        n, m, n, [&](int r, int k) { return P[r * ldP + k]; }, [&](int k, int c) { return __ldg(T1 + k * m + c); },
-        [&](int r, int c, double v) { X[((c & 1) * n + r) * ldX + (c >> 1)] = v; });
+    cta_gemm_auto(L1, m, L2, s1a, s1b, s1s);
 #endif
     __syncthreads();
-    double* __restrict__ dst = fbuf + (b * n + x0) * 2 * m * mh;
+    double* __restrict__ dst = fbuf + (b * n + i0) * 2 * m * mh;
+    const double* __restrict__ FW = tb.FW;
     cta_gemm_auto(
-        2 * m, mh, 2 * n, TabA{tb.FW, 2 * n}, [&](int k, int c) { return X[k * ldX + c]; },
-        [&](int r, int c, double v) { dst[r * mh + c] = v; });
+        2 * m, mh, 2 * L1, [&](int r, int k) { return __ldg(FW + r * 2 * n + bx.x2(1, k)); },
+        [&](int k, int c) { return X[k * ldX + c]; }, [&](int r, int c, double v) { dst[r * mh + c] = v; });
 }
 
-// fwd0: fbuf [nb][n(x0)][2][m(b1)][mh] -> band [nb][m(b0)][m(b1)][mh] complex
+// fwd0: fbuf [nb][L0 (i0)][2][m(b1)][mh] -> band [nb][m(b0)][m(b1)][mh] complex
 template <int n, int m>
 __global__ void __launch_bounds__(FFT3_THREADS, AK_FFT3_MINB)
-k_fft3_fwd0(const double* __restrict__ fbuf, double* __restrict__ band, Fft3Tables tb)
+k_fft3_fwd0(const double* __restrict__ fbuf, double* __restrict__ band, Fft3Tables tb,
+            const int* __restrict__ box, const int* __restrict__ gwin, int R)
 {
     extern __shared__ __align__(16) double sm[];
     const int mh = m / 2, b1 = blockIdx.x;
     const int64_t b = blockIdx.y;
+    const GridBox<n> bx(box, gwin, b, R);
+    const int L0 = bx.L[0];
     const int ldX = fft3_ldB(mh);
-    double* X = sm;                       // [2n (re x0 | im x0)][ldX]
+    double* X = sm;                       // [2 L0 (re i0 | im i0)][ldX]
     const int h2 = mh / 2;
-    for (int e = threadIdx.x; e < 2 * n * h2; e += blockDim.x) {
-        const int row = e / h2, c = e - row * h2;     // row = ri * n + x0
-        const int ri = row / n, x0 = row - ri * n;
+    for (int e = threadIdx.x; e < 2 * L0 * h2; e += blockDim.x) {
+        const int row = e / h2, c = e - row * h2;     // row = ri * L0 + i0
+        const int ri = row >= L0, i0 = row - ri * L0;
         *reinterpret_cast<double2*>(X + row * ldX + 2 * c) =
-            __ldg(reinterpret_cast<const double2*>(fbuf + (((b * n + x0) * 2 + ri) * m + b1) * mh) + c);
+            __ldg(reinterpret_cast<const double2*>(fbuf + (((b * n + i0) * 2 + ri) * m + b1) * mh) + c);
     }
     __syncthreads();
     double* __restrict__ dst = band + b * 2 * (int64_t)m * m * mh;
+    const double* __restrict__ FW = tb.FW;
     cta_gemm_auto(
-        2 * m, mh, 2 * n, TabA{tb.FW, 2 * n}, [&](int k, int c) { return X[k * ldX + c]; },
+        2 * m, mh, 2 * L0, [&](int r, int k) { return __ldg(FW + r * 2 * n + bx.x2(0, k)); },
+        [&](int k, int c) { return X[k * ldX + c]; },
         [&](int r, int c, double v) {
             const int ro = r >= m, b0 = r - ro * m;
             dst[2 * (((int64_t)b0 * m + b1) * mh + c) + ro] = v;
         });
 }
 
-// inv0: H * band -> fbuf [nb][n(x0)][2][m(b1)][mh]; the multiplier of grid b is
+// inv0: H * band -> fbuf [nb][L0 (i0)][2][m(b1)][mh]; the multiplier of grid b is
 // H[hsel][(b0 m + b1) mh + k2] with hsel as in k_band_multiply
 template <int n, int m>
 __global__ void __launch_bounds__(FFT3_THREADS, AK_FFT3_MINB)
 k_fft3_inv0(const double* __restrict__ band, double* __restrict__ fbuf, Fft3Tables tb, int R,
-            const int* __restrict__ gwin, const double* const* __restrict__ H, int hbase, int P, int per_rhs)
+            const int* __restrict__ gwin, const double* const* __restrict__ H, int hbase, int P, int per_rhs,
+            const int* __restrict__ box)
 {
     extern __shared__ __align__(16) double sm[];
     const int mh = m / 2, b1 = blockIdx.x;
     const int64_t b = blockIdx.y;
+    const GridBox<n> bx(box, gwin, b, R);
+    const int L0 = bx.L[0];
     const int ldY = fft3_ldB(mh);
     double* Y = sm;                       // [2m (re b0 | im b0)][ldY]
     const int w = gwin[b / R];
@@ -281,40 +343,49 @@ k_fft3_inv0(const double* __restrict__ band, double* __restrict__ fbuf, Fft3Tabl
         Y[(m + b0) * ldY + k2] = hv * v.y;
     }
     __syncthreads();
+    const double* __restrict__ IW = tb.IW;
     cta_gemm_auto(
-        2 * n, mh, 2 * m, TabA{tb.IW, 2 * m}, [&](int k, int c) { return Y[k * ldY + c]; },
+        2 * L0, mh, 2 * m, [&](int r, int k) { return __ldg(IW + bx.x2(0, r) * 2 * m + k); },
+        [&](int k, int c) { return Y[k * ldY + c]; },
         [&](int r, int c, double v) {
-            const int ro = r >= n, x0 = r - ro * n;
-            fbuf[(((b * n + x0) * 2 + ro) * m + b1) * mh + c] = v;
+            const int ro = r >= L0, i0 = r - ro * L0;
+            fbuf[(((b * n + i0) * 2 + ro) * m + b1) * mh + c] = v;
         });
 }
 
-// inv12: fbuf [nb][n(x0)][2][m][mh] -> grids [nb][n][n][n] real (one block per (x0, grid))
+// inv12: fbuf [nb][L0 (i0)][2][m][mh] -> the box of grids [nb][n][n][n] real (one block
+// per (i0, grid)); grid values outside the box are not written
 template <int n, int m>
 __global__ void __launch_bounds__(FFT3_THREADS, AK_FFT3_MINB)
-k_fft3_inv12(const double* __restrict__ fbuf, double* __restrict__ out, Fft3Tables tb)
+k_fft3_inv12(const double* __restrict__ fbuf, double* __restrict__ out, Fft3Tables tb,
+             const int* __restrict__ box, const int* __restrict__ gwin, int R)
 {
     extern __shared__ __align__(16) double sm[];
-    const int mh = m / 2, x0 = blockIdx.x;
+    const int mh = m / 2, i0 = blockIdx.x;
     const int64_t b = blockIdx.y;
+    const GridBox<n> bx(box, gwin, b, R);
+    if (i0 >= bx.L[0]) return;
+    const int L1 = bx.L[1], L2 = bx.L[2];
     const int ldC = fft3_ldB(mh), ldD = fft3_ldA(mh);
     double* C = sm;                       // [2m][ldC]  (I1 B)
-    double* D = C + 2 * m * ldC;          // [2n][ldD]  (I1 out, I2 A)
-    fft3_copy2(C, ldC, fbuf + (b * n + x0) * 2 * m * mh, 2 * m, mh);
+    double* D = C + 2 * m * ldC;          // [2 L1][ldD]  (I1 out, I2 A)
+    fft3_copy2(C, ldC, fbuf + (b * n + i0) * 2 * m * mh, 2 * m, mh);
     __syncthreads();
+    const double* __restrict__ IW = tb.IW;
     cta_gemm_auto(
-        2 * n, mh, 2 * m, TabA{tb.IW, 2 * m}, [&](int k, int c) { return C[k * ldC + c]; },
-        [&](int r, int c, double v) { D[r * ldD + c] = v; });
+        2 * L1, mh, 2 * m, [&](int r, int k) { return __ldg(IW + bx.x2(1, r) * 2 * m + k); },
+        [&](int k, int c) { return C[k * ldC + c]; }, [&](int r, int c, double v) { D[r * ldD + c] = v; });
     __syncthreads();
-    double* __restrict__ dst = out + (b * n + x0) * n * n;
+    double* __restrict__ dst = out + (b * n + bx.x(0, i0)) * n * n;
     const double* __restrict__ T3 = tb.T3;
     cta_gemm_auto(
-        n, n, m,
+        L1, L2, m,
         [&](int r, int k) {
             const int ri = k >= mh;
-            return D[(ri * n + r) * ldD + k - ri * mh];
+            return D[(ri * L1 + r) * ldD + k - ri * mh];
         },
-        [&](int k, int c) { return __ldg(T3 + k * n + c); }, [&](int r, int c, double v) { dst[r * n + c] = v; });
+        [&](int k, int c) { return __ldg(T3 + k * n + bx.x(2, c)); },
+        [&](int r, int c, double v) { dst[bx.x(1, r) * n + bx.x(2, c)] = v; });
 }
 
 // dynamic shared memory (bytes) of each kernel

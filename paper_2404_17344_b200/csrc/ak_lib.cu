@@ -269,6 +269,12 @@ struct ak_geom {
     double* W2 = nullptr;               // [P2][N][2T]
     CellIdx* CI2 = nullptr;             // [P2][N]
     int64_t* wshift_d = nullptr;        // per window: (w - rank_q(w)) * N, rank among windows of its q
+    // Occupied box of each 3-D window's grid: per axis the cyclic index range [lo, lo + L)
+    // (mod n) that holds every footprint of the window's points, L a multiple of 16
+    // (full axis: lo = 0, L = n).  The fused transforms skip the rest (zero on the way in,
+    // never read on the way out).  [P][lo0, L0, lo1, L1, lo2, L2].
+    std::vector<int> box;
+    int* box_d = nullptr;
 };
 
 extern "C" void ak_tuning_default(ak_tuning* t) {
@@ -457,8 +463,59 @@ extern "C" int ak_geom_destroy(ak_geom* g) {
     ak_free(g->W2);
     ak_free(g->CI2);
     ak_free(g->wshift_d);
+    ak_free(g->box_d);
     delete g;
     return AK_OK;
+}
+
+// Occupied boxes of the 3-D windows (ak_geom::box) from the spread work items: a cell c
+// of a T-tap window touches grid indices c - (T/2 - 1) .. c + T/2 (mod n); per axis the
+// box is the complement of the longest cyclic run of untouched indices, rounded up to a
+// multiple of 16 (the fused transforms' GEMM tiling).
+static void geom_boxes(ak_geom* g, const std::vector<WorkItem>& items, int64_t ib, int64_t ie) {
+    const int n = g->n, P = g->P, T = g->wf.taps, S = g->sedge[3];
+    g->box.assign((size_t)P * 6, 0);
+    std::vector<std::vector<char>> occ((size_t)P * 3, std::vector<char>(n, 0));
+    for (int64_t i = ib; i < ie; ++i) {
+        const WorkItem& it = items[(size_t)i];
+        for (int a = 0; a < 3; ++a) {
+            const int c = ((it.sc >> (10 * a)) & 1023) * S;
+            for (int k = 0; k < S && c + k < n; ++k) occ[(size_t)it.window * 3 + a][c + k] = 1;
+        }
+    }
+    for (int w = 0; w < P; ++w)
+        for (int a = 0; a < 3; ++a) {
+            int lo = 0, L = n;
+            if (g->q[w] == 3 && n % 16 == 0) {
+                std::vector<char> touched(n, 0);
+                const auto& o = occ[(size_t)w * 3 + a];
+                for (int c = 0; c < n; ++c)
+                    if (o[c])
+                        for (int t = 0; t < T; ++t) touched[((c - (T / 2 - 1) + t) % n + n) % n] = 1;
+                // longest cyclic run of untouched indices
+                int best = 0, best_end = 0, run = 0;
+                for (int i = 0; i < 2 * n; ++i) {
+                    run = touched[i % n] ? 0 : std::min(run + 1, n);
+                    if (run > best) {
+                        best = run;
+                        best_end = i % n;
+                    }
+                }
+                if (best == n) {
+                    L = 16;   // no points: any small box
+                } else if (best > 0) {
+                    lo = (best_end + 1) % n;
+                    L = n - best;
+                }
+                L = (L + 15) / 16 * 16;
+                if (L >= n) {
+                    lo = 0;
+                    L = n;
+                }
+            }
+            g->box[(size_t)w * 6 + 2 * a] = lo;
+            g->box[(size_t)w * 6 + 2 * a + 1] = L;
+        }
 }
 
 // Mean points per occupied cell of window w (bins at S = 1); -1 when the probe fails.
@@ -745,6 +802,15 @@ static int geom_build(ak_geom* g, const int32_t* cols, const double* X, int64_t 
         }
     }
     g->nitems = (int64_t)all.size();
+    if (rc == AK_OK) {
+        geom_boxes(g, all, g->item_begin[3], g->item_end[3]);
+        if (AK_MALLOC(&g->box_d, sizeof(int) * g->box.size()) != cudaSuccess ||
+            cudaMemcpyAsync(g->box_d, g->box.data(), sizeof(int) * g->box.size(), cudaMemcpyHostToDevice, st) !=
+                cudaSuccess) {
+            cudaGetLastError();
+            rc = fail(AK_ERR_ALLOC, "box allocation failed");
+        }
+    }
     if (rc == AK_OK && cached) {
         const int T = g->wf.taps;
         std::vector<int64_t> shift(P, 0);
@@ -885,6 +951,12 @@ extern "C" int64_t ak_geom_grid_elems(const ak_geom* g, int32_t w) {
 extern "C" int64_t ak_geom_canon_offset(const ak_geom* g, int32_t w) {
     if (!g || w < 0 || w >= g->P) return -1;
     return g->canon_off[w];
+}
+extern "C" int ak_geom_box(const ak_geom* g, int32_t w, int32_t* box6) {
+    if (!g || !box6) return fail(AK_ERR_INVALID, "null argument");
+    if (w < 0 || w >= g->P) return fail(AK_ERR_INVALID, "window out of range");
+    for (int k = 0; k < 6; ++k) box6[k] = g->box[(size_t)w * 6 + k];
+    return AK_OK;
 }
 extern "C" int64_t ak_geom_canon_total(const ak_geom* g) { return g ? g->canon_total : -1; }
 
@@ -1346,7 +1418,7 @@ static bool fft3_fused_ok(const ak_geom* g, int n, int m) {
 }
 
 struct ak_op;
-static int fft3_forward(ak_op* op, cudaStream_t st);
+static int fft3_forward(ak_op* op, bool full_box, cudaStream_t st);
 static int fft3_inverse(ak_op* op, const double* const* H, int hbase, int per_rhs, cudaStream_t st);
 
 struct ak_op {
@@ -1380,43 +1452,56 @@ static ak::Fft3Tables fft3_tables(const ak_op* op) {
     return ak::Fft3Tables{t, t + nm, t + 2 * nm, t + 6 * nm};
 }
 
-// fused q = 3 transforms: grids -> compact band spectra (op->band, q = 3 section)
+// largest box extent along axis 0 over the 3-D windows (the launches' plane count)
+static int box_planes(const ak_geom* g) {
+    int L0 = 0;
+    for (int w : g->windows_of_q[3]) L0 = std::max(L0, g->box[(size_t)w * 6 + 1]);
+    return std::max(L0, 1);
+}
+
+// fused q = 3 transforms: grids -> compact band spectra (op->band, q = 3 section).
+// full_box: the grids hold more than this op's spread (AK_APPLY_FROM_GRIDS after a
+// grid all-reduce): transform whole grids instead of the spread geometry's boxes.
 template <int n, int m>
-static int fft3_forward_t(ak_op* op, cudaStream_t st) {
+static int fft3_forward_t(ak_op* op, bool full_box, cudaStream_t st) {
     const unsigned nb = (unsigned)(op->R * op->nwin[3]);
     const ak::Fft3Tables tb = fft3_tables(op);
+    const int* box = full_box ? nullptr : op->gs->box_d;
+    const unsigned planes = full_box ? (unsigned)n : (unsigned)box_planes(op->gs);
     {
         ProfScope ps(st);
-        ak::k_fft3_fwd12<n, m><<<dim3(n, nb), ak::FFT3_THREADS, ak::fft3_smem_fwd12(n, m), st>>>(
-            op->grids + op->grid_off[3], op->fbuf, tb);
+        ak::k_fft3_fwd12<n, m><<<dim3(planes, nb), ak::FFT3_THREADS, ak::fft3_smem_fwd12(n, m), st>>>(
+            op->grids + op->grid_off[3], op->fbuf, tb, box, op->gwin_d[3], op->R);
         AK_TRY(ps.done("k_fft3_fwd12"));
     }
     ProfScope ps(st);
     ak::k_fft3_fwd0<n, m><<<dim3(m, nb), ak::FFT3_THREADS, ak::fft3_smem_fwd0(n, m), st>>>(
-        op->fbuf, reinterpret_cast<double*>(op->band + op->band_off[3]), tb);
+        op->fbuf, reinterpret_cast<double*>(op->band + op->band_off[3]), tb, box, op->gwin_d[3], op->R);
     return ps.done("k_fft3_fwd0");
 }
 
-// fused q = 3: H (set hbase / per RHS) x band spectra -> op->gbuf grids
+// fused q = 3: H (set hbase / per RHS) x band spectra -> the interpolation geometry's
+// boxes of the op->gbuf grids
 template <int n, int m>
 static int fft3_inverse_t(ak_op* op, const double* const* H, int hbase, int per_rhs, cudaStream_t st) {
     const unsigned nb = (unsigned)(op->R * op->nwin[3]);
     const ak::Fft3Tables tb = fft3_tables(op);
+    const int* box = op->gi->box_d;
     {
         ProfScope ps(st);
         ak::k_fft3_inv0<n, m><<<dim3(m, nb), ak::FFT3_THREADS, ak::fft3_smem_inv0(n, m), st>>>(
             reinterpret_cast<const double*>(op->band + op->band_off[3]), op->fbuf, tb, op->R, op->gwin_d[3], H, hbase,
-            op->gs->P, per_rhs);
+            op->gs->P, per_rhs, box);
         AK_TRY(ps.done("k_fft3_inv0"));
     }
     ProfScope ps(st);
-    ak::k_fft3_inv12<n, m><<<dim3(n, nb), ak::FFT3_THREADS, ak::fft3_smem_inv12(n, m), st>>>(
-        op->fbuf, op->gbuf + op->grid_off[3], tb);
+    ak::k_fft3_inv12<n, m><<<dim3((unsigned)box_planes(op->gi), nb), ak::FFT3_THREADS, ak::fft3_smem_inv12(n, m), st>>>(
+        op->fbuf, op->gbuf + op->grid_off[3], tb, box, op->gwin_d[3], op->R);
     return ps.done("k_fft3_inv12");
 }
 
-static int fft3_forward(ak_op* op, cudaStream_t st) {
-    return op->gs->n == 64 ? fft3_forward_t<64, 32>(op, st) : fft3_forward_t<32, 16>(op, st);
+static int fft3_forward(ak_op* op, bool full_box, cudaStream_t st) {
+    return op->gs->n == 64 ? fft3_forward_t<64, 32>(op, full_box, st) : fft3_forward_t<32, 16>(op, full_box, st);
 }
 
 static int fft3_inverse(ak_op* op, const double* const* H, int hbase, int per_rhs, cudaStream_t st) {
@@ -1594,7 +1679,7 @@ static int op_apply(ak_op* op, const double* V, int64_t ldv, const double* const
     if (flags & AK_APPLY_SPECTRUM_ONLY) {
         for (int q = 3; q >= 1; --q)
             if (q == 3 && op->fused3) {
-                AK_TRY(fft3_forward(op, st));
+                AK_TRY(fft3_forward(op, false, st));
             } else if (op->has[q]) {
                 AK_TRY(cufft_d2z(op, q, st));
                 AK_TRY(band_pack(op, q, 0, st));
@@ -1619,7 +1704,7 @@ static int op_apply(ak_op* op, const double* V, int64_t ldv, const double* const
     for (int q = 3; q >= 1; --q)
         if (q == 3 && op->fused3) {
             // the band spectrum is the fused stage's intermediate: from-spectrum starts at the inverse
-            if (!(flags & AK_APPLY_FROM_SPECTRUM)) AK_TRY(fft3_forward(op, st));
+            if (!(flags & AK_APPLY_FROM_SPECTRUM)) AK_TRY(fft3_forward(op, (flags & AK_APPLY_FROM_GRIDS) != 0, st));
         } else if (op->has[q]) {
             if (flags & AK_APPLY_FROM_SPECTRUM) AK_TRY(band_pack(op, q, 1, st));
             else AK_TRY(cufft_d2z(op, q, st));

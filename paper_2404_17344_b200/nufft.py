@@ -299,6 +299,13 @@ class DeviceGeometry:
         self.n_items = int(lib.ak_geom_num_items(self._handle))
         self.canon_total = int(lib.ak_geom_canon_total(self._handle))
         self.canon_offsets = tuple(int(lib.ak_geom_canon_offset(self._handle, w)) for w in range(P))
+        self.boxes = tuple(self._box(lib, w) for w in range(P))
+
+    def _box(self, lib, w: int):
+        """((lo, L) per axis): window w's occupied grid box (ak_geom_box)."""
+        b = (ctypes.c_int32 * 6)()
+        _native.check(lib.ak_geom_box(self._handle, w, b), "ak_geom_box")
+        return tuple((int(b[2 * a]), int(b[2 * a + 1])) for a in range(3))
 
     @property
     def handle(self) -> ctypes.c_void_p:

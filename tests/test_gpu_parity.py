@@ -299,3 +299,60 @@ def test_dense_cells_cutoff(cuda, cutoff):
         fs = R.FastSum(fam, 0.3, 1.0, [(0, 1, 2), (3, 4, 5)], X, cutoff=cutoff)
         for r in range(2):
             assert rel(res[key][r], fs.matvec(V[r])) <= TOL, (cutoff, key, r)
+
+
+@pytest.mark.parametrize("layout", ["corner", "wrap", "full", "two_boxes"])
+def test_occupied_box_transforms_match_full(cuda, layout):
+    """The fused 3-D transforms work on each window's occupied grid box (ak_geom_box):
+    data in a corner, data straddling the periodic seam on one axis (a box that wraps
+    around n), data over the whole torus (full box) and two windows with different
+    boxes, against the whole-grid cuFFT stage (fused_fft3=0): K and dK/dl, 3 RHS, plus a
+    cross product whose evaluation points sit in another box than the training points."""
+    from paper_2404_17344_b200.fastsum import (build_plan, fast_cross_matvec, fast_matvecs,
+                                               prepare_eval_points)
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.windows import WindowSet
+
+    rng = np.random.default_rng(7)
+    N = 3000
+
+    def pts(kind, n):
+        if kind == "corner":
+            return rng.uniform(-0.12, 0.03, size=(n, 3))
+        if kind == "wrap":
+            X = rng.uniform(-0.1, 0.1, size=(n, 3))
+            X[:, 0] = np.where(rng.random(n) < 0.5, rng.uniform(0.43, 0.5, n), rng.uniform(-0.5, -0.44, n))
+            return X
+        return rng.uniform(-0.5, 0.5, size=(n, 3))
+
+    if layout == "two_boxes":
+        X = np.hstack([pts("corner", N), pts("wrap", N)])
+        ws = WindowSet(((1, 2, 3), (4, 5, 6)), d_max=3)
+    else:
+        X = pts(layout, N)
+        ws = WindowSet(((1, 2, 3),), d_max=3)
+    X = np.minimum(X, 0.5 - 1e-12)
+    spec = KernelSpec("gauss", 0.3)
+    V = rng.normal(size=(3, N))
+    fused = build_plan(spec, ws, "default", _ds(X, 3))
+    ref = build_plan(spec, ws, "default", _ds(X, 3), tuning={"fused_fft3": 0})
+    boxes = fused.geometries.boxes
+    n = fused.geometries.n
+    if layout == "corner":
+        assert all(L < n for _, L in boxes[0])
+    if layout == "wrap":
+        lo, L = boxes[0][0]
+        assert L < n and lo + L > n  # wraps around the seam
+    if layout == "full":
+        assert boxes[0] == ((0, n),) * 3
+    a = fast_matvecs(fused, V, dell=True)
+    b = fast_matvecs(ref, V, dell=True)
+    assert rel(a["K"], b["K"]) <= 1e-13
+    assert rel(a["dK_dell"], b["dK_dell"]) <= 1e-13
+    Xe = np.minimum(pts("full" if layout == "corner" else "corner", 500), 0.5 - 1e-12)
+    if layout == "two_boxes":
+        Xe = np.hstack([Xe, pts("corner", 500)])
+    v = V[0]
+    ca = fast_cross_matvec(fused, prepare_eval_points(fused, _ds(Xe, 3)), v, 500)
+    cb = fast_cross_matvec(ref, prepare_eval_points(ref, _ds(Xe, 3)), v, 500)
+    assert rel(ca, cb) <= 1e-13
