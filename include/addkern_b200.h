@@ -133,6 +133,10 @@ typedef struct ak_tuning {
                                     (multi-cell) interpolation: 1 or 2 (default 2; the spread keeps
                                     one warp per item: two warps flushing cell runs into one tile
                                     need shared-memory atomics, measured 2.3x slower on config 3)    */
+    int32_t tc_spread3;         /* 3-D spread on the FP64 tensor cores where the DFMA kernels are the
+                                    alternative: bit 0 single-RHS dense cells (rows a < 8 by DMMA,
+                                    a = 8..11 by DFMA), bit 1 supercell items with 8 RHS per CTA
+                                    (RHS-minor data, R % 8 == 0)                                     */
 } ak_tuning;
 
 /* Fill *t with the defaults ak_geom_create uses. */

@@ -75,6 +75,7 @@ class Tuning(ctypes.Structure):
         ("fused_fft3", ctypes.c_int32),
         ("generic_kernels", ctypes.c_int32),
         ("sparse_warps", ctypes.c_int32),
+        ("tc_spread3", ctypes.c_int32),
     ]
 
 

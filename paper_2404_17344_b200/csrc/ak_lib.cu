@@ -28,6 +28,8 @@
 #include "ak_q1r.cuh"
 #include "ak_q2r.cuh"
 #include "ak_fft3.cuh"
+#include "ak_q3b.cuh"
+#include "ak_q3h.cuh"
 
 using namespace ak;
 
@@ -290,6 +292,7 @@ extern "C" void ak_tuning_default(ak_tuning* t) {
     t->fused_fft3 = 1;
     t->generic_kernels = 0;
     t->sparse_warps = 2;
+    t->tc_spread3 = 1;
 }
 
 __global__ void k_count_nonzero(const int* __restrict__ counts, int total, int* __restrict__ nz) {
@@ -1146,9 +1149,25 @@ static const char* launch_spread3_t(const ak_geom* g, int64_t i0, int64_t ni, co
                                                          g->canon_off_d, R, g->n);
                 return "k_spread3c<10>";
             }
+            if (g->tune.tc_spread3 & 1) {
+                k_spread3h<32><<<units, 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, vs, grids,
+                                                     g->canon_off_d, R, g->n);
+                return "k_spread3h";
+            }
             k_spread3c<32><<<units, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, vs, grids,
                                                  g->canon_off_d, R, g->n);
             return "k_spread3c";
+        }
+        if (g->cached && g->sedge[3] == 2 && vs.rs == 1 && R % 8 == 0 && (g->tune.tc_spread3 & 2)) {
+            // 8 RHS per CTA on the FP64 tensor cores, supercell region as the GEMM output (ak_q3b.cuh)
+            static std::once_flag attr;
+            std::call_once(attr, [] {
+                cudaFuncSetAttribute(k_spread3b<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)spread3b_smem<32>());
+            });
+            k_spread3b<32><<<(unsigned)(ni * (R / 8)), 32 * Q3B_WARPS, spread3b_smem<32>(), st>>>(
+                g->CI3, g->W3, g->wshift_d, g->items + i0, V, vs, grids, g->canon_off_d, R, g->n);
+            return "k_spread3b";
         }
         if (g->cached) {
             k_spread3w<12, 2, AK_SPARSE_BATCH><<<units, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, vs, grids,

@@ -1,0 +1,159 @@
+// q = 3 single-cell spread of one right-hand side, split between the FP64 tensor
+// cores and the FP64 FMA pipe (dense 3-D windows: config 4).
+//
+// For one cell and one RHS the spread (nufft.py:231-254) is the GEMM
+//   G[a][(b, c)] += sum_j (w0_j[a]) (v_j w1_j[b] w2_j[c])      M = 12, N = 144, K = points.
+// mma.sync m8n8k4 tiles M in 8s, so rows a = 0..7 go to the tensor cores (one m-tile,
+// no padding) and the 4 rows a = 8..11 are done with DFMAs on the same B operand
+// values the lane already holds for the DMMA:
+//   CTA = 2 warps = one (item, RHS) unit; warp h owns the columns b in [6h, 6h + 6)
+//   (72 columns = 9 n-tiles).  Lane group g = lane / 4 owns a 3 x 3 block of them
+//   (b = 6h + 3 (g / 4) + jb, c = 3 (g % 4) + jc, tile j = 3 jb + jc), lane kk = lane % 4
+//   is the point of the k-step: its 9 B values v w1[b] w2[c] (3 + 9 DMUL) feed 9 DMMA
+//   (rows a < 8, A = w0[lane / 4]) and 36 DFMA (rows a = 8..11 of its own point into
+//   per-lane accumulators, summed over the 4 lanes of a group at the flush).
+// FP64 pipe slots per 4 points and warp: 9 DMMA (= 72 DFMA slots) + 36 DFMA + 12 DMUL
+// = 120 for 108 useful: 90%, against 54 DFMA + 12 DMUL per point and lane (82%) for
+// the register-tiled DFMA kernel (k_spread3c), whose one-RHS output rows would pad
+// 12 -> 16 on the tensor cores alone (70%).
+#pragma once
+#include "ak_q3r.cuh"
+
+namespace ak {
+
+// CTAs (2 warps) per SM the register allocation must allow
+#ifndef AK_SPREAD3H_MINB
+#define AK_SPREAD3H_MINB 5
+#endif
+template <int B>
+__global__ void __launch_bounds__(64, AK_SPREAD3H_MINB)
+k_spread3h(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
+           const WorkItem* __restrict__ items, const double* __restrict__ V, Strides vs,
+           double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
+{
+    constexpr int T = 12, RW = 3 * T;
+    static_assert(B % 4 == 0 && B <= 64, "batch");
+    __shared__ Spread3cSmem<B> sm;
+    auto& wbuf = sm.wbuf;
+    auto& vb = sm.vb;
+    auto& bar = sm.bar;
+    auto& cib = sm.cib;
+
+    const WorkItem it = items[blockIdx.x / nrhs];
+    const int r = blockIdx.x % nrhs;            // RHS fastest: the R CTAs of an item share its rows in L2
+    const int tid = threadIdx.x, h = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, kk = lane & 3;
+    const double* __restrict__ Vr = V + (int64_t)r * vs.rs;
+    const int nbatch = (it.count + B - 1) / B;
+    const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
+    const CellIdx* __restrict__ CIit = ci + (it.start - wshift[it.window]);
+
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (tid == 0) tma_load_1d(&wbuf[0][0][0], Wit, (unsigned)(min(B, it.count) * RW * 8), &bar[0]);
+    if (tid < min(B, it.count)) cp_async8(&cib[0][tid], CIit + tid);
+    if (nbatch > 1 && tid < min(B, it.count - B)) cp_async8(&cib[1][tid], CIit + B + tid);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    if (tid < min(B, it.count)) cp_async8(&vb[0][tid], Vr + (int64_t)cib[0][tid].idx * vs.is);
+    cp_async_commit();
+
+    // this lane's weight offsets: w1 at b0 .. b0 + 2, w2 at c0 .. c0 + 2 (row layout w0 | w1 | w2)
+    const int b0 = T + 6 * h + 3 * (g >> 2), c0 = 2 * T + 3 * (g & 3);
+    double acc[9][2], acc2[4][9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+        acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) acc2[a][j] = 0.0;
+    }
+
+    for (int bi = 0; bi < nbatch; ++bi) {
+        const int s = bi & 1;
+        const int off = bi * B;
+        const int nb = min(B, it.count - off);
+        cp_async_wait_all();
+        mbar_wait(&bar[s], (bi >> 1) & 1);
+        __syncthreads();
+        if (bi + 1 < nbatch) {
+            const int nb1 = min(B, it.count - off - B);
+            if (tid == 0) {
+                fence_proxy_async();
+                tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + B) * RW, (unsigned)(nb1 * RW * 8), &bar[s ^ 1]);
+            }
+            if (tid < nb1) cp_async8(&vb[s ^ 1][tid], Vr + (int64_t)cib[(bi + 1) % 3][tid].idx * vs.is);
+        }
+        if (bi + 2 < nbatch && tid < min(B, it.count - off - 2 * B))
+            cp_async8(&cib[(bi + 2) % 3][tid], CIit + off + 2 * B + tid);
+        cp_async_commit();
+#pragma unroll 2
+        for (int k0 = 0; k0 < nb; k0 += 4) {
+            const int j = k0 + kk;
+            const bool valid = j < nb;
+            const double* w = wbuf[s][valid ? j : 0];
+            const double v = valid ? vb[s][j] : 0.0;
+            double vw1[3], w2[3], w0h[4], bf[9];
+#pragma unroll
+            for (int x = 0; x < 3; ++x) {
+                vw1[x] = v * w[b0 + x];
+                w2[x] = w[c0 + x];
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a) w0h[a] = w[8 + a];
+            const double af = w[g];
+#pragma unroll
+            for (int t = 0; t < 9; ++t) bf[t] = vw1[t / 3] * w2[t % 3];
+#pragma unroll
+            for (int t = 0; t < 9; ++t) dmma_8x8x4(acc[t][0], acc[t][1], af, bf[t]);
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int t = 0; t < 9; ++t) acc2[a][t] = fma(w0h[a], bf[t], acc2[a][t]);
+        }
+    }
+
+    // flush.  DMMA tiles: lane holds D[a = g][col 2 kk + e] of tile t, i.e. column block
+    // g' = 2 kk + e: (b, c) = (6h + 3 (g' / 4) + t / 3, 3 (g' % 4) + t % 3).
+    // DFMA rows: summed over the group's 4 lanes; lane kk adds row a = 8 + kk.
+    const int cc0 = it.sc & 1023, cc1 = (it.sc >> 10) & 1023, cc2 = (it.sc >> 20) & 1023;
+    const int o0 = cc0 - (T / 2 - 1), o1 = cc1 - (T / 2 - 1), o2 = cc2 - (T / 2 - 1);
+    double* __restrict__ gr = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)r * n * n * n;
+    const bool inside = o0 >= 0 && o0 + T <= n && o1 >= 0 && o1 + T <= n && o2 >= 0 && o2 + T <= n;
+    auto X = [&](int o, int i) { return inside ? o + i : wrap(o + i, n); };
+    const int64_t nn = (int64_t)n * n;
+    {
+        double* plane = gr + (int64_t)X(o0, g) * nn;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int gg = 2 * kk + e;
+#pragma unroll
+            for (int t = 0; t < 9; ++t) {
+                const int b = 6 * h + 3 * (gg >> 2) + t / 3, c = 3 * (gg & 3) + t % 3;
+                red_add(plane + (int64_t)X(o1, b) * n + X(o2, c), acc[t][e]);
+            }
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+            acc2[a][t] += __shfl_xor_sync(0xffffffffu, acc2[a][t], 1);
+            acc2[a][t] += __shfl_xor_sync(0xffffffffu, acc2[a][t], 2);
+        }
+    double mine[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) mine[t] = kk == 0 ? acc2[0][t] : (kk == 1 ? acc2[1][t] : (kk == 2 ? acc2[2][t] : acc2[3][t]));
+    double* plane = gr + (int64_t)X(o0, 8 + kk) * nn;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+        const int b = 6 * h + 3 * (g >> 2) + t / 3, c = 3 * (g & 3) + t % 3;
+        red_add(plane + (int64_t)X(o1, b) * n + X(o2, c), mine[t]);
+    }
+}
+
+}  // namespace ak

@@ -47,7 +47,7 @@ def _case(seed):
         X = np.minimum(X, np.nextafter(0.5, 0.0))
     else:
         X = 0.003 + 1e-4 * rng.random((N, 6))
-    R = int(rng.choice([1, 2, 5, 9]))   # 9: the RHS-batched q <= 2 kernels
+    R = int(rng.choice([1, 2, 5, 8, 9, 16]))   # 9: the RHS-batched q <= 2 kernels; 8, 16: RHS chunks of 8 (sparse 3-D spread)
     V = rng.normal(size=(R, N))
     knobs = {}
     k = rng.integers(0, 4)

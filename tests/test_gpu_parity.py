@@ -172,7 +172,10 @@ def test_native_library_is_what_runs(cuda):
     {"cell_items3": 2, "chunk3": 256},          # supercell items, small chunks
     {"cell_items3": 1},                         # single-cell work items (auto-selected for dense data)
     {"cell_items3": 1, "chunk3": 100},
-    {"cell_items3": 1, "rhs_pair_spread": 0},   # single-cell DFMA spread for every RHS
+    {"cell_items3": 1, "rhs_pair_spread": 0},   # single-cell hybrid DMMA + DFMA spread for every RHS
+    {"cell_items3": 1, "rhs_pair_spread": 0, "tc_spread3": 0},   # ... the register-tiled DFMA spread
+    {"cell_items3": 2, "tc_spread3": 0},        # supercell DFMA spread (no 8-RHS tensor-core kernel)
+    {"cell_items3": 2, "tc_spread3": 1},        # supercell DFMA spread, single-cell hybrid only
     # split items: supercell spread, single-cell interpolation over the same sorted points
     {"dense_cells3": 1e9, "dense_cells3_interp": 0},
     {"dense_cells3": 1e9, "dense_cells3_interp": 0, "chunk3": 100},

@@ -85,6 +85,13 @@ def main():
     refd = R.FastSum("der_gauss", 0.5, 1.0, [(0, 1, 2), (3, 4, 5)], Xs).matvec(V[2])
     worst = max(worst, rel(out[2], refd))
     print("sparse dK", rel(out[2], refd), flush=True)
+    # sparse supercell items with 8 RHS per CTA (k_spread3b), two RHS chunks
+    V16 = rng.normal(size=(16, 3000))
+    out = fast_matvecs(splan, V16)["K"]
+    for r in (0, 15):
+        refr = R.FastSum("gauss", 0.5, 1.0, [(0, 1, 2), (3, 4, 5)], Xs).matvec(V16[r])
+        worst = max(worst, rel(out[r], refr))
+    print("sparse R=16 K", rel(out[15], refr), flush=True)
 
     # many RHS (RHS-minor batched kernels: k_spread1r / k_interp1r, k_spread2r / k_interp2r,
     # RHS-pair k_spread3r), mixed kernels with per-window outputs, boundary-hugging nodes
