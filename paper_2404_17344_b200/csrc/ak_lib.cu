@@ -1150,7 +1150,7 @@ static const char* launch_spread3_t(const ak_geom* g, int64_t i0, int64_t ni, co
                 return "k_spread3c<10>";
             }
             if (g->tune.tc_spread3 & 1) {
-                k_spread3h<32><<<units, 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, vs, grids,
+                k_spread3h<AK_SPREAD3H_BATCH, AK_SPREAD3H_WARPS><<<units, 32 * AK_SPREAD3H_WARPS, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V, vs, grids,
                                                      g->canon_off_d, R, g->n);
                 return "k_spread3h";
             }

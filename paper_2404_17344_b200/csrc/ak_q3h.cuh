@@ -21,18 +21,32 @@
 
 namespace ak {
 
-// CTAs (2 warps) per SM the register allocation must allow
+// CTAs (2 warps) per SM the register allocation must allow (5: 168 registers, the
+// per-SMSP register file at 10 warps/SM); points per staged batch.  Measured on config 4
+// (B200, tools/gpu_var.sh): 5 CTAs 1.432 ms, 4 CTAs (198 registers) 1.529, 6 CTAs 1.459;
+// 64-point batches 1.445; 3 warps per CTA (2 b values per lane group, 128 registers,
+// 15 warps/SM) 1.631; operands of the next k-step loaded ahead in registers: 1.605
+// (spills at 168 registers) / 1.619 (198 registers, 8 warps/SM).
 #ifndef AK_SPREAD3H_MINB
 #define AK_SPREAD3H_MINB 5
 #endif
-template <int B>
-__global__ void __launch_bounds__(64, AK_SPREAD3H_MINB)
+#ifndef AK_SPREAD3H_BATCH
+#define AK_SPREAD3H_BATCH 32
+#endif
+#ifndef AK_SPREAD3H_WARPS
+#define AK_SPREAD3H_WARPS 2
+#endif
+template <int B, int WC>
+__global__ void __launch_bounds__(32 * WC, AK_SPREAD3H_MINB)
 k_spread3h(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ V, Strides vs,
            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
 {
     constexpr int T = 12, RW = 3 * T;
-    static_assert(B % 4 == 0 && B <= 64, "batch");
+    constexpr int NB = 6 / WC, NT = 3 * NB;   // b values per lane group, n-tiles per warp
+    constexpr int NTH = 32 * WC;
+    static_assert(WC == 2 || WC == 3, "2 or 3 warps");
+    static_assert(B % 4 == 0 && B <= NTH, "batch");
     __shared__ Spread3cSmem<B> sm;
     auto& wbuf = sm.wbuf;
     auto& vb = sm.vb;
@@ -63,11 +77,11 @@ k_spread3h(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     if (tid < min(B, it.count)) cp_async8(&vb[0][tid], Vr + (int64_t)cib[0][tid].idx * vs.is);
     cp_async_commit();
 
-    // this lane's weight offsets: w1 at b0 .. b0 + 2, w2 at c0 .. c0 + 2 (row layout w0 | w1 | w2)
-    const int b0 = T + 6 * h + 3 * (g >> 2), c0 = 2 * T + 3 * (g & 3);
-    double acc[9][2], acc2[4][9];
+    // this lane's weight offsets: w1 at b0 .. b0 + NB - 1, w2 at c0 .. c0 + 2 (row layout w0 | w1 | w2)
+    const int b0 = T + 2 * NB * h + NB * (g >> 2), c0 = 2 * T + 3 * (g & 3);
+    double acc[NT][2], acc2[4][NT];
 #pragma unroll
-    for (int j = 0; j < 9; ++j) {
+    for (int j = 0; j < NT; ++j) {
         acc[j][0] = acc[j][1] = 0.0;
 #pragma unroll
         for (int a = 0; a < 4; ++a) acc2[a][j] = 0.0;
@@ -97,23 +111,22 @@ k_spread3h(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
             const bool valid = j < nb;
             const double* w = wbuf[s][valid ? j : 0];
             const double v = valid ? vb[s][j] : 0.0;
-            double vw1[3], w2[3], w0h[4], bf[9];
+            double vw1[NB], w2[3], w0h[4], bf[NT];
 #pragma unroll
-            for (int x = 0; x < 3; ++x) {
-                vw1[x] = v * w[b0 + x];
-                w2[x] = w[c0 + x];
-            }
+            for (int x = 0; x < NB; ++x) vw1[x] = v * w[b0 + x];
+#pragma unroll
+            for (int x = 0; x < 3; ++x) w2[x] = w[c0 + x];
 #pragma unroll
             for (int a = 0; a < 4; ++a) w0h[a] = w[8 + a];
             const double af = w[g];
 #pragma unroll
-            for (int t = 0; t < 9; ++t) bf[t] = vw1[t / 3] * w2[t % 3];
+            for (int t = 0; t < NT; ++t) bf[t] = vw1[t / 3] * w2[t % 3];
 #pragma unroll
-            for (int t = 0; t < 9; ++t) dmma_8x8x4(acc[t][0], acc[t][1], af, bf[t]);
+            for (int t = 0; t < NT; ++t) dmma_8x8x4(acc[t][0], acc[t][1], af, bf[t]);
 #pragma unroll
             for (int a = 0; a < 4; ++a)
 #pragma unroll
-                for (int t = 0; t < 9; ++t) acc2[a][t] = fma(w0h[a], bf[t], acc2[a][t]);
+                for (int t = 0; t < NT; ++t) acc2[a][t] = fma(w0h[a], bf[t], acc2[a][t]);
         }
     }
 
@@ -126,34 +139,39 @@ k_spread3h(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     const bool inside = o0 >= 0 && o0 + T <= n && o1 >= 0 && o1 + T <= n && o2 >= 0 && o2 + T <= n;
     auto X = [&](int o, int i) { return inside ? o + i : wrap(o + i, n); };
     const int64_t nn = (int64_t)n * n;
-    {
-        double* plane = gr + (int64_t)X(o0, g) * nn;
+    auto flush9 = [&](int a, int gg, const double (&v)[NT]) {
+        double* plane = gr + (int64_t)X(o0, a) * nn;
+        int xb[NB], xc[3];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int gg = 2 * kk + e;
+        for (int x = 0; x < NB; ++x) xb[x] = X(o1, 2 * NB * h + NB * (gg >> 2) + x) * n;
 #pragma unroll
-            for (int t = 0; t < 9; ++t) {
-                const int b = 6 * h + 3 * (gg >> 2) + t / 3, c = 3 * (gg & 3) + t % 3;
-                red_add(plane + (int64_t)X(o1, b) * n + X(o2, c), acc[t][e]);
-            }
-        }
+        for (int x = 0; x < 3; ++x) xc[x] = X(o2, 3 * (gg & 3) + x);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) red_add(plane + xb[t / 3] + xc[t % 3], v[t]);
+    };
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        double v[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) v[t] = acc[t][e];
+        flush9(g, 2 * kk + e, v);
     }
+    // rows 8..11: reduce-scatter over the group's 4 lanes (lane kk ends with row 8 + kk)
+    const bool hi2 = (kk & 2) != 0, hi1 = (kk & 1) != 0;
+    double keep[2][NT], mine[NT];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int x = 0; x < 2; ++x)
 #pragma unroll
-        for (int t = 0; t < 9; ++t) {
-            acc2[a][t] += __shfl_xor_sync(0xffffffffu, acc2[a][t], 1);
-            acc2[a][t] += __shfl_xor_sync(0xffffffffu, acc2[a][t], 2);
+        for (int t = 0; t < NT; ++t) {
+            const double send = hi2 ? acc2[x][t] : acc2[2 + x][t];
+            keep[x][t] = (hi2 ? acc2[2 + x][t] : acc2[x][t]) + __shfl_xor_sync(0xffffffffu, send, 2);
         }
-    double mine[9];
 #pragma unroll
-    for (int t = 0; t < 9; ++t) mine[t] = kk == 0 ? acc2[0][t] : (kk == 1 ? acc2[1][t] : (kk == 2 ? acc2[2][t] : acc2[3][t]));
-    double* plane = gr + (int64_t)X(o0, 8 + kk) * nn;
-#pragma unroll
-    for (int t = 0; t < 9; ++t) {
-        const int b = 6 * h + 3 * (g >> 2) + t / 3, c = 3 * (g & 3) + t % 3;
-        red_add(plane + (int64_t)X(o1, b) * n + X(o2, c), mine[t]);
+    for (int t = 0; t < NT; ++t) {
+        const double send = hi1 ? keep[0][t] : keep[1][t];
+        mine[t] = (hi1 ? keep[1][t] : keep[0][t]) + __shfl_xor_sync(0xffffffffu, send, 1);
     }
+    flush9(8 + kk, g, mine);
 }
 
 }  // namespace ak
