@@ -136,7 +136,7 @@ typedef struct ak_tuning {
     int32_t tc_spread3;         /* 3-D spread on the FP64 tensor cores where the DFMA kernels are the
                                     alternative: bit 0 single-RHS dense cells (rows a < 8 by DMMA,
                                     a = 8..11 by DFMA), bit 1 supercell items with 8 RHS per CTA
-                                    (RHS-minor data, R % 8 == 0)                                     */
+                                    (RHS-minor data, R % 8 == 0); default 3 (both)                   */
 } ak_tuning;
 
 /* Fill *t with the defaults ak_geom_create uses. */

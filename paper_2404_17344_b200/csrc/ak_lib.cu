@@ -292,7 +292,7 @@ extern "C" void ak_tuning_default(ak_tuning* t) {
     t->fused_fft3 = 1;
     t->generic_kernels = 0;
     t->sparse_warps = 2;
-    t->tc_spread3 = 1;
+    t->tc_spread3 = 3;
 }
 
 __global__ void k_count_nonzero(const int* __restrict__ counts, int total, int* __restrict__ nz) {
@@ -1162,10 +1162,10 @@ static const char* launch_spread3_t(const ak_geom* g, int64_t i0, int64_t ni, co
             // 8 RHS per CTA on the FP64 tensor cores, supercell region as the GEMM output (ak_q3b.cuh)
             static std::once_flag attr;
             std::call_once(attr, [] {
-                cudaFuncSetAttribute(k_spread3b<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)spread3b_smem<32>());
+                cudaFuncSetAttribute(k_spread3b<AK_SPREAD3B_BATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)spread3b_smem<AK_SPREAD3B_BATCH>());
             });
-            k_spread3b<32><<<(unsigned)(ni * (R / 8)), 32 * Q3B_WARPS, spread3b_smem<32>(), st>>>(
+            k_spread3b<AK_SPREAD3B_BATCH><<<(unsigned)(ni * (R / 8) * 2), 32 * Q3B_WARPS, spread3b_smem<AK_SPREAD3B_BATCH>(), st>>>(
                 g->CI3, g->W3, g->wshift_d, g->items + i0, V, vs, grids, g->canon_off_d, R, g->n);
             return "k_spread3b";
         }

@@ -13,10 +13,12 @@
 // the k-steps run across cell boundaries (no per-cell-run flush, no partially filled
 // groups), and the 8 RHS share every B fragment.  The DFMA kernel this replaces
 // (k_spread3w, one RHS per warp) flushes its register tile into a shared region tile
-// at every cell change and reached 35-40% of the FP64 peak on config 3.
-// CTA = 11 warps, one (item, RHS chunk): warp w owns n-tiles w and w + 11 and all 13
-// m-tiles (52 accumulator doubles per lane); the item's accumulators are added to the
-// grids with RED.F64 at the end (zero entries skipped).  Per batch of B points the
+// at every cell change: config 3 spread 0.745 ms there, 0.687 ms here.
+// CTA = 6 warps, one (item, RHS chunk, column half): half h holds n-tiles 11 h .. 11 h
+// + 10, warp w of them w and w + 6 (warp 5: one) and all 13 m-tiles (at most 52
+// accumulator doubles per lane), so two CTAs fit an SM and one's prologue / flush
+// overlaps the other's DMMA stream; the item's accumulators are added to the grids
+// with RED.F64 at the end.  Per batch of B points the
 // weight rows arrive by a TMA bulk copy (double-buffered), the (cell, row) records
 // and the 8 RHS values of each point by cp.async, and the CTA writes the A operand
 // (v_jr w0'_j[a'], 104 values per point) to shared memory once for all warps.
@@ -25,7 +27,10 @@
 
 namespace ak {
 
-constexpr int Q3B_WARPS = 11;
+constexpr int Q3B_WARPS = 6;   // per CTA (two CTAs per SM)
+#ifndef AK_SPREAD3B_BATCH
+#define AK_SPREAD3B_BATCH 48       // points per staged batch (config 3: 32 -> 0.734 ms, 48 -> 0.687, 64 -> 0.693)
+#endif
 constexpr int Q3B_LDA = 108;   // A row stride (doubles): fragment loads (k = lane % 4 rows) conflict-free
 
 template <int B>
@@ -41,7 +46,7 @@ template <int B>
 inline size_t spread3b_smem() { return sizeof(Spread3bSmem<B>); }
 
 template <int B>
-__global__ void __launch_bounds__(32 * Q3B_WARPS, 1)
+__global__ void __launch_bounds__(32 * Q3B_WARPS, 2)
 k_spread3b(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ V, Strides vs,
            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
@@ -50,7 +55,7 @@ k_spread3b(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     constexpr int MT = RG;                                     // 13 m-tiles: rows (r, a') = 8 x 13
     constexpr int NCOL = RG * RG;                              // 169 columns (b', c')
     constexpr int NTH = 32 * Q3B_WARPS;
-    static_assert(B % 4 == 0 && B * 8 <= NTH, "batch");
+    static_assert(B % 4 == 0 && B <= NTH, "batch");
     extern __shared__ __align__(128) unsigned char q3b_raw[];
     auto& sm = *reinterpret_cast<Spread3bSmem<B>*>(q3b_raw);
     auto& wbuf = sm.wbuf;
@@ -59,8 +64,9 @@ k_spread3b(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     auto& bar = sm.bar;
 
     const int nch = nrhs / 8;
-    const WorkItem it = items[blockIdx.x / nch];
-    const int rc = blockIdx.x % nch;               // RHS chunk (fastest: chunks of an item share its rows in L2)
+    const WorkItem it = items[blockIdx.x / (2 * nch)];
+    const int rc = (blockIdx.x >> 1) % nch;        // RHS chunk and column half run fastest: the CTAs of
+    const int hf = blockIdx.x & 1;                 // an item share its weight rows in L2
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int lr = lane >> 2, kk = lane & 3;
     const double* __restrict__ V0 = V + (int64_t)(8 * rc) * vs.rs;
@@ -81,19 +87,20 @@ k_spread3b(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
-    if (tid < 8 * min(B, it.count)) {
-        const int j = tid >> 3, r = tid & 7;
+    for (int e = tid; e < 8 * min(B, it.count); e += NTH) {
+        const int j = e >> 3, r = e & 7;
         cp_async8(&vb[0][j][r], V0 + (int64_t)r * vs.rs + (int64_t)cib[0][j].idx * vs.is);
     }
     cp_async_commit();
 
-    // this lane's B-fragment columns: n-tile warp + 11 t, column 8 nt + lr -> (b', c')
+    // this lane's B-fragment columns: n-tile 11 hf + warp + 6 t, column 8 nt + lr -> (b', c')
     int bcol[2], ccol[2];
     bool cok[2];
+    const bool two = warp + Q3B_WARPS < 11;
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
-        const int col = 8 * (warp + Q3B_WARPS * t) + lr;
-        cok[t] = col < NCOL;
+        const int col = 8 * (11 * hf + warp + Q3B_WARPS * t) + lr;
+        cok[t] = col < NCOL && (t == 0 || two);
         bcol[t] = col / RG;
         ccol[t] = col - bcol[t] * RG;
     }
@@ -117,8 +124,8 @@ k_spread3b(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
                 fence_proxy_async();
                 tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + B) * RW, (unsigned)(nb1 * RW * 8), &bar[s ^ 1]);
             }
-            if (tid < 8 * nb1) {
-                const int j = tid >> 3, r = tid & 7;
+            for (int e = tid; e < 8 * nb1; e += NTH) {
+                const int j = e >> 3, r = e & 7;
                 cp_async8(&vb[s ^ 1][j][r], V0 + (int64_t)r * vs.rs + (int64_t)cib[(bi + 1) % 3][j].idx * vs.is);
             }
         }
@@ -126,17 +133,23 @@ k_spread3b(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
             cp_async8(&cib[(bi + 2) % 3][tid], CIit + off + 2 * B + tid);
         cp_async_commit();
         // A operand of the batch: A[j][(r, a')] = v_jr w0_j[a' - u0_j] (zero outside the
-        // footprint and for rows past nb)
-        for (int e = tid; e < B * 8 * RG; e += NTH) {
-            const int j = e / (8 * RG), row = e - j * (8 * RG);
-            const int r = row / RG, ap = row - r * RG;
-            double a = 0.0;
+        // footprint and for rows past nb); one thread per (point, RHS)
+        for (int e = tid; e < B * 8; e += NTH) {
+            const int j = e >> 3, r = e & 7;
+            double* dst = &sm.A[j][r * RG];
             if (j < nb) {
-                const int ia = ap - (cell_axis(cb[j].cell, 0) - sc0 * S);
-                AK_DCHECK(cell_axis(cb[j].cell, 0) - sc0 * S >= 0 && cell_axis(cb[j].cell, 0) - sc0 * S < S);
-                if ((unsigned)ia < (unsigned)T) a = vb[s][j][r] * wbuf[s][j][ia];
+                const int u0 = cell_axis(cb[j].cell, 0) - sc0 * S;
+                AK_DCHECK(u0 >= 0 && u0 < S);
+                const double v = vb[s][j][r];
+                const double* w0 = wbuf[s][j];
+                dst[0] = u0 ? 0.0 : v * w0[0];
+#pragma unroll
+                for (int a = 1; a < T; ++a) dst[a] = v * w0[u0 ? a - 1 : a];
+                dst[T] = u0 ? v * w0[T - 1] : 0.0;
+            } else {
+#pragma unroll
+                for (int a = 0; a < RG; ++a) dst[a] = 0.0;
             }
-            sm.A[j][row] = a;
         }
         __syncthreads();
 #pragma unroll 2
@@ -160,9 +173,11 @@ k_spread3b(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
 #pragma unroll
             for (int i = 0; i < MT; ++i) af[i] = sm.A[j < B ? j : 0][8 * i + lr];
 #pragma unroll
-            for (int i = 0; i < MT; ++i)
+            for (int i = 0; i < MT; ++i) dmma_8x8x4(acc[i][0][0], acc[i][0][1], af[i], bf[0]);
+            if (two) {
 #pragma unroll
-                for (int t = 0; t < 2; ++t) dmma_8x8x4(acc[i][t][0], acc[i][t][1], af[i], bf[t]);
+                for (int i = 0; i < MT; ++i) dmma_8x8x4(acc[i][1][0], acc[i][1][1], af[i], bf[1]);
+            }
         }
     }
 
@@ -170,28 +185,33 @@ k_spread3b(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     const int o0 = sc0 * S - (T / 2 - 1), o1 = sc1 * S - (T / 2 - 1), o2 = sc2 * S - (T / 2 - 1);
     const int64_t n3 = (int64_t)n * n * n;
     double* __restrict__ g0 = grids + (int64_t)nrhs * canon_off[it.window] + (int64_t)(8 * rc) * n3;
-    int x1[2][2], x2[2][2];
+    int coff[2][2];
     bool ok[2][2];
 #pragma unroll
     for (int t = 0; t < 2; ++t)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-            const int col = 8 * (warp + Q3B_WARPS * t) + 2 * kk + e;
-            ok[t][e] = col < NCOL;
-            const int b = col / RG, c = col - (col / RG) * RG;
-            x1[t][e] = wrap(o1 + (ok[t][e] ? b : 0), n);
-            x2[t][e] = wrap(o2 + (ok[t][e] ? c : 0), n);
+            const int col = 8 * (11 * hf + warp + Q3B_WARPS * t) + 2 * kk + e;
+            ok[t][e] = col < NCOL && (t == 0 || two);
+            const int b = ok[t][e] ? col / RG : 0, c = ok[t][e] ? col - (col / RG) * RG : 0;
+            coff[t][e] = wrap(o1 + b, n) * n + wrap(o2 + c, n);
         }
+    // rows: (r, a') = (row / 13, row % 13), row = 8 i + lr, walked incrementally
+    int r = lr / RG, ap = lr - (lr / RG) * RG;
+    const int64_t nn = (int64_t)n * n;
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
-        const int row = 8 * i + lr;
-        const int r = row / RG, ap = row - r * RG;
-        double* gp = g0 + r * n3 + (int64_t)wrap(o0 + ap, n) * n * n;
+        double* gp = g0 + r * n3 + wrap(o0 + ap, n) * nn;
 #pragma unroll
         for (int t = 0; t < 2; ++t)
 #pragma unroll
             for (int e = 0; e < 2; ++e)
-                if (ok[t][e] && acc[i][t][e] != 0.0) red_add(gp + (int64_t)x1[t][e] * n + x2[t][e], acc[i][t][e]);
+                if (ok[t][e]) red_add(gp + coff[t][e], acc[i][t][e]);
+        ap += 8;
+        if (ap >= RG) {
+            ap -= RG;
+            ++r;
+        }
     }
 }
 
