@@ -82,17 +82,48 @@ __device__ __forceinline__ void fragment_offsets(int (&off)[18], int lane) {
     }
 }
 
+// Region tile of the sparse interpolation and its B-fragment columns.  Lane column n
+// = lane / 4 of tile t is (a, b) = (t / 3 + 6 (n & 1), 3 (n >> 1) + t % 3) -- lane quad q
+// = n >> 1 still owns b = 3q .. 3q+2 (the contraction below), but the two columns of a
+// lane pair are 6 apart in a, and the tile keeps a innermost: element (a, b, c) at
+// a + 13 b + 172 c.  Then the 16 addresses of every half-warp fragment load fall on 16
+// different bank pairs (tools/bank_search.py: 108 wavefronts per 54 loads, the
+// minimum; the dense 13^3 tile with the pairs (i / 3, i % 3), i = 2t + (n & 1), of
+// interp_group_mma costs 216 -- ncu: 38% of the shared wavefronts were conflicts).
+// Measured on config 3 (B200): shared wavefronts per launch 105 M -> 83 M, kernel time
+// unchanged within 0.2% (1.358 vs 1.356 ms per step for the dense layout with the same
+// pairing, AK_INTERP3M_PAD=0): the DMMA group stream, not shared memory, bounds it.
+#ifndef AK_INTERP3M_PAD
+#define AK_INTERP3M_PAD 1
+#endif
+template <int R>
+struct Interp3mTile {
+#if AK_INTERP3M_PAD
+    using L = typename std::conditional<R == 13, TileLayout<1, 13, 172, 12 + 12 * 13 + 12 * 172 + 1>,
+                                        TileLayout<1, R, R * R, R * R * R>>::type;
+#else
+    using L = DenseTile<R>;
+#endif
+};
+template <class L>
+__device__ __forceinline__ void fragment_offsets_s(int (&off)[18], int lane) {
+    const int n = lane >> 2, kk = lane & 3;
+#pragma unroll
+    for (int t = 0; t < 18; ++t) off[t] = L::at(t / 3 + 6 * (n & 1), 3 * (n >> 1) + t % 3, kk);
+}
+
 // G consecutive 8-point groups of one cell run (rows k0 + 8 g + pj, cnt[g] valid rows
 // each) against the same footprint: the B fragments are read from the region tile
 // once per run segment instead of once per group.  The 18 column tiles run in three
-// chunks of six (12 pairs = 4 values of a x 3 of b, lane quad q owning b = 3q .. 3q+2
-// as above): per chunk each group's 6 accumulator tiles are contracted over a right
-// away, so a lane holds 18 fragments + 12 accumulators instead of 36 accumulators.
-// Same operations, in the same order, as interp_group_mma (bit-identical results).
-template <int R, int RW, int G>
+// chunks of six (tiles 6 ch .. 6 ch + 5: a in {2ch, 2ch+1, 2ch+6, 2ch+7}, lane quad q
+// owning b = 3q .. 3q+2 as above): per chunk each group's 6 accumulator tiles are
+// contracted over a right away, so a lane holds 18 fragments + 12 accumulators
+// instead of 36 accumulators.
+template <class L, int RW, int G>
 __device__ __forceinline__ void interp_groups_mma_s(const double* cb, const int (&off)[18], const double (*wrow)[RW],
                                                     int k0, const int (&cnt)[G], int lane, double (&v)[G])
 {
+    constexpr int CS = L::at(0, 0, 1);   // stride of c in the tile
     const int pj = lane >> 2, q = lane & 3;
     const double* w[G];
     double af[G][3], s[G][3];
@@ -102,6 +133,8 @@ __device__ __forceinline__ void interp_groups_mma_s(const double* cb, const int 
         w[g] = wrow[k0 + 8 * g + (valid ? pj : 0)];
 #pragma unroll
         for (int ks = 0; ks < 3; ++ks) af[g][ks] = valid ? w[g][24 + 4 * ks + q] : 0.0;
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb) s[g][bb] = 0.0;
     }
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
@@ -109,25 +142,28 @@ __device__ __forceinline__ void interp_groups_mma_s(const double* cb, const int 
 #pragma unroll
         for (int tt = 0; tt < 6; ++tt)
 #pragma unroll
-            for (int ks = 0; ks < 3; ++ks) B[tt][ks] = cb[off[6 * ch + tt] + 4 * ks];
+            for (int ks = 0; ks < 3; ++ks) B[tt][ks] = cb[off[6 * ch + tt] + 4 * ks * CS];
+        // every group's DMMAs first, then the contractions (no DMMA -> DFMA latency wait
+        // between them when G = 2)
+        double C[G][6][2];
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-            double C[6][2];
+        for (int g = 0; g < G; ++g)
 #pragma unroll
-            for (int tt = 0; tt < 6; ++tt) C[tt][0] = C[tt][1] = 0.0;
+            for (int tt = 0; tt < 6; ++tt) C[g][tt][0] = C[g][tt][1] = 0.0;
 #pragma unroll
-            for (int ks = 0; ks < 3; ++ks)
+        for (int ks = 0; ks < 3; ++ks)
 #pragma unroll
-                for (int tt = 0; tt < 6; ++tt) dmma_8x8x4(C[tt][0], C[tt][1], af[g][ks], B[tt][ks]);
-            // pair j of the chunk: a = 4 ch + j / 3, b = 3 q + j % 3
+            for (int g = 0; g < G; ++g)
 #pragma unroll
-            for (int j = 0; j < 12; ++j) {
-                const double c = C[j >> 1][j & 1];
-                const double w0a = w[g][4 * ch + j / 3];
-                if (ch == 0 && j < 3) s[g][j % 3] = w0a * c;
-                else s[g][j % 3] = fma(w0a, c, s[g][j % 3]);
-            }
-        }
+                for (int tt = 0; tt < 6; ++tt) dmma_8x8x4(C[g][tt][0], C[g][tt][1], af[g][ks], B[tt][ks]);
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+            // column e of tile 6 ch + tt: a = 2 ch + tt / 3 + 6 e, b = 3 q + tt % 3
+#pragma unroll
+            for (int tt = 0; tt < 6; ++tt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    s[g][tt % 3] = fma(w[g][2 * ch + tt / 3 + 6 * e], C[g][tt][e], s[g][tt % 3]);
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -161,7 +197,8 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     constexpr int T = 12;
     constexpr int RW = 3 * T;
     constexpr int R = S + T - 1;
-    constexpr int TILE = R * R * R;
+    using TL = typename Interp3mTile<R>::L;
+    constexpr int TILE = TL::size;
     static_assert(B % 16 == 0 && B <= 32, "batch: multiple of 16, at most 32");
     static_assert(NW == 1 || NW == 2, "one or two warps per item");
     constexpr unsigned FULL = 0xffffffffu;
@@ -215,7 +252,8 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
                        32 * NW);
         if (NW > 1) __syncthreads();
         else __syncwarp();
-        for_region_rows<R>(widx, n, threadIdx.x, 32 * NW, [&](int i, int64_t gi) { cp_async8(&tile[i], g + gi); });
+        for_region_rows<R>(widx, n, threadIdx.x, 32 * NW, [&](int i, int64_t gi) { cp_async8(&tile[i], g + gi); },
+                           TL{});
     }
     cp_async_commit();
     cp_async_wait_all();
@@ -225,7 +263,7 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     double* __restrict__ o = out + (int64_t)it.window * wstride + (int64_t)r * os.rs;
 
     int foff[18];
-    fragment_offsets<R>(foff, lane);
+    fragment_offsets_s<TL>(foff, lane);
     const double* cb = tile;
     int cur = -1;
     const int pj = lane >> 2;
@@ -265,7 +303,7 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         for (int k = 0; k < take;) {
             if ((chg >> k) & 1u) {
                 cur = cst[k];
-                cb = tile + ((cur & 255) * R + ((cur >> 8) & 255)) * R + ((cur >> 16) & 255);
+                cb = tile + TL::at(cur & 255, (cur >> 8) & 255, (cur >> 16) & 255);
             }
             const unsigned later = k < 31 ? chg & ~((2u << k) - 1u) : 0u;
             const int kend = later ? min(__ffs(later) - 1, take) : take;
@@ -284,13 +322,13 @@ k_interp3m(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
                 if (c1 > 0) {
                     const int cnt[2] = {c0, c1};
                     double v[2];
-                    interp_groups_mma_s<R, RW, 2>(cb, foff, wbuf[s], k0, cnt, lane, v);
+                    interp_groups_mma_s<TL, RW, 2>(cb, foff, wbuf[s], k0, cnt, lane, v);
                     emit(0, c0, v[0]);
                     emit(1, c1, v[1]);
                 } else {
                     const int cnt[1] = {c0};
                     double v[1];
-                    interp_groups_mma_s<R, RW, 1>(cb, foff, wbuf[s], k0, cnt, lane, v);
+                    interp_groups_mma_s<TL, RW, 1>(cb, foff, wbuf[s], k0, cnt, lane, v);
                     emit(0, c0, v[0]);
                 }
             }
