@@ -283,7 +283,7 @@ def kernel_roofline(torch, plan, wl, peaks, reps=10):
     alg_bytes = pw3 * (24 + 8)  # coordinates + value (spread) / output (interp), compulsory
     prof = profiled_traffic(name)
     return {
-        "bound": "fp64", "bound_note": "FP64 datapath (DFMA spread / FP64-DMMA interp share it): one FMA per tap, "
+        "bound": "fp64", "bound_note": "FP64 datapath (hybrid DMMA + DFMA spread / FP64-DMMA interp share it): one FMA per tap, "
                                       "12.9 FLOP per compulsory byte vs a ridge of ~5.6 -- neither HBM- nor "
                                       "low-precision-tensor-bound; HBM figures below",
         "kernel": name, "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",

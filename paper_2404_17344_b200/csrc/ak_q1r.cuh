@@ -41,6 +41,15 @@ struct Q1Lanes {
 #ifndef AK_Q1_MINB
 #define AK_Q1_MINB 16
 #endif
+// RHS values gathered one batch ahead (records two ahead) instead of at the batch start:
+// config 5 spread 0.378 -> 0.391 ms (16 CTAs/SM, 12-byte spill) / 0.373 ms (12 CTAs/SM).
+// ncu (k_spread1r, config 5): issue-bound, not gather-latency-bound -- 46.7% issue
+// active, FP64 pipe 33%, 760 warp instructions per 32-point batch of which 84 DFMA
+// evaluate the 12 window weights and ~350 load their coefficients / form gather
+// addresses; DRAM 1.25 GB per launch (3.1 TB/s).
+#ifndef AK_Q1_VPREFETCH
+#define AK_Q1_VPREFETCH 0
+#endif
 
 __device__ __forceinline__ void q1_range(const WorkItem& it, int part, int parts, int& beg, int& end) {
     beg = it.start + (int)((int64_t)it.count * part / parts);
@@ -189,19 +198,38 @@ k_spread1r(const Point* __restrict__ pts, const WorkItem* __restrict__ items, co
 #pragma unroll
         for (int a = 0; a < T; ++a) acc[a] = 0.0;
     };
-    for (int base = beg; base < end; base += 32) {
-        const int nb = min(32, end - base);
-        const Point p = pn;
-        if (lane < end - base - 32) pn = pts[base + 32 + lane];
-        // the stream's RHS values of the batch (point j = sp + SP k, RHS r0 + rl), issued
-        // before the weights are evaluated; a stream's RC lanes read one line per point
-        double vv[PPS];
+    // the stream's RHS values of a batch (point j = sp + SP k, RHS r0 + rl); a stream's RC
+    // lanes read one line per point
+    auto gather = [&](double (&vv)[PPS], const Point& q, int nb) {
 #pragma unroll
         for (int k = 0; k < PPS; ++k) {
             const int j = sp + SP * k;
-            const int idx = __shfl_sync(0xffffffffu, p.idx, j);
+            const int idx = __shfl_sync(0xffffffffu, q.idx, j);
             vv[k] = (j < nb && ract) ? __ldg(Vr + (int64_t)idx * vs.is) : 0.0;
         }
+    };
+#if AK_Q1_VPREFETCH
+    // records two batches ahead, RHS values one batch ahead (the gather latency overlaps
+    // a whole batch instead of the weight evaluation alone)
+    Point pn2;
+    if (lane < end - beg - 32) pn2 = pts[beg + 32 + lane];
+    double vn[PPS];
+    gather(vn, pn, min(32, end - beg));
+#endif
+    for (int base = beg; base < end; base += 32) {
+        const int nb = min(32, end - base);
+        const Point p = pn;
+        double vv[PPS];
+#if AK_Q1_VPREFETCH
+#pragma unroll
+        for (int k = 0; k < PPS; ++k) vv[k] = vn[k];
+        pn = pn2;
+        if (lane < end - base - 64) pn2 = pts[base + 64 + lane];
+        if (base + 32 < end) gather(vn, pn, min(32, end - base - 32));
+#else
+        if (lane < end - base - 32) pn = pts[base + 32 + lane];
+        gather(vv, p, nb);
+#endif
         __syncwarp();
         if (lane < nb) {
             double w[T];
