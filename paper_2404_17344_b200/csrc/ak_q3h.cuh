@@ -26,7 +26,9 @@ namespace ak {
 // (B200, tools/gpu_var.sh): 5 CTAs 1.432 ms, 4 CTAs (198 registers) 1.529, 6 CTAs 1.459;
 // 64-point batches 1.445; 3 warps per CTA (2 b values per lane group, 128 registers,
 // 15 warps/SM) 1.631; operands of the next k-step loaded ahead in registers: 1.605
-// (spills at 168 registers) / 1.619 (198 registers, 8 warps/SM).
+// (spills at 168 registers) / 1.619 (198 registers, 8 warps/SM); rows 8..11 kept
+// XOR-rotated per lane (acc2[j] = row 8 + (j ^ kk): a select-free reduce-scatter, but
+// lane-dependent w0 loads in the loop): 1.470.
 #ifndef AK_SPREAD3H_MINB
 #define AK_SPREAD3H_MINB 5
 #endif
