@@ -33,8 +33,13 @@ namespace ak {
 #define AK_SPREAD3H_MINB 5
 #endif
 #ifndef AK_SPREAD3H_BATCH
-#define AK_SPREAD3H_BATCH 32
+#define AK_SPREAD3H_BATCH 48
 #endif
+#ifndef AK_SPREAD3H_UNROLL
+#define AK_SPREAD3H_UNROLL 1
+#endif
+#define AK_PRAGMA(x) _Pragma(#x)
+#define AK_UNROLL(n) AK_PRAGMA(unroll n)
 #ifndef AK_SPREAD3H_WARPS
 #define AK_SPREAD3H_WARPS 2
 #endif
@@ -107,7 +112,7 @@ k_spread3h(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         if (bi + 2 < nbatch && tid < min(B, it.count - off - 2 * B))
             cp_async8(&cib[(bi + 2) % 3][tid], CIit + off + 2 * B + tid);
         cp_async_commit();
-#pragma unroll 2
+        AK_UNROLL(AK_SPREAD3H_UNROLL)
         for (int k0 = 0; k0 < nb; k0 += 4) {
             const int j = k0 + kk;
             const bool valid = j < nb;
