@@ -4,6 +4,9 @@
 #include <stdint.h>
 #include "../../include/addkern_b200.h"
 
+#define AK_PRAGMA(x) _Pragma(#x)
+#define AK_UNROLL(n) AK_PRAGMA(unroll n)
+
 namespace ak {
 
 // One bin-sorted point of one window (32 B, two 16-B vector loads).

@@ -1140,7 +1140,7 @@ static const char* launch_spread3_t(const ak_geom* g, int64_t i0, int64_t ni, co
         if (g->cached && g->sedge[3] == 1) {
             if (!g->trim3 && R % 2 == 0 && g->tune.rhs_pair_spread) {
                 // pairs of RHS on the FP64 tensor cores (ak_q3r.cuh)
-                k_spread3r<32><<<(unsigned)(ni * (R / 2)), 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V,
+                k_spread3r<AK_SPREAD3R_BATCH><<<(unsigned)(ni * (R / 2)), 64, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, V,
                                                                         vs, grids, g->canon_off_d, R, g->n);
                 return "k_spread3r";
             }

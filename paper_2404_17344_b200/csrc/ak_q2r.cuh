@@ -19,6 +19,10 @@
 #pragma once
 #include "ak_q2c.cuh"
 
+#ifndef AK_SPREAD2R_UNROLL
+#define AK_SPREAD2R_UNROLL 2
+#endif
+
 namespace ak {
 
 constexpr int Q2R_RPW = 8;   // right-hand sides per warp
@@ -242,7 +246,7 @@ k_spread2r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         if (bi + 2 < nbatch && tid < min(B, it.count - off - 2 * B))
             cp_async8(&cib[(bi + 2) % 3][tid], CIit + off + 2 * B + tid);
         cp_async_commit();
-#pragma unroll 2
+AK_UNROLL(AK_SPREAD2R_UNROLL)
         for (int k0 = 0; k0 < nb; k0 += 4) {
             const int j = k0 + kq;                       // rows past nb hold zero RHS values
             const double* w = wbuf[s][j < nb ? j : 0];

@@ -25,6 +25,10 @@
 #pragma once
 #include "ak_q3r.cuh"
 
+#ifndef AK_SPREAD3B_UNROLL
+#define AK_SPREAD3B_UNROLL 2
+#endif
+
 namespace ak {
 
 constexpr int Q3B_WARPS = 6;   // per CTA (two CTAs per SM)
@@ -152,7 +156,7 @@ k_spread3b(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
             }
         }
         __syncthreads();
-#pragma unroll 2
+AK_UNROLL(AK_SPREAD3B_UNROLL)
         for (int k0 = 0; k0 < nb; k0 += 4) {
             const int j = k0 + kk;
             const bool valid = j < nb;

@@ -15,6 +15,12 @@
 #pragma once
 #include "ak_q3m.cuh"
 
+// group loop of the single-cell interpolation: not unrolled (config 4: unroll 2 / 4
+// 1.266 / 1.257 vs 1.255 ms; config 5 +1.4% / +0.6%)
+#ifndef AK_INTERP3C_UNROLL
+#define AK_INTERP3C_UNROLL 1
+#endif
+
 namespace ak {
 
 // Register cap of the single-cell spread (config 4, B200, tools/gpu_var.sh): 196 registers
@@ -282,6 +288,7 @@ __device__ __forceinline__ void interp3c_unit(Interp3cSmem<B>& sm, int unit, con
             if (lane < nb1) cp_async8(&cib[s ^ 1][lane], CIit + off + B + lane);
         }
         cp_async_commit();
+        AK_UNROLL(AK_INTERP3C_UNROLL)
         for (int k0 = 0; k0 < nb; k0 += 8) {
             const int cnt = min(8, nb - k0);
             double v = interp_group_mma<RW, A>(gf, wbuf[s], k0, cnt, lane);

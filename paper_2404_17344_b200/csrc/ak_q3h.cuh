@@ -38,8 +38,6 @@ namespace ak {
 #ifndef AK_SPREAD3H_UNROLL
 #define AK_SPREAD3H_UNROLL 1
 #endif
-#define AK_PRAGMA(x) _Pragma(#x)
-#define AK_UNROLL(n) AK_PRAGMA(unroll n)
 #ifndef AK_SPREAD3H_WARPS
 #define AK_SPREAD3H_WARPS 2
 #endif

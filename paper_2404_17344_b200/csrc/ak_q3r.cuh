@@ -15,6 +15,14 @@
 #pragma once
 #include "ak_q3c.cuh"
 
+// k-step loop unroll (config 5: unroll 2 43.92 ms, 1 43.43) and points per batch
+#ifndef AK_SPREAD3R_UNROLL
+#define AK_SPREAD3R_UNROLL 1
+#endif
+#ifndef AK_SPREAD3R_BATCH
+#define AK_SPREAD3R_BATCH 48   // config 5: 32 -> 43.43 ms, 48 -> 43.14, 64 -> 44.58
+#endif
+
 namespace ak {
 
 template <int B>
@@ -113,7 +121,7 @@ k_spread3r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         if (bi + 2 < nbatch && tid < min(B, it.count - off - 2 * B))
             cp_async8(&cib[(bi + 2) % 3][tid], CIit + off + 2 * B + tid);
         cp_async_commit();
-#pragma unroll 2
+AK_UNROLL(AK_SPREAD3R_UNROLL)
         for (int k0 = 0; k0 < nb; k0 += 4) {
             const int j = k0 + kk;
             const bool valid = j < nb;
