@@ -1233,7 +1233,7 @@ static const char* launch_interp3_t(const ak_geom* g, int64_t i0, int64_t ni, co
                                                          g->canon_off_d, R, g->n, scale, out, os, atomic_out, wstride);
                 return "k_interp3c<10>";
             }
-            k_interp3c<32><<<units, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids, g->canon_off_d, R,
+            k_interp3c<AK_INTERP3C_BATCH><<<units, 32, 0, st>>>(g->CI3, g->W3, g->wshift_d, g->items + i0, grids, g->canon_off_d, R,
                                                  g->n, scale, out, os, atomic_out, wstride);
             return "k_interp3c";
         }
