@@ -1165,7 +1165,7 @@ static const char* launch_spread3_t(const ak_geom* g, int64_t i0, int64_t ni, co
                 cudaFuncSetAttribute(k_spread3b<AK_SPREAD3B_BATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)spread3b_smem<AK_SPREAD3B_BATCH>());
             });
-            k_spread3b<AK_SPREAD3B_BATCH><<<(unsigned)(ni * (R / 8) * 2), 32 * Q3B_WARPS, spread3b_smem<AK_SPREAD3B_BATCH>(), st>>>(
+            k_spread3b<AK_SPREAD3B_BATCH><<<(unsigned)(ni * (R / 8) * Q3B_PARTS), 32 * Q3B_WARPS, spread3b_smem<AK_SPREAD3B_BATCH>(), st>>>(
                 g->CI3, g->W3, g->wshift_d, g->items + i0, V, vs, grids, g->canon_off_d, R, g->n);
             return "k_spread3b";
         }

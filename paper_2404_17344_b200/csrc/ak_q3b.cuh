@@ -14,11 +14,11 @@
 // groups), and the 8 RHS share every B fragment.  The DFMA kernel this replaces
 // (k_spread3w, one RHS per warp) flushes its register tile into a shared region tile
 // at every cell change: config 3 spread 0.745 ms there, 0.687 ms here.
-// CTA = 6 warps, one (item, RHS chunk, column half): half h holds n-tiles 11 h .. 11 h
-// + 10, warp w of them w and w + 6 (warp 5: one) and all 13 m-tiles (at most 52
-// accumulator doubles per lane), so two CTAs fit an SM and one's prologue / flush
-// overlaps the other's DMMA stream; the item's accumulators are added to the grids
-// with RED.F64 at the end.  Per batch of B points the
+// CTA = 4 warps, one (item, RHS chunk, column part): part p of 3 holds n-tiles
+// [22p/3, 22(p+1)/3), warp w of them w and w + 4 and all 13 m-tiles (at most 52
+// accumulator doubles per lane), so several CTAs share an SM and one's prologue /
+// flush overlaps another's DMMA stream; the item's accumulators are added to the
+// grids with RED.F64 at the end.  Per batch of B points the
 // weight rows arrive by a TMA bulk copy (double-buffered), the (cell, row) records
 // and the 8 RHS values of each point by cp.async, and the CTA writes the A operand
 // (v_jr w0'_j[a'], 104 values per point) to shared memory once for all warps.
@@ -31,7 +31,19 @@
 
 namespace ak {
 
-constexpr int Q3B_WARPS = 6;   // per CTA (two CTAs per SM)
+// warps per CTA and CTAs (column parts) per (item, RHS chunk)
+// (config 3, B200: 6 warps x 2 parts 0.687 ms, 4 x 3 0.654 (default), 5 x 3 0.861,
+// 3 x 4 0.851, one CTA of 11 warps per item 0.852; with 4 x 3: 32-point batches
+// 0.661, 40 0.662, 64 0.752)
+#ifndef AK_SPREAD3B_WARPS
+#define AK_SPREAD3B_WARPS 4
+#endif
+#ifndef AK_SPREAD3B_PARTS
+#define AK_SPREAD3B_PARTS 3
+#endif
+constexpr int Q3B_WARPS = AK_SPREAD3B_WARPS;
+constexpr int Q3B_PARTS = AK_SPREAD3B_PARTS;
+static_assert(2 * Q3B_WARPS * Q3B_PARTS >= 22, "22 n-tiles, at most two per warp");
 #ifndef AK_SPREAD3B_BATCH
 #define AK_SPREAD3B_BATCH 48       // points per staged batch (config 3: 32 -> 0.734 ms, 48 -> 0.687, 64 -> 0.693)
 #endif
@@ -50,7 +62,7 @@ template <int B>
 inline size_t spread3b_smem() { return sizeof(Spread3bSmem<B>); }
 
 template <int B>
-__global__ void __launch_bounds__(32 * Q3B_WARPS, 2)
+__global__ void __launch_bounds__(32 * Q3B_WARPS, 12 / Q3B_WARPS)
 k_spread3b(const CellIdx* __restrict__ ci, const double* __restrict__ W, const int64_t* __restrict__ wshift,
            const WorkItem* __restrict__ items, const double* __restrict__ V, Strides vs,
            double* __restrict__ grids, const int64_t* __restrict__ canon_off, int nrhs, int n)
@@ -68,9 +80,10 @@ k_spread3b(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     auto& bar = sm.bar;
 
     const int nch = nrhs / 8;
-    const WorkItem it = items[blockIdx.x / (2 * nch)];
-    const int rc = (blockIdx.x >> 1) % nch;        // RHS chunk and column half run fastest: the CTAs of
-    const int hf = blockIdx.x & 1;                 // an item share its weight rows in L2
+    const WorkItem it = items[blockIdx.x / (Q3B_PARTS * nch)];
+    const int rc = (blockIdx.x / Q3B_PARTS) % nch;   // RHS chunk and column part run fastest: the CTAs
+    const int part = blockIdx.x % Q3B_PARTS;         // of an item share its weight rows in L2
+    const int pbeg = 22 * part / Q3B_PARTS, pcnt = 22 * (part + 1) / Q3B_PARTS - pbeg;   // n-tiles
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int lr = lane >> 2, kk = lane & 3;
     const double* __restrict__ V0 = V + (int64_t)(8 * rc) * vs.rs;
@@ -97,14 +110,14 @@ k_spread3b(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     }
     cp_async_commit();
 
-    // this lane's B-fragment columns: n-tile 11 hf + warp + 6 t, column 8 nt + lr -> (b', c')
+    // this lane's B-fragment columns: n-tile pbeg + warp + W t, column 8 nt + lr -> (b', c')
     int bcol[2], ccol[2];
     bool cok[2];
-    const bool two = warp + Q3B_WARPS < 11;
+    const bool one = warp < pcnt, two = warp + Q3B_WARPS < pcnt;
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
-        const int col = 8 * (11 * hf + warp + Q3B_WARPS * t) + lr;
-        cok[t] = col < NCOL && (t == 0 || two);
+        const int col = 8 * (pbeg + warp + Q3B_WARPS * t) + lr;
+        cok[t] = col < NCOL && (t == 0 ? one : two);
         bcol[t] = col / RG;
         ccol[t] = col - bcol[t] * RG;
     }
@@ -195,8 +208,8 @@ AK_UNROLL(AK_SPREAD3B_UNROLL)
     for (int t = 0; t < 2; ++t)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-            const int col = 8 * (11 * hf + warp + Q3B_WARPS * t) + 2 * kk + e;
-            ok[t][e] = col < NCOL && (t == 0 || two);
+            const int col = 8 * (pbeg + warp + Q3B_WARPS * t) + 2 * kk + e;
+            ok[t][e] = col < NCOL && (t == 0 ? one : two);
             const int b = ok[t][e] ? col / RG : 0, c = ok[t][e] ? col - (col / RG) * RG : 0;
             coff[t][e] = wrap(o1 + b, n) * n + wrap(o2 + c, n);
         }
