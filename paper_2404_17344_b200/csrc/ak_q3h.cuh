@@ -67,11 +67,15 @@ k_spread3h(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
     const CellIdx* __restrict__ CIit = ci + (it.start - wshift[it.window]);
 
+    // rows past a batch's end hold finite weights (zeroed here, then earlier batches)
+    // and zero RHS values, so the k-step loop needs no bounds checks
+    for (int e = tid; e < 2 * B * RW; e += NTH) (&wbuf[0][0][0])[e] = 0.0;
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         mbar_fence_init();
     }
+    fence_proxy_async();
     __syncthreads();
     if (tid == 0) tma_load_1d(&wbuf[0][0][0], Wit, (unsigned)(min(B, it.count) * RW * 8), &bar[0]);
     if (tid < min(B, it.count)) cp_async8(&cib[0][tid], CIit + tid);
@@ -80,6 +84,7 @@ k_spread3h(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     cp_async_wait_all();
     __syncthreads();
     if (tid < min(B, it.count)) cp_async8(&vb[0][tid], Vr + (int64_t)cib[0][tid].idx * vs.is);
+    else if (tid < B) vb[0][tid] = 0.0;
     cp_async_commit();
 
     // this lane's weight offsets: w1 at b0 .. b0 + NB - 1, w2 at c0 .. c0 + 2 (row layout w0 | w1 | w2)
@@ -106,16 +111,16 @@ k_spread3h(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
                 tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + B) * RW, (unsigned)(nb1 * RW * 8), &bar[s ^ 1]);
             }
             if (tid < nb1) cp_async8(&vb[s ^ 1][tid], Vr + (int64_t)cib[(bi + 1) % 3][tid].idx * vs.is);
+            else if (tid < B) vb[s ^ 1][tid] = 0.0;
         }
         if (bi + 2 < nbatch && tid < min(B, it.count - off - 2 * B))
             cp_async8(&cib[(bi + 2) % 3][tid], CIit + off + 2 * B + tid);
         cp_async_commit();
         AK_UNROLL(AK_SPREAD3H_UNROLL)
         for (int k0 = 0; k0 < nb; k0 += 4) {
-            const int j = k0 + kk;
-            const bool valid = j < nb;
-            const double* w = wbuf[s][valid ? j : 0];
-            const double v = valid ? vb[s][j] : 0.0;
+            const int j = k0 + kk;   // < B; rows past nb contribute zero (v = 0)
+            const double* w = wbuf[s][j];
+            const double v = vb[s][j];
             double vw1[NB], w2[3], w0h[4], bf[NT];
 #pragma unroll
             for (int x = 0; x < NB; ++x) vw1[x] = v * w[b0 + x];
