@@ -62,11 +62,15 @@ k_spread3r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     const double* __restrict__ Wit = W + (int64_t)(it.start - wshift[it.window]) * RW;
     const CellIdx* __restrict__ CIit = ci + (it.start - wshift[it.window]);
 
+    // rows past a batch's end hold finite weights (zeroed here, then earlier batches)
+    // and zero RHS values, so the k-step loop needs no bounds checks
+    for (int e = tid; e < 2 * B * RW; e += 64) (&wbuf[0][0][0])[e] = 0.0;
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         mbar_fence_init();
     }
+    fence_proxy_async();
     __syncthreads();
     if (tid == 0) tma_load_1d(&wbuf[0][0][0], Wit, (unsigned)(min(B, it.count) * RW * 8), &bar[0]);
     if (tid < min(B, it.count)) cp_async8(&cib[0][tid], CIit + tid);
@@ -74,9 +78,10 @@ k_spread3r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
     cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
-    for (int e = tid; e < 2 * min(B, it.count); e += 64) {
-        const int r = e / min(B, it.count), j = e - r * min(B, it.count);
-        cp_async8(&vb[0][r][j], V0 + (int64_t)r * vs.rs + (int64_t)cib[0][j].idx * vs.is);
+    for (int e = tid; e < 2 * B; e += 64) {
+        const int r = e / B, j = e - r * B;
+        if (j < min(B, it.count)) cp_async8(&vb[0][r][j], V0 + (int64_t)r * vs.rs + (int64_t)cib[0][j].idx * vs.is);
+        else vb[0][r][j] = 0.0;
     }
     cp_async_commit();
 
@@ -113,9 +118,10 @@ k_spread3r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
                 fence_proxy_async();
                 tma_load_1d(&wbuf[s ^ 1][0][0], Wit + (int64_t)(off + B) * RW, (unsigned)(nb1 * RW * 8), &bar[s ^ 1]);
             }
-            for (int e = tid; e < 2 * nb1; e += 64) {
-                const int r = e / nb1, j = e - r * nb1;
-                cp_async8(&vb[s ^ 1][r][j], V0 + (int64_t)r * vs.rs + (int64_t)cib[(bi + 1) % 3][j].idx * vs.is);
+            for (int e = tid; e < 2 * B; e += 64) {
+                const int r = e / B, j = e - r * B;
+                if (j < nb1) cp_async8(&vb[s ^ 1][r][j], V0 + (int64_t)r * vs.rs + (int64_t)cib[(bi + 1) % 3][j].idx * vs.is);
+                else vb[s ^ 1][r][j] = 0.0;
             }
         }
         if (bi + 2 < nbatch && tid < min(B, it.count - off - 2 * B))
@@ -123,14 +129,13 @@ k_spread3r(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
         cp_async_commit();
 AK_UNROLL(AK_SPREAD3R_UNROLL)
         for (int k0 = 0; k0 < nb; k0 += 4) {
-            const int j = k0 + kk;
-            const bool valid = j < nb;
-            const double* w = wbuf[s][valid ? j : 0];
+            const int j = k0 + kk;   // < B; rows past nb contribute zero (v = 0)
+            const double* w = wbuf[s][j];
             double af[3], bf[NT];
 #pragma unroll
-            for (int i = 0; i < 3; ++i) af[i] = valid ? vb[s][ar[i]][j] * w[aa[i]] : 0.0;
+            for (int i = 0; i < 3; ++i) af[i] = vb[s][ar[i]][j] * w[aa[i]];
 #pragma unroll
-            for (int t = 0; t < NT; ++t) bf[t] = valid ? w[T + bb[t]] * w[2 * T + bc[t]] : 0.0;
+            for (int t = 0; t < NT; ++t) bf[t] = w[T + bb[t]] * w[2 * T + bc[t]];
 #pragma unroll
             for (int i = 0; i < 3; ++i)
 #pragma unroll
