@@ -16,7 +16,8 @@
 #include "ak_q3m.cuh"
 
 // group loop of the single-cell interpolation: not unrolled (config 4: unroll 2 / 4
-// 1.266 / 1.257 vs 1.255 ms; config 5 +1.4% / +0.6%)
+// 1.266 / 1.257 vs 1.255 ms; config 5 +1.4% / +0.6%).  Unmasked groups over zero-
+// initialised weight buffers (as the spreads): 1.231 -> 1.270 ms, config 5 +3.3%.
 #ifndef AK_INTERP3C_UNROLL
 #define AK_INTERP3C_UNROLL 1
 #endif
