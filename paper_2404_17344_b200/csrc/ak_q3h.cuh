@@ -21,9 +21,11 @@
 
 namespace ak {
 
-// CTAs (2 warps) per SM the register allocation must allow (5: 168 registers, the
-// per-SMSP register file at 10 warps/SM); points per staged batch.  Measured on config 4
-// (B200, tools/gpu_var.sh): 5 CTAs 1.432 ms, 4 CTAs (198 registers) 1.529, 6 CTAs 1.459;
+// CTAs (2 warps) per SM the register allocation must allow (5: <= 168 registers, the
+// per-SMSP register file at 10 warps/SM); points per staged batch.  Final: 1.374 ms per
+// config-4 launch (0.686 of the FP64 peak).  Measured on config 4 (B200,
+// tools/gpu_var.sh), with 32-point batches and unroll 2: 5 CTAs 1.432 ms, 4 CTAs (198
+// registers) 1.529, 6 CTAs 1.459;
 // 64-point batches 1.445; 3 warps per CTA (2 b values per lane group, 128 registers,
 // 15 warps/SM) 1.631; operands of the next k-step loaded ahead in registers: 1.605
 // (spills at 168 registers) / 1.619 (198 registers, 8 warps/SM); rows 8..11 kept
