@@ -71,7 +71,13 @@ k_spread3h(const CellIdx* __restrict__ ci, const double* __restrict__ W, const i
 
     // rows past a batch's end hold finite weights (zeroed here, then earlier batches)
     // and zero RHS values, so the k-step loop needs no bounds checks
-    for (int e = tid; e < 2 * B * RW; e += NTH) (&wbuf[0][0][0])[e] = 0.0;
+    // (only rows no batch of this item fills: buffer 0 past the item's count, buffer 1
+    // past count - B when it is used; later batches leave finite earlier rows behind)
+    {
+        const int z0 = min(B, it.count), z1 = it.count > B ? min(B, it.count - B) : B;
+        for (int e = tid; e < (B - z0) * RW; e += NTH) wbuf[0][z0 + e / RW][e % RW] = 0.0;
+        for (int e = tid; e < (B - z1) * RW; e += NTH) wbuf[1][z1 + e / RW][e % RW] = 0.0;
+    }
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
