@@ -883,7 +883,7 @@ extern "C" int ak_geom_create_ex(int32_t n, int32_t P, const int32_t* q, const i
             (t.cell_items2 != 0 && t.cell_items2 != 1 && t.cell_items2 != 8) ||
             (t.chunk3 != 0 && (t.chunk3 < 64 || t.chunk3 > 65536)) || !(t.dense_cells3 >= 0.0) ||
             !(t.dense_cells3_interp >= 0.0) || !(t.dense_cells2 >= 0.0) ||
-            (t.sparse_warps != 1 && t.sparse_warps != 2))
+            (t.sparse_warps != 1 && t.sparse_warps != 2) || t.tc_spread3 < 0 || t.tc_spread3 > 3)
             return fail(AK_ERR_INVALID, "bad tuning value");
     }
     return geom_create(n, P, q, cols, X, N, ld, masks, rows_in, wf, tuning, stream, out);

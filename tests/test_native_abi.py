@@ -112,7 +112,7 @@ def test_tuning_defaults_and_validation():
 
     t = _native.tuning()
     assert (t.weight_tables, t.cell_items3, t.cell_items2, t.chunk3, t.rhs_pair_spread, t.fused_fft3,
-            t.generic_kernels, t.sparse_warps) == (1, 0, 0, 0, 1, 1, 0, 2)
+            t.generic_kernels, t.sparse_warps, t.tc_spread3) == (1, 0, 0, 0, 1, 1, 0, 2, 3)
     assert (t.dense_cells3, t.dense_cells3_interp, t.dense_cells2) == (300.0, 64.0, 2.0)
     with pytest.raises(ValueError):
         _native.tuning(no_such_knob=1)
@@ -122,7 +122,8 @@ def test_tuning_defaults_and_validation():
     q = (ctypes.c_int32 * 1)(3)
     cols = (ctypes.c_int32 * 3)(0, 1, 2)
     X = ctypes.c_void_p(1)
-    for bad in ({"cell_items3": 3}, {"cell_items2": 2}, {"chunk3": 10}, {"dense_cells3": -1.0}, {"sparse_warps": 3}):
+    for bad in ({"cell_items3": 3}, {"cell_items2": 2}, {"chunk3": 10}, {"dense_cells3": -1.0}, {"sparse_warps": 3},
+                {"tc_spread3": 4}):
         rc = lib.ak_geom_create_ex(64, 1, q, cols, X, 10, 3, None, None, ctypes.byref(wf),
                                    ctypes.byref(_native.tuning(**bad)), None, ctypes.byref(out))
         assert rc == _native.AK_ERR_INVALID and b"tuning" in lib.ak_last_error(), bad
