@@ -16,7 +16,10 @@
 #include "ak_q3m.cuh"
 
 // group loop of the single-cell interpolation: not unrolled (config 4: unroll 2 / 4
-// 1.266 / 1.257 vs 1.255 ms; config 5 +1.4% / +0.6%).  Unmasked groups over zero-
+// 1.266 / 1.257 vs 1.255 ms; config 5 +1.4% / +0.6%).  Each group's tail (w1 . s,
+// quad shuffles, output: ~30% of the stall samples) finished inside the next group's
+// DMMA stream: 1.306 ms (176-byte spill at 168 registers), 1.374 at 200 registers,
+// 1.423 at 184 -- the other warps already cover it.  Unmasked groups over zero-
 // initialised weight buffers (as the spreads): 1.231 -> 1.270 ms, config 5 +3.3%.
 #ifndef AK_INTERP3C_UNROLL
 #define AK_INTERP3C_UNROLL 1
