@@ -30,7 +30,8 @@ namespace ak {
 // 15 warps/SM) 1.631; operands of the next k-step loaded ahead in registers: 1.605
 // (spills at 168 registers) / 1.619 (198 registers, 8 warps/SM); rows 8..11 kept
 // XOR-rotated per lane (acc2[j] = row 8 + (j ^ kk): a select-free reduce-scatter, but
-// lane-dependent w0 loads in the loop): 1.470.
+// lane-dependent w0 loads in the loop): 1.470; rows 8..11 summed through shared memory
+// instead of shuffles (one more CTA barrier per item): 1.400 vs 1.371.
 #ifndef AK_SPREAD3H_MINB
 #define AK_SPREAD3H_MINB 5
 #endif
