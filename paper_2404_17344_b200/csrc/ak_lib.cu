@@ -1107,7 +1107,7 @@ static const char* launch_spread2r(const ak_geom* g, int64_t i0, int64_t ni, con
 {
     const int nw = q2r_warps(R);
     const dim3 grid((unsigned)ni, (unsigned)((R + 8 * nw - 1) / (8 * nw)));
-#define AK_S2R(NW) k_spread2r<32, NW><<<grid, 32 * NW, 0, st>>>(g->CI2, g->W2, g->wshift_d, g->items + i0, V, vs, \
+#define AK_S2R(NW) k_spread2r<AK_Q2R_SPREAD_BATCH, NW><<<grid, 32 * NW, 0, st>>>(g->CI2, g->W2, g->wshift_d, g->items + i0, V, vs, \
                                                                grids, g->canon_off_d, R, g->n)
     if (nw == 1) AK_S2R(1);
     else if (nw == 2) AK_S2R(2);
@@ -1122,7 +1122,7 @@ static const char* launch_interp2r(const ak_geom* g, int64_t i0, int64_t ni, con
 {
     const int nw = q2r_warps(R);
     const dim3 grid((unsigned)ni, (unsigned)((R + 8 * nw - 1) / (8 * nw)));
-#define AK_I2R(NW) k_interp2r<32, NW><<<grid, 32 * NW, 0, st>>>(g->CI2, g->W2, g->wshift_d, g->items + i0, grids, \
+#define AK_I2R(NW) k_interp2r<AK_Q2R_INTERP_BATCH, NW><<<grid, 32 * NW, 0, st>>>(g->CI2, g->W2, g->wshift_d, g->items + i0, grids, \
                                                                 g->canon_off_d, R, g->n, scale, out, os, atomic_out, wstride)
     if (nw == 1) AK_I2R(1);
     else if (nw == 2) AK_I2R(2);

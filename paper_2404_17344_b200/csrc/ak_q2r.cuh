@@ -29,6 +29,14 @@ constexpr int Q2R_RPW = 8;   // right-hand sides per warp
 
 // warps per SM the register allocation must allow: 16 (<= 128 registers): config-5
 // interp 1.422 -> 1.347 ms per launch, spread 1.839 -> 1.819 ms; 12 (166 registers) before
+// points per staged batch of the interpolation / spread (config 5: interpolation 16 / 24 /
+// 32 -> 2.762 / 2.712 / 2.692 ms per step, spread 16 / 24 / 32 -> 1.875 / 1.842 / 1.818)
+#ifndef AK_Q2R_INTERP_BATCH
+#define AK_Q2R_INTERP_BATCH 32
+#endif
+#ifndef AK_Q2R_SPREAD_BATCH
+#define AK_Q2R_SPREAD_BATCH 32
+#endif
 #ifndef AK_Q2R_MINW
 #define AK_Q2R_MINW 16
 #endif
