@@ -326,6 +326,10 @@ def ncu_evidence(prof):
            "dram_gbs": prof["bytes"] / dur / 1e9 if dur else None,
            "l2_throughput_pct": m.get("l2_throughput_pct"), "dram_throughput_pct": m.get("dram_throughput_pct"),
            "fp64_pipe_pct": m.get("fp64_pipe_pct"), "dmma_pipe_pct": m.get("dmma_pipe_pct")}
+    if m.get("fp64_pipe_pct") is not None and m.get("dmma_pipe_pct") is not None:
+        # DFMA / DMUL and FP64 DMMA issue to one FP64 datapath (tools/fp64_mix.cu): its busy
+        # share, of which the useful-slot fraction is algorithmic work
+        out["fp64_datapath_busy_pct"] = m["fp64_pipe_pct"] + m["dmma_pipe_pct"]
     red = m.get("red_sectors_to_l2")
     if red is not None and dur:
         out["red_sectors_per_s"] = red / dur
