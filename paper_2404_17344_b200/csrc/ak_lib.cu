@@ -1067,8 +1067,9 @@ static const char* launch_spread_tile(const ak_geom* g, int64_t i0, int64_t ni, 
     return Q == 2 ? "k_spread_tile<2>" : "k_spread_tile<1>";
 }
 
-// q = 1, RHS-minor data, R >= 8: RHS across the lanes (ak_q1r.cuh), RC RHS per warp
-static int q1r_chunk(int R) { return R <= 8 ? 8 : (R <= 16 ? 16 : 32); }
+// q = 1, RHS-minor data, R >= 8: DMMA over RHS chunks (ak_q1r.cuh), RC RHS per warp
+// (more than 16 RHS: chunks of 16 -- a 32-RHS chunk spills in the spread)
+static int q1r_chunk(int R) { return R <= 8 ? 8 : 16; }
 
 static const char* launch_spread1r(const ak_geom* g, int64_t i0, int64_t ni, const double* V, Strides vs, int R,
                                    double* grids, cudaStream_t st)
@@ -1076,8 +1077,7 @@ static const char* launch_spread1r(const ak_geom* g, int64_t i0, int64_t ni, con
     const int rc = q1r_chunk(R);
     const dim3 grid((unsigned)(ni * AK_Q1_SPLIT_SPREAD), (unsigned)((R + rc - 1) / rc));
     if (rc == 8) k_spread1r<12, 8><<<grid, 32, 0, st>>>(g->pts, g->items + i0, V, vs, grids, g->canon_off_d, R, g->n, g->wf);
-    else if (rc == 16) k_spread1r<12, 16><<<grid, 32, 0, st>>>(g->pts, g->items + i0, V, vs, grids, g->canon_off_d, R, g->n, g->wf);
-    else k_spread1r<12, 32><<<grid, 32, 0, st>>>(g->pts, g->items + i0, V, vs, grids, g->canon_off_d, R, g->n, g->wf);
+    else k_spread1r<12, 16><<<grid, 32, 0, st>>>(g->pts, g->items + i0, V, vs, grids, g->canon_off_d, R, g->n, g->wf);
     return "k_spread1r";
 }
 
@@ -1090,11 +1090,8 @@ static const char* launch_interp1r(const ak_geom* g, int64_t i0, int64_t ni, con
     if (rc == 8)
         k_interp1r<12, 8><<<grid, 32, 0, st>>>(g->pts, g->items + i0, grids, g->canon_off_d, R, g->n, g->wf, scale,
                                                out, os, atomic_out, wstride);
-    else if (rc == 16)
-        k_interp1r<12, 16><<<grid, 32, 0, st>>>(g->pts, g->items + i0, grids, g->canon_off_d, R, g->n, g->wf, scale,
-                                                out, os, atomic_out, wstride);
     else
-        k_interp1r<12, 32><<<grid, 32, 0, st>>>(g->pts, g->items + i0, grids, g->canon_off_d, R, g->n, g->wf, scale,
+        k_interp1r<12, 16><<<grid, 32, 0, st>>>(g->pts, g->items + i0, grids, g->canon_off_d, R, g->n, g->wf, scale,
                                                 out, os, atomic_out, wstride);
     return "k_interp1r";
 }
