@@ -17,6 +17,7 @@
  *   ak_type1_band      fftn + band + deconvolution of nufft_type1 (nufft.py:362-365)
  *   ak_type2_grid      deconvolution + zero-pad + ifftn of nufft_type2 (nufft.py:379-383)
  *   ak_dense_apply     dense_matvec / dense_cross_matvec / dense_matrix (kernels.py:92-170)
+ *   ak_cg_step         the body of one cg_solve iteration after the product (solver.py:63-77)
  *
  * Conventions
  *  - All array pointers are DEVICE pointers owned by the caller unless noted.
@@ -277,6 +278,36 @@ int ak_dense_apply(int32_t family, double ell, double scale, int32_t P, const in
                    const int32_t* cols, const double* Xa, int64_t Na, int64_t lda,
                    const double* Xb, int64_t Nb, int64_t ldb, const double* v,
                    double* out, double* matrix, void* stream);
+
+/*
+ * One conjugate-gradient iteration of the reference's cg_solve (solver.py:63-77), given
+ * the product Kp = K p the caller has just computed (fast_matvec(plan, p), ak_op_apply):
+ *   Ap = Kp + beta p;  pAp = p . Ap;  alpha = rs / pAp;  x += alpha p;  r -= alpha Ap;
+ *   rs_new = r . r;  p = r + (rs_new / rs) p unless sqrt(rs_new) <= threshold;  rs = rs_new.
+ * Every scalar lives in `state` on the device, and the step does nothing once
+ * state[AK_CG_ACTIVE] is 0, so a captured graph (product + step) can be replayed
+ * several times between host reads: iterations past convergence or past a breakdown
+ * leave x, the iteration count and the history untouched.
+ *   x, r, p  CG vectors of n doubles, updated in place
+ *   state    AK_CG_STATE doubles, initialised by the caller:
+ *            [AK_CG_RS] r . r, [AK_CG_ACTIVE] 1, [AK_CG_ITERATIONS] 0,
+ *            [AK_CG_BREAKDOWN_AT] 0 (set to the iteration at which p^T A p <= 0, the
+ *            reference's CgBreakdownError, with the value in [AK_CG_BREAKDOWN_PAP]),
+ *            [AK_CG_THRESHOLD] tol * ||y||
+ *   hist     hist[it] = r . r after iteration it, for it < cap (the callback values)
+ *   work     AK_CG_WORK doubles of scratch (partial sums; deterministic two-level dots)
+ * Elementwise arithmetic is unfused (numpy's multiply-then-add).
+ */
+#define AK_CG_RS             0
+#define AK_CG_ACTIVE         1
+#define AK_CG_ITERATIONS     2
+#define AK_CG_BREAKDOWN_AT   3
+#define AK_CG_BREAKDOWN_PAP  4
+#define AK_CG_THRESHOLD      5
+#define AK_CG_STATE          8
+#define AK_CG_WORK           2048
+int ak_cg_step(const double* Kp, double beta, double* x, double* r, double* p, int64_t n,
+               double* state, double* hist, int64_t cap, double* work, void* stream);
 
 /*
  * Per-kernel device timing (diagnostics; off by default, no cost when off).

@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libaddkern_b200.so"
-SOURCES = ["ak_lib.cu", "ak_probe.cu", "ak_dense.cu"]
+SOURCES = ["ak_lib.cu", "ak_probe.cu", "ak_dense.cu", "ak_cg.cu"]
 
 
 def _nvcc() -> str:

@@ -38,6 +38,8 @@ DEFAULT_CG_MAX_ITER = 5000
 #: krr_fit replays each CG iteration as a captured CUDA graph (falls back to eager launches
 #: if the product cannot be captured)
 GRAPHED_CG = True
+#: graph replays (CG iterations) between host reads of the device-side CG state
+CG_CHECK_EVERY = 8
 
 DENSE = "dense"
 FASTSUM = "fastsum"
@@ -107,28 +109,49 @@ def cg_solve(matvec, y, beta: float, tol: float = DEFAULT_CG_TOL, max_iter: int 
 
 
 def _cg_solve_graphed(matvec, y, beta, tol, max_iter, callback):
-    """_cg_solve_device with one CG iteration captured as a CUDA graph and replayed:
-    the ~10 launches of an iteration (the product's memsets, kernels and cuFFT
-    executions, the vector updates and dots) cost one graph launch, so the host
-    time between iterations (the one read of p^T A p and ||r||^2 per iteration)
-    no longer exposes per-launch Python overhead.  Same arithmetic, same
-    iterations.  Returns None if the product cannot be captured (caller falls back)."""
+    """cg_solve on the device with one CG iteration -- the product plus the native
+    `ak_cg_step` (dots, vector updates, convergence / breakdown tests, iteration count and
+    residual history, all on the device) -- captured as a CUDA graph.  The step does
+    nothing once the residual test has passed or p^T A p <= 0, so the graph is replayed
+    CG_CHECK_EVERY times between host reads of the state: the host round trip that a
+    per-iteration test costs (20-45% of an iteration below N = 100k) is paid once per
+    CG_CHECK_EVERY iterations, and the result, the iteration count and the callback
+    values are exactly those of the iteration-by-iteration loop (at most
+    CG_CHECK_EVERY - 1 no-op replays at the end).  The callback is invoked with the
+    whole residual history once the solve ends.  Returns None if the product cannot
+    be captured (caller falls back)."""
     import torch
 
-    y = y.to(torch.float64)
+    from . import _native
+
+    y = y.to(torch.float64).contiguous()
     x = torch.zeros_like(y)
     y_norm = float(torch.linalg.vector_norm(y))
     if y_norm == 0.0:
         return x, 0
     r = y.clone()
     p = r.clone()
-    rs = torch.dot(r, r).reshape(1)
-    rs_h = float(rs)
+    rs_h = float(torch.dot(r, r))
     if callback is not None:
         callback(math.sqrt(rs_h))
     if math.sqrt(rs_h) <= tol * y_norm:
         return x, 0
-    stats = torch.empty(2, dtype=torch.float64, device=y.device)
+    n = y.numel()
+    init = [0.0] * _native.AK_CG_STATE
+    init[_native.AK_CG_RS] = rs_h
+    init[_native.AK_CG_ACTIVE] = 1.0
+    init[_native.AK_CG_THRESHOLD] = tol * y_norm
+    state = torch.tensor(init, dtype=torch.float64, device=y.device)
+    hist = torch.zeros(max_iter + 1, dtype=torch.float64, device=y.device)
+    work = torch.empty(_native.AK_CG_WORK, dtype=torch.float64, device=y.device)
+    lib = _native.lib()
+
+    def step(Kp):
+        Kp = Kp.contiguous()
+        _native.check(lib.ak_cg_step(Kp.data_ptr(), float(beta), x.data_ptr(), r.data_ptr(), p.data_ptr(), n,
+                                     state.data_ptr(), hist.data_ptr(), hist.numel(), work.data_ptr(),
+                                     torch.cuda.current_stream().cuda_stream), "ak_cg_step")
+
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     try:
@@ -137,15 +160,7 @@ def _cg_solve_graphed(matvec, y, beta, tol, max_iter, callback):
             torch.cuda.current_stream().synchronize()
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=s):
-                Ap = matvec(p) + beta * p
-                pAp = torch.dot(p, Ap).reshape(1)
-                alpha = rs / pAp
-                x.add_(alpha * p)
-                r.sub_(alpha * Ap)
-                rs_new = torch.dot(r, r).reshape(1)
-                stats.copy_(torch.cat([pAp, rs_new]))
-                p.mul_(rs_new / rs).add_(r)
-                rs.copy_(rs_new)
+                step(matvec(p))
     except RuntimeError as exc:
         # CUDA-graph capture refused (e.g. an op the capture cannot record): fall back to
         # the eager device loop.  Library, allocation and argument errors propagate.
@@ -156,15 +171,28 @@ def _cg_solve_graphed(matvec, y, beta, tol, max_iter, callback):
                       RuntimeWarning, stacklevel=3)
         return None
     torch.cuda.current_stream().wait_stream(s)
-    for it in range(1, max_iter + 1):
-        graph.replay()
-        pAp_h, rs_new_h = stats.tolist()
-        if pAp_h <= 0.0:
-            raise CgBreakdownError(f"p^T A p = {pAp_h:.3e} <= 0 at iteration {it}")
-        if callback is not None:
-            callback(math.sqrt(rs_new_h))
-        if math.sqrt(rs_new_h) <= tol * y_norm:
-            return x, it
+
+    def report(upto):
+        if callback is not None and upto >= 1:
+            for rs_it in hist[1:upto + 1].tolist():
+                callback(math.sqrt(rs_it))
+
+    done = 0
+    while done < max_iter:
+        k = min(CG_CHECK_EVERY, max_iter - done)
+        for _ in range(k):
+            graph.replay()
+        done += k
+        st = state.tolist()                   # one host read per CG_CHECK_EVERY iterations
+        iters = int(st[_native.AK_CG_ITERATIONS])
+        if st[_native.AK_CG_BREAKDOWN_AT] > 0.0:
+            report(iters)
+            raise CgBreakdownError(f"p^T A p = {st[_native.AK_CG_BREAKDOWN_PAP]:.3e} <= 0 "
+                                   f"at iteration {int(st[_native.AK_CG_BREAKDOWN_AT])}")
+        if st[_native.AK_CG_ACTIVE] == 0.0:
+            report(iters)
+            return x, iters
+    report(max_iter)
     raise MaxIterationsError(f"CG did not reach tol={tol} within {max_iter} iterations")
 
 

@@ -374,3 +374,104 @@ def test_fast_dell_matches_central_difference(cuda):
         kp = fast_matvec(build_plan(KernelSpec(fam, ell + h), ws, "fine", ds), v)
         km = fast_matvec(build_plan(KernelSpec(fam, ell - h), ws, "fine", ds), v)
         assert rel(d, (kp - km) / (2 * h)) < 1e-6, fam
+
+
+def _cg_problem(n=3000, seed=11):
+    import torch
+
+    from paper_2404_17344_b200.fastsum import build_plan, fast_matvec
+    from paper_2404_17344_b200.kernels import KernelSpec
+    from paper_2404_17344_b200.solver import default_sigma_f
+    from paper_2404_17344_b200.windows import WindowSet
+
+    rng = np.random.default_rng(seed)
+    X = rng.uniform(-0.25, 0.25, size=(n, 6)) / math.sqrt(3)
+    y = np.sin(9 * X[:, 0]) + np.cos(7 * X[:, 3] * X[:, 4]) + 0.1 * rng.normal(size=n)
+    ws = WindowSet(((1, 2, 3), (4, 5, 6)), d_max=3)
+    plan = build_plan(KernelSpec("gauss", 0.2 / math.sqrt(3), default_sigma_f(2)), ws, "default", _ds(X, y, 3))
+    return (lambda p: fast_matvec(plan, p)), torch.as_tensor(y, device="cuda"), plan
+
+
+def _spd_problem(n=2000, seed=5):
+    """A deterministic SPD operator (dense cuBLAS product): iteration counts are reproducible,
+    unlike the fast product's (its window sums are RED.F64 atomics, ~1e-15 run to run)."""
+    import torch
+
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    Q = torch.randn(n, 64, dtype=torch.float64, device="cuda", generator=g)
+    A = Q @ Q.T / 64.0
+    y = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    return (lambda p: A @ p), y
+
+
+@pytest.mark.parametrize("every", [1, 3, 8])
+def test_native_cg_step_equals_torch_loop(cuda, monkeypatch, every):
+    """The graph-replayed native CG iteration (ak_cg_step, state on the device, host reads
+    every CG_CHECK_EVERY replays) against the torch loop of the same arithmetic
+    (solver.py:43-80) on a deterministic operator: same iteration count, same residual
+    history, same solution; no-op replays past convergence change nothing (bit-identical
+    x for every check interval)."""
+    import torch
+
+    from paper_2404_17344_b200 import solver
+
+    matvec, y = _spd_problem()
+    log_t, log_n = [], []
+    x_t, it_t = solver._cg_solve_device(matvec, y, 0.05, 1e-8, 500, log_t.append)
+    monkeypatch.setattr(solver, "CG_CHECK_EVERY", every)
+    x_n, it_n = solver._cg_solve_graphed(matvec, y, 0.05, 1e-8, 500, log_n.append)
+    assert it_n == it_t and it_t > 10
+    assert len(log_n) == len(log_t) == it_t + 1
+    assert np.allclose(log_n, log_t, rtol=1e-6, atol=0)
+    assert rel(x_n.cpu().numpy(), x_t.cpu().numpy()) <= 1e-9
+    monkeypatch.setattr(solver, "CG_CHECK_EVERY", 1)
+    x_1, it_1 = solver._cg_solve_graphed(matvec, y, 0.05, 1e-8, 500, None)
+    assert it_1 == it_n and torch.equal(x_1, x_n)
+
+
+def test_native_cg_on_the_fast_product(cuda):
+    """Same solve through the fast product (nondeterministic at ~1e-15, so iteration counts may
+    differ by a few): both loops solve (K + beta I) x = y to the requested residual."""
+    from paper_2404_17344_b200 import solver
+
+    matvec, y, _plan = _cg_problem()
+    x_t, it_t = solver._cg_solve_device(matvec, y, 0.05, 1e-6, 2000, None)
+    log = []
+    x_n, it_n = solver._cg_solve_graphed(matvec, y, 0.05, 1e-6, 2000, log.append)
+    assert abs(it_n - it_t) <= max(5, it_t // 5) and len(log) == it_n + 1
+    for x in (x_t, x_n):
+        res = (matvec(x) + 0.05 * x - y).norm() / y.norm()
+        assert float(res) <= 3e-6
+    assert rel(x_n.cpu().numpy(), x_t.cpu().numpy()) <= 1e-3
+
+
+def test_native_cg_step_breakdown_and_cap(cuda):
+    """CgBreakdownError at the iteration where p^T A p <= 0 and MaxIterationsError at the cap
+    (not a multiple of the check interval), as the reference raises them (solver.py:66-80)."""
+    import torch
+
+    from paper_2404_17344_b200 import solver
+    from paper_2404_17344_b200.errors import CgBreakdownError, MaxIterationsError
+
+    matvec, y, _plan = _cg_problem(n=1500)
+    log = []
+    with pytest.raises(MaxIterationsError):
+        solver._cg_solve_graphed(matvec, y, 0.05, 1e-12, 11, log.append)
+    assert len(log) == 12                                  # ||r|| at iterations 0..11
+    log = []
+    with pytest.raises(CgBreakdownError, match=r"<= 0 at iteration 1$"):
+        solver._cg_solve_graphed(lambda p: -3.0 * p, y, 0.5, 1e-6, 50, log.append)
+    assert len(log) == 1
+    # breakdown after some good iterations: an indefinite deterministic operator
+    spd, ys = _spd_problem(n=800)
+    shifted = lambda p: spd(p) - 0.06 * p  # noqa: E731   (beta 0.05: curvature -0.01 off the range of A)
+    log = []
+    with pytest.raises(CgBreakdownError) as exc:
+        solver._cg_solve_graphed(shifted, ys, 0.05, 1e-10, 200, log.append)
+    at = int(str(exc.value).rsplit(" ", 1)[1])
+    assert at > 1 and len(log) == at                       # callbacks for iterations 0..at-1
+    with pytest.raises(CgBreakdownError) as exc_t:
+        solver._cg_solve_device(shifted, ys, 0.05, 1e-10, 200, None)
+    assert int(str(exc_t.value).rsplit(" ", 1)[1]) == at
+    x0, it0 = solver._cg_solve_graphed(matvec, torch.zeros_like(y), 0.05, 1e-6, 50, None)
+    assert it0 == 0 and float(x0.abs().max()) == 0.0
