@@ -18,6 +18,7 @@
  *   ak_type2_grid      deconvolution + zero-pad + ifftn of nufft_type2 (nufft.py:379-383)
  *   ak_dense_apply     dense_matvec / dense_cross_matvec / dense_matrix (kernels.py:92-170)
  *   ak_cg_step         the body of one cg_solve iteration after the product (solver.py:63-77)
+ *   ak_cg_step_batched the same for the grid search's cells in lockstep (solver.py:157-198)
  *
  * Conventions
  *  - All array pointers are DEVICE pointers owned by the caller unless noted.
@@ -308,6 +309,22 @@ int ak_dense_apply(int32_t family, double ell, double scale, int32_t P, const in
 #define AK_CG_WORK           2048
 int ak_cg_step(const double* Kp, double beta, double* x, double* r, double* p, int64_t n,
                double* state, double* hist, int64_t cap, double* work, void* stream);
+
+/*
+ * The same step for independent systems (A_s + beta_s I) x_s = y_s in lockstep -- the KRR
+ * grid search runs one system per (ell, beta) cell where the reference's grid_search
+ * (solver.py:157-198) calls cg_solve cell by cell.  Kp holds B product rows ("slots") of
+ * n doubles; slot b updates system slot_sys[b] (NULL: slot b is system b; -1: a padding
+ * row, skipped), whose vectors are rows of X, R, P ([S][n]), whose scalars are
+ * state[slot_sys[b]][AK_CG_STATE] and whose ridge is betas[slot_sys[b]] (device array).
+ * Systems that have ended are skipped, so converged cells may stay in the batch until the
+ * caller next reads the states and compacts it.
+ *   hist  NULL, or [S][cap] residual histories
+ *   work  B * AK_CG_WORK doubles
+ */
+int ak_cg_step_batched(const double* Kp, const int32_t* slot_sys, int32_t B, const double* betas,
+                       double* X, double* R, double* P, int64_t n, double* state, double* hist,
+                       int64_t cap, double* work, void* stream);
 
 /*
  * Per-kernel device timing (diagnostics; off by default, no cost when off).

@@ -45,7 +45,7 @@ EXPORTED = (
     "ak_spread", "ak_interp", "ak_op_create", "ak_op_destroy", "ak_op_apply", "ak_op_grids", "ak_op_band",
     "ak_type1_band", "ak_type2_grid", "ak_dense_apply", "ak_probe_fp64", "ak_probe_dmma",
     "ak_tuning_default", "ak_geom_create_ex", "ak_geom_describe", "ak_prof_enable", "ak_prof_reset",
-    "ak_prof_report", "ak_geom_box", "ak_cg_step",
+    "ak_prof_report", "ak_geom_box", "ak_cg_step", "ak_cg_step_batched",
 )
 
 # ak_cg_step state layout (include/addkern_b200.h)
@@ -142,6 +142,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "ak_dense_apply": (_c_int, [_i32, ctypes.c_double, ctypes.c_double, _i32, ctypes.POINTER(_i32),
                                     ctypes.POINTER(_i32), _dp, _i64, _i64, _dp, _i64, _i64, _dp, _dp, _dp, _vp]),
         "ak_cg_step": (_c_int, [_dp, ctypes.c_double, _dp, _dp, _dp, _i64, _dp, _dp, _i64, _dp, _vp]),
+        "ak_cg_step_batched": (_c_int, [_dp, _dp, _i32, _dp, _dp, _dp, _dp, _i64, _dp, _dp, _i64, _dp, _vp]),
         "ak_probe_fp64": (_c_int, [_i64, _vp, ctypes.POINTER(ctypes.c_double)]),
         "ak_probe_dmma": (_c_int, [_i64, _vp, ctypes.POINTER(ctypes.c_double)]),
     }

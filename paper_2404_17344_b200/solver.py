@@ -357,7 +357,9 @@ def _subset_applier(plan, specs, full_op):
             b *= 2
         return min(b, R)
 
-    def apply_subset(Pa, idx):
+    def bind(idx):
+        """The product for a fixed active set: operator bucket, multiplier tables and the
+        padded input buffer prepared once."""
         n = len(idx)
         B = bucket(n)
         op = ops.get(B)
@@ -365,16 +367,28 @@ def _subset_applier(plan, specs, full_op):
             op = _grid_operator(plan, specs[:B], B)
             ops[B] = op
         rows = np.concatenate([idx, np.full(B - n, idx[0])]) if B > n else idx
-        op.set_rhs_multipliers(table[torch.as_tensor(rows, device=table.device)].reshape(-1))
-        if B > n:
-            Pp = torch.zeros((B, Pa.shape[1]), dtype=Pa.dtype, device=Pa.device)
-            Pp[:n] = Pa
-        else:
-            Pp = Pa
-        out = torch.empty_like(Pp)
-        op.apply(Pp, [out], [True])
-        return out[:n]
+        tables = table[torch.as_tensor(rows, device=table.device)].reshape(-1)
+        Pp = [None]
 
+        def product(Pa):
+            op.set_rhs_multipliers(tables)   # buckets are shared between active sets
+            if B > n:
+                if Pp[0] is None:
+                    Pp[0] = torch.zeros((B, Pa.shape[1]), dtype=Pa.dtype, device=Pa.device)
+                Pp[0][:n] = Pa
+                src = Pp[0]
+            else:
+                src = Pa
+            out = torch.empty_like(src)
+            op.apply(src, [out], [True])
+            return out[:n]
+
+        return product
+
+    def apply_subset(Pa, idx):
+        return bind(idx)(Pa)
+
+    apply_subset.bind = bind
     return apply_subset
 
 
@@ -385,60 +399,78 @@ def cg_solve_batched(apply, Y, betas, tol: float = DEFAULT_CG_TOL, max_iter: int
     ``apply`` maps an (R, N) tensor of directions to (A_r p_r)_r.  If
     ``apply_subset(P_active, idx)`` is given, only the still-active systems are
     multiplied ((R_active, N) -> (R_active, N), idx = their indices), so
-    converged systems stop costing products.  Returns (X, iterations,
-    messages); iterations[r] = -1 for a failed system, whose message says why.
-    Each system follows exactly the iteration of cg_solve.
+    converged systems stop costing products; an ``apply_subset.bind(idx)`` method,
+    if present, returns the product for a fixed active set (per-set preparation
+    done once).  Returns (X, iterations, messages); iterations[r] = -1 for a
+    failed system, whose message says why.  Each system follows exactly the
+    iteration of cg_solve.
+
+    Everything after the product is the native `ak_cg_step_batched` (per-system
+    dots, updates, convergence / breakdown tests and iteration counts on the
+    device); the host reads the systems' states and compacts the active set every
+    CG_CHECK_EVERY iterations -- systems that end in between are skipped by the
+    step and merely ride along in the product until then.
     """
     import torch
 
+    from . import _native
+
     R, N = Y.shape
-    betas = torch.as_tensor(np.asarray(betas, dtype=np.float64), device=Y.device).reshape(R, 1)
+    Y = Y.to(torch.float64).contiguous()
+    dev = Y.device
+    betas_d = torch.as_tensor(np.asarray(betas, dtype=np.float64), device=dev).reshape(R).contiguous()
     X = torch.zeros_like(Y)
     Rr = Y.clone()
     P = Rr.clone()
-    ynorm = torch.linalg.vector_norm(Y, dim=1)
-    rs = (Rr * Rr).sum(dim=1)
+    yn = torch.linalg.vector_norm(Y, dim=1).cpu().numpy()
+    rs_h = (Rr * Rr).sum(dim=1).cpu().numpy()
     iters = np.full(R, -1, dtype=np.int64)
     msgs = [""] * R
-    yn = ynorm.cpu().numpy()
-    rs_h = rs.cpu().numpy()
     active = np.ones(R, dtype=bool)
     for r in range(R):
         if yn[r] == 0.0 or math.sqrt(rs_h[r]) <= tol * yn[r]:
             iters[r] = 0
             active[r] = False
-    act = torch.as_tensor(active, device=Y.device)
-    P[~act] = 0.0
-    for it in range(1, max_iter + 1):
-        if not active.any():
-            break
-        if apply_subset is not None:
-            idx = np.nonzero(active)[0]
-            idx_d = torch.as_tensor(idx, device=Y.device)
-            AP = torch.zeros_like(P)
-            AP[idx_d] = apply_subset(P[idx_d].contiguous(), idx)
-            AP += betas * P
+    init = np.zeros((R, _native.AK_CG_STATE))
+    init[:, _native.AK_CG_RS] = rs_h
+    init[:, _native.AK_CG_ACTIVE] = active
+    init[:, _native.AK_CG_THRESHOLD] = tol * yn
+    state = torch.as_tensor(init, device=dev)
+    work = torch.empty(R * _native.AK_CG_WORK, dtype=torch.float64, device=dev)
+    lib = _native.lib()
+    done = 0
+    while done < max_iter and active.any():
+        idx = np.nonzero(active)[0]
+        idx_d = torch.as_tensor(idx, device=dev)
+        slots = torch.as_tensor(idx.astype(np.int32), device=dev)
+        if apply_subset is None:
+            product = None
+        elif hasattr(apply_subset, "bind"):
+            product = apply_subset.bind(idx)
         else:
-            AP = apply(P) + betas * P
-        pAp = (P * AP).sum(dim=1)
-        act = torch.as_tensor(active, device=Y.device)
-        ok = act & (pAp > 0.0)                      # breakdown: frozen before the update
-        alpha = torch.where(ok, rs / torch.where(ok, pAp, torch.ones_like(pAp)), torch.zeros_like(rs))
-        X += alpha.reshape(R, 1) * P
-        Rr -= alpha.reshape(R, 1) * AP
-        rs_new = (Rr * Rr).sum(dim=1)
-        pAp_h, rs_new_h = torch.stack([pAp, rs_new]).cpu().numpy()   # one host read per iteration
-        for r in np.nonzero(active)[0]:
-            if pAp_h[r] <= 0.0:
-                msgs[r] = f"p^T A p = {pAp_h[r]:.3e} <= 0 at iteration {it}"
+            product = lambda Pa, idx=idx: apply_subset(Pa, idx)  # noqa: E731
+        k = min(CG_CHECK_EVERY, max_iter - done)
+        for _ in range(k):
+            if product is None:
+                Kp = apply(P).contiguous()
+                slot_ptr, B = 0, R                      # slot r is system r
+            else:
+                Kp = product(P.index_select(0, idx_d)).contiguous()
+                slot_ptr, B = slots.data_ptr(), len(idx)
+            _native.check(lib.ak_cg_step_batched(Kp.data_ptr(), slot_ptr, B, betas_d.data_ptr(), X.data_ptr(),
+                                                 Rr.data_ptr(), P.data_ptr(), N, state.data_ptr(), 0, 0,
+                                                 work.data_ptr(), torch.cuda.current_stream().cuda_stream),
+                          "ak_cg_step_batched")
+        done += k
+        st = state.cpu().numpy()                        # one host read per CG_CHECK_EVERY iterations
+        for r in idx:
+            if st[r, _native.AK_CG_BREAKDOWN_AT] > 0.0:
+                msgs[r] = (f"p^T A p = {st[r, _native.AK_CG_BREAKDOWN_PAP]:.3e} <= 0 "
+                           f"at iteration {int(st[r, _native.AK_CG_BREAKDOWN_AT])}")
                 active[r] = False
-            elif math.sqrt(rs_new_h[r]) <= tol * yn[r]:
-                iters[r] = it
+            elif st[r, _native.AK_CG_ACTIVE] == 0.0:
+                iters[r] = int(st[r, _native.AK_CG_ITERATIONS])
                 active[r] = False
-        act = torch.as_tensor(active, device=Y.device)
-        ratio = torch.where(act, rs_new / torch.where(act, rs, torch.ones_like(rs)), torch.zeros_like(rs))
-        P = torch.where(act.reshape(R, 1), Rr + ratio.reshape(R, 1) * P, torch.zeros_like(P))
-        rs = torch.where(act, rs_new, rs)
     for r in np.nonzero(active)[0]:
         msgs[r] = f"CG did not reach tol={tol} within {max_iter} iterations"
     return X, iters, msgs
