@@ -35,11 +35,15 @@ from .windows import WindowSet
 
 DEFAULT_CG_TOL = 1e-3
 DEFAULT_CG_MAX_ITER = 5000
-#: krr_fit replays each CG iteration as a captured CUDA graph (falls back to eager launches
-#: if the product cannot be captured)
+#: long krr_fit solves replay the CG iteration as a captured CUDA graph (eager launches of the
+#: same iteration if the product cannot be captured)
 GRAPHED_CG = True
-#: graph replays (CG iterations) between host reads of the device-side CG state
+#: CG iterations between host reads of the device-side CG state
 CG_CHECK_EVERY = 8
+#: iterations launched eagerly before the iteration is captured as a CUDA graph: the capture
+#: costs ~6 ms and a replayed iteration saves ~0.02 ms over an eager one (B200, N = 20k .. 1M),
+#: so only solves with some 300 iterations still to run gain from it
+CG_GRAPH_AFTER = 256
 
 DENSE = "dense"
 FASTSUM = "fastsum"
@@ -109,17 +113,20 @@ def cg_solve(matvec, y, beta: float, tol: float = DEFAULT_CG_TOL, max_iter: int 
 
 
 def _cg_solve_graphed(matvec, y, beta, tol, max_iter, callback):
-    """cg_solve on the device with one CG iteration -- the product plus the native
+    """cg_solve on the device with one CG iteration = the product plus the native
     `ak_cg_step` (dots, vector updates, convergence / breakdown tests, iteration count and
-    residual history, all on the device) -- captured as a CUDA graph.  The step does
+    residual history, all on the device).  The first CG_GRAPH_AFTER iterations are
+    launched eagerly (capturing a graph costs ~6 ms, more than a short solve); a solve
+    that is still running then captures the iteration as a CUDA graph and replays it
+    (one launch per iteration instead of the product's ~0.13 ms of host launch work).
+    The step does
     nothing once the residual test has passed or p^T A p <= 0, so the graph is replayed
     CG_CHECK_EVERY times between host reads of the state: the host round trip that a
     per-iteration test costs (20-45% of an iteration below N = 100k) is paid once per
     CG_CHECK_EVERY iterations, and the result, the iteration count and the callback
     values are exactly those of the iteration-by-iteration loop (at most
     CG_CHECK_EVERY - 1 no-op replays at the end).  The callback is invoked with the
-    whole residual history once the solve ends.  Returns None if the product cannot
-    be captured (caller falls back)."""
+    whole residual history once the solve ends."""
     import torch
 
     from . import _native
@@ -152,25 +159,28 @@ def _cg_solve_graphed(matvec, y, beta, tol, max_iter, callback):
                                      state.data_ptr(), hist.data_ptr(), hist.numel(), work.data_ptr(),
                                      torch.cuda.current_stream().cuda_stream), "ak_cg_step")
 
-    s = torch.cuda.Stream()
-    s.wait_stream(torch.cuda.current_stream())
-    try:
-        with torch.cuda.stream(s):
-            matvec(p)                         # warm-up: operators / cuFFT plans exist before capture
-            torch.cuda.current_stream().synchronize()
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=s):
-                step(matvec(p))
-    except RuntimeError as exc:
-        # CUDA-graph capture refused (e.g. an op the capture cannot record): fall back to
-        # the eager device loop.  Library, allocation and argument errors propagate.
+    def capture():
+        """The iteration as a CUDA graph (None if the product cannot be captured)."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        try:
+            with torch.cuda.stream(s):
+                matvec(p)                     # operators / cuFFT plans exist on this stream before capture
+                torch.cuda.current_stream().synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    step(matvec(p))
+        except RuntimeError as exc:
+            # capture refused (e.g. an op the capture cannot record): stay with eager
+            # launches of the same iteration.  Library, allocation and argument errors propagate.
+            torch.cuda.current_stream().wait_stream(s)
+            if isinstance(exc, NativeLibraryError) or "out of memory" in str(exc):
+                raise
+            warnings.warn(f"CUDA-graph capture of the CG iteration failed ({exc}); running it eagerly",
+                          RuntimeWarning, stacklevel=4)
+            return None
         torch.cuda.current_stream().wait_stream(s)
-        if isinstance(exc, NativeLibraryError) or "out of memory" in str(exc):
-            raise
-        warnings.warn(f"CUDA-graph capture of the CG iteration failed ({exc}); running it eagerly",
-                      RuntimeWarning, stacklevel=3)
-        return None
-    torch.cuda.current_stream().wait_stream(s)
+        return g
 
     def report(upto):
         if callback is not None and upto >= 1:
@@ -178,10 +188,16 @@ def _cg_solve_graphed(matvec, y, beta, tol, max_iter, callback):
                 callback(math.sqrt(rs_it))
 
     done = 0
+    graph, try_graph = None, GRAPHED_CG
     while done < max_iter:
         k = min(CG_CHECK_EVERY, max_iter - done)
+        if try_graph and done >= CG_GRAPH_AFTER:
+            graph, try_graph = capture(), False
         for _ in range(k):
-            graph.replay()
+            if graph is not None:
+                graph.replay()
+            else:
+                step(matvec(p))
         done += k
         st = state.tolist()                   # one host read per CG_CHECK_EVERY iterations
         iters = int(st[_native.AK_CG_ITERATIONS])
@@ -267,14 +283,7 @@ def krr_fit(train: Dataset, ws: WindowSet, spec: KernelSpec, beta: float, backen
 
         plan = build_plan(spec, ws, preset, train)
         y = torch.as_tensor(train.targets, device="cuda")
-        res = None
-        if GRAPHED_CG:
-            res = _cg_solve_graphed(lambda p: fast_matvec(plan, p), y, beta, tol, max_iter, log.append)
-            if res is None:
-                log.clear()
-        if res is None:
-            res = cg_solve(lambda p: fast_matvec(plan, p), y, beta, tol=tol, max_iter=max_iter, callback=log.append)
-        v, iters = res
+        v, iters = _cg_solve_graphed(lambda p: fast_matvec(plan, p), y, beta, tol, max_iter, log.append)
         coef = v.cpu().numpy()
     elif backend == DENSE:
         coef, iters = cg_solve(lambda p: dense_matvec(spec, ws, train, p), train.targets, beta, tol=tol,

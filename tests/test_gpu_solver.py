@@ -401,42 +401,48 @@ def _spd_problem(n=2000, seed=5):
     import torch
 
     g = torch.Generator(device="cuda").manual_seed(seed)
-    Q = torch.randn(n, 64, dtype=torch.float64, device="cuda", generator=g)
-    A = Q @ Q.T / 64.0
+    Q = torch.randn(n, 300, dtype=torch.float64, device="cuda", generator=g)
+    A = Q @ Q.T / 300.0
     y = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
     return (lambda p: A @ p), y
 
 
+@pytest.mark.parametrize("graph_after", [0, 16, 10**9])
 @pytest.mark.parametrize("every", [1, 3, 8])
-def test_native_cg_step_equals_torch_loop(cuda, monkeypatch, every):
+def test_native_cg_step_equals_torch_loop(cuda, monkeypatch, every, graph_after):
     """The graph-replayed native CG iteration (ak_cg_step, state on the device, host reads
     every CG_CHECK_EVERY replays) against the torch loop of the same arithmetic
     (solver.py:43-80) on a deterministic operator: same iteration count, same residual
     history, same solution; no-op replays past convergence change nothing (bit-identical
-    x for every check interval)."""
+    x for every check interval), whether the iteration is launched eagerly, replayed as a
+    CUDA graph from the start, or switched to the graph mid-solve."""
     import torch
 
     from paper_2404_17344_b200 import solver
 
     matvec, y = _spd_problem()
     log_t, log_n = [], []
-    x_t, it_t = solver._cg_solve_device(matvec, y, 0.05, 1e-8, 500, log_t.append)
+    x_t, it_t = solver._cg_solve_device(matvec, y, 0.01, 1e-10, 500, log_t.append)
     monkeypatch.setattr(solver, "CG_CHECK_EVERY", every)
-    x_n, it_n = solver._cg_solve_graphed(matvec, y, 0.05, 1e-8, 500, log_n.append)
-    assert it_n == it_t and it_t > 10
+    monkeypatch.setattr(solver, "CG_GRAPH_AFTER", graph_after)
+    x_n, it_n = solver._cg_solve_graphed(matvec, y, 0.01, 1e-10, 500, log_n.append)
+    assert it_n == it_t and it_t > 20
     assert len(log_n) == len(log_t) == it_t + 1
     assert np.allclose(log_n, log_t, rtol=1e-6, atol=0)
     assert rel(x_n.cpu().numpy(), x_t.cpu().numpy()) <= 1e-9
     monkeypatch.setattr(solver, "CG_CHECK_EVERY", 1)
-    x_1, it_1 = solver._cg_solve_graphed(matvec, y, 0.05, 1e-8, 500, None)
+    monkeypatch.setattr(solver, "CG_GRAPH_AFTER", 0)
+    x_1, it_1 = solver._cg_solve_graphed(matvec, y, 0.01, 1e-10, 500, None)
     assert it_1 == it_n and torch.equal(x_1, x_n)
 
 
-def test_native_cg_on_the_fast_product(cuda):
+@pytest.mark.parametrize("graph_after", [0, 10**9])
+def test_native_cg_on_the_fast_product(cuda, monkeypatch, graph_after):
     """Same solve through the fast product (nondeterministic at ~1e-15, so iteration counts may
     differ by a few): both loops solve (K + beta I) x = y to the requested residual."""
     from paper_2404_17344_b200 import solver
 
+    monkeypatch.setattr(solver, "CG_GRAPH_AFTER", graph_after)
     matvec, y, _plan = _cg_problem()
     x_t, it_t = solver._cg_solve_device(matvec, y, 0.05, 1e-6, 2000, None)
     log = []
@@ -448,7 +454,8 @@ def test_native_cg_on_the_fast_product(cuda):
         assert float(res) <= 3e-6
 
 
-def test_native_cg_step_breakdown_and_cap(cuda):
+@pytest.mark.parametrize("graph_after", [0, 10**9])
+def test_native_cg_step_breakdown_and_cap(cuda, monkeypatch, graph_after):
     """CgBreakdownError at the iteration where p^T A p <= 0 and MaxIterationsError at the cap
     (not a multiple of the check interval), as the reference raises them (solver.py:66-80)."""
     import torch
@@ -456,6 +463,7 @@ def test_native_cg_step_breakdown_and_cap(cuda):
     from paper_2404_17344_b200 import solver
     from paper_2404_17344_b200.errors import CgBreakdownError, MaxIterationsError
 
+    monkeypatch.setattr(solver, "CG_GRAPH_AFTER", graph_after)
     matvec, y, _plan = _cg_problem(n=1500)
     log = []
     with pytest.raises(MaxIterationsError):

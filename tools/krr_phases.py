@@ -39,7 +39,7 @@ for n in (20_000, 100_000, 1_000_000):
     def per_iteration(fn):
         """Fixed iteration counts (tolerance 0): the difference of two caps is the per-iteration cost."""
         out = []
-        for cap in (40, 240):
+        for cap in (100, 1100):
             best = 1e9
             for _ in range(3):
                 t0 = tick()
@@ -49,12 +49,18 @@ for n in (20_000, 100_000, 1_000_000):
                     pass
                 best = min(best, tick() - t0)
             out.append(best)
-        return (out[1] - out[0]) / 200, out[0] - 40 * (out[1] - out[0]) / 200
+        return (out[1] - out[0]) / 1000, out[0] - 100 * (out[1] - out[0]) / 1000
 
     res = {}
-    for every in (1, 4, 8, 16):
+    solver.CG_GRAPH_AFTER = 0
+    for every in (1, 8):
         solver.CG_CHECK_EVERY = every
         res[f"graphed/{every}"] = per_iteration(lambda cap: solver._cg_solve_graphed(mv, yd, 0.1, 0.0, cap, None))
-    solver.CG_CHECK_EVERY = 8
+    solver.GRAPHED_CG = False
+    for every in (1, 8):
+        solver.CG_CHECK_EVERY = every
+        res[f"native eager/{every}"] = per_iteration(lambda cap: solver._cg_solve_graphed(mv, yd, 0.1, 0.0, cap, None))
+    solver.GRAPHED_CG, solver.CG_GRAPH_AFTER, solver.CG_CHECK_EVERY = True, 256, 8
+    res["default (eager 256, then graph)"] = per_iteration(lambda cap: solver._cg_solve_graphed(mv, yd, 0.1, 0.0, cap, None))
     res["eager torch"] = per_iteration(lambda cap: solver._cg_solve_device(mv, yd, 0.1, 0.0, cap, None))
     print(f"N={n}: product {1e3 * prod:.3f} ms; " + "; ".join(f"{k}: {1e3 * a:.3f} ms/it (+{1e3 * b:.1f} ms setup)" for k, (a, b) in res.items()))
