@@ -98,6 +98,10 @@ def test_argument_validation_without_a_device():
     code(lib.ak_type1_band(4, 64, 32, None, None, None, None, None), "type1")
     code(lib.ak_type2_grid(3, 64, 128, None, None, None, None, None), "type2")
     code(lib.ak_dense_apply(9, 1.0, 1.0, 1, q, cols, None, 0, 3, None, 0, 3, None, None, None, None), "dense")
+    code(lib.ak_cg_step(None, 0.1, X, X, X, 10, X, X, 5, X, None), "CG step")
+    code(lib.ak_cg_step(X, 0.1, X, X, X, 0, X, X, 5, X, None), "CG step")
+    code(lib.ak_cg_step_batched(X, None, 0, X, X, X, X, 10, X, None, 0, X, None), "batched CG")
+    code(lib.ak_cg_step_batched(X, None, 2, None, X, X, X, 10, X, None, 0, X, None), "batched CG")
 
 
 def test_tuning_defaults_and_validation():
