@@ -115,18 +115,19 @@ def cg_solve(matvec, y, beta: float, tol: float = DEFAULT_CG_TOL, max_iter: int 
 def _cg_solve_graphed(matvec, y, beta, tol, max_iter, callback):
     """cg_solve on the device with one CG iteration = the product plus the native
     `ak_cg_step` (dots, vector updates, convergence / breakdown tests, iteration count and
-    residual history, all on the device).  The first CG_GRAPH_AFTER iterations are
-    launched eagerly (capturing a graph costs ~6 ms, more than a short solve); a solve
-    that is still running then captures the iteration as a CUDA graph and replays it
-    (one launch per iteration instead of the product's ~0.13 ms of host launch work).
-    The step does
-    nothing once the residual test has passed or p^T A p <= 0, so the graph is replayed
-    CG_CHECK_EVERY times between host reads of the state: the host round trip that a
+    residual history, all on the device; solver.py:43-80 of the reference).
+
+    The step does nothing once the residual test has passed or p^T A p <= 0, so the host
+    reads the state only every CG_CHECK_EVERY iterations: the round trip that a
     per-iteration test costs (20-45% of an iteration below N = 100k) is paid once per
     CG_CHECK_EVERY iterations, and the result, the iteration count and the callback
     values are exactly those of the iteration-by-iteration loop (at most
-    CG_CHECK_EVERY - 1 no-op replays at the end).  The callback is invoked with the
-    whole residual history once the solve ends."""
+    CG_CHECK_EVERY - 1 no-op iterations at the end).  The first CG_GRAPH_AFTER
+    iterations are launched eagerly (capturing a graph costs ~6 ms, more than a short
+    solve); a solve that is still running then captures the iteration as a CUDA graph
+    and replays it (one launch per iteration instead of the product's ~0.13 ms of host
+    launch work).  The callback is invoked with the whole residual history once the
+    solve ends."""
     import torch
 
     from . import _native
